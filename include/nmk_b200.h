@@ -1,0 +1,168 @@
+/*
+ * nmk_b200.h — C ABI of the B200 (sm_100a) NUMARCK hot path.
+ *
+ * The reference (arXiv 1703.02438 re-implementation, package `nmk`) is pure
+ * Python; its hot path is the body of `pipeline.compress_pair` phases 1-4a
+ * (pkg/src/nmk/pipeline.py:185-288) and the decode chain
+ * `pipeline.decompress` -> `codec._decode_range` -> `codec.unpack_block` +
+ * `core.reconstruct` (pipeline.py:327-340, codec.py:95-105,204-239,
+ * core.py:158-208).  This library replaces exactly those phases.  The Python
+ * mirror `paper_1703_02438_b200` binds these symbols through ctypes and keeps
+ * the reference's public API (compress_pair / decompress / compress_series /
+ * partial_decode) on top; see INTEGRATION.md for the binding.
+ *
+ * Conventions
+ *  - All buffers are caller-owned DEVICE pointers unless named h_*; the
+ *    stream is the last argument; every call is stream-ordered and returns
+ *    0 (NMK_OK) or a negative NMK_ERR_* code with a thread-local message in
+ *    nmk_last_error().  No call synchronises the stream.
+ *  - dtype: NMK_F32 / NMK_F64, matching the container's dtype codes
+ *    (container.py:28-31).
+ *  - Element indices are 64-bit (n up to 4e9 per call).
+ *  - Arithmetic is IEEE binary64 without contraction (built -fmad=false),
+ *    bit-identical to the reference's numpy expressions.
+ */
+#ifndef NMK_B200_H
+#define NMK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NMK_OK               0
+#define NMK_ERR_ARG         -1   /* bad argument (ValueError in Python)            */
+#define NMK_ERR_CUDA        -2   /* CUDA runtime / launch failure                   */
+#define NMK_ERR_EMPTY_HIST  -6   /* no selectable bin: binning.py:145-146          */
+
+#define NMK_F32 0
+#define NMK_F64 1
+
+/* Device scalars produced by nmk_minmax (phase 1, pipeline.py:190-212).
+ * For a multi-GPU run the caller all-reduces gmin (MIN), gmax (MAX) and
+ * nvalid (SUM) before the histogram. */
+typedef struct nmk_stats {
+    double gmin;
+    double gmax;
+    unsigned long long nvalid;
+    unsigned long long reserved;
+} nmk_stats;
+
+/* Device model header produced by nmk_select (phase 2 decisions,
+ * pipeline.py:127-140,229; binning.py:142-206). */
+typedef struct nmk_model {
+    int32_t bits;          /* index length B                                    */
+    int32_t k;             /* number of (quantised) centers                     */
+    int32_t status;        /* 0 ok, NMK_ERR_EMPTY_HIST                          */
+    int32_t m_selectable;  /* nonempty bins with a finite center                */
+    double  tol_bin;       /* BinModel.tolerance: (2E)/2, or E when degenerate  */
+    unsigned long long coverage[17]; /* auto-B: covered elements for B=2..16    */
+} nmk_model;
+
+/* Decode error word (device), checked by the caller after nmk_decode. */
+typedef struct nmk_decode_err {
+    unsigned int bad_index;        /* 1 if any code in [k, sentinel)            */
+    unsigned int max_bad_index;    /* largest such code                         */
+    unsigned int exhausted;        /* 1 if an exact value past the end was read */
+    unsigned int reserved;
+} nmk_decode_err;
+
+/* Per-segment decode bookkeeping (device, written by nmk_decode). */
+typedef struct nmk_segment_info {
+    unsigned long long inc_before;   /* exact values before segment start,
+                                        relative to the exact pointer passed   */
+    unsigned long long n_sentinel;   /* sentinels inside the segment            */
+} nmk_segment_info;
+
+const char* nmk_last_error(void);
+int nmk_version(void);
+
+/* -- A1 standalone: ratio + validity (core.py:115-137) -------------------- */
+int nmk_ratio(const void* base, const void* cur, uint64_t n, int dtype,
+              double* ratios, uint8_t* valid, void* stream);
+
+/* -- K1: fused ratio + min/max + valid count (pipeline.py:190-212) -------- */
+size_t nmk_minmax_ws_bytes(uint64_t n);
+int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
+               nmk_stats* stats, void* ws, size_t ws_bytes, void* stream);
+
+/* -- K2: histogram of floor((r - gmin) / width) over valid r
+ *        (binning.py:110-116 via pipeline.py:214-224).
+ * Dense: counts[q] for q in [0, nbins), nbins = floor((gmax-gmin)/width)+1;
+ *        counts is zeroed by the call.
+ * Sparse: sorted distinct keys (bit patterns of the non-negative double
+ *        ordinal, -0 canonicalised) + counts + *nruns, for spans too wide to
+ *        densify. */
+int nmk_hist_dense(const void* base, const void* cur, uint64_t n, int dtype,
+                   const nmk_stats* stats, double width, uint64_t nbins,
+                   unsigned long long* counts, void* stream);
+size_t nmk_hist_sparse_ws_bytes(uint64_t n);
+int nmk_hist_sparse(const void* base, const void* cur, uint64_t n, int dtype,
+                    const nmk_stats* stats, double width,
+                    unsigned long long* keys, unsigned long long* counts,
+                    unsigned long long* nruns, void* ws, size_t ws_bytes, void* stream);
+/* Merge of gathered sparse histograms (binning.py:119-132): sort by key and
+ * sum counts of equal keys. keys/counts hold n_in entries; output in place. */
+size_t nmk_hist_merge_ws_bytes(uint64_t n_in);
+int nmk_hist_merge(unsigned long long* keys, unsigned long long* counts, uint64_t n_in,
+                   unsigned long long* nruns, void* ws, size_t ws_bytes, void* stream);
+
+/* -- K3: single-CTA top-k + auto-B + quantisation + cuts
+ *        (binning.py:135-152,155-206; pipeline.py:112-124,163-167,229).
+ * keys == NULL selects the dense form (ordinal = array index, nbins = m_max).
+ * nruns: device count for the sparse form (NULL for dense).
+ * bits < 0 selects B automatically over [2, 16].
+ * centers/cuts: capacity cap_k doubles; centers_t: cap_k elements of dtype. */
+int nmk_select(const unsigned long long* keys, const unsigned long long* counts,
+               uint64_t m_max, const unsigned long long* nruns,
+               const nmk_stats* stats, double width, double tolerance,
+               int bits, uint64_t n_total, int dtype,
+               double* centers, double* cuts, void* centers_t, uint64_t cap_k,
+               nmk_model* model, void* stream);
+
+/* -- K4: fused classify + round-trip filter + B-bit pack + stable compaction
+ *        (binning.py:287-301,350-359; pipeline.py:143-160,238-288; codec.py:83-92)
+ * Encodes the local element range [elem0, elem0 + n_local) of a global
+ * stream of n_total elements.  Block b (global ordinal) of the packed index
+ * stream lands at packed + (b - b0) * block_stride, b0 = elem0 / epb,
+ * block_stride >= ceil(epb*bits/8) and a multiple of 16.
+ * exact: n_local elements of capacity; prefix: local prefix per local block
+ * (entry for a block whose start precedes elem0 is left untouched);
+ * n_inc: device u64 total of local incompressible values. */
+size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t epb);
+int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
+               uint64_t n_total, int dtype, const double* centers, const double* cuts,
+               int k, int bits, double tol_bin, double tolerance, uint64_t epb,
+               uint8_t* packed, uint64_t block_stride, void* exact,
+               unsigned long long* prefix, unsigned long long* n_inc,
+               void* ws, size_t ws_bytes, void* stream);
+
+/* -- K5: fused unpack + sentinel scan + reconstruct, batched over segments
+ *        (codec.py:95-105,204-239; core.py:158-208)
+ * packed: blocks first_block .. at block_stride; prefix_rel[b - first_block]
+ * = incompressible count before block b minus that before first_block; exact
+ * points at the first exact value of first_block (n_exact available).
+ * Segment s decodes [seg_start[s], seg_start[s]+seg_count[s]) (global element
+ * indices) reading base[seg_out[s] + i] and writing out[seg_out[s] + i].
+ * seg_* are HOST arrays of nseg entries. */
+size_t nmk_decode_ws_bytes(const uint64_t* h_seg_start, const uint64_t* h_seg_count,
+                           int nseg, uint64_t epb);
+int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_block,
+               int bits, uint64_t epb, uint64_t n_total,
+               const unsigned long long* prefix_rel, const double* centers, int k,
+               const void* exact, uint64_t n_exact, const void* base, void* out, int dtype,
+               const uint64_t* h_seg_start, const uint64_t* h_seg_count,
+               const uint64_t* h_seg_out, int nseg,
+               nmk_segment_info* seg_info, nmk_decode_err* err,
+               void* ws, size_t ws_bytes, void* stream);
+
+/* -- standalone codec kernels (codec.py:83-105) ---------------------------- */
+int nmk_pack(const uint32_t* codes, uint64_t n, int bits, uint8_t* out, void* stream);
+int nmk_unpack(const uint8_t* packed, uint64_t n, int bits, uint32_t* codes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMK_B200_H */

@@ -1,0 +1,241 @@
+"""Block codec surface (mirror of nmk.codec, pkg/src/nmk/codec.py).
+
+* Block geometry (`BlockLayout`) is plain integer arithmetic, as in the
+  reference (codec.py:28-59).
+* Bit packing / unpacking and range decoding run on the GPU (K4/K5 and the
+  standalone nmk_pack / nmk_unpack kernels).
+* The lossless per-block DEFLATE stage (`compress_block` /
+  `decompress_block`) is OUTSIDE the accelerated path: it is the same raw
+  RFC 1951 stream at the same level, produced by the host's zlib exactly as
+  the reference does (codec.py:108-128), and is looked up through this
+  module's attributes so fault injection by monkeypatching still works.
+"""
+
+from __future__ import annotations
+
+import zlib
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+DEFAULT_BLOCK_BYTES = 1 << 20
+DEFAULT_DEFLATE_LEVEL = 6
+MIN_BLOCK_BYTES = 4096
+
+
+class CodecError(Exception):
+    """Packing or lossless-backend failure (codec.py:24-25)."""
+
+
+@dataclass(frozen=True)
+class BlockLayout:
+    """Partition of an n-element index stream into byte-capacity blocks."""
+
+    block_bytes: int
+    bits: int
+    n: int
+
+    def __post_init__(self) -> None:
+        if self.elements_per_block < 1:
+            raise ValueError("block capacity below one element")
+
+    @property
+    def elements_per_block(self) -> int:
+        return (self.block_bytes * 8) // self.bits
+
+    @property
+    def nblocks(self) -> int:
+        return -(-self.n // self.elements_per_block)
+
+    def block_range(self, ordinal: int) -> tuple[int, int]:
+        epb = self.elements_per_block
+        start = ordinal * epb
+        return start, min(start + epb, self.n)
+
+    def covering_blocks(self, start: int, count: int) -> range:
+        if count <= 0:
+            return range(0)
+        epb = self.elements_per_block
+        return range(start // epb, (start + count - 1) // epb + 1)
+
+
+def packed_size(element_count: int, bits: int) -> int:
+    return (element_count * bits + 7) // 8
+
+
+# ---------------------------------------------------------------------------
+# GPU bit packing (codec.py:83-105)
+# ---------------------------------------------------------------------------
+
+def pack_block(indices, bits: int) -> bytes:
+    """MSB-first B-bit packing, zero-padded to a byte, on the GPU."""
+    import torch
+    idx = np.asarray(indices)
+    if idx.size == 0:
+        return b""
+    if idx.min() < 0 or int(idx.max()) >= (1 << bits):
+        raise CodecError(f"index out of range for {bits}-bit packing")
+    N.require_cuda()
+    n = idx.size
+    codes = torch.from_numpy(idx.astype(np.uint32).view(np.int32)).cuda()
+    out = torch.empty(packed_size(n, bits), dtype=torch.uint8, device=codes.device)
+    N.check(N.lib().nmk_pack(codes.data_ptr(), n, bits, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    return out.cpu().numpy().tobytes()
+
+
+def unpack_block(data: bytes, bits: int, element_count: int) -> np.ndarray:
+    """Exact inverse of :func:`pack_block` on the GPU; pad bits ignored."""
+    import torch
+    expected = packed_size(element_count, bits)
+    if len(data) < expected:
+        raise CodecError(f"short buffer: {len(data)} bytes, need {expected}")
+    if element_count == 0:
+        return np.zeros(0, dtype=np.int32)
+    N.require_cuda()
+    raw = torch.from_numpy(np.frombuffer(data, dtype=np.uint8, count=expected).copy()).cuda()
+    codes = torch.empty(element_count, dtype=torch.int32, device=raw.device)
+    N.check(N.lib().nmk_unpack(raw.data_ptr(), element_count, bits, codes.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream))
+    return codes.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# Lossless stage (outside the accelerated path; host zlib, codec.py:108-128)
+# ---------------------------------------------------------------------------
+
+def compress_block(packed: bytes, level: int = DEFAULT_DEFLATE_LEVEL) -> bytes:
+    """Deflate one packed block as a raw RFC 1951 stream (no zlib wrapper)."""
+    if not 0 <= level <= 9:
+        raise CodecError(f"deflate level {level} outside 0..9")
+    try:
+        c = zlib.compressobj(level, zlib.DEFLATED, -zlib.MAX_WBITS)
+        return c.compress(packed) + c.flush()
+    except zlib.error as exc:  # pragma: no cover
+        raise CodecError(f"deflate failed: {exc}") from exc
+
+
+def decompress_block(data: bytes) -> bytes:
+    """Inflate one raw deflate stream produced by :func:`compress_block`."""
+    try:
+        d = zlib.decompressobj(-zlib.MAX_WBITS)
+        out = d.decompress(data) + d.flush()
+    except zlib.error as exc:
+        raise CodecError(f"inflate failed: {exc}") from exc
+    if not d.eof or d.unused_data:
+        raise CodecError("corrupt block: truncated or trailing bytes")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Range decode on the GPU (codec.py:181-258)
+# ---------------------------------------------------------------------------
+
+def _block_bytes_of(variable, ordinal: int) -> bytes:
+    offsets = variable.index_offsets
+    lo = int(offsets[ordinal])
+    hi = int(offsets[ordinal + 1]) if ordinal + 1 < len(offsets) else len(variable.index_table)
+    return variable.index_table[lo:hi]
+
+
+def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_offset, start, count, base):
+    """Decode [start, start+count) from the inflated packed ``blocks`` of the
+    covering block ordinals first..last on the GPU.
+
+    ``prefix`` = incompressible_prefix (global), ``exact`` = the exact values
+    from global index ``exact_offset`` on.  Returns
+    (out, need, have, bad_index, max_bad_index) with need/have the sentinel
+    count inside the range and the exact values available for it."""
+    import torch
+    from . import engine
+    N.require_cuda()
+    first = start // epb
+    nb = len(blocks)
+    stride = engine.block_stride(epb, bits)
+    host = np.zeros(nb * stride, dtype=np.uint8)
+    for i, blk in enumerate(blocks):
+        s, e = (first + i) * epb, min((first + i + 1) * epb, n)
+        need_b = packed_size(e - s, bits)
+        if len(blk) < need_b:
+            raise CodecError(f"short buffer: {len(blk)} bytes, need {need_b}")
+        host[i * stride: i * stride + need_b] = np.frombuffer(blk, dtype=np.uint8, count=need_b)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_packed = torch.from_numpy(host).to(dev)
+    pre = np.asarray(prefix, dtype=np.uint64)[first:first + nb].astype(np.int64)
+    base_inc = int(pre[0])
+    d_prefix_rel = torch.from_numpy(pre - base_inc).to(dev)
+    d_centers = torch.from_numpy(np.ascontiguousarray(centers64, dtype=np.float64)).to(dev)
+    ex = np.ascontiguousarray(exact[max(base_inc - exact_offset, 0):])
+    if base_inc < exact_offset:
+        raise ValueError("exact values start after the covering block")
+    d_exact = torch.from_numpy(ex).to(dev) if ex.size else torch.empty(0, dtype=_tdt(base.dtype), device=dev)
+    d_base = torch.from_numpy(np.ascontiguousarray(base)).to(dev)
+    res = engine.decode(d_packed, stride, first, bits, epb, n, d_prefix_rel, d_centers, d_exact, d_base,
+                        [(start, count, 0)])
+    need = int(res.n_sentinel[0])
+    avail = ex.shape[0] - int(res.inc_before[0])
+    have = max(0, min(need, avail))
+    return res.out.cpu().numpy(), need, have, res.bad_index, res.max_bad_index
+
+
+def _tdt(np_dtype):
+    import torch
+    return torch.float64 if np.dtype(np_dtype).itemsize == 8 else torch.float32
+
+
+def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> np.ndarray:
+    """Shared range decoder (codec.py:204-239): validation, inflate of the
+    covering blocks on the host, then one K5 launch."""
+    if start < 0 or count < 0 or start + count > variable.n:
+        raise ValueError(f"range [{start}, {start + count}) outside 0..{variable.n}")
+    base = np.asarray(base)
+    if base.shape[0] != count:
+        raise ValueError(f"base slice holds {base.shape[0]} elements, need {count}")
+    if count == 0:
+        return np.zeros(0, dtype=variable.numpy_dtype)
+    epb = variable.elements_per_block
+    first = start // epb
+    last = (start + count - 1) // epb
+    blocks = [decompress_block(block_bytes(b)) for b in range(first, last + 1)]
+    for i, b in enumerate(range(first, last + 1)):
+        s, e = b * epb, min((b + 1) * epb, variable.n)
+        if len(blocks[i]) < packed_size(e - s, variable.bits):
+            raise CodecError(f"short buffer: {len(blocks[i])} bytes, need {packed_size(e - s, variable.bits)}")
+    inc_lo = int(variable.incompressible_prefix[first])
+    exact, exact_offset = inc_slice_all(inc_lo)
+    exact = np.asarray(exact)
+    if exact.dtype != base.dtype:
+        exact = exact.astype(base.dtype)   # core.py:207 (astype to the base dtype)
+    centers = variable.centers.astype(np.float64, copy=False)
+    out, need, have, bad, maxbad = _gpu_decode_blocks(
+        blocks, variable.bits, epb, variable.n, variable.incompressible_prefix, centers, exact,
+        exact_offset, start, count, base)
+    if bad:
+        raise ValueError(f"index {maxbad} out of range for {len(centers)} centers")
+    if have < need:
+        raise ValueError(f"incompressible values exhausted: need {need}, have {have}")
+    return out
+
+
+def partial_decode(variable, start: int, count: int, base_reconstructed) -> np.ndarray:
+    """Reconstruct ``[start, start + count)`` touching only the covering
+    blocks (codec.py:242-258); bit-identical to a full-decode slice."""
+    return _decode_range(variable, start, count, base_reconstructed,
+                         lambda b: _block_bytes_of(variable, b),
+                         lambda lo: (variable.incompressible_table[lo:], lo))
+
+
+def decode_block_indices(variable, ordinal: int) -> np.ndarray:
+    start = ordinal * variable.elements_per_block
+    stop = min(start + variable.elements_per_block, variable.n)
+    packed = decompress_block(_block_bytes_of(variable, ordinal))
+    return unpack_block(packed, variable.bits, stop - start)
+
+
+def decode_all_indices(variable) -> np.ndarray:
+    """Full index stream (sentinels included), unpacked on the GPU."""
+    parts = [decode_block_indices(variable, b) for b in range(variable.nblocks)]
+    if not parts:
+        return np.zeros(0, dtype=np.int64)
+    return np.concatenate(parts)

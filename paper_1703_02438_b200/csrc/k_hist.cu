@@ -1,0 +1,425 @@
+// k_hist.cu — K2: histogram of bin ordinals floor((r - gmin) / 2E) over the
+// valid change ratios (binning.py:110-116, merged per pipeline.py:214-224).
+//
+// Three forms, chosen by the host from the dense span nbins = q(gmax) + 1:
+//  * smem   (nbins <= kSmemBins): per-warp-replica u32 counters in shared
+//           memory, per-thread run-length coalescing of equal consecutive
+//           ordinals (skewed fields put >90 % of elements in one bin), one
+//           u64 global atomic per nonzero bin per CTA at the end;
+//  * global (nbins <= kGlobalBins): run-length coalesced u64 atomics into an
+//           L2-resident dense array;
+//  * sparse (wider spans, e.g. 5e8 bins with 2e3 nonempty in the reference's
+//           planted-outlier test): emit the canonical bit pattern of the
+//           non-negative double ordinal (invalid -> UINT64_MAX), radix sort,
+//           run-length encode.  Output = np.unique(ords, return_counts=True).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "nmk_common.cuh"
+
+namespace nmk {
+
+constexpr uint64_t kSmemBins = 48 * 1024;       // 192 KB of u32 counters max
+constexpr uint64_t kGlobalBins = 1ULL << 22;    // 32 MB of u64 counters max
+
+template <typename T> struct HVec;
+template <> struct HVec<double> { using V = double2; static constexpr int N = 2; };
+template <> struct HVec<float>  { using V = float4;  static constexpr int N = 4; };
+__device__ __forceinline__ void hv_get(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
+__device__ __forceinline__ void hv_get(const float4& v, double* o) {
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+
+// Visit every element's (ratio, valid) with 16-byte loads when aligned.
+template <typename T, int UNROLL, typename F>
+__device__ __forceinline__ void for_each_ratio(const T* __restrict__ base, const T* __restrict__ cur,
+                                               uint64_t n, bool vec_ok, F&& f) {
+  using V = typename HVec<T>::V;
+  constexpr int VN = HVec<T>::N;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t done = 0;
+  if (vec_ok) {
+    const uint64_t nvec = n / VN;
+    const V* bv = reinterpret_cast<const V*>(base);
+    const V* cv = reinterpret_cast<const V*>(cur);
+    uint64_t i = tid;
+    for (; i + (UNROLL - 1) * nthr < nvec; i += UNROLL * nthr) {
+      V b[UNROLL], c[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        b[u] = __ldg(bv + i + u * nthr);
+        c[u] = __ldg(cv + i + u * nthr);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        double bb[VN], cc[VN];
+        hv_get(b[u], bb);
+        hv_get(c[u], cc);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          bool v;
+          double r = change_ratio(bb[e], cc[e], v);
+          f(r, v, (i + u * nthr) * VN + e);
+        }
+      }
+    }
+    for (; i < nvec; i += nthr) {
+      double bb[VN], cc[VN];
+      hv_get(__ldg(bv + i), bb);
+      hv_get(__ldg(cv + i), cc);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        bool v;
+        double r = change_ratio(bb[e], cc[e], v);
+        f(r, v, i * VN + e);
+      }
+    }
+    done = nvec * VN;
+  }
+  for (uint64_t j = done + tid; j < n; j += nthr) {
+    bool v;
+    double r = change_ratio(to_f64(base[j]), to_f64(cur[j]), v);
+    f(r, v, j);
+  }
+}
+
+// counts[nbins] is an out-of-range tripwire (must stay 0).
+template <typename T>
+__global__ void __launch_bounds__(512)
+k_hist_smem(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
+            const nmk_stats* __restrict__ st, double width, uint32_t nbins, int reps,
+            unsigned long long* __restrict__ counts, bool vec_ok) {
+  extern __shared__ uint32_t h[];
+  for (uint32_t i = threadIdx.x; i < nbins * (uint32_t)reps; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const double gmin = st->gmin;
+  uint32_t* my = h + (uint32_t)((threadIdx.x >> 5) % reps) * nbins;
+  uint32_t last = 0xffffffffu, run = 0;
+  for_each_ratio<T, 4>(base, cur, n, vec_ok, [&](double r, bool v, uint64_t) {
+    if (!v) return;
+    double q = bin_ordinal(r, gmin, width);
+    uint32_t qi = (q < (double)nbins) ? (uint32_t)q : nbins;  // nbins = tripwire
+    if (qi == last) {
+      ++run;
+    } else {
+      if (run) {
+        if (last < nbins) atomicAdd(&my[last], run);
+        else atomicAdd(&counts[nbins], (unsigned long long)run);
+      }
+      last = qi;
+      run = 1;
+    }
+  });
+  if (run) {
+    if (last < nbins) atomicAdd(&my[last], run);
+    else atomicAdd(&counts[nbins], (unsigned long long)run);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) {
+    uint32_t s = 0;
+    for (int r = 0; r < reps; ++r) s += h[r * nbins + i];
+    if (s) atomicAdd(&counts[i], (unsigned long long)s);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_hist_global(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
+              const nmk_stats* __restrict__ st, double width, uint64_t nbins,
+              unsigned long long* __restrict__ counts, bool vec_ok) {
+  const double gmin = st->gmin;
+  uint64_t last = ~0ULL;
+  unsigned long long run = 0;
+  for_each_ratio<T, 2>(base, cur, n, vec_ok, [&](double r, bool v, uint64_t) {
+    if (!v) return;
+    double q = bin_ordinal(r, gmin, width);
+    uint64_t qi = (q < (double)nbins) ? (uint64_t)q : nbins;
+    if (qi == last) {
+      ++run;
+    } else {
+      if (run) atomicAdd(&counts[last], run);
+      last = qi;
+      run = 1;
+    }
+  });
+  if (run) atomicAdd(&counts[last], run);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_hist_keys(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
+            const nmk_stats* __restrict__ st, double width,
+            unsigned long long* __restrict__ keys, bool vec_ok) {
+  const double gmin = st->gmin;
+  for_each_ratio<T, 2>(base, cur, n, vec_ok, [&](double r, bool v, uint64_t j) {
+    keys[j] = v ? (unsigned long long)__double_as_longlong(bin_ordinal(r, gmin, width)) : ~0ULL;
+  });
+}
+
+// ---- run-length / reduce-by-key over sorted keys ---------------------------
+constexpr int kRleThreads = 256;
+constexpr int kRleItems = 16;
+constexpr int kRleChunk = kRleThreads * kRleItems;
+
+__global__ void __launch_bounds__(kRleThreads)
+k_rle_count(const unsigned long long* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ chunk_heads) {
+  uint64_t c0 = (uint64_t)blockIdx.x * kRleChunk;
+  unsigned cnt = 0;
+  for (int it = 0; it < kRleItems; ++it) {
+    uint64_t i = c0 + (uint64_t)it * kRleThreads + threadIdx.x;
+    if (i < n && keys[i] != ~0ULL && (i == 0 || keys[i] != keys[i - 1])) ++cnt;
+  }
+  typedef cub::BlockReduce<unsigned, kRleThreads> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned tot = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0) chunk_heads[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kRleThreads)
+k_rle_scatter(const unsigned long long* __restrict__ keys, uint64_t n,
+              const unsigned long long* __restrict__ chunk_off,
+              unsigned long long* __restrict__ run_key, unsigned long long* __restrict__ run_start,
+              unsigned long long* __restrict__ nruns, unsigned long long nchunks) {
+  typedef cub::BlockScan<unsigned, kRleThreads> BS;
+  __shared__ typename BS::TempStorage tmp;
+  uint64_t c0 = (uint64_t)blockIdx.x * kRleChunk;
+  // thread-contiguous items so ranks follow element order
+  uint64_t i0 = c0 + (uint64_t)threadIdx.x * kRleItems;
+  unsigned flags = 0, cnt = 0;
+  for (int it = 0; it < kRleItems; ++it) {
+    uint64_t i = i0 + it;
+    bool hd = i < n && keys[i] != ~0ULL && (i == 0 || keys[i] != keys[i - 1]);
+    flags |= (hd ? 1u : 0u) << it;
+    cnt += hd;
+  }
+  unsigned ex;
+  BS(tmp).ExclusiveSum(cnt, ex);
+  unsigned long long pos = chunk_off[blockIdx.x] + ex;
+  for (int it = 0; it < kRleItems; ++it) {
+    if (flags >> it & 1u) {
+      run_key[pos] = keys[i0 + it];
+      run_start[pos] = i0 + it;
+      ++pos;
+    }
+  }
+  if (blockIdx.x == nchunks - 1 && threadIdx.x == kRleThreads - 1) *nruns = pos;
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+// first index whose key is UINT64_MAX (keys sorted ascending), else n
+__global__ void k_valid_end(const unsigned long long* __restrict__ keys, uint64_t n,
+                            unsigned long long* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    bool here = keys[i] == ~0ULL && (i == 0 || keys[i - 1] != ~0ULL);
+    if (here) *out = i;
+  }
+}
+
+static int sm_count_h() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Workspace layout shared by the sparse histogram and the merge.
+struct RleWs {
+  unsigned long long* keys_a;     // n
+  unsigned long long* keys_b;     // n
+  unsigned long long* run_start;  // n
+  unsigned long long* chunk;      // nchunks
+  unsigned long long* chunk_off;  // nchunks
+  unsigned long long* scal;       // 4 scalars
+  unsigned long long* vals_b;     // n (merge only)
+  unsigned long long* incl;       // n (merge only)
+  void* cub_tmp;
+  size_t cub_bytes;
+  size_t total;
+};
+
+static RleWs rle_layout(uint64_t n, bool with_vals, void* base) {
+  RleWs w{};
+  uint64_t nchunks = (n + kRleChunk - 1) / kRleChunk;
+  size_t sort_bytes = 0, scan_bytes = 0, scan2 = 0;
+  if (with_vals)
+    cub::DeviceRadixSort::SortPairs((void*)nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, (const unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, n);
+  else
+    cub::DeviceRadixSort::SortKeys((void*)nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                   (unsigned long long*)nullptr, n);
+  cub::DeviceScan::ExclusiveSum((void*)nullptr, scan_bytes, (unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, nchunks ? nchunks : 1);
+  if (with_vals)
+    cub::DeviceScan::InclusiveSum((void*)nullptr, scan2, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, n);
+  size_t cub_bytes = sort_bytes;
+  if (scan_bytes > cub_bytes) cub_bytes = scan_bytes;
+  if (scan2 > cub_bytes) cub_bytes = scan2;
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* q = p ? p + off : nullptr; off += align256(bytes); return q; };
+  w.keys_a = (unsigned long long*)take(n * 8);
+  w.keys_b = (unsigned long long*)take(n * 8);
+  w.run_start = (unsigned long long*)take(n * 8);
+  w.chunk = (unsigned long long*)take((nchunks + 1) * 8);
+  w.chunk_off = (unsigned long long*)take((nchunks + 1) * 8);
+  w.scal = (unsigned long long*)take(4 * 8);
+  if (with_vals) {
+    w.vals_b = (unsigned long long*)take(n * 8);
+    w.incl = (unsigned long long*)take(n * 8);
+  }
+  w.cub_tmp = take(cub_bytes);
+  w.cub_bytes = cub_bytes;
+  w.total = off;
+  return w;
+}
+
+// Shared tail: sorted keys in w.keys_b (and values in w.vals_b for merge)
+// -> run keys + counts written to out_keys/out_counts, *nruns.
+static int rle_tail(RleWs& w, uint64_t n, bool with_vals, unsigned long long* out_keys,
+                    unsigned long long* out_counts, unsigned long long* nruns, cudaStream_t s) {
+  uint64_t nchunks = (n + kRleChunk - 1) / kRleChunk;
+  k_rle_count<<<(unsigned)nchunks, kRleThreads, 0, s>>>(w.keys_b, n, w.chunk);
+  size_t tb = w.cub_bytes;
+  cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.chunk, w.chunk_off, nchunks, s);
+  k_rle_scatter<<<(unsigned)nchunks, kRleThreads, 0, s>>>(w.keys_b, n, w.chunk_off, out_keys,
+                                                         w.run_start, nruns, nchunks);
+  k_set_u64<<<1, 1, 0, s>>>(w.scal, n);  // default end = n (no invalid key)
+  unsigned grid = (unsigned)((n + 255) / 256);
+  if (grid > (unsigned)sm_count_h() * 8) grid = sm_count_h() * 8;
+  k_valid_end<<<grid, 256, 0, s>>>(w.keys_b, n, w.scal);
+  if (with_vals) {
+    tb = w.cub_bytes;
+    cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, w.vals_b, w.incl, n, s);
+  }
+  return 0;
+}
+
+__global__ void k_rle_lengths_dev(const unsigned long long* __restrict__ run_start,
+                                  const unsigned long long* __restrict__ nruns_p,
+                                  const unsigned long long* __restrict__ valid_end_p,
+                                  const unsigned long long* __restrict__ incl,
+                                  unsigned long long* __restrict__ out_counts) {
+  uint64_t nr = *nruns_p;
+  uint64_t vend = *valid_end_p;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nr;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t s = run_start[p];
+    uint64_t e = (p + 1 < nr) ? run_start[p + 1] : vend;
+    out_counts[p] = incl ? (incl[e - 1] - (s ? incl[s - 1] : 0ULL)) : (e - s);
+  }
+}
+
+}  // namespace nmk
+
+using namespace nmk;
+
+extern "C" int nmk_hist_dense(const void* base, const void* cur, uint64_t n, int dtype,
+                              const nmk_stats* stats, double width, uint64_t nbins,
+                              unsigned long long* counts, void* stream) {
+  if (!base || !cur || !stats || !counts || n == 0 || nbins == 0)
+    return set_error(NMK_ERR_ARG, "nmk_hist_dense: bad argument");
+  if (nbins > kGlobalBins) return set_error(NMK_ERR_ARG, "nmk_hist_dense: nbins %llu too large", (unsigned long long)nbins);
+  if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_hist_dense: bad dtype");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(counts, 0, (nbins + 1) * sizeof(unsigned long long), s);
+  bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  int sms = sm_count_h();
+  if (nbins <= kSmemBins) {
+    // replicas: one private copy per warp when it fits in ~48 KB, at least 1
+    size_t one = nbins * 4;
+    int reps = (int)((48 * 1024) / one);
+    if (reps > 16) reps = 16;
+    if (reps < 1) reps = 1;
+    size_t smem = one * reps;
+    int per_sm = (int)((220 * 1024) / (smem + 1024));
+    if (per_sm > 4) per_sm = 4;
+    if (per_sm < 1) per_sm = 1;
+    uint64_t want = (n + 8191) / 8192;
+    uint64_t grid = (uint64_t)sms * per_sm;
+    if (want < grid) grid = want ? want : 1;
+    if (dtype == NMK_F64) {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(k_hist_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_hist_smem<double><<<(unsigned)grid, 512, smem, s>>>((const double*)base, (const double*)cur, n, stats,
+                                                             width, (uint32_t)nbins, reps, counts, aligned);
+    } else {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(k_hist_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_hist_smem<float><<<(unsigned)grid, 512, smem, s>>>((const float*)base, (const float*)cur, n, stats,
+                                                           width, (uint32_t)nbins, reps, counts, aligned);
+    }
+    return check_launch("k_hist_smem");
+  }
+  uint64_t want = (n + 4095) / 4096;
+  uint64_t grid = (uint64_t)sms * 8;
+  if (want < grid) grid = want ? want : 1;
+  if (dtype == NMK_F64)
+    k_hist_global<double><<<(unsigned)grid, 256, 0, s>>>((const double*)base, (const double*)cur, n, stats,
+                                                         width, nbins, counts, aligned);
+  else
+    k_hist_global<float><<<(unsigned)grid, 256, 0, s>>>((const float*)base, (const float*)cur, n, stats,
+                                                        width, nbins, counts, aligned);
+  return check_launch("k_hist_global");
+}
+
+extern "C" size_t nmk_hist_sparse_ws_bytes(uint64_t n) { return rle_layout(n, false, nullptr).total; }
+extern "C" size_t nmk_hist_merge_ws_bytes(uint64_t n_in) { return rle_layout(n_in, true, nullptr).total; }
+
+extern "C" int nmk_hist_sparse(const void* base, const void* cur, uint64_t n, int dtype,
+                               const nmk_stats* stats, double width, unsigned long long* keys,
+                               unsigned long long* counts, unsigned long long* nruns, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (!base || !cur || !stats || !keys || !counts || !nruns || !ws || n == 0)
+    return set_error(NMK_ERR_ARG, "nmk_hist_sparse: bad argument");
+  if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_hist_sparse: bad dtype");
+  RleWs w = rle_layout(n, false, ws);
+  if (ws_bytes < w.total) return set_error(NMK_ERR_ARG, "nmk_hist_sparse: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  uint64_t want = (n + 4095) / 4096;
+  uint64_t grid = (uint64_t)sm_count_h() * 8;
+  if (want < grid) grid = want ? want : 1;
+  if (dtype == NMK_F64)
+    k_hist_keys<double><<<(unsigned)grid, 256, 0, s>>>((const double*)base, (const double*)cur, n, stats, width,
+                                                       w.keys_a, aligned);
+  else
+    k_hist_keys<float><<<(unsigned)grid, 256, 0, s>>>((const float*)base, (const float*)cur, n, stats, width,
+                                                      w.keys_a, aligned);
+  size_t tb = w.cub_bytes;
+  cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keys_a, w.keys_b, n, 0, 64, s);
+  rle_tail(w, n, false, keys, counts, nruns, s);
+  unsigned g2 = (unsigned)((n + 255) / 256);
+  if (g2 > (unsigned)sm_count_h() * 8) g2 = sm_count_h() * 8;
+  k_rle_lengths_dev<<<g2, 256, 0, s>>>(w.run_start, nruns, w.scal, nullptr, counts);
+  return check_launch("nmk_hist_sparse");
+}
+
+extern "C" int nmk_hist_merge(unsigned long long* keys, unsigned long long* counts, uint64_t n_in,
+                              unsigned long long* nruns, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_in == 0) {
+    cudaMemsetAsync(nruns, 0, 8, s);
+    return check_launch("nmk_hist_merge");
+  }
+  if (!keys || !counts || !nruns || !ws) return set_error(NMK_ERR_ARG, "nmk_hist_merge: bad argument");
+  RleWs w = rle_layout(n_in, true, ws);
+  if (ws_bytes < w.total) return set_error(NMK_ERR_ARG, "nmk_hist_merge: workspace too small");
+  size_t tb = w.cub_bytes;
+  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, keys, w.keys_b, counts, w.vals_b, n_in, 0, 64, s);
+  rle_tail(w, n_in, true, keys, counts, nruns, s);
+  unsigned g2 = (unsigned)((n_in + 255) / 256);
+  if (g2 > (unsigned)sm_count_h() * 8) g2 = sm_count_h() * 8;
+  k_rle_lengths_dev<<<g2, 256, 0, s>>>(w.run_start, nruns, w.scal, w.incl, counts);
+  return check_launch("nmk_hist_merge");
+}

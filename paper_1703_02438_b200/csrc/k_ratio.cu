@@ -1,0 +1,236 @@
+// k_ratio.cu — K1: fused change ratio + min/max + valid count.
+//
+// Restates phase 1 of compress_pair (pkg/src/nmk/pipeline.py:190-212) with
+// core.ratio_arrays (core.py:115-137) computed on the fly: the ratio field is
+// never materialised, each pass recomputes it from the two snapshots.
+// Streaming kernel: 16-byte vector loads of both snapshots, 4 vectors in
+// flight per thread, warp-shuffle + smem CTA reduction, last-CTA grid
+// reduction (no second launch).
+#include <cfloat>
+
+#include "nmk_common.cuh"
+
+namespace nmk {
+
+constexpr int kMinmaxThreads = 256;
+constexpr int kMinmaxUnroll = 4;
+
+struct MinMax {
+  double lo, hi;
+  unsigned long long nv;
+};
+
+__device__ __forceinline__ void mm_add(MinMax& a, double r, bool v) {
+  if (v) {
+    a.lo = fmin(a.lo, r);
+    a.hi = fmax(a.hi, r);
+    a.nv += 1;
+  }
+}
+
+__device__ __forceinline__ MinMax mm_merge(MinMax a, const MinMax& b) {
+  a.lo = fmin(a.lo, b.lo);
+  a.hi = fmax(a.hi, b.hi);
+  a.nv += b.nv;
+  return a;
+}
+
+template <typename T> struct Vec;
+template <> struct Vec<double> { using V = double2; static constexpr int N = 2; };
+template <> struct Vec<float>  { using V = float4;  static constexpr int N = 4; };
+
+__device__ __forceinline__ void vec_get(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
+__device__ __forceinline__ void vec_get(const float4& v, double* o) {
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kMinmaxThreads)
+k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
+         MinMax* __restrict__ partials, unsigned int* __restrict__ ticket,
+         nmk_stats* __restrict__ out, bool vec_ok) {
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
+  MinMax acc;
+  acc.nv = 0;
+  acc.lo = __longlong_as_double(0x7ff0000000000000LL);   // +inf
+  acc.hi = __longlong_as_double(0xfff0000000000000LL);   // -inf
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t done = 0;
+  if (vec_ok) {
+    const uint64_t nvec = n / VN;
+    const V* bv = reinterpret_cast<const V*>(base);
+    const V* cv = reinterpret_cast<const V*>(cur);
+    uint64_t i = tid;
+    for (; i + (kMinmaxUnroll - 1) * nthr < nvec; i += kMinmaxUnroll * nthr) {
+      V b[kMinmaxUnroll], c[kMinmaxUnroll];
+#pragma unroll
+      for (int u = 0; u < kMinmaxUnroll; ++u) {
+        b[u] = __ldg(bv + i + u * nthr);
+        c[u] = __ldg(cv + i + u * nthr);
+      }
+#pragma unroll
+      for (int u = 0; u < kMinmaxUnroll; ++u) {
+        double bb[VN], cc[VN];
+        vec_get(b[u], bb);
+        vec_get(c[u], cc);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          bool v;
+          double r = change_ratio(bb[e], cc[e], v);
+          mm_add(acc, r, v);
+        }
+      }
+    }
+    for (; i < nvec; i += nthr) {
+      double bb[VN], cc[VN];
+      vec_get(__ldg(bv + i), bb);
+      vec_get(__ldg(cv + i), cc);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        bool v;
+        double r = change_ratio(bb[e], cc[e], v);
+        mm_add(acc, r, v);
+      }
+    }
+    done = nvec * VN;
+  }
+  for (uint64_t j = done + tid; j < n; j += nthr) {
+    bool v;
+    double r = change_ratio(to_f64(base[j]), to_f64(cur[j]), v);
+    mm_add(acc, r, v);
+  }
+  // warp reduce
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MinMax other;
+    other.lo = __shfl_xor_sync(0xffffffffu, acc.lo, o);
+    other.hi = __shfl_xor_sync(0xffffffffu, acc.hi, o);
+    other.nv = __shfl_xor_sync(0xffffffffu, acc.nv, o);
+    acc = mm_merge(acc, other);
+  }
+  __shared__ MinMax warp_mm[kMinmaxThreads / 32];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) warp_mm[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    MinMax m = warp_mm[0];
+    for (int w = 1; w < kMinmaxThreads / 32; ++w) m = mm_merge(m, warp_mm[w]);
+    partials[blockIdx.x] = m;
+    __threadfence();
+    unsigned prev = atomicAdd(ticket, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  // last CTA: reduce all partials (memory ordering via the fence above)
+  __threadfence();
+  MinMax m;
+  m.lo = __longlong_as_double(0x7ff0000000000000LL);
+  m.hi = __longlong_as_double(0xfff0000000000000LL);
+  m.nv = 0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+    MinMax p;
+    p.lo = __ldcg(&partials[i].lo);
+    p.hi = __ldcg(&partials[i].hi);
+    p.nv = __ldcg(&partials[i].nv);
+    m = mm_merge(m, p);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MinMax other;
+    other.lo = __shfl_xor_sync(0xffffffffu, m.lo, o);
+    other.hi = __shfl_xor_sync(0xffffffffu, m.hi, o);
+    other.nv = __shfl_xor_sync(0xffffffffu, m.nv, o);
+    m = mm_merge(m, other);
+  }
+  __syncthreads();
+  if (lane == 0) warp_mm[wid] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    MinMax f = warp_mm[0];
+    for (int w = 1; w < kMinmaxThreads / 32; ++w) f = mm_merge(f, warp_mm[w]);
+    out->gmin = f.lo;
+    out->gmax = f.hi;
+    out->nvalid = f.nv;
+    out->reserved = 0;
+    *ticket = 0;  // self-reset for the next launch
+  }
+}
+
+template <typename T>
+__global__ void k_ratio(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
+                        double* __restrict__ ratios, uint8_t* __restrict__ valid) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    bool v;
+    double r = change_ratio(to_f64(base[j]), to_f64(cur[j]), v);
+    ratios[j] = r;
+    valid[j] = v ? 1 : 0;
+  }
+}
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+static unsigned minmax_grid(uint64_t n) {
+  uint64_t want = (n + 4095) / 4096;  // >= 4096 elements per CTA
+  uint64_t cap = (uint64_t)sm_count() * 8;
+  if (want < 1) want = 1;
+  return (unsigned)(want < cap ? want : cap);
+}
+
+}  // namespace nmk
+
+using namespace nmk;
+
+extern "C" size_t nmk_minmax_ws_bytes(uint64_t n) {
+  return 256 + (size_t)minmax_grid(n) * sizeof(MinMax);
+}
+
+extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
+                          nmk_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  if (n == 0 || !base || !cur || !stats || !ws) return set_error(NMK_ERR_ARG, "nmk_minmax: bad argument");
+  if (ws_bytes < nmk_minmax_ws_bytes(n)) return set_error(NMK_ERR_ARG, "nmk_minmax: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned grid = minmax_grid(n);
+  unsigned* ticket = (unsigned*)ws;
+  MinMax* partials = (MinMax*)((char*)ws + 256);
+  // The ticket word must be zero on entry: callers zero a fresh workspace
+  // once and the kernel's last CTA resets it after every launch.
+  bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  if (dtype == NMK_F64)
+    k_minmax<double><<<grid, kMinmaxThreads, 0, s>>>((const double*)base, (const double*)cur, n,
+                                                     partials, ticket, stats, aligned);
+  else if (dtype == NMK_F32)
+    k_minmax<float><<<grid, kMinmaxThreads, 0, s>>>((const float*)base, (const float*)cur, n,
+                                                    partials, ticket, stats, aligned);
+  else
+    return set_error(NMK_ERR_ARG, "nmk_minmax: bad dtype %d", dtype);
+  return check_launch("k_minmax");
+}
+
+extern "C" int nmk_ratio(const void* base, const void* cur, uint64_t n, int dtype,
+                         double* ratios, uint8_t* valid, void* stream) {
+  if (n == 0) return NMK_OK;
+  if (!base || !cur || !ratios || !valid) return set_error(NMK_ERR_ARG, "nmk_ratio: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned grid = minmax_grid(n);
+  if (dtype == NMK_F64)
+    k_ratio<double><<<grid, 256, 0, s>>>((const double*)base, (const double*)cur, n, ratios, valid);
+  else if (dtype == NMK_F32)
+    k_ratio<float><<<grid, 256, 0, s>>>((const float*)base, (const float*)cur, n, ratios, valid);
+  else
+    return set_error(NMK_ERR_ARG, "nmk_ratio: bad dtype %d", dtype);
+  return check_launch("k_ratio");
+}

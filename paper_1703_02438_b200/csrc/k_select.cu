@@ -1,0 +1,280 @@
+// k_select.cu — K3: single-CTA bin selection.
+//
+// Restates, in one 1024-thread CTA and without leaving the device:
+//  * _selectable           (binning.py:135-139): bins with a finite center;
+//  * select_index_length   (binning.py:155-206): auto B over [2, 16] with the
+//    Eq. 6 size model, ties to the smaller B;
+//  * top_k_bins            (binning.py:142-152): the k = min(2^B-1, m) bins
+//    ordered by (count desc, ordinal asc), centers sorted and deduplicated;
+//  * _quantize_centers     (pipeline.py:112-124): round to the storage dtype,
+//    deduplicate, drop non-finite, fall back to [0.0];
+//  * _degenerate_model     (pipeline.py:163-167) when no ratio is valid;
+//  * the midpoint cuts used by nearest_center (binning.py:299).
+//
+// The k-th largest count is found with an MSB-first radix select (8-bit
+// digits) over the bin counts instead of a full lexsort: the selected set is
+// {count > t} plus the lowest-ordinal bins with count == t, which is exactly
+// the first k rows of lexsort((ordinal, -count)).  Bins arrive in ordinal
+// order and centers are monotone in the ordinal, so compacting the selected
+// bins in ordinal order yields np.unique's sorted order directly.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "nmk_common.cuh"
+
+namespace nmk {
+
+constexpr int kSelThreads = 1024;
+constexpr int kAutoLo = 2, kAutoHi = 16;           // binning.py:22
+constexpr int kNSel = kAutoHi - kAutoLo + 1;       // 15 simultaneous selects
+
+struct BinView {
+  const unsigned long long* keys;    // null -> dense (ordinal = index)
+  const unsigned long long* counts;
+  uint64_t m;
+  double origin, width;
+  __device__ __forceinline__ double ord(uint64_t i) const {
+    return keys ? __longlong_as_double((long long)keys[i]) : (double)i;
+  }
+  __device__ __forceinline__ double center(uint64_t i) const { return bin_center(ord(i), origin, width); }
+  // count if the bin is nonempty and selectable, else 0
+  __device__ __forceinline__ unsigned long long sel_count(uint64_t i) const {
+    unsigned long long c = counts[i];
+    if (c == 0) return 0;
+    return finite64(center(i)) ? c : 0ULL;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ double quantize(double c) { return to_f64(narrow<T>(c)); }
+
+template <typename T>
+__global__ void __launch_bounds__(kSelThreads)
+k_select(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ counts,
+         uint64_t m_max, const unsigned long long* __restrict__ nruns,
+         const nmk_stats* __restrict__ st, double width, double tolerance, int bits_cfg,
+         uint64_t n_total, double* __restrict__ centers, double* __restrict__ cuts,
+         T* __restrict__ centers_t, uint64_t cap_k, nmk_model* __restrict__ model) {
+  typedef cub::BlockReduce<unsigned long long, kSelThreads> BRed;
+  typedef cub::BlockScan<unsigned, kSelThreads> BScan;
+  __shared__ union {
+    typename BRed::TempStorage red;
+    typename BScan::TempStorage scan;
+  } tmp;
+  __shared__ unsigned hist[kNSel][256];
+  __shared__ unsigned long long s_prefix[kNSel], s_mask[kNSel], s_left[kNSel], s_kk[kNSel];
+  __shared__ unsigned long long s_cov[kNSel];
+  __shared__ unsigned long long s_bcast[4];
+  __shared__ int s_bits;
+  __shared__ double s_prev;
+
+  const int tid = threadIdx.x;
+  const uint64_t nvalid = st->nvalid;
+  if (nvalid == 0) {  // degenerate model (pipeline.py:163-167)
+    if (tid == 0) {
+      model->bits = bits_cfg >= 0 ? bits_cfg : 2;
+      model->k = 1;
+      model->status = 0;
+      model->m_selectable = 0;
+      model->tol_bin = tolerance;
+      for (int b = 0; b < 17; ++b) model->coverage[b] = 0;
+      centers[0] = 0.0;
+      centers_t[0] = narrow<T>(0.0);
+    }
+    return;
+  }
+  BinView bv{keys, counts, nruns ? (uint64_t)*nruns : m_max, st->gmin, width};
+  const uint64_t M = bv.m;
+
+  // ---- pass A: m (selectable bins), max count, total selectable count ----
+  unsigned long long my_m = 0, my_max = 0, my_tot = 0;
+  for (uint64_t i = tid; i < M; i += kSelThreads) {
+    unsigned long long c = bv.sel_count(i);
+    if (c) { ++my_m; my_tot += c; if (c > my_max) my_max = c; }
+  }
+  unsigned long long m = BRed(tmp.red).Sum(my_m);
+  __syncthreads();
+  unsigned long long maxc = BRed(tmp.red).Reduce(my_max, cub::Max());
+  __syncthreads();
+  unsigned long long tot = BRed(tmp.red).Sum(my_tot);
+  if (tid == 0) { s_bcast[0] = m; s_bcast[1] = maxc; s_bcast[2] = tot; }
+  __syncthreads();
+  m = s_bcast[0]; maxc = s_bcast[1]; tot = s_bcast[2];
+  if (m == 0) {
+    if (tid == 0) { model->status = NMK_ERR_EMPTY_HIST; model->k = 0; model->m_selectable = 0; }
+    return;
+  }
+
+  // ---- multi radix select: one lane per requested k --------------------
+  // slot s requests kk[s]; slot inactive when kk >= m (everything selected)
+  const bool autob = bits_cfg < 0;
+  if (tid < kNSel) {
+    int b = autob ? kAutoLo + tid : bits_cfg;
+    unsigned long long kk = (b >= 63) ? ~0ULL : ((1ULL << b) - 1);
+    if (kk > m) kk = m;
+    s_kk[tid] = (autob || tid == 0) ? kk : m;  // fixed B uses slot 0 only
+    s_prefix[tid] = 0; s_mask[tid] = 0; s_left[tid] = s_kk[tid];
+  }
+  __syncthreads();
+  int top = 63 - __clzll(maxc | 1ULL);
+  for (int shift = (top / 8) * 8; shift >= 0; shift -= 8) {
+    for (int i = tid; i < kNSel * 256; i += kSelThreads) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    for (uint64_t i = tid; i < M; i += kSelThreads) {
+      unsigned long long c = bv.sel_count(i);
+      if (!c) continue;
+      unsigned d = (unsigned)(c >> shift) & 255u;
+#pragma unroll
+      for (int s = 0; s < kNSel; ++s)
+        if (s_kk[s] < m && (c & s_mask[s]) == s_prefix[s]) atomicAdd(&hist[s][d], 1u);
+    }
+    __syncthreads();
+    if (tid < kNSel && s_kk[tid] < m) {
+      unsigned long long cum = 0, left = s_left[tid];
+      int d = 255;
+      for (; d > 0; --d) {
+        if (cum + hist[tid][d] >= left) break;
+        cum += hist[tid][d];
+      }
+      s_left[tid] = left - cum;  // still needed among bins equal on this digit
+      s_prefix[tid] |= (unsigned long long)d << shift;
+      s_mask[tid] |= 255ULL << shift;
+    }
+    __syncthreads();
+  }
+  // now for active slot s: threshold t = s_prefix[s]; need s_left[s] bins with
+  // count == t (lowest ordinals) on top of every bin with count > t.
+
+  // ---- auto B: coverage per B, then the Eq. 6 argmin ---------------------
+  if (autob) {
+    unsigned long long acc[kNSel];
+#pragma unroll
+    for (int s = 0; s < kNSel; ++s) acc[s] = 0;
+    for (uint64_t i = tid; i < M; i += kSelThreads) {
+      unsigned long long c = bv.sel_count(i);
+      if (!c) continue;
+#pragma unroll
+      for (int s = 0; s < kNSel; ++s)
+        if (s_kk[s] < m && c > s_prefix[s]) acc[s] += c;
+    }
+#pragma unroll
+    for (int s = 0; s < kNSel; ++s) {
+      unsigned long long v = BRed(tmp.red).Sum(acc[s]);
+      if (tid == 0) s_cov[s] = (s_kk[s] < m) ? v + s_left[s] * s_prefix[s] : tot;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      // size(B) = 2^B*L + n*B/8 + (n - cov)*L, evaluated exactly as 8*size in
+      // integers (every term is an exact integer or a multiple of 1/8 far below
+      // 2^50, so the reference's float arithmetic is exact too).
+      const unsigned long long L = sizeof(T);
+      int best = kAutoLo;
+      unsigned long long best8 = 0;
+      for (int s = 0; s < kNSel; ++s) {
+        int b = kAutoLo + s;
+        unsigned long long s8 = 8ULL * (1ULL << b) * L + (unsigned long long)n_total * b +
+                                8ULL * (n_total - s_cov[s]) * L;
+        if (s == 0 || s8 < best8) { best8 = s8; best = b; }
+      }
+      s_bits = best;
+    }
+    __syncthreads();
+  } else if (tid == 0) {
+    s_bits = bits_cfg;
+  }
+  __syncthreads();
+  const int bits = s_bits;
+  const int slot = autob ? bits - kAutoLo : 0;
+  const unsigned long long K = s_kk[slot];
+  const bool take_all = (K >= m);
+  const unsigned long long t = s_prefix[slot];
+  const unsigned long long need_eq = s_left[slot];
+  if (K > cap_k) {
+    if (tid == 0) { model->status = NMK_ERR_ARG; model->k = (int)K; }
+    return;
+  }
+
+  // ---- compaction of selected bins in ordinal order -> raw centers (cuts buf)
+  unsigned long long run_eq = 0, run_pos = 0;
+  for (uint64_t c0 = 0; c0 < M; c0 += kSelThreads) {
+    uint64_t i = c0 + tid;
+    unsigned long long c = (i < M) ? bv.sel_count(i) : 0ULL;
+    unsigned eq = (!take_all && c && c == t) ? 1u : 0u;
+    unsigned eq_ex, eq_tot;
+    BScan(tmp.scan).ExclusiveSum(eq, eq_ex, eq_tot);
+    __syncthreads();
+    bool chosen = c && (take_all || c > t || (eq && run_eq + eq_ex < need_eq));
+    unsigned ch = chosen ? 1u : 0u, ch_ex, ch_tot;
+    BScan(tmp.scan).ExclusiveSum(ch, ch_ex, ch_tot);
+    __syncthreads();
+    if (chosen) cuts[run_pos + ch_ex] = bv.center(i);
+    run_eq += eq_tot;
+    run_pos += ch_tot;
+  }
+  __syncthreads();
+  const uint64_t kraw = run_pos;  // == K
+
+  // ---- quantise + dedupe + drop non-finite (np.unique semantics) -----------
+  unsigned long long kq = 0;
+  if (tid == 0) s_prev = 0.0;
+  __syncthreads();
+  for (uint64_t c0 = 0; c0 < kraw; c0 += kSelThreads) {
+    uint64_t i = c0 + tid;
+    double q = 0.0;
+    bool keep = false;
+    if (i < kraw) {
+      q = quantize<T>(cuts[i]);
+      double prevq = (i == 0) ? 0.0 : quantize<T>(cuts[i - 1]);
+      keep = finite64(q) && (i == 0 || !(q == prevq) || !finite64(prevq));
+    }
+    unsigned kp = keep ? 1u : 0u, ex, tot2;
+    BScan(tmp.scan).ExclusiveSum(kp, ex, tot2);
+    __syncthreads();
+    if (keep) centers[kq + ex] = q;
+    kq += tot2;
+  }
+  __syncthreads();
+  if (kq == 0) {
+    if (tid == 0) centers[0] = 0.0;
+    kq = 1;
+  }
+  __syncthreads();
+  for (uint64_t i = tid; i < kq; i += kSelThreads) {
+    centers_t[i] = narrow<T>(centers[i]);
+    if (i + 1 < kq) cuts[i] = __dmul_rn(0.5, __dadd_rn(centers[i], centers[i + 1]));
+  }
+  if (tid == 0) {
+    model->bits = bits;
+    model->k = (int)kq;
+    model->status = 0;
+    model->m_selectable = (int)(m > 0x7fffffffULL ? 0x7fffffff : m);
+    model->tol_bin = width / 2.0;
+    for (int b = 0; b < 17; ++b) model->coverage[b] = 0;
+    if (autob)
+      for (int s = 0; s < kNSel; ++s) model->coverage[kAutoLo + s] = s_cov[s];
+  }
+}
+
+}  // namespace nmk
+
+using namespace nmk;
+
+extern "C" int nmk_select(const unsigned long long* keys, const unsigned long long* counts, uint64_t m_max,
+                          const unsigned long long* nruns, const nmk_stats* stats, double width,
+                          double tolerance, int bits, uint64_t n_total, int dtype, double* centers,
+                          double* cuts, void* centers_t, uint64_t cap_k, nmk_model* model, void* stream) {
+  if (!counts || !stats || !centers || !cuts || !centers_t || !model || cap_k < 1)
+    return set_error(NMK_ERR_ARG, "nmk_select: bad argument");
+  if (bits >= 0 && (bits < 2 || bits > 30)) return set_error(NMK_ERR_ARG, "nmk_select: bits %d outside [2, 30]", bits);
+  if (keys && !nruns) return set_error(NMK_ERR_ARG, "nmk_select: sparse form needs nruns");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == NMK_F64)
+    k_select<double><<<1, kSelThreads, 0, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
+                                               centers, cuts, (double*)centers_t, cap_k, model);
+  else if (dtype == NMK_F32)
+    k_select<float><<<1, kSelThreads, 0, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
+                                              centers, cuts, (float*)centers_t, cap_k, model);
+  else
+    return set_error(NMK_ERR_ARG, "nmk_select: bad dtype");
+  return check_launch("k_select");
+}

@@ -1,0 +1,259 @@
+"""Compression pipeline — the reference's drop-in API on the B200.
+
+Mirrors pkg/src/nmk/pipeline.py: same names, arguments, outputs and error
+behaviour (`PipelineConfig`, `PhaseTimings`, `PipelineError`,
+`compress_pair`, `decompress`, `compress_series`).  Phases 1-4a run as the
+four CUDA kernels of engine.encode; phase 4b (per-block DEFLATE) stays on the
+host as in the reference and is timed separately in `PhaseTimings.zlib`.
+Output bytes are identical to the reference's for every input and config.
+"""
+
+from __future__ import annotations
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import codec, container, engine
+from .core import TemporalPair, Tolerance
+
+DEFAULT_TOLERANCE = 1e-3
+STRATEGIES = ("top_k", "equal_width", "log_scale", "kmeans")   # binning.py:18
+MIN_BITS, MAX_BITS = 2, 30
+ACCELERATED_STRATEGIES = ("top_k",)
+
+
+class PipelineError(Exception):
+    """Failure inside a pipeline phase; ``phase`` names where."""
+
+    def __init__(self, phase: str, message: str):
+        super().__init__(f"phase {phase}: {message}")
+        self.phase = phase
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    """Knobs for one compression run (pipeline.py:36-58)."""
+
+    workers: int = 1
+    tolerance: float = DEFAULT_TOLERANCE
+    strategy: str = "top_k"
+    bits: int | None = None
+    block_bytes: int = codec.DEFAULT_BLOCK_BYTES
+    deflate_level: int = codec.DEFAULT_DEFLATE_LEVEL
+
+    def __post_init__(self) -> None:
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.block_bytes < codec.MIN_BLOCK_BYTES:
+            raise ValueError(f"block_bytes must be >= {codec.MIN_BLOCK_BYTES}")
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {self.strategy!r}")
+        if self.bits is not None and not MIN_BITS <= self.bits <= MAX_BITS:
+            raise ValueError(f"bits must be in [{MIN_BITS}, {MAX_BITS}]")
+        if not 0 <= self.deflate_level <= 9:
+            raise ValueError("deflate level must be in 0..9")
+        Tolerance(self.tolerance)
+
+
+@dataclass
+class PhaseTimings:
+    """Seconds per pipeline phase (pipeline.py:61-81).
+
+    GPU phases are CUDA-event times: change_ratio = H2D + K1, binning = K2+K3,
+    assign_index = K4 (which also performs index_alignment and bits_packing,
+    fused), bits_packing = D2H of the packed stream; zlib = host DEFLATE.
+    """
+
+    change_ratio: float = 0.0
+    binning: float = 0.0
+    assign_index: float = 0.0
+    index_alignment: float = 0.0
+    bits_packing: float = 0.0
+    zlib: float = 0.0
+    io: float = 0.0
+
+    PHASES = ("change_ratio", "binning", "assign_index", "index_alignment", "bits_packing", "zlib", "io")
+
+    def total(self) -> float:
+        return sum(getattr(self, p) for p in self.PHASES)
+
+    def records(self) -> list[str]:
+        return [f"timing.{p}={getattr(self, p):.6f}" for p in self.PHASES]
+
+
+# ---------------------------------------------------------------------------
+# host <-> device staging
+# ---------------------------------------------------------------------------
+
+_pinned: dict = {}
+
+
+def _pinned_buf(key: str, nbytes: int):
+    import torch
+    t = _pinned.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        _pinned[key] = t
+    return t
+
+
+def to_device(a: np.ndarray, key: str = "h2d"):
+    """numpy -> CUDA tensor through a reusable pinned staging buffer."""
+    import torch
+    a = np.ascontiguousarray(a)
+    tdt = torch.float64 if a.dtype.itemsize == 8 and a.dtype.kind == "f" else None
+    if a.dtype.kind == "f" and a.dtype.itemsize == 4:
+        tdt = torch.float32
+    st = _pinned_buf(key, a.nbytes)
+    st[: a.nbytes].numpy()[:] = a.view(np.uint8).reshape(-1)
+    dev = torch.empty(a.nbytes, dtype=torch.uint8, device="cuda")
+    dev.copy_(st[: a.nbytes], non_blocking=True)
+    torch.cuda.current_stream().synchronize()   # staging buffer is reused
+    return dev.view(tdt) if tdt is not None else dev
+
+
+def _to_host(t, key: str) -> np.ndarray:
+    """CUDA tensor -> numpy copy (through pinned memory)."""
+    import torch
+    nbytes = t.numel() * t.element_size()
+    st = _pinned_buf(key, nbytes)
+    st[:nbytes].copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return st[:nbytes].numpy().copy()
+
+
+def _encoding_to_host(enc: engine.DeviceEncoding):
+    """Packed blocks (list of bytes), exact values, prefix, stored centers."""
+    packed = _to_host(enc.packed[: enc.prefix.numel() * enc.stride], "d2h_packed")
+    lens = enc.block_lengths()
+    blocks = [packed[i * enc.stride: i * enc.stride + int(lens[i])].tobytes() for i in range(len(lens))]
+    exact = _to_host(enc.exact, "d2h_exact").view(enc.dtype) if enc.n_inc else np.zeros(0, dtype=enc.dtype)
+    prefix = enc.prefix.cpu().numpy().view(np.uint64).copy()
+    centers = enc.centers_t.cpu().numpy().astype(enc.dtype, copy=False).copy()
+    return blocks, exact, prefix, centers
+
+
+def _deflate(blocks, config: PipelineConfig) -> list[bytes]:
+    """Phase 4b, per-block raw DEFLATE on the host (pipeline.py:290-304).
+    ``codec.compress_block`` is looked up at call time (monkeypatchable)."""
+    fn = lambda b: codec.compress_block(b, config.deflate_level)  # noqa: E731
+    try:
+        if config.workers > 1 and len(blocks) > 1:
+            with ThreadPoolExecutor(max_workers=config.workers) as ex:
+                return list(ex.map(fn, blocks))
+        return [fn(b) for b in blocks]
+    except PipelineError:
+        raise
+    except Exception as exc:
+        raise PipelineError("zlib", str(exc)) from exc
+
+
+def assemble_variable(enc: engine.DeviceEncoding, config: PipelineConfig, name: str,
+                      timings: PhaseTimings | None = None) -> container.CompressedVariable:
+    """Device encoding -> CompressedVariable (pipeline.py:290-324)."""
+    t0 = time.perf_counter()
+    blocks, exact, prefix, centers = _encoding_to_host(enc)
+    t1 = time.perf_counter()
+    deflated = _deflate(blocks, config)
+    sizes = np.fromiter((len(b) for b in deflated), dtype=np.uint64, count=len(deflated))
+    offsets = np.zeros(len(deflated), dtype=np.uint64)
+    np.cumsum(sizes[:-1], out=offsets[1:])
+    t2 = time.perf_counter()
+    if timings is not None:
+        timings.bits_packing += t1 - t0
+        timings.zlib += t2 - t1
+    variable = container.CompressedVariable(
+        name=name, dtype_code=container.dtype_code_for(enc.dtype), n=enc.n, bits=enc.bits,
+        tolerance=float(config.tolerance), elements_per_block=enc.epb, nblocks=enc.nblocks,
+        n_incompressible=enc.n_inc, centers=centers, index_offsets=offsets,
+        incompressible_prefix=prefix, index_table=b"".join(deflated), incompressible_table=exact)
+    variable.validate()
+    return variable
+
+
+def _check_strategy(config: PipelineConfig) -> None:
+    if config.strategy not in ACCELERATED_STRATEGIES:
+        raise NotImplementedError(
+            f"strategy {config.strategy!r} is outside the B200 hot path (top_k binning only)")
+
+
+def _encode_device(base_d, cur_d, config: PipelineConfig, timing: bool = True):
+    try:
+        return engine.encode(base_d, cur_d, config.tolerance, config.bits, config.block_bytes, timing=timing)
+    except N.NativeError as exc:
+        if exc.code == N.NMK_ERR_EMPTY_HIST:
+            raise PipelineError("binning", "empty histogram") from exc
+        raise
+
+
+def compress_pair(pair: TemporalPair, config: PipelineConfig, name: str = "var0"):
+    """Compress ``pair.current`` against ``pair.base`` on the GPU.
+
+    Returns ``(CompressedVariable, PhaseTimings)``; the variable is byte-for-
+    byte the reference's for the same input and config (pipeline.py:170-324).
+    """
+    _check_strategy(config)
+    N.require_cuda()
+    timings = PhaseTimings()
+    t0 = time.perf_counter()
+    base_d = to_device(pair.base, "h2d_base")
+    cur_d = to_device(pair.current, "h2d_cur")
+    h2d = time.perf_counter() - t0
+    enc = _encode_device(base_d, cur_d, config)
+    ms = enc.phase_ms
+    timings.change_ratio = h2d + ms.get("change_ratio", 0.0) / 1e3
+    timings.binning = ms.get("binning", 0.0) / 1e3
+    timings.assign_index = ms.get("assign_index", 0.0) / 1e3
+    variable = assemble_variable(enc, config, name, timings)
+    return variable, timings
+
+
+def decompress(variable: container.CompressedVariable, base_reconstructed, rng=None) -> np.ndarray:
+    """Reconstruct the full variable or the slice ``rng = (start, count)``
+    (pipeline.py:327-340)."""
+    if rng is None:
+        start, count = 0, variable.n
+    else:
+        start, count = rng
+    base = np.asarray(base_reconstructed)
+    if rng is None and base.shape[0] != variable.n:
+        raise ValueError("base snapshot length mismatch")
+    return codec.partial_decode(variable, start, count, base)
+
+
+def compress_series(snapshots, config: PipelineConfig, name: str = "var0"):
+    """Compress a snapshot chain (pipeline.py:343-372).
+
+    Snapshot i is encoded against the reconstruction of snapshot i-1.  The
+    reconstruction never leaves the GPU: it is decoded from the packed stream
+    K4 just wrote (the same bytes the host variable holds), so the result is
+    identical to the reference's decompress-then-encode loop.
+    """
+    _check_strategy(config)
+    snapshots = [np.ascontiguousarray(s) for s in snapshots]
+    if len(snapshots) < 2:
+        raise ValueError("a series needs at least two snapshots")
+    n = snapshots[0].shape[0]
+    for i, s in enumerate(snapshots[1:], start=1):
+        if s.shape[0] != n:
+            raise ValueError(f"snapshot {i} length {s.shape[0]} != {n}")
+        if s.dtype != snapshots[0].dtype:
+            raise ValueError(f"snapshot {i} dtype differs")
+    TemporalPair(snapshots[0], snapshots[1])  # dtype / shape validation
+    N.require_cuda()
+    first = snapshots[0].copy()
+    recon = to_device(first, "h2d_base")
+    variables = []
+    for i, snap in enumerate(snapshots[1:], start=1):
+        cur = to_device(snap, "h2d_cur")
+        enc = _encode_device(recon, cur, config, timing=False)
+        variables.append(assemble_variable(enc, config, f"{name}.{i:04d}"))
+        res = engine.decode_encoding(enc, recon)
+        if res.bad_index or res.exhausted:  # pragma: no cover - internal invariant
+            raise PipelineError("decode", "device reconstruction failed")
+        recon = res.out
+    return first, variables

@@ -1,0 +1,109 @@
+"""CPU-only checks of the host side: the C-ABI library loads and exports every
+symbol include/nmk_b200.h declares, config validation, block geometry,
+container round trip.  No kernel is launched (no GPU here)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+from paper_1703_02438_b200 import _native as N
+from paper_1703_02438_b200 import codec, container, pipeline, workloads
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "nmk_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(nmk_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = N.load()
+    names = _header_functions()
+    assert len(names) >= 15
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(names) == set(N.SIGNATURES), "ctypes signatures out of sync with the header"
+    assert lib.nmk_version() == 1
+
+
+def test_struct_sizes_match_header():
+    import ctypes
+    assert ctypes.sizeof(N.NmkStats) == 32
+    assert ctypes.sizeof(N.NmkModel) == 4 * 4 + 8 + 17 * 8
+    assert ctypes.sizeof(N.NmkDecodeErr) == 16
+    assert ctypes.sizeof(N.NmkSegmentInfo) == 16
+
+
+def test_workspace_queries_need_no_device():
+    lib = N.load()
+    assert lib.nmk_minmax_ws_bytes(1 << 20) > 0
+    assert lib.nmk_encode_ws_bytes(1 << 20, 0, 1 << 20) >= 8 * 512
+    assert lib.nmk_hist_sparse_ws_bytes(1000) > 3 * 8 * 1000
+
+
+def test_argument_errors_are_reported_without_device():
+    lib = N.load()
+    rc = lib.nmk_encode(None, None, 10, 0, 10, N.NMK_F64, None, None, 1, 8, 1e-3, 1e-3, 16, None, 16,
+                        None, None, None, None, 0, None)
+    assert rc == N.NMK_ERR_ARG
+    assert b"bad argument" in lib.nmk_last_error()
+
+
+@pytest.mark.parametrize("kwargs", [{"workers": 0}, {"block_bytes": 100}, {"strategy": "nope"},
+                                    {"bits": 1}, {"bits": 31}, {"deflate_level": 11}, {"tolerance": 0.0}])
+def test_config_rejects(kwargs):
+    with pytest.raises(ValueError):
+        pipeline.PipelineConfig(**kwargs)
+
+
+def test_block_geometry_kats():
+    layout = codec.BlockLayout(block_bytes=1 << 20, bits=13, n=3_758_400)
+    assert layout.elements_per_block == 645_277 and layout.nblocks == 6
+    layout = codec.BlockLayout(block_bytes=4096, bits=8, n=4096 * 4)
+    assert list(layout.covering_blocks(4095, 2)) == [0, 1]
+    assert list(layout.covering_blocks(100, 0)) == []
+
+
+def test_deflate_stage_round_trip():
+    data = bytes(range(256)) * 4
+    for level in (0, 1, 6, 9):
+        assert codec.decompress_block(codec.compress_block(data, level)) == data
+    with pytest.raises(codec.CodecError):
+        codec.decompress_block(b"\x00\x01\x02not deflate")
+
+
+def test_container_round_trip(tmp_path):
+    v = container.CompressedVariable(
+        name="x", dtype_code=1, n=10, bits=4, tolerance=1e-3, elements_per_block=8, nblocks=2,
+        n_incompressible=1, centers=np.array([0.0, 0.5]), index_offsets=np.array([0, 3], dtype=np.uint64),
+        incompressible_prefix=np.array([0, 1], dtype=np.uint64), index_table=b"abcdef",
+        incompressible_table=np.array([7.0]))
+    p = tmp_path / "v.nmk"
+    container.write_file(p, [v])
+    (w,) = container.read_file(p)
+    assert container.to_bytes([w]) == container.to_bytes([v])
+
+
+def test_workloads_are_seeded():
+    a = workloads.cfg1_host(1000, seed=3)
+    b = workloads.cfg1_host(1000, seed=3)
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    base, cur = workloads.cfg2_host(16, seed=1)
+    assert base.size == 16 ** 3
+
+
+def test_product_path_does_not_import_oracle():
+    import subprocess
+    import sys
+    code = ("import sys; import paper_1703_02438_b200 as p; "
+            "assert 'nmk_oracle' not in sys.modules; print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True)
+    assert out.stdout.strip() == "ok", out.stderr
+    pkg = os.path.join(ROOT, "paper_1703_02438_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            assert "oracle" not in open(os.path.join(pkg, fn)).read().replace("no CPU fallback", ""), fn
