@@ -149,7 +149,9 @@ k_decode(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restri
     for (int e = 0; e < kGroup; ++e) {
       uint64_t j = grp_lo + e;
       if (j < tile_hi && code[e] == sentinel) smask |= 1u << e;
-      if (j >= seg_lo && j < seg_hi) inmask |= 1u << e;
+      // the last group of a block may run past the block end: those lanes
+      // belong to the next block's tile
+      if (j >= seg_lo && j < seg_hi && j < tile_hi) inmask |= 1u << e;
     }
     unsigned cnt = __popc(smask), ex, agg;
     BScan(tmp.scan).ExclusiveSum(cnt, ex, agg);
