@@ -225,6 +225,111 @@ def decompress(variable: container.CompressedVariable, base_reconstructed, rng=N
     return codec.partial_decode(variable, start, count, base)
 
 
+@dataclass
+class HostEncoding:
+    """Pre-deflate outputs of phases 1-4a on the host (what phase 4b and the
+    container consume).  Arrays alias reusable pinned buffers: they stay valid
+    until the next encode_host call."""
+
+    n: int
+    dtype: np.dtype
+    bits: int
+    k: int
+    epb: int
+    nblocks: int
+    stride: int
+    b0: int
+    packed: np.ndarray      # u8, block b at (b - b0) * stride
+    exact: np.ndarray
+    prefix: np.ndarray      # u64 per local block
+    centers: np.ndarray     # stored dtype
+    n_inc: int
+
+    def block(self, b: int) -> memoryview:
+        ln = packed_len(self, b)
+        i = b - self.b0
+        return memoryview(self.packed)[i * self.stride: i * self.stride + ln]
+
+
+def packed_len(h, b: int) -> int:
+    cnt = min((b + 1) * h.epb, h.n) - b * h.epb
+    return (cnt * h.bits + 7) // 8
+
+
+def _host_tensor(a, key):
+    """numpy array or CPU tensor -> pinned CPU tensor (no copy if pinned)."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_pinned():
+            return a
+        a = a.numpy()
+    a = np.ascontiguousarray(a)
+    st = _pinned_buf(key, a.nbytes)
+    st[: a.nbytes].numpy()[:] = a.view(np.uint8).reshape(-1)
+    tdt = torch.float64 if a.dtype.itemsize == 8 else torch.float32
+    return st[: a.nbytes].view(tdt)
+
+
+def _d2h_pinned(t, key: str) -> np.ndarray:
+    import torch
+    nbytes = t.numel() * t.element_size()
+    st = _pinned_buf(key, nbytes)
+    if nbytes:
+        st[:nbytes].copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+    return st[:nbytes].numpy()
+
+
+def encode_host(base, current, config: PipelineConfig, *, elem0: int = 0, n_total: int | None = None,
+                comm=None) -> HostEncoding:
+    """Phases 1-4a from HOST buffers to HOST buffers: H2D of both snapshots,
+    K1..K4, D2H of the packed stream, exact values and prefix table.  This is
+    the reference-facing call the e2e benchmark times (zlib excluded)."""
+    import torch
+    from . import distributed
+    _check_strategy(config)
+    N.require_cuda()
+    hb = _host_tensor(base, "e2e_base")
+    hc = _host_tensor(current, "e2e_cur")
+    db = hb.to("cuda", non_blocking=True)
+    dc = hc.to("cuda", non_blocking=True)
+    try:
+        enc, _, _ = distributed.encode_shard(db, dc, elem0, n_total if n_total is not None else db.numel(),
+                                             config.tolerance, config.bits, config.block_bytes, comm=comm)
+    except N.NativeError as exc:
+        if exc.code == N.NMK_ERR_EMPTY_HIST:
+            raise PipelineError("binning", "empty histogram") from exc
+        raise
+    nlb = enc.prefix.numel()
+    packed = _d2h_pinned(enc.packed[: nlb * enc.stride], "e2e_packed")
+    exact = _d2h_pinned(enc.exact, "e2e_exact").view(enc.dtype)
+    prefix = _d2h_pinned(enc.prefix, "e2e_prefix").view(np.uint64)
+    centers = _d2h_pinned(enc.centers_t, "e2e_centers").view(enc.dtype)
+    torch.cuda.current_stream().synchronize()
+    return HostEncoding(enc.n, enc.dtype, enc.bits, enc.k, enc.epb, enc.nblocks, enc.stride, enc.b0, packed,
+                        exact, prefix, centers, enc.n_inc)
+
+
+def decode_host(h: HostEncoding, base, *, elem0: int = 0, count: int | None = None) -> np.ndarray:
+    """Full (or [elem0, elem0+count) of this encoding's range) reconstruction
+    from HOST buffers: H2D of packed stream, exact values, prefix, centers
+    and base, K5, D2H of the output.  Returns a view of a pinned buffer."""
+    import torch
+    N.require_cuda()
+    count = h.n - elem0 if count is None else count
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_packed = torch.from_numpy(h.packed).to(dev, non_blocking=True)
+    d_exact = torch.from_numpy(h.exact).to(dev, non_blocking=True)
+    d_prefix = torch.from_numpy(h.prefix.view(np.int64)).to(dev, non_blocking=True)
+    d_centers = torch.from_numpy(h.centers.astype(np.float64)).to(dev, non_blocking=True)
+    hb = _host_tensor(base, "e2e_dbase")
+    d_base = hb.to(dev, non_blocking=True)
+    res = engine.decode(d_packed, h.stride, h.b0, h.bits, h.epb, h.n, d_prefix, d_centers, d_exact, d_base,
+                        [(elem0, count, 0)], check=False)
+    out = _d2h_pinned(res.out, "e2e_out").view(h.dtype)
+    torch.cuda.current_stream().synchronize()
+    return out
+
+
 def compress_series(snapshots, config: PipelineConfig, name: str = "var0"):
     """Compress a snapshot chain (pipeline.py:343-372).
 

@@ -70,12 +70,12 @@ def cfg2_host(side: int = 64, seed: int = 0):
     base = 1.0 + 0.5 * s[:, None, None] * s[None, :, None] * s[None, None, :]
     base = base + rng.normal(0.0, 0.01, base.shape)
     noise = rng.normal(0.0, 0.003, base.shape)
-    r = np.zeros_like(noise)
-    for dz in range(-2, 3):          # periodic 5^3 box filter
-        for dy in range(-2, 3):
-            for dx in range(-2, 3):
-                r += np.roll(noise, (dz, dy, dx), axis=(0, 1, 2))
-    r /= 125.0
+    r = noise
+    for axis in range(3):            # periodic 5^3 box filter, separable
+        acc = np.zeros_like(r)
+        for d in range(-2, 3):
+            acc += np.roll(r, d, axis=axis)
+        r = acc / 5.0
     out = rng.uniform(size=base.shape) < 0.02
     r[out] += rng.laplace(0.0, 0.1, int(out.sum()))
     cur = base * (1.0 + r)
