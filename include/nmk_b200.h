@@ -131,7 +131,7 @@ int nmk_select(const unsigned long long* keys, const unsigned long long* counts,
  * exact: n_local elements of capacity; prefix: local prefix per local block
  * (entry for a block whose start precedes elem0 is left untouched);
  * n_inc: device u64 total of local incompressible values. */
-size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t epb);
+size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t epb, int dtype);
 int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
                uint64_t n_total, int dtype, const double* centers, const double* cuts,
                int k, int bits, double tol_bin, double tolerance, uint64_t epb,
@@ -148,7 +148,7 @@ int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t ele
  * indices) reading base[seg_out[s] + i] and writing out[seg_out[s] + i].
  * seg_* are HOST arrays of nseg entries. */
 size_t nmk_decode_ws_bytes(const uint64_t* h_seg_start, const uint64_t* h_seg_count,
-                           int nseg, uint64_t epb);
+                           int nseg, uint64_t epb, uint64_t first_block);
 int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_block,
                int bits, uint64_t epb, uint64_t n_total,
                const unsigned long long* prefix_rel, const double* centers, int k,

@@ -1,4 +1,4 @@
-// k_decode.cu — K5: fused unpack + sentinel scan + reconstruct, batched over
+// k_decode.cu — K5: fused unpack + sentinel rank + reconstruct, batched over
 // element ranges ("segments").
 //
 // Replaces, for full and partial decompression, the per-block loop of
@@ -9,17 +9,21 @@
 // bits), otherwise T((1 + c[idx]) * f64(base)); ids in [k, sentinel) are an
 // error, as is running out of exact values.
 //
-// Tiles are the encode tiles (2048 elements on the block grid).  A segment
-// covers a run of consecutive tiles; its first tile is seeded with
-// prefix_rel[block] + #sentinels between the block start and the tile (one
-// small pre-count CTA per segment), and the running sentinel rank inside the
-// segment is carried by a decoupled look-back, so no element is read twice.
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
-
+// Chunks are the encoder's 256-element warp chunks on the block grid.
+//   1. k_dec_count: sentinels per chunk of the covering span (reads the
+//      packed stream only, B/8 bytes per element);
+//   2. chunk_scan (k_scan.cu): chunk offsets;
+//   3. k_dec_chunks: one warp per (segment, chunk): unpack, rank the
+//      sentinels (block prefix + in-block chunk offset + warp scan), gather
+//      exact values, reconstruct, store.  No inter-warp dependency.
 #include "nmk_common.cuh"
+#include "nmk_scan.cuh"
 
 namespace nmk {
+
+constexpr int kDChunk = 32 * kGroup;   // 256 elements per warp chunk
+constexpr int kDecThreads = 256;
+constexpr int kSmemCenters = 4096;     // centers in shared memory up to this k
 
 template <int B>
 __device__ __forceinline__ void unpack8d(const uint8_t* src, uint32_t (&code)[kGroup]) {
@@ -41,133 +45,141 @@ __device__ __forceinline__ void unpack8d(const uint8_t* src, uint32_t (&code)[kG
 
 struct Seg {
   uint64_t start, count, out;   // global element range, output offset
-  uint64_t tile0;               // first tile (linear, across segments)
-  uint64_t gfirst;              // block-grid tile id of the first tile
+  uint64_t item0;               // first work item (linear across segments)
+  uint64_t gfirst;              // global chunk id of the segment's first chunk
 };
 
 struct DecodeGeom {
-  uint64_t epb, tpb, n_total, first_block, stride, n_exact, total_tiles;
+  uint64_t epb, cpb, n_total, first_block, stride, n_exact, nchunks, nitems;
   int nseg, k;
 };
+
+struct DChunk {
+  uint64_t b, ci, blk_start, blk_end, chunk_lo, chunk_hi, crel;
+};
+
+__device__ __forceinline__ DChunk dchunk(const DecodeGeom& geo, uint64_t g) {
+  DChunk d;
+  d.b = g / geo.cpb;
+  d.ci = g - d.b * geo.cpb;
+  d.blk_start = d.b * geo.epb;
+  d.blk_end = d.blk_start + geo.epb;
+  if (d.blk_end > geo.n_total) d.blk_end = geo.n_total;
+  d.chunk_lo = d.blk_start + d.ci * kDChunk;
+  d.chunk_hi = d.chunk_lo + kDChunk;
+  if (d.chunk_hi > d.blk_end) d.chunk_hi = d.blk_end;
+  d.crel = g - geo.first_block * geo.cpb;
+  return d;
+}
+
+// Stage one chunk's 32*B packed bytes into warp-private shared memory
+// (zero beyond the block's byte length).
+template <int B>
+__device__ __forceinline__ void stage_chunk_bytes(const uint8_t* __restrict__ packed, const DecodeGeom& geo,
+                                                  const DChunk& d, uint8_t* my, int lane) {
+  const uint64_t blk_bytes = ((d.blk_end - d.blk_start) * B + 7) / 8;
+  const uint64_t off = d.ci * (uint64_t)(32 * B);
+  uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
+  if (nbytes > (uint64_t)(32 * B)) nbytes = 32 * B;
+  const uint8_t* src = packed + (d.b - geo.first_block) * geo.stride + off;
+  const uint32_t nvec = (uint32_t)(nbytes / 16);
+  for (uint32_t i = lane; i < (uint32_t)(2 * B); i += 32)   // 32*B/16 = 2B vectors
+    reinterpret_cast<uint4*>(my)[i] = (i < nvec) ? __ldg(reinterpret_cast<const uint4*>(src) + i)
+                                                 : make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) my[i] = __ldg(src + i);
+  __syncwarp();
+}
+
+template <int B>
+__global__ void __launch_bounds__(kDecThreads)
+k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
+  __shared__ __align__(16) uint8_t wbytes[kDecThreads / 32][32 * B + 16];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t sentinel = (1u << B) - 1u;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kDecThreads / 32);
+  const uint64_t g0 = geo.first_block * geo.cpb;
+  for (uint64_t c = (uint64_t)blockIdx.x * (kDecThreads / 32) + wid; c < geo.nchunks; c += nwarps) {
+    const DChunk d = dchunk(geo, g0 + c);
+    stage_chunk_bytes<B>(packed, geo, d, wbytes[wid], lane);
+    uint32_t code[kGroup];
+    unpack8d<B>(wbytes[wid] + lane * B, code);
+    const uint64_t grp_lo = d.chunk_lo + (uint64_t)lane * kGroup;
+    unsigned n = 0;
+#pragma unroll
+    for (int e = 0; e < kGroup; ++e) n += (grp_lo + e < d.chunk_hi && code[e] == sentinel);
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0) counts[c] = n;
+    __syncwarp();
+  }
+}
 
 template <typename T> struct DVec;
 template <> struct DVec<double> { using V = double2; static constexpr int N = 2; };
 template <> struct DVec<float>  { using V = float4;  static constexpr int N = 4; };
 
-// pre-count: seed[s] = prefix_rel[block(start)] + #sentinels in
-// [block start, first tile start) — one CTA per segment.
-template <int B>
-__global__ void __launch_bounds__(kTileThreads)
-k_decode_seed(const uint8_t* __restrict__ packed, const Seg* __restrict__ segs, DecodeGeom geo,
-              const unsigned long long* __restrict__ prefix_rel, unsigned long long* __restrict__ seed) {
-  typedef cub::BlockReduce<unsigned long long, kTileThreads> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const Seg sg = segs[blockIdx.x];
-  const uint64_t b = sg.gfirst / geo.tpb, ti = sg.gfirst % geo.tpb;
-  const uint32_t sentinel = (1u << B) - 1u;
-  const uint8_t* blk = packed + (b - geo.first_block) * geo.stride;
-  unsigned long long cnt = 0;
-  const uint64_t ngrp = ti * kTileThreads;  // whole groups before the first tile
-  for (uint64_t gi = threadIdx.x; gi < ngrp; gi += kTileThreads) {
-    uint32_t c[kGroup];
-    unpack8d<B>(blk + gi * B, c);
-#pragma unroll
-    for (int e = 0; e < kGroup; ++e) cnt += (c[e] == sentinel);
-  }
-  unsigned long long tot = BR(tmp).Sum(cnt);
-  if (threadIdx.x == 0) seed[blockIdx.x] = prefix_rel[b - geo.first_block] + tot;
-}
-
 template <typename T, int B>
-__global__ void __launch_bounds__(kTileThreads)
-k_decode(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs,
-         const unsigned long long* __restrict__ seed, const double* __restrict__ centers_g,
-         const T* __restrict__ exact, const T* __restrict__ base, T* __restrict__ out,
-         nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err,
-         unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket) {
-  typedef cub::BlockScan<unsigned, kTileThreads> BScan;
-  typedef cub::BlockReduce<unsigned, kTileThreads> BRed;
-  __shared__ union {
-    typename BScan::TempStorage scan;
-    typename BRed::TempStorage red;
-  } tmp;
-  __shared__ __align__(16) uint8_t tile_bytes[kTileThreads * B + 16];
-  __shared__ unsigned long long s_tile, s_excl;
-  extern __shared__ double smc[];
-
-  const int tid = threadIdx.x;
+__global__ void __launch_bounds__(kDecThreads)
+k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs,
+             const unsigned long long* __restrict__ offsets, const unsigned long long* __restrict__ prefix_rel,
+             const double* __restrict__ centers_g, const T* __restrict__ exact, const T* __restrict__ base,
+             T* __restrict__ out, nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err) {
+  __shared__ __align__(16) uint8_t wbytes[kDecThreads / 32][32 * B + 16];
+  extern __shared__ double centers_s[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int k = geo.k;
-  const double* C = centers_g;
-  if (k <= 4096) {
-    for (int i = tid; i < k; i += kTileThreads) smc[i] = centers_g[i];
-    C = smc;
-  }
+  const bool c_smem = k <= kSmemCenters;
+  if (c_smem)
+    for (int i = threadIdx.x; i < k; i += kDecThreads) centers_s[i] = centers_g[i];
+  __syncthreads();
+  const double* C = c_smem ? centers_s : centers_g;
   const uint32_t sentinel = (1u << B) - 1u;
+  constexpr int VN = DVec<T>::N;
+  using V = typename DVec<T>::V;
+  const bool out_al = (((uintptr_t)out | (uintptr_t)base) & 15) == 0;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kDecThreads / 32);
 
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint64_t t = s_tile;
-    if (t >= geo.total_tiles) break;
-    // segment lookup (segments are few; binary search over tile0)
+  for (uint64_t it = (uint64_t)blockIdx.x * (kDecThreads / 32) + wid; it < geo.nitems; it += nwarps) {
     int lo_s = 0, hi_s = geo.nseg - 1;
     while (lo_s < hi_s) {
       int mid = (lo_s + hi_s + 1) >> 1;
-      if (segs[mid].tile0 <= t) lo_s = mid; else hi_s = mid - 1;
+      if (segs[mid].item0 <= it) lo_s = mid; else hi_s = mid - 1;
     }
     const Seg sg = segs[lo_s];
-    const uint64_t lt = t - sg.tile0;
-    const uint64_t g = sg.gfirst + lt;
-    const uint64_t b = g / geo.tpb, ti = g % geo.tpb;
-    const uint64_t blk_start = b * geo.epb;
-    uint64_t blk_end = blk_start + geo.epb;
-    if (blk_end > geo.n_total) blk_end = geo.n_total;
-    const uint64_t tile_lo = blk_start + ti * kTile;
-    uint64_t tile_hi = tile_lo + kTile;
-    if (tile_hi > blk_end) tile_hi = blk_end;
-    const uint64_t seg_lo = sg.start, seg_hi = sg.start + sg.count;
-
-    // stage this tile's packed bytes
-    {
-      const uint64_t blk_bytes = ((blk_end - blk_start) * B + 7) / 8;
-      const uint64_t off = ti * (uint64_t)(kTileThreads * B);
-      uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
-      if (nbytes > (uint64_t)kTileThreads * B) nbytes = (uint64_t)kTileThreads * B;
-      const uint8_t* src = packed + (b - geo.first_block) * geo.stride + off;
-      const uint32_t nvec = (uint32_t)(nbytes / 16);
-      for (uint32_t i = tid; i < nvec; i += kTileThreads)
-        reinterpret_cast<uint4*>(tile_bytes)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
-      for (uint32_t i = nvec * 16 + tid; i < (uint32_t)kTileThreads * B; i += kTileThreads)
-        tile_bytes[i] = (i < nbytes) ? src[i] : 0;
-    }
-    __syncthreads();
+    const uint64_t g = sg.gfirst + (it - sg.item0);
+    const DChunk d = dchunk(geo, g);
+    stage_chunk_bytes<B>(packed, geo, d, wbytes[wid], lane);
     uint32_t code[kGroup];
-    unpack8d<B>(tile_bytes + tid * B, code);
-    const uint64_t grp_lo = tile_lo + (uint64_t)tid * kGroup;
-    unsigned smask = 0, inmask = 0;
+    unpack8d<B>(wbytes[wid] + lane * B, code);
+    const uint64_t seg_lo = sg.start, seg_hi = sg.start + sg.count;
+    const uint64_t grp_lo = d.chunk_lo + (uint64_t)lane * kGroup;
+    unsigned smask = 0, inmask = 0, ahead = 0;
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) {
-      uint64_t j = grp_lo + e;
-      if (j < tile_hi && code[e] == sentinel) smask |= 1u << e;
-      // the last group of a block may run past the block end: those lanes
-      // belong to the next block's tile
-      if (j >= seg_lo && j < seg_hi && j < tile_hi) inmask |= 1u << e;
+      const uint64_t j = grp_lo + e;
+      const bool inblk = j < d.chunk_hi;
+      if (inblk && code[e] == sentinel) {
+        smask |= 1u << e;
+        if (j < seg_lo) ++ahead;
+      }
+      if (inblk && j >= seg_lo && j < seg_hi) inmask |= 1u << e;
     }
-    unsigned cnt = __popc(smask), ex, agg;
-    BScan(tmp.scan).ExclusiveSum(cnt, ex, agg);
-    if (tid == 0) {
-      if (lt == 0) st_relaxed(status + t, kFlagInc | (seed[lo_s] + agg));
-      else st_relaxed(status + t, kFlagAgg | agg);
+    // rank of this lane's first sentinel, anchored like the reference on the
+    // prefix entry of the segment's FIRST block and counted from there
+    // (codec.py:231-236): prefix + chunk offset + warp exclusive scan
+    const uint64_t ab = sg.gfirst / geo.cpb - geo.first_block;
+    const unsigned long long chunk_off = prefix_rel[ab] + (offsets[d.crel] - offsets[ab * geo.cpb]);
+    const unsigned cnt = __popc(smask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    // compressible outputs do not need the look-back: do them first
-    const bool full_tile = tile_lo >= seg_lo && tile_hi <= seg_hi;
-    const bool full_grp = (inmask == 0xffu);
     T bv[kGroup], ov[kGroup];
-    const uint64_t oi = sg.out + (grp_lo - seg_lo);  // valid when grp_lo >= seg_lo
-    constexpr int VN = DVec<T>::N;
-    const bool vec = full_grp && (oi % VN == 0) && ((((uintptr_t)base | (uintptr_t)out) & 15) == 0);
+    const int64_t oi = (int64_t)sg.out + ((int64_t)grp_lo - (int64_t)seg_lo);
+    const bool vec = inmask == 0xffu && out_al && (oi % VN) == 0;
     if (vec) {
-      using V = typename DVec<T>::V;
 #pragma unroll
       for (int q = 0; q < kGroup / VN; ++q) {
         V w = __ldg(reinterpret_cast<const V*>(base + oi) + q);
@@ -177,77 +189,50 @@ k_decode(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restri
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < kGroup; ++e)
-        bv[e] = (inmask >> e & 1u) ? __ldg(base + sg.out + (grp_lo + e - seg_lo)) : T(0);
+      for (int e = 0; e < kGroup; ++e) bv[e] = (inmask >> e & 1u) ? __ldg(base + (oi + e)) : T(0);
     }
-    unsigned bad = 0, maxbad = 0;
+    unsigned long long pos = chunk_off + (incl - cnt);
+    unsigned bad = 0, maxbad = 0, exhausted = 0;
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) {
       ov[e] = T(0);
-      if (!(inmask >> e & 1u) || (smask >> e & 1u)) continue;
-      if (code[e] >= (uint32_t)k) {
-        bad = 1;
-        maxbad = code[e] > maxbad ? code[e] : maxbad;
-        continue;
+      if (smask >> e & 1u) {
+        if (inmask >> e & 1u) {
+          if (pos < geo.n_exact) ov[e] = exact[pos];
+          else exhausted = 1;
+        }
+        ++pos;
+      } else if (inmask >> e & 1u) {
+        if (code[e] >= (uint32_t)k) {
+          bad = 1;
+          maxbad = code[e] > maxbad ? code[e] : maxbad;
+        } else {
+          ov[e] = apply_center<T>(C[code[e]], to_f64(bv[e]));
+        }
       }
-      ov[e] = apply_center<T>(C[code[e]], to_f64(bv[e]));
+    }
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < kGroup / VN; ++q)
+        reinterpret_cast<V*>(out + oi)[q] = *reinterpret_cast<const V*>(&ov[q * VN]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e)
+        if (inmask >> e & 1u) out[oi + e] = ov[e];
     }
     if (bad) {
       atomicOr(&err->bad_index, 1u);
       atomicMax(&err->max_bad_index, maxbad);
     }
-    // running sentinel rank
-    if (tid < 32) {
-      unsigned long long excl = (lt == 0) ? seed[lo_s] : lookback(status, (long long)t, (long long)sg.tile0);
-      if (tid == 0) {
-        if (lt != 0) st_relaxed(status + t, kFlagInc | (excl + agg));
-        s_excl = excl;
-      }
-    }
-    __syncthreads();
-    const unsigned long long excl = s_excl;
-    unsigned long long pos = excl + ex;
-    bool exhausted = false;
-#pragma unroll
-    for (int e = 0; e < kGroup; ++e) {
-      if (smask >> e & 1u) {
-        if (inmask >> e & 1u) {
-          if (pos < geo.n_exact) ov[e] = exact[pos];
-          else exhausted = true;
-        }
-        ++pos;
-      }
-    }
     if (exhausted) atomicOr(&err->exhausted, 1u);
-    if (vec) {
-      using V = typename DVec<T>::V;
-#pragma unroll
-      for (int q = 0; q < kGroup / VN; ++q) reinterpret_cast<V*>(out + oi)[q] = *reinterpret_cast<const V*>(&ov[q * VN]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < kGroup; ++e)
-        if (inmask >> e & 1u) out[sg.out + (grp_lo + e - seg_lo)] = ov[e];
+    // segment bookkeeping
+    const unsigned in_s = __reduce_add_sync(0xffffffffu, __popc(smask & inmask));
+    if (lane == 0 && in_s) atomicAdd(&info[lo_s].n_sentinel, (unsigned long long)in_s);
+    if (g == sg.gfirst) {
+      const unsigned ah = __reduce_add_sync(0xffffffffu, ahead);
+      if (lane == 0) info[lo_s].inc_before = chunk_off + ah;
     }
-    // segment bookkeeping: sentinels inside the segment, and ahead of it
-    if (full_tile) {
-      if (tid == 0) atomicAdd(&info[lo_s].n_sentinel, (unsigned long long)agg);
-    } else {
-      unsigned in_cnt = __popc(smask & inmask);
-      unsigned ahead = 0;
-#pragma unroll
-      for (int e = 0; e < kGroup; ++e)
-        if ((smask >> e & 1u) && grp_lo + e < seg_lo) ++ahead;
-      __syncthreads();
-      unsigned tot_in = BRed(tmp.red).Sum(in_cnt);
-      __syncthreads();
-      unsigned tot_ahead = BRed(tmp.red).Sum(ahead);
-      if (tid == 0) {
-        if (tot_in) atomicAdd(&info[lo_s].n_sentinel, (unsigned long long)tot_in);
-        if (lt == 0) info[lo_s].inc_before = excl + tot_ahead;
-      }
-    }
-    if (full_tile && lt == 0 && tid == 0) info[lo_s].inc_before = excl;
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -265,56 +250,69 @@ static int sm_count_d() {
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct DecodePlan {
-  uint64_t total_tiles;
-  size_t off_status, off_segs, off_seed, total;
+  uint64_t cpb, nchunks, nitems;
+  size_t off_counts, off_offsets, off_scan, off_segs, total;
 };
 
-static uint64_t seg_first_tile(uint64_t start, uint64_t epb, uint64_t tpb) {
-  uint64_t b = start / epb;
-  return b * tpb + (start - b * epb) / kTile;
-}
-
-static DecodePlan decode_plan(const uint64_t* st, const uint64_t* ct, int nseg, uint64_t epb) {
+static DecodePlan decode_plan(const uint64_t* st, const uint64_t* ct, int nseg, uint64_t epb, uint64_t first_block) {
   DecodePlan p{};
-  uint64_t tpb = (epb + kTile - 1) / kTile;
-  uint64_t tiles = 0;
+  p.cpb = (epb + kDChunk - 1) / kDChunk;
+  uint64_t items = 0, last = 0;
+  const uint64_t g0 = first_block * p.cpb;
   for (int s = 0; s < nseg; ++s) {
     if (ct[s] == 0) continue;
-    uint64_t a = seg_first_tile(st[s], epb, tpb), z = seg_first_tile(st[s] + ct[s] - 1, epb, tpb);
-    tiles += z - a + 1;
+    uint64_t e = st[s] + ct[s] - 1;
+    uint64_t ga = (st[s] / epb) * p.cpb + (st[s] % epb) / kDChunk;
+    uint64_t gz = (e / epb) * p.cpb + (e % epb) / kDChunk;
+    items += gz - ga + 1;
+    if (gz + 1 - g0 > last) last = gz + 1 - g0;
   }
-  p.total_tiles = tiles;
-  p.off_status = 256;
-  p.off_segs = p.off_status + al256((tiles + 1) * 8);
-  p.off_seed = p.off_segs + al256((size_t)(nseg + 1) * sizeof(Seg));
-  p.total = p.off_seed + al256((size_t)(nseg + 1) * 8);
+  p.nchunks = last;
+  p.nitems = items;
+  p.off_counts = 0;
+  p.off_offsets = al256(p.nchunks * 4);
+  p.off_scan = p.off_offsets + al256(p.nchunks * 8 + 8);
+  p.off_segs = p.off_scan + al256(chunk_scan_ws_bytes(p.nchunks));
+  p.total = p.off_segs + al256((size_t)(nseg + 1) * sizeof(Seg));
   return p;
 }
 
 template <typename T, int B>
-static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, unsigned long long* seed,
-                          const unsigned long long* prefix_rel, const double* centers, const void* exact,
-                          const void* base, void* out, nmk_segment_info* info, nmk_decode_err* err,
-                          unsigned long long* status, unsigned* ticket, cudaStream_t s) {
-  k_decode_seed<B><<<geo.nseg, kTileThreads, 0, s>>>(packed, segs, geo, prefix_rel, seed);
-  size_t smem = (geo.k <= 4096) ? 4096 * sizeof(double) : 0;
+static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, uint32_t* counts,
+                          unsigned long long* offsets, void* scan_ws, const unsigned long long* prefix_rel,
+                          const double* centers, const void* exact, const void* base, void* out,
+                          nmk_segment_info* info, nmk_decode_err* err, cudaStream_t s) {
+  const int sms = sm_count_d();
+  uint64_t g1 = (geo.nchunks + 7) / 8;
+  unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
+  k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
+  chunk_scan(counts, geo.nchunks, offsets, nullptr, scan_ws, s);
+  const size_t smem = (geo.k <= kSmemCenters) ? (size_t)geo.k * 8 : 0;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_dec_chunks<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode<T, B>, kTileThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B>, kDecThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (uint64_t)sm_count_d() * per_sm;
-  if (grid > geo.total_tiles) grid = geo.total_tiles;
-  k_decode<T, B><<<(unsigned)grid, kTileThreads, smem, s>>>(packed, geo, segs, seed, centers, (const T*)exact,
-                                                            (const T*)base, (T*)out, info, err, status, ticket);
+  uint64_t grid = (uint64_t)sms * per_sm;
+  uint64_t need = (geo.nitems + 7) / 8;
+  if (grid > need) grid = need;
+  k_dec_chunks<T, B><<<(unsigned)grid, kDecThreads, smem, s>>>(packed, geo, segs, offsets, prefix_rel, centers,
+                                                                (const T*)exact, (const T*)base, (T*)out, info,
+                                                                err);
 }
 
 template <typename T>
-static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& geo, const Seg* segs,
-                           unsigned long long* seed, const unsigned long long* prefix_rel, const double* centers,
-                           const void* exact, const void* base, void* out, nmk_segment_info* info,
-                           nmk_decode_err* err, unsigned long long* status, unsigned* ticket, cudaStream_t s) {
+static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, uint32_t* counts,
+                           unsigned long long* offsets, void* scan_ws, const unsigned long long* prefix_rel,
+                           const double* centers, const void* exact, const void* base, void* out,
+                           nmk_segment_info* info, nmk_decode_err* err, cudaStream_t s) {
   switch (bits) {
-#define NMK_DEC_CASE(BB) \
-  case BB: launch_decode<T, BB>(packed, geo, segs, seed, prefix_rel, centers, exact, base, out, info, err, status, ticket, s); break;
+#define NMK_DEC_CASE(BB)                                                                                    \
+  case BB: launch_decode<T, BB>(packed, geo, segs, counts, offsets, scan_ws, prefix_rel, centers, exact, base, \
+                                out, info, err, s); break;
     NMK_DEC_CASE(2) NMK_DEC_CASE(3) NMK_DEC_CASE(4) NMK_DEC_CASE(5) NMK_DEC_CASE(6) NMK_DEC_CASE(7)
     NMK_DEC_CASE(8) NMK_DEC_CASE(9) NMK_DEC_CASE(10) NMK_DEC_CASE(11) NMK_DEC_CASE(12) NMK_DEC_CASE(13)
     NMK_DEC_CASE(14) NMK_DEC_CASE(15) NMK_DEC_CASE(16) NMK_DEC_CASE(17) NMK_DEC_CASE(18) NMK_DEC_CASE(19)
@@ -323,7 +321,7 @@ static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& ge
 #undef NMK_DEC_CASE
     default: return set_error(NMK_ERR_ARG, "nmk_decode: bits %d outside [2, 30]", bits);
   }
-  return check_launch("k_decode");
+  return check_launch("k_dec_chunks");
 }
 
 }  // namespace nmk
@@ -331,9 +329,9 @@ static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& ge
 using namespace nmk;
 
 extern "C" size_t nmk_decode_ws_bytes(const uint64_t* h_seg_start, const uint64_t* h_seg_count, int nseg,
-                                      uint64_t epb) {
+                                      uint64_t epb, uint64_t first_block) {
   if (nseg < 0 || epb == 0) return 0;
-  return decode_plan(h_seg_start, h_seg_count, nseg, epb).total;
+  return decode_plan(h_seg_start, h_seg_count, nseg, epb, first_block).total;
 }
 
 extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
@@ -347,49 +345,42 @@ extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t
     return set_error(NMK_ERR_ARG, "nmk_decode: bad argument");
   if (bits < 2 || bits > 30 || epb == 0 || k < 1) return set_error(NMK_ERR_ARG, "nmk_decode: bad geometry");
   if (block_stride % 16 || ((uintptr_t)packed & 15)) return set_error(NMK_ERR_ARG, "nmk_decode: packed alignment");
-  DecodePlan p = decode_plan(h_seg_start, h_seg_count, nseg, epb);
-  if (ws_bytes < p.total) return set_error(NMK_ERR_ARG, "nmk_decode: workspace too small");
-  const uint64_t tpb = (epb + kTile - 1) / kTile;
-  // host-side segment table (only non-empty segments get tiles)
-  Seg* hs = (Seg*)malloc(sizeof(Seg) * (size_t)nseg);
-  int ns = 0;
-  uint64_t tile0 = 0;
+  if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_decode: bad dtype");
   for (int i = 0; i < nseg; ++i) {
     uint64_t st = h_seg_start[i], ct = h_seg_count[i];
-    if (st + ct > n_total) { free(hs); return set_error(NMK_ERR_ARG, "nmk_decode: segment out of range"); }
-    if (ct == 0) continue;
-    if (st / epb < first_block) { free(hs); return set_error(NMK_ERR_ARG, "nmk_decode: segment before first block"); }
-    Seg sg;
-    sg.start = st; sg.count = ct; sg.out = h_seg_out[i];
-    sg.gfirst = seg_first_tile(st, epb, tpb);
-    sg.tile0 = tile0;
-    tile0 += seg_first_tile(st + ct - 1, epb, tpb) - sg.gfirst + 1;
-    hs[ns++] = sg;
+    if (ct == 0 || st + ct > n_total || st / epb < first_block)
+      return set_error(NMK_ERR_ARG, "nmk_decode: segment %d empty or outside the covered blocks", i);
   }
-  cudaMemsetAsync(seg_info, 0, sizeof(nmk_segment_info) * (size_t)nseg, s);
-  cudaMemsetAsync(err, 0, sizeof(nmk_decode_err), s);
-  if (ns == 0) { free(hs); return check_launch("nmk_decode(empty)"); }
-  if (!packed || !centers || !base || !out || !prefix_rel) { free(hs); return set_error(NMK_ERR_ARG, "nmk_decode: null pointer"); }
-  if (ns != nseg) {  // empty segments are skipped: info indices follow non-empty order
-    free(hs);
-    return set_error(NMK_ERR_ARG, "nmk_decode: empty segments must be filtered by the caller");
+  if (!packed || !centers || !base || !out || !prefix_rel) return set_error(NMK_ERR_ARG, "nmk_decode: null pointer");
+  DecodePlan p = decode_plan(h_seg_start, h_seg_count, nseg, epb, first_block);
+  if (ws_bytes < p.total) return set_error(NMK_ERR_ARG, "nmk_decode: workspace too small");
+  Seg* hs = (Seg*)malloc(sizeof(Seg) * (size_t)nseg);
+  uint64_t item0 = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const uint64_t st = h_seg_start[i], ct = h_seg_count[i], e = st + ct - 1;
+    Seg sg;
+    sg.start = st;
+    sg.count = ct;
+    sg.out = h_seg_out[i];
+    sg.gfirst = (st / epb) * p.cpb + (st % epb) / kDChunk;
+    sg.item0 = item0;
+    item0 += (e / epb) * p.cpb + (e % epb) / kDChunk - sg.gfirst + 1;
+    hs[i] = sg;
   }
   char* w = (char*)ws;
-  unsigned* ticket = (unsigned*)w;
-  unsigned long long* status = (unsigned long long*)(w + p.off_status);
+  uint32_t* counts = (uint32_t*)(w + p.off_counts);
+  unsigned long long* offsets = (unsigned long long*)(w + p.off_offsets);
   Seg* dsegs = (Seg*)(w + p.off_segs);
-  unsigned long long* seed = (unsigned long long*)(w + p.off_seed);
-  cudaMemsetAsync(w, 0, p.off_segs, s);
-  cudaMemcpyAsync(dsegs, hs, sizeof(Seg) * (size_t)ns, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(seg_info, 0, sizeof(nmk_segment_info) * (size_t)nseg, s);
+  cudaMemsetAsync(err, 0, sizeof(nmk_decode_err), s);
   // a pageable H2D cudaMemcpyAsync returns after staging the source, so the
   // host table can be released immediately (no stream synchronisation)
+  cudaMemcpyAsync(dsegs, hs, sizeof(Seg) * (size_t)nseg, cudaMemcpyHostToDevice, s);
   free(hs);
-  DecodeGeom geo{epb, tpb, n_total, first_block, block_stride, n_exact, p.total_tiles, ns, k};
+  DecodeGeom geo{epb, p.cpb, n_total, first_block, block_stride, n_exact, p.nchunks, p.nitems, nseg, k};
   if (dtype == NMK_F64)
-    return dispatch_decode<double>(bits, packed, geo, dsegs, seed, prefix_rel, centers, exact, base, out, seg_info, err,
-                                   status, ticket, s);
-  if (dtype == NMK_F32)
-    return dispatch_decode<float>(bits, packed, geo, dsegs, seed, prefix_rel, centers, exact, base, out, seg_info, err,
-                                  status, ticket, s);
-  return set_error(NMK_ERR_ARG, "nmk_decode: bad dtype");
+    return dispatch_decode<double>(bits, packed, geo, dsegs, counts, offsets, w + p.off_scan, prefix_rel, centers,
+                                   exact, base, out, seg_info, err, s);
+  return dispatch_decode<float>(bits, packed, geo, dsegs, counts, offsets, w + p.off_scan, prefix_rel, centers,
+                                exact, base, out, seg_info, err, s);
 }

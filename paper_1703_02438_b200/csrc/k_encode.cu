@@ -9,20 +9,23 @@
 //   incompressible prefix (pipeline.py:257-276), and pack_block MSB-first
 //   (codec.py:83-92) into the block layout of codec.BlockLayout (codec.py:28-59).
 //
-// Work unit: a tile of 2048 elements = 256 threads x 8 consecutive elements,
-// laid on the grid of index blocks (tiles never straddle a block), so each
-// thread's 8 codes occupy exactly B whole bytes of its block.  Tiles are
-// claimed in order through an atomic ticket; the running incompressible count
-// is carried across tiles with a decoupled look-back (single pass, no second
-// read of the inputs).  The packed bytes of a tile are staged in shared
-// memory and written out with 16-byte stores before the look-back wait.
-#include <cub/block/block_scan.cuh>
-
+// Work unit: a CHUNK of 256 elements = one warp x 8 consecutive elements per
+// lane, laid on the grid of index blocks (chunks never straddle a block), so
+// each lane's 8 codes are exactly B whole bytes of its block and a chunk's
+// 32*B bytes start 16-byte aligned.  Warps run independently (no block-wide
+// barrier): a chunk writes its packed bytes, its incompressible count and
+// its incompressible values into its own 256-slot scratch window.  A short
+// finalize pass (k_scan.cu + k_enc_finalize) turns the counts into positions,
+// moves the (rare) values into the compacted list and fills the per-block
+// prefix table.
 #include "nmk_common.cuh"
+#include "nmk_scan.cuh"
 
 namespace nmk {
 
-constexpr int kSmemCenters = 2048;  // centers + cuts in smem up to this k
+constexpr int kChunk = 32 * kGroup;   // 256 elements per warp chunk
+constexpr int kEncThreads = 256;      // 8 warps per CTA
+constexpr int kSmemCuts = 4096;       // cuts in shared memory up to this many
 
 template <int B>
 __device__ __forceinline__ void pack8(const uint32_t (&code)[kGroup], uint8_t* dst) {
@@ -43,7 +46,7 @@ __device__ __forceinline__ void pack8(const uint32_t (&code)[kGroup], uint8_t* d
       }
     }
   }
-  // widest aligned store the byte offset tid*B allows
+  // widest aligned store the byte offset lane*B allows
   if constexpr (B % 16 == 0) {
 #pragma unroll
     for (int w = 0; w < B / 16; ++w) {
@@ -78,157 +81,186 @@ __device__ __forceinline__ void pack8(const uint32_t (&code)[kGroup], uint8_t* d
   }
 }
 
+struct EncodeGeom {
+  uint64_t n_local, elem0, n_total, epb, cpb, g0, nchunks, b0, stride;
+};
+
+// Chunk c of this range: block, in-block chunk index and element spans.
+struct ChunkSpan {
+  uint64_t b, ci, blk_start, blk_end, lo, hi, chunk_lo;
+};
+
+__device__ __forceinline__ ChunkSpan chunk_span(const EncodeGeom& geo, uint64_t c) {
+  ChunkSpan s;
+  const uint64_t g = geo.g0 + c;
+  s.b = g / geo.cpb;
+  s.ci = g - s.b * geo.cpb;
+  s.blk_start = s.b * geo.epb;
+  s.blk_end = s.blk_start + geo.epb;
+  if (s.blk_end > geo.n_total) s.blk_end = geo.n_total;
+  s.chunk_lo = s.blk_start + s.ci * kChunk;
+  uint64_t chunk_hi = s.chunk_lo + kChunk;
+  if (chunk_hi > s.blk_end) chunk_hi = s.blk_end;
+  const uint64_t local_end = geo.elem0 + geo.n_local;
+  s.lo = s.chunk_lo > geo.elem0 ? s.chunk_lo : geo.elem0;
+  s.hi = chunk_hi < local_end ? chunk_hi : local_end;
+  return s;
+}
+
 template <typename T> struct EVec;
 template <> struct EVec<double> { using V = double2; static constexpr int N = 2; };
 template <> struct EVec<float>  { using V = float4;  static constexpr int N = 4; };
 
 template <typename T>
-__device__ __forceinline__ void load_group(const T* __restrict__ p, bool vec, int ne, T (&v)[kGroup]) {
+__device__ __forceinline__ void load8(const T* __restrict__ p, T (&v)[kGroup]) {
   using V = typename EVec<T>::V;
   constexpr int VN = EVec<T>::N;
-  if (vec) {
 #pragma unroll
-    for (int q = 0; q < kGroup / VN; ++q) {
-      V w = __ldg(reinterpret_cast<const V*>(p) + q);
-      const T* t = reinterpret_cast<const T*>(&w);
+  for (int q = 0; q < kGroup / VN; ++q) {
+    V w = __ldg(reinterpret_cast<const V*>(p) + q);
+    const T* t = reinterpret_cast<const T*>(&w);
 #pragma unroll
-      for (int e = 0; e < VN; ++e) v[q * VN + e] = t[e];
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < kGroup; ++e) v[e] = (e < ne) ? __ldg(p + e) : T(0);
+    for (int e = 0; e < VN; ++e) v[q * VN + e] = t[e];
   }
 }
 
-struct EncodeGeom {
-  uint64_t n_local, elem0, n_total, epb, tpb, g0, ntiles, b0, stride;
-};
+// Per-element classification: returns the code (idx or sentinel).
+template <typename T>
+__device__ __forceinline__ uint32_t classify(T bt, T xt, const CutLut& finder, const double* __restrict__ centers,
+                                             double tol_bin, double tol, uint32_t sentinel) {
+  const double bd = to_f64(bt), xd = to_f64(xt);
+  // core.py:129-136: finite(r) already implies finite(b) and finite(x)
+  double r = __ddiv_rn(__dsub_rn(xd, bd), bd);
+  bool valid = finite64(r);
+  if (!valid) {
+    valid = (bd == 0.0 && xd == 0.0);
+    r = 0.0;
+  }
+  const uint32_t idx = finder.find(r);
+  const double c = __ldg(centers + idx);
+  const bool near = valid && (fabs(__dsub_rn(r, c)) <= tol_bin);
+  const bool rt = roundtrip_ok<T>(c, bd, xd, tol);   // branch-free
+  return (near && rt) ? idx : sentinel;
+}
 
 template <typename T, int B>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kEncThreads, 3)
 k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
-         double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ exact,
-         unsigned long long* __restrict__ prefix, unsigned long long* __restrict__ n_inc,
-         unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket) {
-  typedef cub::BlockScan<unsigned, kTileThreads> BScan;
-  __shared__ typename BScan::TempStorage scan_tmp;
-  __shared__ __align__(16) uint8_t tile_bytes[kTileThreads * B + 16];
-  __shared__ unsigned long long s_tile, s_excl;
-  extern __shared__ double smc[];
+         double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
+         uint32_t* __restrict__ counts) {
+  __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
+  __shared__ uint16_t lut[kLutCells];
+  __shared__ double s_lo, s_scale;
+  __shared__ bool s_use;
+  extern __shared__ __align__(16) double cuts_s[];
 
-  const int tid = threadIdx.x;
-  const bool in_smem = k <= kSmemCenters;
-  const double* C = centers_g;
-  const double* X = cuts_g;
-  if (in_smem) {
-    for (int i = tid; i < k; i += kTileThreads) smc[i] = centers_g[i];
-    for (int i = tid; i < k - 1; i += kTileThreads) smc[kSmemCenters + i] = cuts_g[i];
-    C = smc;
-    X = smc + kSmemCenters;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ncuts = k - 1;
+  const bool cuts_in_smem = k <= kSmemCuts + 1;
+  if (cuts_in_smem)
+    for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cuts_s[i] = cuts_g[i];
+  __syncthreads();
+  if (cuts_in_smem) {
+    double lo, sc;
+    bool use;
+    build_cut_lut(cuts_s, ncuts, lut, lo, sc, use);
+    if (threadIdx.x == 0) { s_lo = lo; s_scale = sc; s_use = use; }
+  } else if (threadIdx.x == 0) {
+    s_lo = 0.0; s_scale = 0.0; s_use = false;
   }
+  __syncthreads();
+  CutLut finder;
+  finder.cuts = cuts_in_smem ? cuts_s : cuts_g;
+  finder.lut = lut;
+  finder.ncuts = ncuts;
+  finder.lo = s_lo;
+  finder.scale = s_scale;
+  finder.use_lut = s_use;
   const uint32_t sentinel = (1u << B) - 1u;
   const uint64_t local_end = geo.elem0 + geo.n_local;
+  const bool ptr_al = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  uint8_t* my = wbytes[wid];
 
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint64_t t = s_tile;
-    if (t >= geo.ntiles) break;
-    const uint64_t g = geo.g0 + t;
-    const uint64_t b = g / geo.tpb, ti = g % geo.tpb;
-    const uint64_t blk_start = b * geo.epb;
-    uint64_t blk_end = blk_start + geo.epb;
-    if (blk_end > geo.n_total) blk_end = geo.n_total;
-    const uint64_t tile_lo = blk_start + ti * kTile;
-    const uint64_t grp_lo = tile_lo + (uint64_t)tid * kGroup;
-    // elements of this group inside [elem0, local_end) and inside the block
-    uint64_t hi = blk_end < local_end ? blk_end : local_end;
-    uint64_t lo = geo.elem0;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kEncThreads / 32);
+  for (uint64_t c = (uint64_t)blockIdx.x * (kEncThreads / 32) + wid; c < geo.nchunks; c += nwarps) {
+    const ChunkSpan sp = chunk_span(geo, c);
+    const uint64_t grp_lo = sp.chunk_lo + (uint64_t)lane * kGroup;
+    const bool full = sp.chunk_lo >= geo.elem0 && sp.chunk_lo + kChunk <= sp.blk_end &&
+                      sp.chunk_lo + kChunk <= local_end;  // warp-uniform
+    T bv[kGroup], xv[kGroup];
     uint32_t code[kGroup];
     unsigned inc_mask = 0;
-    T xv[kGroup];
-    {
-      T bv[kGroup];
-      bool full = grp_lo >= lo && grp_lo + kGroup <= hi;
-      int ne = 0;
-      uint64_t first = grp_lo;
-      if (full) {
-        ne = kGroup;
-      } else if (grp_lo + kGroup > lo && grp_lo < hi) {
-        // partial group: clamp to [lo, hi); out-of-range lanes get code 0
-        ne = -1;
-      }
-      if (ne == kGroup) {
-        const uint64_t li = first - geo.elem0;
-        constexpr int VN = EVec<T>::N;
-        bool vec = (li % VN == 0) && ((((uintptr_t)base | (uintptr_t)cur) & 15) == 0);
-        load_group<T>(base + li, vec, kGroup, bv);
-        load_group<T>(cur + li, vec, kGroup, xv);
-      } else {
-#pragma unroll
-        for (int e = 0; e < kGroup; ++e) {
-          uint64_t j = grp_lo + e;
-          bool in = (ne != 0) && j >= lo && j < hi;
-          bv[e] = in ? __ldg(base + (j - geo.elem0)) : T(0);
-          xv[e] = in ? __ldg(cur + (j - geo.elem0)) : T(0);
-        }
-      }
+    const int64_t li = (int64_t)grp_lo - (int64_t)geo.elem0;
+    constexpr int VN = EVec<T>::N;
+    if (full && ptr_al && (li % VN) == 0) {
+      load8<T>(base + li, bv);
+      load8<T>(cur + li, xv);
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
-        uint64_t j = grp_lo + e;
-        bool in = (ne == kGroup) || (ne != 0 && j >= lo && j < hi);
-        code[e] = 0;
-        if (!in) continue;
-        double bd = to_f64(bv[e]), xd = to_f64(xv[e]);
-        bool valid;
-        double r = change_ratio(bd, xd, valid);
-        uint32_t idx = lower_bound_cuts(X, k - 1, r);
-        double c = C[idx];
-        bool flag = valid && (fabs(__dsub_rn(r, c)) <= tol_bin);
-        if (flag) flag = roundtrip_ok<T>(c, bd, xd, tol);
-        code[e] = flag ? idx : sentinel;
-        if (!flag) inc_mask |= 1u << e;
+        code[e] = classify<T>(bv[e], xv[e], finder, centers_g, tol_bin, tol, sentinel);
+        inc_mask |= (code[e] == sentinel ? 1u : 0u) << e;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e) {
+        const uint64_t j = grp_lo + e;
+        const bool in = j >= sp.lo && j < sp.hi;
+        bv[e] = in ? __ldg(base + (li + e)) : T(0);
+        xv[e] = in ? __ldg(cur + (li + e)) : T(0);
+        code[e] = in ? classify<T>(bv[e], xv[e], finder, centers_g, tol_bin, tol, sentinel) : 0u;
+        inc_mask |= (in && code[e] == sentinel ? 1u : 0u) << e;
       }
     }
-    unsigned cnt = __popc(inc_mask), ex, agg;
-    BScan(scan_tmp).ExclusiveSum(cnt, ex, agg);
-    if (tid == 0) st_relaxed(status + t, (t == 0 ? kFlagInc : kFlagAgg) | agg);
-    pack8<B>(code, tile_bytes + tid * B);
-    __syncthreads();
-    // copy-out, clipped to this block's packed length
-    {
-      const uint64_t blk_bytes = ((blk_end - blk_start) * B + 7) / 8;
-      const uint64_t off = ti * (uint64_t)(kTileThreads * B);
-      uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
-      if (nbytes > (uint64_t)kTileThreads * B) nbytes = (uint64_t)kTileThreads * B;
-      uint8_t* dst = packed + (b - geo.b0) * geo.stride + off;
-      const uint32_t nvec = (uint32_t)(nbytes / 16);
-      for (uint32_t i = tid; i < nvec; i += kTileThreads)
-        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(tile_bytes)[i];
-      for (uint32_t i = nvec * 16 + tid; i < nbytes; i += kTileThreads) dst[i] = tile_bytes[i];
+    // warp-level compaction of the incompressible values into the chunk's
+    // scratch window (element order)
+    const unsigned cnt = __popc(inc_mask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    // look-back for the running incompressible count
-    if (tid < 32) {
-      unsigned long long excl = (t == 0) ? 0ULL : lookback(status, (long long)t, 0);
-      if (tid == 0) {
-        if (t != 0) st_relaxed(status + t, kFlagInc | (excl + agg));
-        s_excl = excl;
-      }
-    }
-    __syncthreads();
-    const unsigned long long excl = s_excl;
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
     if (inc_mask) {
-      unsigned long long pos = excl + ex;
+      T* w = scratch + c * kChunk + (incl - cnt);
 #pragma unroll
       for (int e = 0; e < kGroup; ++e)
-        if (inc_mask >> e & 1u) exact[pos++] = xv[e];   // raw bits (NaN payloads kept)
+        if (inc_mask >> e & 1u) *w++ = xv[e];   // raw bits (NaN payloads kept)
     }
-    if (tid == 0) {
-      if (ti == 0 && blk_start >= geo.elem0) prefix[b - geo.b0] = excl;
-      if (t == geo.ntiles - 1) *n_inc = excl + agg;
+    if (lane == 0) counts[c] = total;
+    // packed bytes: stage per warp, then 16-byte stores clipped to the block
+    pack8<B>(code, my + lane * B);
+    __syncwarp();
+    const uint64_t blk_bytes = ((sp.blk_end - sp.blk_start) * B + 7) / 8;
+    const uint64_t off = sp.ci * (uint64_t)(32 * B);
+    uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
+    if (nbytes > (uint64_t)(32 * B)) nbytes = 32 * B;
+    uint8_t* dst = packed + (sp.b - geo.b0) * geo.stride + off;
+    const uint32_t nvec = (uint32_t)(nbytes / 16);
+    for (uint32_t i = lane; i < nvec; i += 32)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(my)[i];
+    for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) dst[i] = my[i];
+    __syncwarp();
+  }
+}
+
+// Finalize: chunk offsets -> compacted exact list + per-block prefix.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsigned long long* __restrict__ offsets,
+               const T* __restrict__ scratch, T* __restrict__ exact, unsigned long long* __restrict__ prefix) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+  for (uint64_t c = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); c < geo.nchunks; c += nwarps) {
+    const unsigned n = counts[c];
+    const unsigned long long off = offsets[c];
+    for (unsigned i = lane; i < n; i += 32) exact[off + i] = scratch[c * kChunk + i];
+    if (lane == 0) {
+      const uint64_t g = geo.g0 + c;
+      const uint64_t b = g / geo.cpb;
+      if (g == b * geo.cpb && b * geo.epb >= geo.elem0) prefix[b - geo.b0] = off;
     }
-    // next iteration's ticket write to s_tile is ordered by its __syncthreads
   }
 }
 
@@ -307,53 +339,68 @@ static int sm_count_e() {
   return sms;
 }
 
-struct EncodeTiles {
-  uint64_t b0, tpb, g0, ntiles;
+struct EncodeChunks {
+  uint64_t b0, cpb, g0, nchunks;
 };
 
-static EncodeTiles encode_tiles(uint64_t n_local, uint64_t elem0, uint64_t epb) {
-  EncodeTiles et{};
+static EncodeChunks encode_chunks(uint64_t n_local, uint64_t elem0, uint64_t epb) {
+  EncodeChunks et{};
   if (n_local == 0 || epb == 0) return et;
-  et.tpb = (epb + kTile - 1) / kTile;
+  et.cpb = (epb + kChunk - 1) / kChunk;
   uint64_t last = elem0 + n_local - 1;
   uint64_t b0 = elem0 / epb, b1 = last / epb;
-  uint64_t t0 = (elem0 - b0 * epb) / kTile, t1 = (last - b1 * epb) / kTile;
+  uint64_t c0 = (elem0 - b0 * epb) / kChunk, c1 = (last - b1 * epb) / kChunk;
   et.b0 = b0;
-  et.g0 = b0 * et.tpb + t0;
-  et.ntiles = (b1 * et.tpb + t1) - et.g0 + 1;
+  et.g0 = b0 * et.cpb + c0;
+  et.nchunks = (b1 * et.cpb + c1) - et.g0 + 1;
   return et;
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// workspace: counts u32[nchunks] | offsets u64[nchunks] | total | scan ws | scratch T[nchunks*256]
+struct EncodeWs {
+  size_t off_counts, off_offsets, off_total, off_scan, off_scratch, total;
+};
+
+static EncodeWs encode_ws_layout(uint64_t nchunks, int elem_bytes) {
+  EncodeWs w{};
+  w.off_counts = 0;
+  w.off_offsets = al256(nchunks * 4);
+  w.off_total = w.off_offsets + al256(nchunks * 8);
+  w.off_scan = w.off_total + 256;
+  w.off_scratch = w.off_scan + al256(chunk_scan_ws_bytes(nchunks));
+  w.total = w.off_scratch + al256(nchunks * kChunk * (size_t)elem_bytes);
+  return w;
 }
 
 template <typename T, int B>
 static void launch_encode(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
-                          const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* exact,
-                          unsigned long long* prefix, unsigned long long* n_inc, unsigned long long* status,
-                          unsigned* ticket, cudaStream_t s) {
-  size_t smem = (k <= kSmemCenters) ? 2 * kSmemCenters * sizeof(double) : 0;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_encode<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(2 * kSmemCenters * sizeof(double)));
-    attr_set = true;
+                          const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
+                          uint32_t* counts, cudaStream_t s) {
+  const size_t smem = (k <= kSmemCuts + 1 && k > 1) ? (size_t)(k - 1) * 8 : 0;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_encode<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode<T, B>, kTileThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode<T, B>, kEncThreads, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)sm_count_e() * per_sm;
-  if (grid > geo.ntiles) grid = geo.ntiles;
-  k_encode<T, B><<<(unsigned)grid, kTileThreads, smem, s>>>((const T*)base, (const T*)cur, geo, centers, cuts, k,
-                                                            tol_bin, tol, packed, (T*)exact, prefix, n_inc,
-                                                            status, ticket);
+  uint64_t need = (geo.nchunks + 7) / 8;
+  if (grid > need) grid = need;
+  k_encode<T, B><<<(unsigned)grid, kEncThreads, smem, s>>>((const T*)base, (const T*)cur, geo, centers, cuts, k,
+                                                           tol_bin, tol, packed, (T*)scratch, counts);
 }
 
 template <typename T>
 static int dispatch_encode(int bits, const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
-                           const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* exact,
-                           unsigned long long* prefix, unsigned long long* n_inc, unsigned long long* status,
-                           unsigned* ticket, cudaStream_t s) {
+                           const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
+                           uint32_t* counts, cudaStream_t s) {
   switch (bits) {
 #define NMK_ENC_CASE(BB) \
-  case BB: launch_encode<T, BB>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, exact, prefix, n_inc, status, ticket, s); break;
+  case BB: launch_encode<T, BB>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, s); break;
     NMK_ENC_CASE(2) NMK_ENC_CASE(3) NMK_ENC_CASE(4) NMK_ENC_CASE(5) NMK_ENC_CASE(6) NMK_ENC_CASE(7)
     NMK_ENC_CASE(8) NMK_ENC_CASE(9) NMK_ENC_CASE(10) NMK_ENC_CASE(11) NMK_ENC_CASE(12) NMK_ENC_CASE(13)
     NMK_ENC_CASE(14) NMK_ENC_CASE(15) NMK_ENC_CASE(16) NMK_ENC_CASE(17) NMK_ENC_CASE(18) NMK_ENC_CASE(19)
@@ -369,9 +416,9 @@ static int dispatch_encode(int bits, const void* base, const void* cur, const En
 
 using namespace nmk;
 
-extern "C" size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t epb) {
-  EncodeTiles et = encode_tiles(n_local, elem0, epb);
-  return 256 + (size_t)(et.ntiles + 1) * sizeof(unsigned long long);
+extern "C" size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t epb, int dtype) {
+  EncodeChunks et = encode_chunks(n_local, elem0, epb);
+  return encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8).total;
 }
 
 extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
@@ -386,6 +433,7 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
   }
   if (!base || !cur || !centers || !packed || !exact || !prefix || !n_inc || !ws || k < 1)
     return set_error(NMK_ERR_ARG, "nmk_encode: bad argument");
+  if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_encode: bad dtype");
   if (k > 1 && !cuts) return set_error(NMK_ERR_ARG, "nmk_encode: cuts required for k > 1");
   if (bits < 2 || bits > 30) return set_error(NMK_ERR_ARG, "nmk_encode: bits %d outside [2, 30]", bits);
   if ((uint64_t)k > (1ULL << bits) - 1) return set_error(NMK_ERR_ARG, "nmk_encode: k %d exceeds 2^B-1", k);
@@ -393,27 +441,37 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
   if (block_stride % 16 || block_stride < (epb * bits + 7) / 8)
     return set_error(NMK_ERR_ARG, "nmk_encode: block_stride must be >= ceil(epb*B/8) and a multiple of 16");
   if ((uintptr_t)packed & 15) return set_error(NMK_ERR_ARG, "nmk_encode: packed must be 16-byte aligned");
-  if (ws_bytes < nmk_encode_ws_bytes(n_local, elem0, epb)) return set_error(NMK_ERR_ARG, "nmk_encode: workspace too small");
-  EncodeTiles et = encode_tiles(n_local, elem0, epb);
-  EncodeGeom geo{n_local, elem0, n_total, epb, et.tpb, et.g0, et.ntiles, et.b0, block_stride};
-  unsigned* ticket = (unsigned*)ws;
-  unsigned long long* status = (unsigned long long*)((char*)ws + 256);
-  cudaMemsetAsync(ws, 0, nmk_encode_ws_bytes(n_local, elem0, epb), s);
-  // A range starting inside a block: zero the packed bytes of the tiles in
+  const size_t need = nmk_encode_ws_bytes(n_local, elem0, epb, dtype);
+  if (ws_bytes < need) return set_error(NMK_ERR_ARG, "nmk_encode: workspace too small");
+  EncodeChunks et = encode_chunks(n_local, elem0, epb);
+  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride};
+  EncodeWs w = encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8);
+  char* wb = (char*)ws;
+  uint32_t* counts = (uint32_t*)(wb + w.off_counts);
+  unsigned long long* offsets = (unsigned long long*)(wb + w.off_offsets);
+  void* scratch = wb + w.off_scratch;
+  // A range starting inside a block: zero the packed bytes of the chunks in
   // front of it so they decode as non-sentinel codes and OR-merge neutrally.
-  const uint64_t t0_in_blk = (elem0 - et.b0 * epb) / kTile;
-  if (t0_in_blk) cudaMemsetAsync(packed, 0, t0_in_blk * (uint64_t)kTileThreads * bits, s);
+  const uint64_t c0_in_blk = (elem0 - et.b0 * epb) / kChunk;
+  if (c0_in_blk) cudaMemsetAsync(packed, 0, c0_in_blk * (uint64_t)(32 * bits), s);
+  int rc = (dtype == NMK_F64)
+               ? dispatch_encode<double>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
+                                         scratch, counts, s)
+               : dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
+                                        scratch, counts, s);
+  if (rc) return rc;
+  chunk_scan(counts, et.nchunks, offsets, n_inc, wb + w.off_scan, s);
+  unsigned grid = (unsigned)((et.nchunks + 7) / 8);
+  if (grid > (unsigned)sm_count_e() * 8) grid = sm_count_e() * 8;
   if (dtype == NMK_F64)
-    return dispatch_encode<double>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed, exact, prefix,
-                                   n_inc, status, ticket, s);
-  if (dtype == NMK_F32)
-    return dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed, exact, prefix,
-                                  n_inc, status, ticket, s);
-  return set_error(NMK_ERR_ARG, "nmk_encode: bad dtype");
+    k_enc_finalize<double><<<grid, 256, 0, s>>>(geo, counts, offsets, (const double*)scratch, (double*)exact, prefix);
+  else
+    k_enc_finalize<float><<<grid, 256, 0, s>>>(geo, counts, offsets, (const float*)scratch, (float*)exact, prefix);
+  return check_launch("k_enc_finalize");
 }
 
 template <int B>
-static void launch_pack(const uint32_t* codes, uint64_t n, uint8_t* out, uint8_t* unused, cudaStream_t s, bool unpack,
+static void launch_pack(const uint32_t* codes, uint64_t n, uint8_t* out, cudaStream_t s, bool unpack,
                         const uint8_t* in, uint32_t* codes_out) {
   uint64_t ngrp = (n + kGroup - 1) / kGroup;
   unsigned grid = (unsigned)((ngrp + 255) / 256);
@@ -426,7 +484,7 @@ static void launch_pack(const uint32_t* codes, uint64_t n, uint8_t* out, uint8_t
 static int dispatch_pack(int bits, bool unpack, const uint32_t* codes, uint64_t n, uint8_t* out, const uint8_t* in,
                          uint32_t* codes_out, cudaStream_t s) {
   switch (bits) {
-#define NMK_PK_CASE(BB) case BB: launch_pack<BB>(codes, n, out, nullptr, s, unpack, in, codes_out); break;
+#define NMK_PK_CASE(BB) case BB: launch_pack<BB>(codes, n, out, s, unpack, in, codes_out); break;
     NMK_PK_CASE(2) NMK_PK_CASE(3) NMK_PK_CASE(4) NMK_PK_CASE(5) NMK_PK_CASE(6) NMK_PK_CASE(7) NMK_PK_CASE(8)
     NMK_PK_CASE(9) NMK_PK_CASE(10) NMK_PK_CASE(11) NMK_PK_CASE(12) NMK_PK_CASE(13) NMK_PK_CASE(14)
     NMK_PK_CASE(15) NMK_PK_CASE(16) NMK_PK_CASE(17) NMK_PK_CASE(18) NMK_PK_CASE(19) NMK_PK_CASE(20)

@@ -87,8 +87,10 @@ __device__ __forceinline__ void for_each_ratio(const T* __restrict__ base, const
 }
 
 // counts[nbins] is an out-of-range tripwire (must stay 0).
+constexpr int kHistThreads = 256;
+
 template <typename T>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(kHistThreads, 4)
 k_hist_smem(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
             const nmk_stats* __restrict__ st, double width, uint32_t nbins, int reps,
             unsigned long long* __restrict__ counts, bool vec_ok) {
@@ -341,7 +343,7 @@ extern "C" int nmk_hist_dense(const void* base, const void* cur, uint64_t n, int
     // replicas: one private copy per warp when it fits in ~48 KB, at least 1
     size_t one = nbins * 4;
     int reps = (int)((48 * 1024) / one);
-    if (reps > 16) reps = 16;
+    if (reps > kHistThreads / 32) reps = kHistThreads / 32;
     if (reps < 1) reps = 1;
     size_t smem = one * reps;
     int per_sm = (int)((220 * 1024) / (smem + 1024));
@@ -352,11 +354,11 @@ extern "C" int nmk_hist_dense(const void* base, const void* cur, uint64_t n, int
     if (want < grid) grid = want ? want : 1;
     if (dtype == NMK_F64) {
       if (smem > 48 * 1024) cudaFuncSetAttribute(k_hist_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_hist_smem<double><<<(unsigned)grid, 512, smem, s>>>((const double*)base, (const double*)cur, n, stats,
+      k_hist_smem<double><<<(unsigned)grid, kHistThreads, smem, s>>>((const double*)base, (const double*)cur, n, stats,
                                                              width, (uint32_t)nbins, reps, counts, aligned);
     } else {
       if (smem > 48 * 1024) cudaFuncSetAttribute(k_hist_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_hist_smem<float><<<(unsigned)grid, 512, smem, s>>>((const float*)base, (const float*)cur, n, stats,
+      k_hist_smem<float><<<(unsigned)grid, kHistThreads, smem, s>>>((const float*)base, (const float*)cur, n, stats,
                                                            width, (uint32_t)nbins, reps, counts, aligned);
     }
     return check_launch("k_hist_smem");

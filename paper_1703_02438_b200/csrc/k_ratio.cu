@@ -45,7 +45,7 @@ __device__ __forceinline__ void vec_get(const float4& v, double* o) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kMinmaxThreads)
+__global__ void __launch_bounds__(kMinmaxThreads, 4)
 k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
          MinMax* __restrict__ partials, unsigned int* __restrict__ ticket,
          nmk_stats* __restrict__ out, bool vec_ok) {

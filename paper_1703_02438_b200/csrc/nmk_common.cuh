@@ -82,6 +82,116 @@ __device__ __forceinline__ uint32_t lower_bound_cuts(const double* cuts, int ncu
   return (uint32_t)lo;
 }
 
+// ---- O(1) nearest-center search -------------------------------------------
+// A uniform grid of kLutCells cells over [cuts[0], cuts[ncuts-1]] stores, per
+// cell, #cuts below the cell's left edge.  The cell of r gives a starting
+// guess; two exact compare loops then land on #cuts < r.  The answer is
+// exact whatever the rounding of the cell computation (monotone cuts), the
+// grid only makes it O(1) on average.
+constexpr int kLutCells = 4096;
+
+struct CutLut {
+  const double* cuts;      // shared memory
+  const uint16_t* lut;     // shared memory, kLutCells entries
+  int ncuts;
+  double lo, scale;
+  bool use_lut;
+
+  __device__ __forceinline__ uint32_t find(double r) const {
+    if (!use_lut) return lower_bound_cuts(cuts, ncuts, r);
+    double f = (r - lo) * scale;
+    f = fmin(fmax(f, 0.0), (double)(kLutCells - 1));
+    int i = lut[(int)f];
+    while (i < ncuts && cuts[i] < r) ++i;
+    while (i > 0 && cuts[i - 1] >= r) --i;
+    return (uint32_t)i;
+  }
+};
+
+// Build the grid over `ncuts` cuts already in shared memory (all threads).
+__device__ __forceinline__ void build_cut_lut(const double* cuts, int ncuts, uint16_t* lut, double& lo,
+                                              double& scale, bool& use) {
+  use = false;
+  lo = 0.0;
+  scale = 0.0;
+  if (ncuts >= 2 && ncuts < 65535) {
+    double a = cuts[0], z = cuts[ncuts - 1];
+    double sc = (double)kLutCells / (z - a);
+    if (z > a && finite64(a) && finite64(z) && finite64(sc) && sc > 0.0) {
+      use = true;
+      lo = a;
+      scale = sc;
+      for (int g = threadIdx.x; g < kLutCells; g += blockDim.x) {
+        double edge = a + (double)g / sc;
+        lut[g] = (uint16_t)lower_bound_cuts(cuts, ncuts, edge);
+      }
+    }
+  }
+}
+
+// ---- cp.async (LDGSTS) helpers ---------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+// 4/8-byte copy with zero fill when !valid (src-size 0 reads nothing)
+template <int N>
+__device__ __forceinline__ void cp_async_zfill(void* s, const void* g, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(s)), "l"(g), "n"(N),
+               "r"(valid ? N : 0) : "memory");
+}
+// 4-byte slot filled with the first `have` (0..4) source bytes, rest zero
+__device__ __forceinline__ void cp_async_bytes4(void* s, const void* g, int have) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(s)), "l"(g), "r"(have) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Element stage: thread t's 8 consecutive elements at t*kRow(T) bytes, a row
+// padded by 16 bytes so 128-bit shared loads of 8 threads hit distinct banks.
+template <typename T> struct Stage {
+  static constexpr int kRow = kGroup * (int)sizeof(T) + 16;        // 80 (f64) / 48 (f32)
+  static constexpr int kBytes = kTileThreads * kRow;               // one array of a tile
+  __device__ __forceinline__ static int off(int e) {               // element e of the tile
+    return (e / kGroup) * kRow + (e % kGroup) * (int)sizeof(T);
+  }
+};
+
+// Issue the loads of `src[li0 .. li0 + cnt)` (tile elements e0 .. e0 + cnt)
+// into a Stage array.  Fast path: whole tile, 16-byte aligned.
+template <typename T>
+__device__ __forceinline__ void stage_tile(unsigned char* stage, const T* __restrict__ src, int64_t li_first,
+                                           int e0, int cnt) {
+  constexpr int VN = 16 / (int)sizeof(T);
+  const T* g = src + li_first;  // element e of the tile lives at g[e]
+  if (e0 == 0 && cnt == kTile && (((uintptr_t)g) & 15) == 0) {
+#pragma unroll
+    for (int m = 0; m < kTile / VN / kTileThreads; ++m) {
+      int c = threadIdx.x + m * kTileThreads;   // 16-byte chunk
+      cp_async16(stage + Stage<T>::off(c * VN), g + c * VN);
+    }
+  } else {
+    for (int e = threadIdx.x; e < kTile; e += kTileThreads) {
+      bool ok = e >= e0 && e < e0 + cnt;
+      cp_async_zfill<(int)sizeof(T)>(stage + Stage<T>::off(e), ok ? (const void*)(g + e) : (const void*)src, ok);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void unstage_group(const unsigned char* stage, T (&v)[kGroup]) {
+  const unsigned char* row = stage + threadIdx.x * Stage<T>::kRow;
+#pragma unroll
+  for (int q = 0; q < (int)(kGroup * sizeof(T)) / 16; ++q) {
+    uint4 w = *reinterpret_cast<const uint4*>(row + 16 * q);
+    const T* tw = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int e = 0; e < 16 / (int)sizeof(T); ++e) v[q * (16 / (int)sizeof(T)) + e] = tw[e];
+  }
+}
+
 // ---- relaxed 64-bit status words for decoupled look-back ------------------
 __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

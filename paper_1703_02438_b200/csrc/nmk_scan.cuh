@@ -1,0 +1,12 @@
+// nmk_scan.cuh — host launcher of the chunk-count scan (k_scan.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nmk {
+// offsets[i] = sum(counts[0..i)), *total = sum(counts) (total may be null).
+size_t chunk_scan_ws_bytes(uint64_t n);
+void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets, unsigned long long* total,
+                void* ws, cudaStream_t s);
+}  // namespace nmk

@@ -298,7 +298,7 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
     prefix.zero_()
     n_inc_t = ws.typed("n_inc", 1, torch.int64)
     if n_local > 0:
-        e_bytes = lib.nmk_encode_ws_bytes(n_local, elem0, epb)
+        e_bytes = lib.nmk_encode_ws_bytes(n_local, elem0, epb, dt)
         e_ws = ws.get("encode_ws", e_bytes)
         N.check(lib.nmk_encode(_p(base), _p(cur), n_local, elem0, n, dt, _p(centers), _p(cuts), k, B,
                                float(model.tol_bin), float(tolerance), epb, _p(packed), stride, _p(exact),
@@ -348,7 +348,7 @@ def decode(packed, stride: int, first_block: int, bits: int, epb: int, n_total: 
     if out is None:
         out = torch.empty(total_out, dtype=base.dtype, device=base.device)
     k = centers.numel()
-    d_bytes = lib.nmk_decode_ws_bytes(s_start, s_count, nseg, epb)
+    d_bytes = lib.nmk_decode_ws_bytes(s_start, s_count, nseg, epb, first_block)
     d_ws = ws.get("decode_ws", d_bytes)
     info = ws.typed("seg_info", 2 * nseg, torch.int64)
     err = ws.typed("decode_err", 2, torch.int64)

@@ -41,7 +41,7 @@ def test_struct_sizes_match_header():
 def test_workspace_queries_need_no_device():
     lib = N.load()
     assert lib.nmk_minmax_ws_bytes(1 << 20) > 0
-    assert lib.nmk_encode_ws_bytes(1 << 20, 0, 1 << 20) >= 8 * 512
+    assert lib.nmk_encode_ws_bytes(1 << 20, 0, 1 << 20, N.NMK_F64) >= 8 * (1 << 20)
     assert lib.nmk_hist_sparse_ws_bytes(1000) > 3 * 8 * 1000
 
 
