@@ -23,25 +23,6 @@ namespace nmk {
 
 constexpr int kDChunk = 32 * kGroup;   // 256 elements per warp chunk
 constexpr int kDecThreads = 256;
-constexpr int kSmemCenters = 4096;     // centers in shared memory up to this k
-
-template <int B>
-__device__ __forceinline__ void unpack8d(const uint8_t* src, uint32_t (&code)[kGroup]) {
-  unsigned long long acc = 0;
-  int nacc = 0, bi = 0;
-#pragma unroll
-  for (int e = 0; e < kGroup; ++e) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (nacc < B) {
-        acc = (acc << 8) | src[bi++];
-        nacc += 8;
-      }
-    }
-    code[e] = (uint32_t)(acc >> (nacc - B)) & ((1u << B) - 1u);
-    nacc -= B;
-  }
-}
 
 struct Seg {
   uint64_t start, count, out;   // global element range, output offset
@@ -72,45 +53,84 @@ __device__ __forceinline__ DChunk dchunk(const DecodeGeom& geo, uint64_t g) {
   return d;
 }
 
-// Stage one chunk's 32*B packed bytes into warp-private shared memory
-// (zero beyond the block's byte length).
+// Packed-byte span of a chunk: base pointer and valid byte count (bytes at
+// or beyond it are padding and decode as zero bits).
+struct ChunkBytes {
+  const uint8_t* src;
+  uint32_t nbytes;
+};
+
 template <int B>
-__device__ __forceinline__ void stage_chunk_bytes(const uint8_t* __restrict__ packed, const DecodeGeom& geo,
-                                                  const DChunk& d, uint8_t* my, int lane) {
+__device__ __forceinline__ ChunkBytes chunk_bytes(const uint8_t* __restrict__ packed, const DecodeGeom& geo,
+                                                  const DChunk& d) {
   const uint64_t blk_bytes = ((d.blk_end - d.blk_start) * B + 7) / 8;
   const uint64_t off = d.ci * (uint64_t)(32 * B);
   uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
   if (nbytes > (uint64_t)(32 * B)) nbytes = 32 * B;
-  const uint8_t* src = packed + (d.b - geo.first_block) * geo.stride + off;
-  const uint32_t nvec = (uint32_t)(nbytes / 16);
-  for (uint32_t i = lane; i < (uint32_t)(2 * B); i += 32)   // 32*B/16 = 2B vectors
-    reinterpret_cast<uint4*>(my)[i] = (i < nvec) ? __ldg(reinterpret_cast<const uint4*>(src) + i)
-                                                 : make_uint4(0, 0, 0, 0);
-  __syncwarp();
-  for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) my[i] = __ldg(src + i);
-  __syncwarp();
+  return ChunkBytes{packed + (d.b - geo.first_block) * geo.stride + off, (uint32_t)nbytes};
+}
+
+// This lane's B bytes (offset lane*B of a 16-byte aligned chunk) with the
+// widest aligned loads B allows; the chunk's last lanes may be clipped.
+template <int B>
+__device__ __forceinline__ void lane_bytes(const ChunkBytes& cb, int lane, uint8_t (&o)[B]) {
+  const uint32_t s0 = (uint32_t)lane * B;
+  constexpr int W = (B % 8 == 0) ? 8 : (B % 4 == 0) ? 4 : (B % 2 == 0) ? 2 : 1;
+  if (s0 + B <= cb.nbytes) {
+#pragma unroll
+    for (int w = 0; w < B / W; ++w) {
+      const uint8_t* p = cb.src + s0 + w * W;
+      unsigned long long v;
+      if constexpr (W == 8) v = __ldg(reinterpret_cast<const unsigned long long*>(p));
+      else if constexpr (W == 4) v = __ldg(reinterpret_cast<const unsigned int*>(p));
+      else if constexpr (W == 2) v = __ldg(reinterpret_cast<const unsigned short*>(p));
+      else v = __ldg(p);
+#pragma unroll
+      for (int i = 0; i < W; ++i) o[w * W + i] = (uint8_t)(v >> (8 * i));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < B; ++i) o[i] = (s0 + i < cb.nbytes) ? __ldg(cb.src + s0 + i) : (uint8_t)0;
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void codes_of(const uint8_t (&src)[B], uint32_t (&code)[kGroup]) {
+  unsigned long long acc = 0;
+  int nacc = 0, bi = 0;
+#pragma unroll
+  for (int e = 0; e < kGroup; ++e) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (nacc < B) {
+        acc = (acc << 8) | src[bi++];
+        nacc += 8;
+      }
+    }
+    code[e] = (uint32_t)(acc >> (nacc - B)) & ((1u << B) - 1u);
+    nacc -= B;
+  }
 }
 
 template <int B>
 __global__ void __launch_bounds__(kDecThreads)
 k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
-  __shared__ __align__(16) uint8_t wbytes[kDecThreads / 32][32 * B + 16];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t sentinel = (1u << B) - 1u;
   const uint64_t nwarps = (uint64_t)gridDim.x * (kDecThreads / 32);
   const uint64_t g0 = geo.first_block * geo.cpb;
   for (uint64_t c = (uint64_t)blockIdx.x * (kDecThreads / 32) + wid; c < geo.nchunks; c += nwarps) {
     const DChunk d = dchunk(geo, g0 + c);
-    stage_chunk_bytes<B>(packed, geo, d, wbytes[wid], lane);
+    uint8_t raw[B];
+    lane_bytes<B>(chunk_bytes<B>(packed, geo, d), lane, raw);
     uint32_t code[kGroup];
-    unpack8d<B>(wbytes[wid] + lane * B, code);
+    codes_of<B>(raw, code);
     const uint64_t grp_lo = d.chunk_lo + (uint64_t)lane * kGroup;
     unsigned n = 0;
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) n += (grp_lo + e < d.chunk_hi && code[e] == sentinel);
     n = __reduce_add_sync(0xffffffffu, n);
     if (lane == 0) counts[c] = n;
-    __syncwarp();
   }
 }
 
@@ -119,20 +139,13 @@ template <> struct DVec<double> { using V = double2; static constexpr int N = 2;
 template <> struct DVec<float>  { using V = float4;  static constexpr int N = 4; };
 
 template <typename T, int B>
-__global__ void __launch_bounds__(kDecThreads)
+__global__ void __launch_bounds__(kDecThreads, 3)
 k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs,
              const unsigned long long* __restrict__ offsets, const unsigned long long* __restrict__ prefix_rel,
              const double* __restrict__ centers_g, const T* __restrict__ exact, const T* __restrict__ base,
              T* __restrict__ out, nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err) {
-  __shared__ __align__(16) uint8_t wbytes[kDecThreads / 32][32 * B + 16];
-  extern __shared__ double centers_s[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int k = geo.k;
-  const bool c_smem = k <= kSmemCenters;
-  if (c_smem)
-    for (int i = threadIdx.x; i < k; i += kDecThreads) centers_s[i] = centers_g[i];
-  __syncthreads();
-  const double* C = c_smem ? centers_s : centers_g;
   const uint32_t sentinel = (1u << B) - 1u;
   constexpr int VN = DVec<T>::N;
   using V = typename DVec<T>::V;
@@ -148,33 +161,14 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     const Seg sg = segs[lo_s];
     const uint64_t g = sg.gfirst + (it - sg.item0);
     const DChunk d = dchunk(geo, g);
-    stage_chunk_bytes<B>(packed, geo, d, wbytes[wid], lane);
-    uint32_t code[kGroup];
-    unpack8d<B>(wbytes[wid] + lane * B, code);
     const uint64_t seg_lo = sg.start, seg_hi = sg.start + sg.count;
     const uint64_t grp_lo = d.chunk_lo + (uint64_t)lane * kGroup;
-    unsigned smask = 0, inmask = 0, ahead = 0;
+    // base values first (independent of the codes), then the packed bytes
+    unsigned inmask = 0;
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) {
       const uint64_t j = grp_lo + e;
-      const bool inblk = j < d.chunk_hi;
-      if (inblk && code[e] == sentinel) {
-        smask |= 1u << e;
-        if (j < seg_lo) ++ahead;
-      }
-      if (inblk && j >= seg_lo && j < seg_hi) inmask |= 1u << e;
-    }
-    // rank of this lane's first sentinel, anchored like the reference on the
-    // prefix entry of the segment's FIRST block and counted from there
-    // (codec.py:231-236): prefix + chunk offset + warp exclusive scan
-    const uint64_t ab = sg.gfirst / geo.cpb - geo.first_block;
-    const unsigned long long chunk_off = prefix_rel[ab] + (offsets[d.crel] - offsets[ab * geo.cpb]);
-    const unsigned cnt = __popc(smask);
-    unsigned incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      if (j < d.chunk_hi && j >= seg_lo && j < seg_hi) inmask |= 1u << e;
     }
     T bv[kGroup], ov[kGroup];
     const int64_t oi = (int64_t)sg.out + ((int64_t)grp_lo - (int64_t)seg_lo);
@@ -190,6 +184,31 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     } else {
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) bv[e] = (inmask >> e & 1u) ? __ldg(base + (oi + e)) : T(0);
+    }
+    uint8_t raw[B];
+    lane_bytes<B>(chunk_bytes<B>(packed, geo, d), lane, raw);
+    uint32_t code[kGroup];
+    codes_of<B>(raw, code);
+    unsigned smask = 0, ahead = 0;
+#pragma unroll
+    for (int e = 0; e < kGroup; ++e) {
+      const uint64_t j = grp_lo + e;
+      if (j < d.chunk_hi && code[e] == sentinel) {
+        smask |= 1u << e;
+        if (j < seg_lo) ++ahead;
+      }
+    }
+    // rank of this lane's first sentinel, anchored like the reference on the
+    // prefix entry of the segment's FIRST block and counted from there
+    // (codec.py:231-236): prefix + chunk offset + warp exclusive scan
+    const uint64_t ab = sg.gfirst / geo.cpb - geo.first_block;
+    const unsigned long long chunk_off = prefix_rel[ab] + (offsets[d.crel] - offsets[ab * geo.cpb]);
+    const unsigned cnt = __popc(smask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
     unsigned long long pos = chunk_off + (incl - cnt);
     unsigned bad = 0, maxbad = 0, exhausted = 0;
@@ -207,7 +226,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
           bad = 1;
           maxbad = code[e] > maxbad ? code[e] : maxbad;
         } else {
-          ov[e] = apply_center<T>(C[code[e]], to_f64(bv[e]));
+          ov[e] = apply_center<T>(__ldg(centers_g + code[e]), to_f64(bv[e]));   // L1-resident table
         }
       }
     }
@@ -287,12 +306,7 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
   k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   chunk_scan(counts, geo.nchunks, offsets, nullptr, scan_ws, s);
-  const size_t smem = (geo.k <= kSmemCenters) ? (size_t)geo.k * 8 : 0;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_dec_chunks<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  const size_t smem = 0;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B>, kDecThreads, smem);
   if (per_sm < 1) per_sm = 1;

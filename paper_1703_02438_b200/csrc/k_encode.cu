@@ -125,8 +125,8 @@ __device__ __forceinline__ void load8(const T* __restrict__ p, T (&v)[kGroup]) {
 }
 
 // Per-element classification: returns the code (idx or sentinel).
-template <typename T>
-__device__ __forceinline__ uint32_t classify(T bt, T xt, const CutLut& finder, const double* __restrict__ centers,
+template <typename T, typename Find>
+__device__ __forceinline__ uint32_t classify(T bt, T xt, Find&& find, const double* __restrict__ centers,
                                              double tol_bin, double tol, uint32_t sentinel) {
   const double bd = to_f64(bt), xd = to_f64(xt);
   // core.py:129-136: finite(r) already implies finite(b) and finite(x)
@@ -136,58 +136,36 @@ __device__ __forceinline__ uint32_t classify(T bt, T xt, const CutLut& finder, c
     valid = (bd == 0.0 && xd == 0.0);
     r = 0.0;
   }
-  const uint32_t idx = finder.find(r);
+  const uint32_t idx = find(r);
   const double c = __ldg(centers + idx);
   const bool near = valid && (fabs(__dsub_rn(r, c)) <= tol_bin);
   const bool rt = roundtrip_ok<T>(c, bd, xd, tol);   // branch-free
   return (near && rt) ? idx : sentinel;
 }
 
-template <typename T, int B>
-__global__ void __launch_bounds__(kEncThreads, 3)
-k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
-         const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
-         double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
-         uint32_t* __restrict__ counts) {
-  __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
-  __shared__ uint16_t lut[kLutCells];
-  __shared__ double s_lo, s_scale;
-  __shared__ bool s_use;
-  extern __shared__ __align__(16) double cuts_s[];
-
+// The chunk loop, instantiated once per nearest-center search flavour.
+template <typename T, int B, typename Find>
+__device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const T* __restrict__ cur,
+                                              const EncodeGeom& geo, const double* __restrict__ centers_g,
+                                              double tol_bin, double tol, uint8_t* __restrict__ packed,
+                                              T* __restrict__ scratch, uint32_t* __restrict__ counts,
+                                              uint8_t* my, Find&& find) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int ncuts = k - 1;
-  const bool cuts_in_smem = k <= kSmemCuts + 1;
-  if (cuts_in_smem)
-    for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cuts_s[i] = cuts_g[i];
-  __syncthreads();
-  if (cuts_in_smem) {
-    double lo, sc;
-    bool use;
-    build_cut_lut(cuts_s, ncuts, lut, lo, sc, use);
-    if (threadIdx.x == 0) { s_lo = lo; s_scale = sc; s_use = use; }
-  } else if (threadIdx.x == 0) {
-    s_lo = 0.0; s_scale = 0.0; s_use = false;
-  }
-  __syncthreads();
-  CutLut finder;
-  finder.cuts = cuts_in_smem ? cuts_s : cuts_g;
-  finder.lut = lut;
-  finder.ncuts = ncuts;
-  finder.lo = s_lo;
-  finder.scale = s_scale;
-  finder.use_lut = s_use;
   const uint32_t sentinel = (1u << B) - 1u;
   const uint64_t local_end = geo.elem0 + geo.n_local;
   const bool ptr_al = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
-  uint8_t* my = wbytes[wid];
-
-  const uint64_t nwarps = (uint64_t)gridDim.x * (kEncThreads / 32);
-  for (uint64_t c = (uint64_t)blockIdx.x * (kEncThreads / 32) + wid; c < geo.nchunks; c += nwarps) {
-    const ChunkSpan sp = chunk_span(geo, c);
-    const uint64_t grp_lo = sp.chunk_lo + (uint64_t)lane * kGroup;
-    const bool full = sp.chunk_lo >= geo.elem0 && sp.chunk_lo + kChunk <= sp.blk_end &&
-                      sp.chunk_lo + kChunk <= local_end;  // warp-uniform
+  // chunk ids fit 32 bits (n < 2^40): cheap block / in-block split
+  const uint32_t cpb = (uint32_t)geo.cpb;
+  const uint32_t nw = gridDim.x * (kEncThreads / 32);
+  for (uint32_t c = blockIdx.x * (kEncThreads / 32) + wid; c < (uint32_t)geo.nchunks; c += nw) {
+    const uint32_t g = (uint32_t)geo.g0 + c;
+    const uint32_t b = g / cpb, ci = g - b * cpb;
+    const uint64_t blk_start = (uint64_t)b * geo.epb;
+    const uint64_t blk_end = min(blk_start + geo.epb, geo.n_total);
+    const uint64_t chunk_lo = blk_start + (uint64_t)ci * kChunk;
+    const uint64_t lo = max(chunk_lo, geo.elem0), hi = min(blk_end, local_end);
+    const uint64_t grp_lo = chunk_lo + (uint64_t)lane * kGroup;
+    const bool full = chunk_lo >= geo.elem0 && chunk_lo + kChunk <= hi;  // warp-uniform
     T bv[kGroup], xv[kGroup];
     uint32_t code[kGroup];
     unsigned inc_mask = 0;
@@ -198,17 +176,17 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
       load8<T>(cur + li, xv);
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
-        code[e] = classify<T>(bv[e], xv[e], finder, centers_g, tol_bin, tol, sentinel);
+        code[e] = classify<T>(bv[e], xv[e], find, centers_g, tol_bin, tol, sentinel);
         inc_mask |= (code[e] == sentinel ? 1u : 0u) << e;
       }
     } else {
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
         const uint64_t j = grp_lo + e;
-        const bool in = j >= sp.lo && j < sp.hi;
+        const bool in = j >= lo && j < hi;
         bv[e] = in ? __ldg(base + (li + e)) : T(0);
         xv[e] = in ? __ldg(cur + (li + e)) : T(0);
-        code[e] = in ? classify<T>(bv[e], xv[e], finder, centers_g, tol_bin, tol, sentinel) : 0u;
+        code[e] = in ? classify<T>(bv[e], xv[e], find, centers_g, tol_bin, tol, sentinel) : 0u;
         inc_mask |= (in && code[e] == sentinel ? 1u : 0u) << e;
       }
     }
@@ -223,7 +201,7 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
     }
     const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
     if (inc_mask) {
-      T* w = scratch + c * kChunk + (incl - cnt);
+      T* w = scratch + (uint64_t)c * kChunk + (incl - cnt);
 #pragma unroll
       for (int e = 0; e < kGroup; ++e)
         if (inc_mask >> e & 1u) *w++ = xv[e];   // raw bits (NaN payloads kept)
@@ -232,16 +210,68 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
     // packed bytes: stage per warp, then 16-byte stores clipped to the block
     pack8<B>(code, my + lane * B);
     __syncwarp();
-    const uint64_t blk_bytes = ((sp.blk_end - sp.blk_start) * B + 7) / 8;
-    const uint64_t off = sp.ci * (uint64_t)(32 * B);
-    uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
-    if (nbytes > (uint64_t)(32 * B)) nbytes = 32 * B;
-    uint8_t* dst = packed + (sp.b - geo.b0) * geo.stride + off;
-    const uint32_t nvec = (uint32_t)(nbytes / 16);
+    const uint64_t blk_bytes = ((blk_end - blk_start) * B + 7) / 8;
+    const uint64_t off = (uint64_t)ci * (32 * B);
+    const uint32_t nbytes = (uint32_t)min(blk_bytes > off ? blk_bytes - off : 0, (uint64_t)(32 * B));
+    uint8_t* dst = packed + (uint64_t)(b - geo.b0) * geo.stride + off;
+    const uint32_t nvec = nbytes / 16;
     for (uint32_t i = lane; i < nvec; i += 32)
       reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(my)[i];
     for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) dst[i] = my[i];
     __syncwarp();
+  }
+}
+
+template <typename T, int B>
+__global__ void __launch_bounds__(kEncThreads, 3)
+k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
+         const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
+         double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
+         uint32_t* __restrict__ counts) {
+  __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
+  __shared__ uint16_t lut[kLutCells];
+  __shared__ double s_lo, s_scale;
+  __shared__ bool s_use;
+  extern __shared__ __align__(16) double cuts_s[];
+
+  const int ncuts = k - 1;
+  const bool cuts_in_smem = k <= kSmemCuts + 1;
+  if (cuts_in_smem)
+    for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cuts_s[i] = cuts_g[i];
+  __syncthreads();
+  if (cuts_in_smem) {
+    double lo, sc;
+    bool use;
+    build_cut_lut(cuts_s, ncuts, lut, lo, sc, use);
+    if (threadIdx.x == 0) { s_lo = lo; s_scale = sc; s_use = use; }
+  } else if (threadIdx.x == 0) {
+    s_lo = 0.0; s_scale = 0.0; s_use = false;
+  }
+  __syncthreads();
+  uint8_t* my = wbytes[threadIdx.x >> 5];
+  if (s_use) {
+    // O(1) search: grid cell -> first candidate, exact compares against the
+    // shared-memory cuts settle it (normally zero or one step)
+    const double lo = s_lo, scale = s_scale;
+    encode_chunks<T, B>(base, cur, geo, centers_g, tol_bin, tol, packed, scratch, counts, my,
+                        [&](double r) -> uint32_t {
+                          int g = __double2int_rz((r - lo) * scale);   // saturating
+                          g = min(max(g, 0), kLutCells - 1);
+                          int i = lut[g];
+                          while (i < ncuts && cuts_s[i] < r) ++i;
+                          while (i > 0 && cuts_s[i - 1] >= r) --i;
+                          return (uint32_t)i;
+                        });
+  } else {
+    encode_chunks<T, B>(base, cur, geo, centers_g, tol_bin, tol, packed, scratch, counts, my,
+                        [&](double r) -> uint32_t {
+                          int a = 0, z = ncuts;
+                          while (a < z) {
+                            int mid = (a + z) >> 1;
+                            if (__ldg(cuts_g + mid) < r) a = mid + 1; else z = mid;
+                          }
+                          return (uint32_t)a;
+                        });
   }
 }
 

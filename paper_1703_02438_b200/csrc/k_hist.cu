@@ -32,9 +32,9 @@ __device__ __forceinline__ void hv_get(const float4& v, double* o) {
   o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 }
 
-// Visit every element's (ratio, valid) with 16-byte loads when aligned.
+// Visit every element's (base, current) pair with 16-byte loads when aligned.
 template <typename T, int UNROLL, typename F>
-__device__ __forceinline__ void for_each_ratio(const T* __restrict__ base, const T* __restrict__ cur,
+__device__ __forceinline__ void for_each_pair(const T* __restrict__ base, const T* __restrict__ cur,
                                                uint64_t n, bool vec_ok, F&& f) {
   using V = typename HVec<T>::V;
   constexpr int VN = HVec<T>::N;
@@ -59,11 +59,7 @@ __device__ __forceinline__ void for_each_ratio(const T* __restrict__ base, const
         hv_get(b[u], bb);
         hv_get(c[u], cc);
 #pragma unroll
-        for (int e = 0; e < VN; ++e) {
-          bool v;
-          double r = change_ratio(bb[e], cc[e], v);
-          f(r, v, (i + u * nthr) * VN + e);
-        }
+        for (int e = 0; e < VN; ++e) f(bb[e], cc[e], (i + u * nthr) * VN + e);
       }
     }
     for (; i < nvec; i += nthr) {
@@ -71,19 +67,11 @@ __device__ __forceinline__ void for_each_ratio(const T* __restrict__ base, const
       hv_get(__ldg(bv + i), bb);
       hv_get(__ldg(cv + i), cc);
 #pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        bool v;
-        double r = change_ratio(bb[e], cc[e], v);
-        f(r, v, i * VN + e);
-      }
+      for (int e = 0; e < VN; ++e) f(bb[e], cc[e], i * VN + e);
     }
     done = nvec * VN;
   }
-  for (uint64_t j = done + tid; j < n; j += nthr) {
-    bool v;
-    double r = change_ratio(to_f64(base[j]), to_f64(cur[j]), v);
-    f(r, v, j);
-  }
+  for (uint64_t j = done + tid; j < n; j += nthr) f(to_f64(base[j]), to_f64(cur[j]), j);
 }
 
 // counts[nbins] is an out-of-range tripwire (must stay 0).
@@ -100,9 +88,10 @@ k_hist_smem(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
   const double gmin = st->gmin;
   uint32_t* my = h + (uint32_t)((threadIdx.x >> 5) % reps) * nbins;
   uint32_t last = 0xffffffffu, run = 0;
-  for_each_ratio<T, 4>(base, cur, n, vec_ok, [&](double r, bool v, uint64_t) {
-    if (!v) return;
-    double q = bin_ordinal(r, gmin, width);
+  const double inv_w = 1.0 / width;
+  for_each_pair<T, 4>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
+    double q;
+    if (!element_ordinal(b, x, gmin, width, inv_w, q)) return;
     uint32_t qi = (q < (double)nbins) ? (uint32_t)q : nbins;  // nbins = tripwire
     if (qi == last) {
       ++run;
@@ -135,9 +124,10 @@ k_hist_global(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
   const double gmin = st->gmin;
   uint64_t last = ~0ULL;
   unsigned long long run = 0;
-  for_each_ratio<T, 2>(base, cur, n, vec_ok, [&](double r, bool v, uint64_t) {
-    if (!v) return;
-    double q = bin_ordinal(r, gmin, width);
+  const double inv_w = 1.0 / width;
+  for_each_pair<T, 2>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
+    double q;
+    if (!element_ordinal(b, x, gmin, width, inv_w, q)) return;
     uint64_t qi = (q < (double)nbins) ? (uint64_t)q : nbins;
     if (qi == last) {
       ++run;
@@ -156,8 +146,10 @@ k_hist_keys(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
             const nmk_stats* __restrict__ st, double width,
             unsigned long long* __restrict__ keys, bool vec_ok) {
   const double gmin = st->gmin;
-  for_each_ratio<T, 2>(base, cur, n, vec_ok, [&](double r, bool v, uint64_t j) {
-    keys[j] = v ? (unsigned long long)__double_as_longlong(bin_ordinal(r, gmin, width)) : ~0ULL;
+  const double inv_w = 1.0 / width;
+  for_each_pair<T, 2>(base, cur, n, vec_ok, [&](double b, double x, uint64_t j) {
+    double q;
+    keys[j] = element_ordinal(b, x, gmin, width, inv_w, q) ? (unsigned long long)__double_as_longlong(q) : ~0ULL;
   });
 }
 

@@ -20,17 +20,31 @@ struct MinMax {
   unsigned long long nv;
 };
 
-__device__ __forceinline__ void mm_add(MinMax& a, double r, bool v) {
+// One element into the running (min, max, count) over valid ratios
+// (core.py:115-137, pipeline.py:194-197).  The IEEE quotient is only formed
+// when the fast approximation cannot rule the element out as a new extreme.
+__device__ __forceinline__ void mm_visit(MinMax& a, double b, double x) {
+  double ra, ea;
+  if (fast_ratio(b, x, ra, ea)) {
+    a.nv += 1;                                          // finite quotient: valid
+    if (__dsub_rn(ra, ea) > a.lo && __dadd_rn(ra, ea) < a.hi) return;
+    const double r = __ddiv_rn(__dsub_rn(x, b), b);
+    a.lo = r < a.lo ? r : a.lo;
+    a.hi = r > a.hi ? r : a.hi;
+    return;
+  }
+  bool v;
+  const double r = change_ratio(b, x, v);
   if (v) {
-    a.lo = fmin(a.lo, r);
-    a.hi = fmax(a.hi, r);
     a.nv += 1;
+    a.lo = r < a.lo ? r : a.lo;
+    a.hi = r > a.hi ? r : a.hi;
   }
 }
 
 __device__ __forceinline__ MinMax mm_merge(MinMax a, const MinMax& b) {
-  a.lo = fmin(a.lo, b.lo);
-  a.hi = fmax(a.hi, b.hi);
+  a.lo = b.lo < a.lo ? b.lo : a.lo;
+  a.hi = b.hi > a.hi ? b.hi : a.hi;
   a.nv += b.nv;
   return a;
 }
@@ -76,11 +90,7 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
         vec_get(b[u], bb);
         vec_get(c[u], cc);
 #pragma unroll
-        for (int e = 0; e < VN; ++e) {
-          bool v;
-          double r = change_ratio(bb[e], cc[e], v);
-          mm_add(acc, r, v);
-        }
+        for (int e = 0; e < VN; ++e) mm_visit(acc, bb[e], cc[e]);
       }
     }
     for (; i < nvec; i += nthr) {
@@ -88,19 +98,11 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
       vec_get(__ldg(bv + i), bb);
       vec_get(__ldg(cv + i), cc);
 #pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        bool v;
-        double r = change_ratio(bb[e], cc[e], v);
-        mm_add(acc, r, v);
-      }
+      for (int e = 0; e < VN; ++e) mm_visit(acc, bb[e], cc[e]);
     }
     done = nvec * VN;
   }
-  for (uint64_t j = done + tid; j < n; j += nthr) {
-    bool v;
-    double r = change_ratio(to_f64(base[j]), to_f64(cur[j]), v);
-    mm_add(acc, r, v);
-  }
+  for (uint64_t j = done + tid; j < n; j += nthr) mm_visit(acc, to_f64(base[j]), to_f64(cur[j]));
   // warp reduce
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

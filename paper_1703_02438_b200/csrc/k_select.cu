@@ -129,16 +129,38 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
         if (s_kk[s] < m && (c & s_mask[s]) == s_prefix[s]) atomicAdd(&hist[s][d], 1u);
     }
     __syncthreads();
-    if (tid < kNSel && s_kk[tid] < m) {
-      unsigned long long cum = 0, left = s_left[tid];
-      int d = 255;
-      for (; d > 0; --d) {
-        if (cum + hist[tid][d] >= left) break;
-        cum += hist[tid][d];
+    {
+      // one warp per active slot: lane l owns digits 255-8l .. 248-8l; a warp
+      // scan from the top digit finds where the running count reaches `left`
+      const int w = tid >> 5, lane = tid & 31;
+      if (w < kNSel && s_kk[w] < m) {
+        unsigned long long h[8], sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          h[i] = hist[w][255 - 8 * lane - i];
+          sum += h[i];
+        }
+        unsigned long long inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += v;
+        }
+        const unsigned long long left = s_left[w];
+        const unsigned ball = __ballot_sync(0xffffffffu, inc - sum < left && left <= inc);
+        const int src = ball ? __ffs(ball) - 1 : 31;
+        if (lane == src) {
+          unsigned long long cum = inc - sum;
+          int d = 255 - 8 * lane;
+          for (int i = 0; i < 7; ++i, --d) {
+            if (cum + h[i] >= left) break;
+            cum += h[i];
+          }
+          s_left[w] = left - cum;  // still needed among bins equal on this digit
+          s_prefix[w] |= (unsigned long long)d << shift;
+          s_mask[w] |= 255ULL << shift;
+        }
       }
-      s_left[tid] = left - cum;  // still needed among bins equal on this digit
-      s_prefix[tid] |= (unsigned long long)d << shift;
-      s_mask[tid] |= 255ULL << shift;
     }
     __syncthreads();
   }

@@ -54,6 +54,60 @@ __device__ __forceinline__ double bin_ordinal(double r, double origin, double wi
   return __dadd_rn(q, 0.0);
 }
 
+// ---- division-free fast path with a rigorous error bound -------------------
+// ra approximates r = RN((x - b) / b) through a reciprocal seed refined by two
+// Newton steps (relative error <= 2^-50 even from a 2^-13 seed), so
+//     |ra - r| <= ea = |ra| * 2^-44        (a >= 16x safety margin).
+// Callers decide from ra whenever every decision threshold is farther than
+// the bound and fall back to the IEEE path otherwise, so results stay
+// bit-identical.  Applies to normal b in [2^-900, 2^900] with a finite,
+// non-tiny quotient; returns false otherwise (IEEE path, incl. all invalid).
+__device__ __forceinline__ double rcp_approx(double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  return y;
+}
+
+__device__ __forceinline__ bool fast_ratio(double b, double x, double& ra, double& ea) {
+  const int eb = (__double2hiint(b) >> 20) & 0x7ff;
+  const double d = __dsub_rn(x, b);
+  if (eb < 1023 - 900 || eb > 1023 + 900) return false;
+  double y = rcp_approx(b);
+  double e = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(y, e, y);
+  ra = __dmul_rn(d, y);
+  const double a = fabs(ra);
+  ea = a * 0x1p-44;
+  // finite, and either exactly zero or far from the subnormal range
+  return (a <= 0x1p+900) && (a >= 0x1p-900 || ra == 0.0);
+}
+
+// Bin ordinal of the element's ratio (binning.py:113) or false if invalid.
+// Fast path: t = (ra - origin) * inv_w is within et of RN(RN(r - origin)/w);
+// floor(t) is the exact ordinal unless an integer lies within et of t.
+__device__ __forceinline__ bool element_ordinal(double b, double x, double origin, double width, double inv_w,
+                                                double& q) {
+  double ra, ea;
+  if (fast_ratio(b, x, ra, ea)) {
+    const double s = __dsub_rn(ra, origin);
+    const double t = __dmul_rn(s, inv_w);
+    const double et = __dadd_rn(__dmul_rn(__dadd_rn(ea, fabs(s) * 0x1p-48), inv_w * 1.0000001),
+                                fabs(t) * 0x1p-46);
+    const double fl = floor(t);
+    if (t < 0x1p+50 && __dsub_rn(t, fl) > et && __dsub_rn(__dadd_rn(fl, 1.0), t) > et) {
+      q = __dadd_rn(fl, 0.0);
+      return true;
+    }
+  }
+  bool valid;
+  const double r = change_ratio(b, x, valid);
+  if (!valid) return false;
+  q = bin_ordinal(r, origin, width);
+  return true;
+}
+
 // origin + (q + 0.5) * width, add -> mul -> add (binning.py:50-51).
 __device__ __forceinline__ double bin_center(double q, double origin, double width) {
   return __dadd_rn(origin, __dmul_rn(__dadd_rn(q, 0.5), width));
