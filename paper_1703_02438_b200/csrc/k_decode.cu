@@ -13,16 +13,22 @@
 //   1. k_dec_count: sentinels per chunk of the covering span (reads the
 //      packed stream only, B/8 bytes per element);
 //   2. chunk_scan (k_scan.cu): chunk offsets;
-//   3. k_dec_chunks: one warp per (segment, chunk): unpack, rank the
-//      sentinels (block prefix + in-block chunk offset + warp scan), gather
-//      exact values, reconstruct, store.  No inter-warp dependency.
+//   3. k_dec_chunks: per-warp TMA pipeline over (segment, chunk) items:
+//      rank the sentinels (segment anchor + chunk offset + warp scan),
+//      gather exact values, reconstruct, store.  No inter-warp dependency.
+// Geometry is computed once per chunk in 32-bit form (magic-number division
+// for chunk -> block); elements only do 32-bit compares.
 #include "nmk_common.cuh"
 #include "nmk_scan.cuh"
 
 namespace nmk {
 
 constexpr int kDChunk = 32 * kGroup;   // 256 elements per warp chunk
-constexpr int kDecThreads = 256;
+constexpr int kDecThreads = 256;       // k_dec_count CTA
+constexpr int kSmemSegs = 64;          // segment records cached in shared memory
+constexpr int kTmaWarps = 4;           // k_dec_chunks CTA = 4 independent warps
+constexpr int kTmaThreads = 32 * kTmaWarps;
+constexpr int kStages = 4;             // chunks in flight per warp
 
 struct Seg {
   uint64_t start, count, out;   // global element range, output offset
@@ -31,55 +37,53 @@ struct Seg {
 };
 
 struct DecodeGeom {
-  uint64_t epb, cpb, n_total, first_block, stride, n_exact, nchunks, nitems;
+  uint64_t epb, n_total, first_block, stride, n_exact, nchunks, nitems;
+  uint32_t cpb;
+  FastDiv fd_cpb;
   int nseg, k;
 };
 
+// One chunk: block b, in-block chunk ci, element/byte extents (32-bit).
 struct DChunk {
-  uint64_t b, ci, blk_start, blk_end, chunk_lo, chunk_hi, crel;
+  uint32_t b, ci;
+  uint64_t chunk_lo;   // global index of the chunk's first element
+  uint32_t valid;      // elements of the chunk inside its block (<= 256)
+  uint32_t nbytes;     // packed bytes of the chunk inside its block
+  uint32_t crel;       // chunk id relative to first_block's first chunk
 };
 
-__device__ __forceinline__ DChunk dchunk(const DecodeGeom& geo, uint64_t g) {
+template <int B>
+__device__ __forceinline__ DChunk dchunk(const DecodeGeom& geo, uint32_t g) {
   DChunk d;
-  d.b = g / geo.cpb;
+  d.b = geo.fd_cpb.div(g);
   d.ci = g - d.b * geo.cpb;
-  d.blk_start = d.b * geo.epb;
-  d.blk_end = d.blk_start + geo.epb;
-  if (d.blk_end > geo.n_total) d.blk_end = geo.n_total;
-  d.chunk_lo = d.blk_start + d.ci * kDChunk;
-  d.chunk_hi = d.chunk_lo + kDChunk;
-  if (d.chunk_hi > d.blk_end) d.chunk_hi = d.blk_end;
-  d.crel = g - geo.first_block * geo.cpb;
+  const uint64_t blk_start = (uint64_t)d.b * geo.epb;
+  const uint64_t rem = geo.n_total - blk_start;
+  const uint32_t blk_len = (uint32_t)(rem < geo.epb ? rem : geo.epb);
+  const uint32_t off = d.ci * kDChunk;
+  d.chunk_lo = blk_start + off;
+  d.valid = min((uint32_t)kDChunk, blk_len - off);
+  const uint32_t blk_bytes = (uint32_t)(((uint64_t)blk_len * B + 7) / 8);
+  d.nbytes = min((uint32_t)(32 * B), blk_bytes - d.ci * (32 * B));
+  d.crel = g - (uint32_t)(geo.first_block * geo.cpb);
   return d;
 }
 
-// Packed-byte span of a chunk: base pointer and valid byte count (bytes at
-// or beyond it are padding and decode as zero bits).
-struct ChunkBytes {
-  const uint8_t* src;
-  uint32_t nbytes;
-};
-
 template <int B>
-__device__ __forceinline__ ChunkBytes chunk_bytes(const uint8_t* __restrict__ packed, const DecodeGeom& geo,
-                                                  const DChunk& d) {
-  const uint64_t blk_bytes = ((d.blk_end - d.blk_start) * B + 7) / 8;
-  const uint64_t off = d.ci * (uint64_t)(32 * B);
-  uint64_t nbytes = blk_bytes > off ? blk_bytes - off : 0;
-  if (nbytes > (uint64_t)(32 * B)) nbytes = 32 * B;
-  return ChunkBytes{packed + (d.b - geo.first_block) * geo.stride + off, (uint32_t)nbytes};
+__device__ __forceinline__ const uint8_t* chunk_src(const uint8_t* packed, const DecodeGeom& geo, const DChunk& d) {
+  return packed + (uint64_t)(d.b - (uint32_t)geo.first_block) * geo.stride + (uint64_t)d.ci * (32 * B);
 }
 
 // This lane's B bytes (offset lane*B of a 16-byte aligned chunk) with the
-// widest aligned loads B allows; the chunk's last lanes may be clipped.
+// widest aligned loads B allows; bytes at or past nbytes read as zero.
 template <int B>
-__device__ __forceinline__ void lane_bytes(const ChunkBytes& cb, int lane, uint8_t (&o)[B]) {
+__device__ __forceinline__ void lane_bytes(const uint8_t* src, uint32_t nbytes, int lane, uint8_t (&o)[B]) {
   const uint32_t s0 = (uint32_t)lane * B;
   constexpr int W = (B % 8 == 0) ? 8 : (B % 4 == 0) ? 4 : (B % 2 == 0) ? 2 : 1;
-  if (s0 + B <= cb.nbytes) {
+  if (s0 + B <= nbytes) {
 #pragma unroll
     for (int w = 0; w < B / W; ++w) {
-      const uint8_t* p = cb.src + s0 + w * W;
+      const uint8_t* p = src + s0 + w * W;
       unsigned long long v;
       if constexpr (W == 8) v = __ldg(reinterpret_cast<const unsigned long long*>(p));
       else if constexpr (W == 4) v = __ldg(reinterpret_cast<const unsigned int*>(p));
@@ -90,7 +94,7 @@ __device__ __forceinline__ void lane_bytes(const ChunkBytes& cb, int lane, uint8
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < B; ++i) o[i] = (s0 + i < cb.nbytes) ? __ldg(cb.src + s0 + i) : (uint8_t)0;
+    for (int i = 0; i < B; ++i) o[i] = (s0 + i < nbytes) ? __ldg(src + s0 + i) : (uint8_t)0;
   }
 }
 
@@ -112,146 +116,277 @@ __device__ __forceinline__ void codes_of(const uint8_t (&src)[B], uint32_t (&cod
   }
 }
 
+// ---- 1. sentinels per chunk -------------------------------------------------
+template <int B>
+__device__ __forceinline__ unsigned lane_sentinels(const uint8_t (&raw)[B], uint32_t valid, int lane) {
+  const uint32_t sentinel = (1u << B) - 1u;
+  if constexpr (B == 8) {
+    // one code per byte: count 0xff bytes four at a time (bytes past the
+    // block end read as zero, never 0xff)
+    const uint32_t lo = raw[0] | (raw[1] << 8) | (raw[2] << 16) | ((uint32_t)raw[3] << 24);
+    const uint32_t hi = raw[4] | (raw[5] << 8) | (raw[6] << 16) | ((uint32_t)raw[7] << 24);
+    return (__popc(__vcmpeq4(lo, 0xffffffffu)) + __popc(__vcmpeq4(hi, 0xffffffffu))) >> 3;
+  } else {
+    uint32_t code[kGroup];
+    codes_of<B>(raw, code);
+    const int s0 = lane * kGroup;
+    unsigned n = 0;
+#pragma unroll
+    for (int e = 0; e < kGroup; ++e) n += (s0 + e < (int)valid && code[e] == sentinel);
+    return n;
+  }
+}
+
 template <int B>
 __global__ void __launch_bounds__(kDecThreads)
 k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t sentinel = (1u << B) - 1u;
-  const uint64_t nwarps = (uint64_t)gridDim.x * (kDecThreads / 32);
-  const uint64_t g0 = geo.first_block * geo.cpb;
-  for (uint64_t c = (uint64_t)blockIdx.x * (kDecThreads / 32) + wid; c < geo.nchunks; c += nwarps) {
-    const DChunk d = dchunk(geo, g0 + c);
+  const uint32_t nwarps = gridDim.x * (kDecThreads / 32);
+  const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
+  for (uint32_t c = blockIdx.x * (kDecThreads / 32) + wid; c < (uint32_t)geo.nchunks; c += nwarps) {
+    const DChunk d = dchunk<B>(geo, g0 + c);
     uint8_t raw[B];
-    lane_bytes<B>(chunk_bytes<B>(packed, geo, d), lane, raw);
-    uint32_t code[kGroup];
-    codes_of<B>(raw, code);
-    const uint64_t grp_lo = d.chunk_lo + (uint64_t)lane * kGroup;
-    unsigned n = 0;
-#pragma unroll
-    for (int e = 0; e < kGroup; ++e) n += (grp_lo + e < d.chunk_hi && code[e] == sentinel);
-    n = __reduce_add_sync(0xffffffffu, n);
+    lane_bytes<B>(chunk_src<B>(packed, geo, d), d.nbytes, lane, raw);
+    const unsigned n = __reduce_add_sync(0xffffffffu, lane_sentinels<B>(raw, d.valid, lane));
     if (lane == 0) counts[c] = n;
   }
 }
 
+// ---- 3. reconstruct: per-warp TMA pipeline ---------------------------------
+// Each warp owns kStages shared-memory stages.  Lane 0 keeps kStages chunks in
+// flight with 1-D bulk copies (the chunk's base values + its packed bytes),
+// completion tracked by one mbarrier per stage (transaction bytes), so the
+// bytes in flight cost no registers.  Lanes read a stage conflict-free (lane
+// l takes 16-byte vector l of each 512-byte row) and store fully coalesced.
+// Chunks that cannot be bulk-copied (segment edges, misaligned base, packed
+// bytes running past the block's stride) fall back to direct loads.
 template <typename T> struct DVec;
 template <> struct DVec<double> { using V = double2; static constexpr int N = 2; };
 template <> struct DVec<float>  { using V = float4;  static constexpr int N = 4; };
 
 template <typename T, int B>
-__global__ void __launch_bounds__(kDecThreads, 3)
+struct DecStage {
+  static constexpr int kBase = kDChunk * (int)sizeof(T);   // 2048 (f64) / 1024 (f32)
+  static constexpr int kPk = 32 * B;                        // a multiple of 16
+  static constexpr int kBytes = kBase + kPk + 16;           // +16: 8-byte code windows
+  static constexpr size_t kSmem = (size_t)kTmaWarps * kStages * kBytes;
+};
+
+// B-bit code of chunk element e from the staged packed bytes (MSB-first).
+template <int B>
+__device__ __forceinline__ uint32_t code_at(const uint8_t* pk, int e) {
+  if constexpr (B == 8) {
+    return pk[e];
+  } else {
+    const int bit = e * B;
+    const int w = (bit >> 5) << 2;                          // aligned 4-byte word
+    const uint32_t a = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w), 0, 0x0123);
+    const uint32_t z = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w + 4), 0, 0x0123);
+    const unsigned long long x = ((unsigned long long)a << 32) | z;
+    const int off = bit & 31;                               // off + B <= 61
+    return (uint32_t)(x >> (64 - off - B)) & ((1u << B) - 1u);
+  }
+}
+
+struct DItem {
+  int seg;
+  DChunk d;
+  uint32_t lo_rel, hi_rel;   // in-segment elements of the chunk: [lo_rel, hi_rel)
+  int64_t oi0;               // base/out index of the chunk's first element
+  uint32_t anchor;           // block (relative) of the segment's first chunk
+  bool first;                // the segment's first chunk
+  bool base_tma, pk_tma;
+};
+
+template <typename T, int B>
+__device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo, const Seg* SG,
+                                             const T* __restrict__ base) {
+  int s = 0;
+  if (geo.nseg > 1) {
+    int hi_s = geo.nseg - 1;
+    while (s < hi_s) {
+      int mid = (s + hi_s + 1) >> 1;
+      if (SG[mid].item0 <= it) s = mid; else hi_s = mid - 1;
+    }
+  }
+  const Seg sg = SG[s];
+  DItem t;
+  t.seg = s;
+  const uint32_t rel = (uint32_t)(it - sg.item0);
+  t.d = dchunk<B>(geo, (uint32_t)sg.gfirst + rel);
+  t.first = rel == 0;
+  const int64_t lo = (int64_t)sg.start - (int64_t)t.d.chunk_lo;
+  const int64_t hi = lo + (int64_t)sg.count;
+  t.lo_rel = (uint32_t)(lo < 0 ? 0 : lo);
+  t.hi_rel = (uint32_t)(hi > (int64_t)t.d.valid ? (int64_t)t.d.valid : hi);
+  t.oi0 = (int64_t)sg.out - lo;
+  t.anchor = geo.fd_cpb.div((uint32_t)sg.gfirst) - (uint32_t)geo.first_block;
+  t.base_tma = t.lo_rel == 0 && t.hi_rel == kDChunk && ((uintptr_t)(base + t.oi0) & 15) == 0;
+  t.pk_tma = (uint64_t)(t.d.ci + 1) * (32 * B) <= geo.stride;
+  return t;
+}
+
+template <typename T, int B>
+__global__ void __launch_bounds__(kTmaThreads, 6)
 k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs,
              const unsigned long long* __restrict__ offsets, const unsigned long long* __restrict__ prefix_rel,
              const double* __restrict__ centers_g, const T* __restrict__ exact, const T* __restrict__ base,
              T* __restrict__ out, nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int k = geo.k;
-  const uint32_t sentinel = (1u << B) - 1u;
-  constexpr int VN = DVec<T>::N;
+  using ST = DecStage<T, B>;
+  constexpr int VN = DVec<T>::N;          // elements per 16-byte vector
+  constexpr int Q = kGroup / VN;          // vectors per lane per chunk
   using V = typename DVec<T>::V;
-  const bool out_al = (((uintptr_t)out | (uintptr_t)base) & 15) == 0;
-  const uint64_t nwarps = (uint64_t)gridDim.x * (kDecThreads / 32);
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ __align__(8) unsigned long long bars[kTmaWarps][kStages];
+  __shared__ Seg s_segs[kSmemSegs];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool seg_smem = geo.nseg <= kSmemSegs;
+  if (seg_smem)
+    for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = segs[i];
+  if (lane == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&bars[wid][st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const Seg* SG = seg_smem ? s_segs : segs;
+  uint8_t* wst = dsm + (size_t)wid * kStages * ST::kBytes;
+  const uint32_t sentinel = (1u << B) - 1u;
+  const uint32_t k = (uint32_t)geo.k;
+  const bool out_al = ((uintptr_t)out & 15) == 0;
+  const uint64_t gw = (uint64_t)blockIdx.x * kTmaWarps + wid, nw = (uint64_t)gridDim.x * kTmaWarps;
 
-  for (uint64_t it = (uint64_t)blockIdx.x * (kDecThreads / 32) + wid; it < geo.nitems; it += nwarps) {
-    int lo_s = 0, hi_s = geo.nseg - 1;
-    while (lo_s < hi_s) {
-      int mid = (lo_s + hi_s + 1) >> 1;
-      if (segs[mid].item0 <= it) lo_s = mid; else hi_s = mid - 1;
-    }
-    const Seg sg = segs[lo_s];
-    const uint64_t g = sg.gfirst + (it - sg.item0);
-    const DChunk d = dchunk(geo, g);
-    const uint64_t seg_lo = sg.start, seg_hi = sg.start + sg.count;
-    const uint64_t grp_lo = d.chunk_lo + (uint64_t)lane * kGroup;
-    // base values first (independent of the codes), then the packed bytes
-    unsigned inmask = 0;
+  auto issue = [&](int st, uint64_t it) {       // lane 0 only
+    const DItem t = decode_item<T, B>(it, geo, SG, base);
+    uint8_t* sb = wst + st * ST::kBytes;
+    mbar_arrive_tx(&bars[wid][st], (t.base_tma ? ST::kBase : 0) + (t.pk_tma ? ST::kPk : 0));
+    if (t.base_tma) tma_load_1d(sb, base + t.oi0, ST::kBase, &bars[wid][st]);
+    if (t.pk_tma) tma_load_1d(sb + ST::kBase, chunk_src<B>(packed, geo, t.d), ST::kPk, &bars[wid][st]);
+  };
+  if (lane == 0)
+    for (int st = 0; st < kStages; ++st)
+      if (gw + st * nw < geo.nitems) issue(st, gw + st * nw);
+
+  for (uint64_t kk = 0;; ++kk) {
+    const uint64_t it = gw + kk * nw;
+    if (it >= geo.nitems) break;
+    const int st = (int)(kk % kStages);
+    uint8_t* sb = wst + st * ST::kBytes;
+    const DItem t = decode_item<T, B>(it, geo, SG, base);
+    // independent global loads first: the chunk's rank anchor (codec.py:231-
+    // 236: prefix of the segment's first block + sentinels counted since)
+    const unsigned long long chunk_off =
+        prefix_rel[t.anchor] + (offsets[t.d.crel] - offsets[t.anchor * geo.cpb]);
+    T bv[Q][VN];
+    if (!t.base_tma) {
 #pragma unroll
-    for (int e = 0; e < kGroup; ++e) {
-      const uint64_t j = grp_lo + e;
-      if (j < d.chunk_hi && j >= seg_lo && j < seg_hi) inmask |= 1u << e;
-    }
-    T bv[kGroup], ov[kGroup];
-    const int64_t oi = (int64_t)sg.out + ((int64_t)grp_lo - (int64_t)seg_lo);
-    const bool vec = inmask == 0xffu && out_al && (oi % VN) == 0;
-    if (vec) {
+      for (int q = 0; q < Q; ++q)
 #pragma unroll
-      for (int q = 0; q < kGroup / VN; ++q) {
-        V w = __ldg(reinterpret_cast<const V*>(base + oi) + q);
+        for (int v = 0; v < VN; ++v) {
+          const uint32_t e = VN * lane + 32 * VN * q + v;
+          bv[q][v] = (e >= t.lo_rel && e < t.hi_rel) ? __ldg(base + (t.oi0 + e)) : T(0);
+        }
+    }
+    mbar_wait(&bars[wid][st], (unsigned)((kk / kStages) & 1));
+    if (!t.pk_tma) {
+      const uint8_t* src = chunk_src<B>(packed, geo, t.d);
+      for (int i = lane; i < 32 * B; i += 32) sb[ST::kBase + i] = (uint32_t)i < t.d.nbytes ? __ldg(src + i) : 0;
+      __syncwarp();
+    }
+    if (t.base_tma) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const V w = *reinterpret_cast<const V*>(sb + 16 * lane + 512 * q);
         const T* tw = reinterpret_cast<const T*>(&w);
 #pragma unroll
-        for (int e = 0; e < VN; ++e) bv[q * VN + e] = tw[e];
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < kGroup; ++e) bv[e] = (inmask >> e & 1u) ? __ldg(base + (oi + e)) : T(0);
-    }
-    uint8_t raw[B];
-    lane_bytes<B>(chunk_bytes<B>(packed, geo, d), lane, raw);
-    uint32_t code[kGroup];
-    codes_of<B>(raw, code);
-    unsigned smask = 0, ahead = 0;
-#pragma unroll
-    for (int e = 0; e < kGroup; ++e) {
-      const uint64_t j = grp_lo + e;
-      if (j < d.chunk_hi && code[e] == sentinel) {
-        smask |= 1u << e;
-        if (j < seg_lo) ++ahead;
+        for (int v = 0; v < VN; ++v) bv[q][v] = tw[v];
       }
     }
-    // rank of this lane's first sentinel, anchored like the reference on the
-    // prefix entry of the segment's FIRST block and counted from there
-    // (codec.py:231-236): prefix + chunk offset + warp exclusive scan
-    const uint64_t ab = sg.gfirst / geo.cpb - geo.first_block;
-    const unsigned long long chunk_off = prefix_rel[ab] + (offsets[d.crel] - offsets[ab * geo.cpb]);
-    const unsigned cnt = __popc(smask);
-    unsigned incl = cnt;
+    // codes and masks; element order is (q, lane, v)
+    uint32_t code[Q][VN];
+    unsigned smask = 0, inmask = 0, cnt_pk = 0, ahead = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      unsigned c = 0;
+#pragma unroll
+      for (int v = 0; v < VN; ++v) {
+        const uint32_t e = VN * lane + 32 * VN * q + v;
+        code[q][v] = code_at<B>(sb + ST::kBase, e);
+        const int bitp = q * VN + v;
+        if (e < t.d.valid && code[q][v] == sentinel) {
+          smask |= 1u << bitp;
+          ++c;
+          ahead += e < t.lo_rel;
+        }
+        if (e >= t.lo_rel && e < t.hi_rel) inmask |= 1u << bitp;
+      }
+      cnt_pk |= c << (8 * q);
+    }
+    // per-q sentinel ranks with one packed warp scan (byte lanes, <= 128 each)
+    unsigned incl = cnt_pk;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    unsigned long long pos = chunk_off + (incl - cnt);
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    const unsigned excl = incl - cnt_pk;
+    T ov[Q][VN];
     unsigned bad = 0, maxbad = 0, exhausted = 0;
+    unsigned long long before_q = 0;
 #pragma unroll
-    for (int e = 0; e < kGroup; ++e) {
-      ov[e] = T(0);
-      if (smask >> e & 1u) {
-        if (inmask >> e & 1u) {
-          if (pos < geo.n_exact) ov[e] = exact[pos];
-          else exhausted = 1;
-        }
-        ++pos;
-      } else if (inmask >> e & 1u) {
-        if (code[e] >= (uint32_t)k) {
-          bad = 1;
-          maxbad = code[e] > maxbad ? code[e] : maxbad;
-        } else {
-          ov[e] = apply_center<T>(__ldg(centers_g + code[e]), to_f64(bv[e]));   // L1-resident table
+    for (int q = 0; q < Q; ++q) {
+      unsigned long long pos = chunk_off + before_q + ((excl >> (8 * q)) & 255u);
+      before_q += (tot >> (8 * q)) & 255u;
+#pragma unroll
+      for (int v = 0; v < VN; ++v) {
+        const int bitp = q * VN + v;
+        ov[q][v] = T(0);
+        if (smask >> bitp & 1u) {
+          if (inmask >> bitp & 1u) {
+            if (pos < geo.n_exact) ov[q][v] = exact[pos];
+            else exhausted = 1;
+          }
+          ++pos;
+        } else if (inmask >> bitp & 1u) {
+          const uint32_t cd = code[q][v];
+          if (cd >= k) {
+            bad = 1;
+            maxbad = cd > maxbad ? cd : maxbad;
+          } else {
+            ov[q][v] = apply_center<T>(__ldg(centers_g + cd), to_f64(bv[q][v]));
+          }
         }
       }
     }
-    if (vec) {
+    if (t.base_tma && out_al) {
 #pragma unroll
-      for (int q = 0; q < kGroup / VN; ++q)
-        reinterpret_cast<V*>(out + oi)[q] = *reinterpret_cast<const V*>(&ov[q * VN]);
+      for (int q = 0; q < Q; ++q)
+        *reinterpret_cast<V*>(out + t.oi0 + VN * lane + 32 * VN * q) = *reinterpret_cast<const V*>(&ov[q][0]);
     } else {
 #pragma unroll
-      for (int e = 0; e < kGroup; ++e)
-        if (inmask >> e & 1u) out[oi + e] = ov[e];
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int v = 0; v < VN; ++v)
+          if (inmask >> (q * VN + v) & 1u) out[t.oi0 + VN * lane + 32 * VN * q + v] = ov[q][v];
     }
     if (bad) {
       atomicOr(&err->bad_index, 1u);
       atomicMax(&err->max_bad_index, maxbad);
     }
     if (exhausted) atomicOr(&err->exhausted, 1u);
-    // segment bookkeeping
     const unsigned in_s = __reduce_add_sync(0xffffffffu, __popc(smask & inmask));
-    if (lane == 0 && in_s) atomicAdd(&info[lo_s].n_sentinel, (unsigned long long)in_s);
-    if (g == sg.gfirst) {
+    if (lane == 0 && in_s) atomicAdd(&info[t.seg].n_sentinel, (unsigned long long)in_s);
+    if (t.first) {
       const unsigned ah = __reduce_add_sync(0xffffffffu, ahead);
-      if (lane == 0) info[lo_s].inc_before = chunk_off + ah;
+      if (lane == 0) info[t.seg].inc_before = chunk_off + ah;
     }
+    // stage consumed: refill it kStages chunks ahead
     __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      const uint64_t nx = it + (uint64_t)kStages * nw;
+      if (nx < geo.nitems) issue(st, nx);
+    }
   }
 }
 
@@ -302,18 +437,23 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
                           const double* centers, const void* exact, const void* base, void* out,
                           nmk_segment_info* info, nmk_decode_err* err, cudaStream_t s) {
   const int sms = sm_count_d();
-  uint64_t g1 = (geo.nchunks + 7) / 8;
-  unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
+  const uint64_t g1 = (geo.nchunks + 7) / 8;
+  const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
   k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   chunk_scan(counts, geo.nchunks, offsets, nullptr, scan_ws, s);
-  const size_t smem = 0;
+  const size_t smem = DecStage<T, B>::kSmem;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dec_chunks<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B>, kDecThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B>, kTmaThreads, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)sms * per_sm;
-  uint64_t need = (geo.nitems + 7) / 8;
+  const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;
   if (grid > need) grid = need;
-  k_dec_chunks<T, B><<<(unsigned)grid, kDecThreads, smem, s>>>(packed, geo, segs, offsets, prefix_rel, centers,
+  k_dec_chunks<T, B><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, offsets, prefix_rel, centers,
                                                                 (const T*)exact, (const T*)base, (T*)out, info,
                                                                 err);
 }
@@ -358,6 +498,8 @@ extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t
   if (nseg < 1 || !h_seg_start || !h_seg_count || !h_seg_out || !seg_info || !err || !ws)
     return set_error(NMK_ERR_ARG, "nmk_decode: bad argument");
   if (bits < 2 || bits > 30 || epb == 0 || k < 1) return set_error(NMK_ERR_ARG, "nmk_decode: bad geometry");
+  if (epb >= (1ULL << 31) || (n_total + kDChunk - 1) / kDChunk >= (1ULL << 32))
+    return set_error(NMK_ERR_ARG, "nmk_decode: block or stream too large for 32-bit chunk indexing");
   if (block_stride % 16 || ((uintptr_t)packed & 15)) return set_error(NMK_ERR_ARG, "nmk_decode: packed alignment");
   if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_decode: bad dtype");
   for (int i = 0; i < nseg; ++i) {
@@ -391,7 +533,18 @@ extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t
   // host table can be released immediately (no stream synchronisation)
   cudaMemcpyAsync(dsegs, hs, sizeof(Seg) * (size_t)nseg, cudaMemcpyHostToDevice, s);
   free(hs);
-  DecodeGeom geo{epb, p.cpb, n_total, first_block, block_stride, n_exact, p.nchunks, p.nitems, nseg, k};
+  DecodeGeom geo{};
+  geo.epb = epb;
+  geo.n_total = n_total;
+  geo.first_block = first_block;
+  geo.stride = block_stride;
+  geo.n_exact = n_exact;
+  geo.nchunks = p.nchunks;
+  geo.nitems = p.nitems;
+  geo.cpb = (uint32_t)p.cpb;
+  geo.fd_cpb.init((uint32_t)p.cpb);
+  geo.nseg = nseg;
+  geo.k = k;
   if (dtype == NMK_F64)
     return dispatch_decode<double>(bits, packed, geo, dsegs, counts, offsets, w + p.off_scan, prefix_rel, centers,
                                    exact, base, out, seg_info, err, s);

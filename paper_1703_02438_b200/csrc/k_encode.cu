@@ -83,6 +83,7 @@ __device__ __forceinline__ void pack8(const uint32_t (&code)[kGroup], uint8_t* d
 
 struct EncodeGeom {
   uint64_t n_local, elem0, n_total, epb, cpb, g0, nchunks, b0, stride;
+  FastDiv fd_cpb;   // chunk id -> block
 };
 
 // Chunk c of this range: block, in-block chunk index and element spans.
@@ -159,7 +160,7 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
   const uint32_t nw = gridDim.x * (kEncThreads / 32);
   for (uint32_t c = blockIdx.x * (kEncThreads / 32) + wid; c < (uint32_t)geo.nchunks; c += nw) {
     const uint32_t g = (uint32_t)geo.g0 + c;
-    const uint32_t b = g / cpb, ci = g - b * cpb;
+    const uint32_t b = geo.fd_cpb.div(g), ci = g - b * cpb;
     const uint64_t blk_start = (uint64_t)b * geo.epb;
     const uint64_t blk_end = min(blk_start + geo.epb, geo.n_total);
     const uint64_t chunk_lo = blk_start + (uint64_t)ci * kChunk;
@@ -223,7 +224,7 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
 }
 
 template <typename T, int B>
-__global__ void __launch_bounds__(kEncThreads, 3)
+__global__ void __launch_bounds__(kEncThreads, 4)
 k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
          double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
@@ -276,20 +277,35 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
 }
 
 // Finalize: chunk offsets -> compacted exact list + per-block prefix.
+// One thread per chunk for the bookkeeping; chunks with more than a few
+// incompressible values are copied by the whole warp, one chunk at a time.
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsigned long long* __restrict__ offsets,
                const T* __restrict__ scratch, T* __restrict__ exact, unsigned long long* __restrict__ prefix) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * 8;
-  for (uint64_t c = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); c < geo.nchunks; c += nwarps) {
-    const unsigned n = counts[c];
-    const unsigned long long off = offsets[c];
-    for (unsigned i = lane; i < n; i += 32) exact[off + i] = scratch[c * kChunk + i];
-    if (lane == 0) {
-      const uint64_t g = geo.g0 + c;
-      const uint64_t b = g / geo.cpb;
-      if (g == b * geo.cpb && b * geo.epb >= geo.elem0) prefix[b - geo.b0] = off;
+  const uint32_t cpb = (uint32_t)geo.cpb;
+  const uint32_t nthr = gridDim.x * blockDim.x;
+  for (uint32_t c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); c0 < (uint32_t)geo.nchunks; c0 += nthr) {
+    const uint32_t c = c0 + lane;
+    const bool in = c < (uint32_t)geo.nchunks;
+    const unsigned n = in ? counts[c] : 0u;
+    const unsigned long long off = in ? offsets[c] : 0ULL;
+    if (in) {
+      const uint32_t g = (uint32_t)geo.g0 + c;
+      const uint32_t b = geo.fd_cpb.div(g);
+      if (g == b * cpb && (uint64_t)b * geo.epb >= geo.elem0) prefix[b - geo.b0] = off;
+      if (n <= 4)
+        for (unsigned i = 0; i < n; ++i) exact[off + i] = scratch[(uint64_t)c * kChunk + i];
+    }
+    unsigned big = __ballot_sync(0xffffffffu, n > 4);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const unsigned nn = __shfl_sync(0xffffffffu, n, src);
+      const unsigned long long oo = __shfl_sync(0xffffffffu, off, src);
+      const uint64_t cs = (uint64_t)(c0 + src) * kChunk;
+      for (unsigned i = lane; i < nn; i += 32) exact[oo + i] = scratch[cs + i];
     }
   }
 }
@@ -474,7 +490,10 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
   const size_t need = nmk_encode_ws_bytes(n_local, elem0, epb, dtype);
   if (ws_bytes < need) return set_error(NMK_ERR_ARG, "nmk_encode: workspace too small");
   EncodeChunks et = encode_chunks(n_local, elem0, epb);
-  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride};
+  if (epb >= (1ULL << 31) || (n_total + kChunk - 1) / kChunk >= (1ULL << 32))
+    return set_error(NMK_ERR_ARG, "nmk_encode: block or stream too large for 32-bit chunk indexing");
+  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride, FastDiv{}};
+  geo.fd_cpb.init((uint32_t)et.cpb);
   EncodeWs w = encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8);
   char* wb = (char*)ws;
   uint32_t* counts = (uint32_t*)(wb + w.off_counts);
@@ -491,7 +510,7 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
                                         scratch, counts, s);
   if (rc) return rc;
   chunk_scan(counts, et.nchunks, offsets, n_inc, wb + w.off_scan, s);
-  unsigned grid = (unsigned)((et.nchunks + 7) / 8);
+  unsigned grid = (unsigned)((et.nchunks + 255) / 256);
   if (grid > (unsigned)sm_count_e() * 8) grid = sm_count_e() * 8;
   if (dtype == NMK_F64)
     k_enc_finalize<double><<<grid, 256, 0, s>>>(geo, counts, offsets, (const double*)scratch, (double*)exact, prefix);

@@ -28,17 +28,21 @@ constexpr int kSelThreads = 1024;
 constexpr int kAutoLo = 2, kAutoHi = 16;           // binning.py:22
 constexpr int kNSel = kAutoHi - kAutoLo + 1;       // 15 simultaneous selects
 
+constexpr uint64_t kSelCache = 8192;  // bins whose selectable counts live in smem
+
 struct BinView {
   const unsigned long long* keys;    // null -> dense (ordinal = index)
   const unsigned long long* counts;
   uint64_t m;
   double origin, width;
+  const unsigned long long* cache;   // shared-memory copy of sel_count, or null
   __device__ __forceinline__ double ord(uint64_t i) const {
     return keys ? __longlong_as_double((long long)keys[i]) : (double)i;
   }
   __device__ __forceinline__ double center(uint64_t i) const { return bin_center(ord(i), origin, width); }
   // count if the bin is nonempty and selectable, else 0
   __device__ __forceinline__ unsigned long long sel_count(uint64_t i) const {
+    if (cache) return cache[i];
     unsigned long long c = counts[i];
     if (c == 0) return 0;
     return finite64(center(i)) ? c : 0ULL;
@@ -67,6 +71,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
   __shared__ unsigned long long s_bcast[4];
   __shared__ int s_bits;
   __shared__ double s_prev;
+  extern __shared__ unsigned long long s_cache[];
 
   const int tid = threadIdx.x;
   const uint64_t nvalid = st->nvalid;
@@ -83,8 +88,13 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     }
     return;
   }
-  BinView bv{keys, counts, nruns ? (uint64_t)*nruns : m_max, st->gmin, width};
+  BinView bv{keys, counts, nruns ? (uint64_t)*nruns : m_max, st->gmin, width, nullptr};
   const uint64_t M = bv.m;
+  if (m_max <= kSelCache) {   // every pass below then reads shared memory
+    for (uint64_t i = tid; i < M; i += kSelThreads) s_cache[i] = bv.sel_count(i);
+    __syncthreads();
+    bv.cache = s_cache;
+  }
 
   // ---- pass A: m (selectable bins), max count, total selectable count ----
   unsigned long long my_m = 0, my_max = 0, my_tot = 0;
@@ -120,13 +130,21 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
   for (int shift = (top / 8) * 8; shift >= 0; shift -= 8) {
     for (int i = tid; i < kNSel * 256; i += kSelThreads) (&hist[0][0])[i] = 0;
     __syncthreads();
-    for (uint64_t i = tid; i < M; i += kSelThreads) {
-      unsigned long long c = bv.sel_count(i);
-      if (!c) continue;
-      unsigned d = (unsigned)(c >> shift) & 255u;
-#pragma unroll
-      for (int s = 0; s < kNSel; ++s)
-        if (s_kk[s] < m && (c & s_mask[s]) == s_prefix[s]) atomicAdd(&hist[s][d], 1u);
+    for (uint64_t i0 = 0; i0 < M; i0 += kSelThreads) {   // warp-uniform trip count
+      const uint64_t i = i0 + tid;
+      const unsigned long long c = i < M ? bv.sel_count(i) : 0ULL;
+      const unsigned d = (unsigned)(c >> shift) & 255u;
+      for (int s = 0; s < kNSel; ++s) {
+        if (!(s_kk[s] < m)) continue;                      // uniform
+        const bool want = c && (c & s_mask[s]) == s_prefix[s];
+        const unsigned act = __ballot_sync(0xffffffffu, want);
+        if (want) {
+          // skewed digits (the top digit is nearly constant): one atomic per
+          // distinct digit per warp
+          const unsigned peers = __match_any_sync(act, d);
+          if ((tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[s][d], (unsigned)__popc(peers));
+        }
+      }
     }
     __syncthreads();
     {
@@ -290,11 +308,18 @@ extern "C" int nmk_select(const unsigned long long* keys, const unsigned long lo
   if (bits >= 0 && (bits < 2 || bits > 30)) return set_error(NMK_ERR_ARG, "nmk_select: bits %d outside [2, 30]", bits);
   if (keys && !nruns) return set_error(NMK_ERR_ARG, "nmk_select: sparse form needs nruns");
   cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = m_max <= kSelCache ? (size_t)m_max * 8 : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_select<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelCache * 8));
+    cudaFuncSetAttribute(k_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelCache * 8));
+    attr = true;
+  }
   if (dtype == NMK_F64)
-    k_select<double><<<1, kSelThreads, 0, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
+    k_select<double><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
                                                centers, cuts, (double*)centers_t, cap_k, model);
   else if (dtype == NMK_F32)
-    k_select<float><<<1, kSelThreads, 0, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
+    k_select<float><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
                                               centers, cuts, (float*)centers_t, cap_k, model);
   else
     return set_error(NMK_ERR_ARG, "nmk_select: bad dtype");

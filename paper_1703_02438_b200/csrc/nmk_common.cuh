@@ -203,6 +203,45 @@ __device__ __forceinline__ void cp_async_bytes4(void* s, const void* g, int have
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// ---- TMA bulk copies + mbarriers (sm_90+/sm_100a) --------------------------
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arrive once and expect `bytes` of async-proxy transactions on the phase
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D TMA: global -> shared, completion counted on `bar` (16-byte aligned,
+// size a multiple of 16)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// order this thread's (and, after __syncwarp, its warp's) generic shared
+// accesses before subsequent async-proxy writes to the same buffer
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Element stage: thread t's 8 consecutive elements at t*kRow(T) bytes, a row
 // padded by 16 bytes so 128-bit shared loads of 8 threads hit distinct banks.
 template <typename T> struct Stage {
@@ -245,6 +284,25 @@ __device__ __forceinline__ void unstage_group(const unsigned char* stage, T (&v)
     for (int e = 0; e < 16 / (int)sizeof(T); ++e) v[q * (16 / (int)sizeof(T)) + e] = tw[e];
   }
 }
+
+// ---- division by a run-time invariant (Granlund-Montgomery) ---------------
+// q = n / d for any 32-bit n with one mul-hi, an add and two shifts.
+struct FastDiv {
+  uint32_t d, m;
+  int s1, s2;
+  void init(uint32_t dd) {
+    d = dd;
+    int l = 0;
+    while ((1ull << l) < dd) ++l;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - dd)) / dd + 1);
+    s1 = l > 0 ? 1 : 0;
+    s2 = l > 0 ? l - 1 : 0;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t = __umulhi(m, n);
+    return (t + ((n - t) >> s1)) >> s2;
+  }
+};
 
 // ---- relaxed 64-bit status words for decoupled look-back ------------------
 __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
