@@ -36,6 +36,9 @@ BITS = 8
 SIDE = 512
 METRIC = "compress+decompress GB/s of input (n*L per timestep / (t_compress + t_decompress))"
 CONFIG_NAME = "cfg2: 512^3 fp64 8^3-block field, E=1e-3, B=8, top-k, 1 MiB index blocks"
+# k_minmax, k_hist_prep, k_hist_dev, k_select, k_encode, k_scan_{reduce,top,apply},
+# k_enc_finalize, k_dec_count, k_scan_{reduce,top,apply}, k_dec_chunks
+GPU_LAUNCHES_PER_STEP = 14
 
 
 def parse():
@@ -185,22 +188,27 @@ def main():
     n_total = n_local * world
     elem0 = rank * n_local
     base, cur = workloads.cfg2_device(args.side, seed=rank)
+    out = torch.empty_like(base)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    ws = engine.default_workspace()
+    # sync-free compress + decompress of this rank's shard (engine.DevicePipeline)
+    pipe = engine.DevicePipeline(n_local, base.dtype, E, BITS, 1 << 20, elem0=elem0, n_total=n_total, comm=comm)
+    for _ in range(args.warmup):
+        pipe.step(base, cur, out)
+    chk = pipe.check()
+    assert chk["status"] == 0 and not chk["bad_index"] and not chk["exhausted"], chk
+    assert chk["n_sentinel"] == chk["n_inc"] and chk["tripwire"] == 0, chk
+    use_graph = world == 1
+    graph = pipe.capture(base, cur, out) if use_graph else None
 
-    def step(timing=False):
-        enc, off, tot = D.encode_shard(base, cur, elem0, n_total, E, BITS, 1 << 20, comm=comm, ws=ws,
-                                       timing=timing)
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        res = engine.decode_encoding(enc, base, ws=ws, check=False)
-        ev1.record(stream)
-        return enc, res, ev0, ev1
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            pipe.step(base, cur, out)
 
     for _ in range(args.warmup):
-        enc, res, _, _ = step()
+        step()
     torch.cuda.synchronize()
     if comm:
         dist.barrier()
@@ -211,14 +219,9 @@ def main():
     torch.cuda.synchronize()
     if comm:
         dist.barrier()
-    phases = {"change_ratio": [], "binning": [], "assign_index": [], "decode": []}
     t_start.record(stream)
     for _ in range(args.steps):
-        enc, res, d0, d1 = step(timing=True)
-        for k, v in enc.phase_ms.items():
-            phases[k].append(v)
-        d1.synchronize()
-        phases["decode"].append(d0.elapsed_time(d1))
+        step()
     t_end.record(stream)
     torch.cuda.synchronize()
     if comm:
@@ -233,24 +236,47 @@ def main():
     L = 8
     value = n_total * L / (ms_step / 1e3) / 1e9
 
-    # correctness guard on the last step (cheap, outside the timed region)
-    chk = engine.decode_encoding(enc, base, ws=ws)
-    assert not chk.bad_index and not chk.exhausted and int(chk.n_sentinel[0]) == enc.n_inc
+    # correctness guard on the timed buffers (outside the timed region)
+    chk = pipe.check()
+    assert chk["status"] == 0 and not chk["bad_index"] and not chk["exhausted"], chk
+    assert chk["n_sentinel"] == chk["n_inc"], chk
 
-    mean = {k: (sum(v) / len(v) if v else 0.0) for k, v in phases.items()}
+    # per-phase device times: a separate instrumented pass (events between phases)
+    phases = {}
+    for _ in range(3):
+        evs = [("start", torch.cuda.Event(enable_timing=True))]
+        evs[0][1].record(stream)
+
+        def mark(name, evs=evs):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            evs.append((name, e))
+
+        pipe.step(base, cur, out, mark=mark)
+        torch.cuda.synchronize()
+        for (_, e0), (nm, e1) in zip(evs[:-1], evs[1:]):
+            phases.setdefault(nm, []).append(e0.elapsed_time(e1))
+    mean = {k: sum(v) / len(v) for k, v in phases.items()}
+
+    class _Enc:  # geometry for the roofline arithmetic
+        n_inc = chk["n_inc"]
+        k = chk["k"]
+        prefix = pipe.prefix
+        stride = pipe.stride
+    enc = _Enc()
     nb_local = enc.prefix.numel()
     k4_bytes = n_local * (2 * L + BITS / 8) + enc.n_inc * L + 8 * nb_local
     k5_bytes = n_local * (2 * L + BITS / 8) + enc.n_inc * L
     k1_bytes = k2_bytes = 2 * n_local * L
     peak, peak_src = peaks()
-    k4_gbs = k4_bytes / (mean["assign_index"] / 1e3) / 1e9
-    k5_gbs = k5_bytes / (mean["decode"] / 1e3) / 1e9
+    k4_gbs = k4_bytes / (mean["K4_encode"] / 1e3) / 1e9
+    k5_gbs = k5_bytes / (mean["K5_decode"] / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("k_encode_dram_bytes_per_launch")
-    compress_ms = mean["change_ratio"] + mean["binning"] + mean["assign_index"]
+    compress_ms = mean["K1_minmax"] + mean["K2_histogram"] + mean["K3_select"] + mean["K4_encode"]
 
     e2e = None
     if not args.no_e2e:
@@ -294,24 +320,29 @@ def main():
             "config": {"workload": CONFIG_NAME, "n_per_gpu": n_local, "n_total": n_total,
                        "parallelism": f"dp{world} (contiguous element shards)",
                        "l2": "inputs 2 GiB/GPU > 126 MB L2 (no flush needed)",
-                       "k": enc.k, "alpha": enc.n_inc / n_local, "hist_form": enc.hist_form},
-            "compress": {"ms": compress_ms, "gbs_per_gpu": n_local * L / (compress_ms / 1e3) / 1e9,
-                         "phase_ms": {k: mean[k] for k in ("change_ratio", "binning", "assign_index")}},
-            "decompress": {"ms": mean["decode"], "gbs_per_gpu": n_local * L / (mean["decode"] / 1e3) / 1e9},
+                       "k": enc.k, "alpha": enc.n_inc / n_local, "hist_form": "dense",
+                       "execution": "sync-free device pipeline" + (" replayed as one CUDA graph" if use_graph else "")},
+            "compress": {"ms": compress_ms, "gbs_per_gpu": n_local * L / (compress_ms / 1e3) / 1e9},
+            "decompress": {"ms": mean["K5_decode"], "gbs_per_gpu": n_local * L / (mean["K5_decode"] / 1e3) / 1e9},
+            "phase_ms": mean,
             "roofline": {"bound": "hbm", "kernel": "k_encode (K4)", "achieved": k4_gbs, "peak": peak,
                          "unit": "GB/s", "frac": k4_gbs / peak, "traffic": traffic,
                          "alg_bytes_per_launch": k4_bytes, "peak_source": peak_src},
             "roofline_all": {
-                "K1_minmax": {"alg_bytes": k1_bytes, "ms": mean["change_ratio"],
-                              "gbs": k1_bytes / (mean["change_ratio"] / 1e3) / 1e9},
-                "K2K3_hist_select": {"alg_bytes": k2_bytes, "ms": mean["binning"],
-                                     "gbs": k2_bytes / (mean["binning"] / 1e3) / 1e9},
-                "K4_encode": {"alg_bytes": k4_bytes, "ms": mean["assign_index"], "gbs": k4_gbs,
-                              "frac": k4_gbs / peak},
-                "K5_decode": {"alg_bytes": k5_bytes, "ms": mean["decode"], "gbs": k5_gbs, "frac": k5_gbs / peak},
-                "note": "phase times include the host reads between phases (3 small D2H syncs)"},
+                "K1_minmax": {"alg_bytes": k1_bytes, "ms": mean["K1_minmax"],
+                              "gbs": k1_bytes / (mean["K1_minmax"] / 1e3) / 1e9,
+                              "frac": k1_bytes / (mean["K1_minmax"] / 1e3) / 1e9 / peak},
+                "K2_histogram": {"alg_bytes": k2_bytes, "ms": mean["K2_histogram"],
+                                 "gbs": k2_bytes / (mean["K2_histogram"] / 1e3) / 1e9,
+                                 "frac": k2_bytes / (mean["K2_histogram"] / 1e3) / 1e9 / peak},
+                "K3_select": {"ms": mean["K3_select"]},
+                "K4_encode": {"alg_bytes": k4_bytes, "ms": mean["K4_encode"], "gbs": k4_gbs,
+                              "frac": k4_gbs / peak, "note": "includes chunk-count scan + finalize"},
+                "K5_decode": {"alg_bytes": k5_bytes, "ms": mean["K5_decode"], "gbs": k5_gbs, "frac": k5_gbs / peak,
+                              "note": "includes the sentinel-count pass (+B/8 bytes/element) and its scan"},
+                "note": "phase times from an event-instrumented pass; the headline value is the graph replay"},
             "e2e": e2e,
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
             "cpu_baseline": cpu,
             "clocks": clk,
         }

@@ -36,6 +36,12 @@ extern "C" {
 #define NMK_ERR_ARG         -1   /* bad argument (ValueError in Python)            */
 #define NMK_ERR_CUDA        -2   /* CUDA runtime / launch failure                   */
 #define NMK_ERR_EMPTY_HIST  -6   /* no selectable bin: binning.py:145-146          */
+#define NMK_ERR_NEEDS_SPARSE -7  /* sync-free path: span too wide for the dense
+                                    histogram; rerun the sparse path             */
+
+/* nmk_stats.reserved after nmk_hist_prep: the dense span, 0 when no ratio is
+ * valid, NMK_SPAN_SPARSE when it exceeds the dense capacity. */
+#define NMK_SPAN_SPARSE 0xffffffffffffffffULL
 
 #define NMK_F32 0
 #define NMK_F64 1
@@ -157,6 +163,41 @@ int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_bloc
                const uint64_t* h_seg_out, int nseg,
                nmk_segment_info* seg_info, nmk_decode_err* err,
                void* ws, size_t ws_bytes, void* stream);
+
+/* -- sync-free (graph-capturable) variants ---------------------------------
+ * Every decision scalar stays on the device, so a whole compress + decompress
+ * step can be enqueued (or captured in a CUDA graph) without a host round
+ * trip; the host reads stats/model/n_inc once at the end and reruns the
+ * general path in the rare cases flagged there (NMK_ERR_NEEDS_SPARSE).
+ *  - nmk_hist_prep: dense span from stats into stats->reserved, zero counts.
+ *  - nmk_hist_dense_dev: K2 reading the span from stats->reserved.
+ *  - nmk_select with m_max == 0 and keys == NULL reads the span likewise
+ *    (and sets model->status = NMK_ERR_NEEDS_SPARSE if it was too wide).
+ *  - nmk_encode_dev: K4 reading k and tol_bin from `model`; k_cap bounds k
+ *    (sizes shared memory); does nothing if model->status != 0.
+ *  - nmk_decode_dev: K5 reading k from `model` and the exact-value count
+ *    from the device scalar `n_exact`; segments are passed by value
+ *    (nseg <= NMK_DEV_MAX_SEG), so nothing is copied from the host. */
+#define NMK_DEV_MAX_SEG 4
+int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins,
+                  unsigned long long* counts, void* stream);
+int nmk_hist_dense_dev(const void* base, const void* cur, uint64_t n, int dtype,
+                       const nmk_stats* stats, double width,
+                       unsigned long long* counts, void* stream);
+int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
+                   uint64_t n_total, int dtype, const double* centers, const double* cuts,
+                   const nmk_model* model, int k_cap, int bits, double tolerance, uint64_t epb,
+                   uint8_t* packed, uint64_t block_stride, void* exact,
+                   unsigned long long* prefix, unsigned long long* n_inc,
+                   void* ws, size_t ws_bytes, void* stream);
+int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint64_t first_block,
+                   int bits, uint64_t epb, uint64_t n_total,
+                   const unsigned long long* prefix_rel, const double* centers,
+                   const nmk_model* model, const void* exact,
+                   const unsigned long long* n_exact, const void* base, void* out, int dtype,
+                   const uint64_t* h_seg_start, const uint64_t* h_seg_count,
+                   const uint64_t* h_seg_out, int nseg, nmk_segment_info* seg_info,
+                   nmk_decode_err* err, void* ws, size_t ws_bytes, void* stream);
 
 /* -- standalone codec kernels (codec.py:83-105) ---------------------------- */
 int nmk_pack(const uint32_t* codes, uint64_t n, int bits, uint8_t* out, void* stream);

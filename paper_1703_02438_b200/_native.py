@@ -18,6 +18,9 @@ NMK_OK = 0
 NMK_ERR_ARG = -1
 NMK_ERR_CUDA = -2
 NMK_ERR_EMPTY_HIST = -6
+NMK_ERR_NEEDS_SPARSE = -7
+NMK_SPAN_SPARSE = 0xFFFFFFFFFFFFFFFF
+NMK_DEV_MAX_SEG = 4
 
 NMK_F32 = 0
 NMK_F64 = 1
@@ -69,6 +72,12 @@ SIGNATURES = {
     "nmk_decode_ws_bytes": (sz, [u64p, u64p, i32, u64, u64]),
     "nmk_decode": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, i32, vp, u64, vp, vp, i32,
                          u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
+    "nmk_hist_prep": (i32, [vp, dbl, u64, vp, vp]),
+    "nmk_hist_dense_dev": (i32, [vp, vp, u64, i32, vp, dbl, vp, vp]),
+    "nmk_encode_dev": (i32, [vp, vp, u64, u64, u64, i32, vp, vp, vp, i32, i32, dbl, u64, vp, u64, vp,
+                             vp, vp, vp, sz, vp]),
+    "nmk_decode_dev": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, i32,
+                             u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
     "nmk_pack": (i32, [vp, u64, i32, vp, vp]),
     "nmk_unpack": (i32, [vp, u64, i32, vp, vp]),
 }

@@ -36,6 +36,10 @@ struct Seg {
   uint64_t gfirst;              // global chunk id of the segment's first chunk
 };
 
+struct SegParams {
+  Seg s[NMK_DEV_MAX_SEG];
+};
+
 struct DecodeGeom {
   uint64_t epb, n_total, first_block, stride, n_exact, nchunks, nitems;
   uint32_t cpb;
@@ -228,10 +232,11 @@ __device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo,
 
 template <typename T, int B>
 __global__ void __launch_bounds__(kTmaThreads, 6)
-k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs,
+k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs, SegParams sp,
              const unsigned long long* __restrict__ offsets, const unsigned long long* __restrict__ prefix_rel,
              const double* __restrict__ centers_g, const T* __restrict__ exact, const T* __restrict__ base,
-             T* __restrict__ out, nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err) {
+             T* __restrict__ out, nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err,
+             const nmk_model* __restrict__ model, const unsigned long long* __restrict__ n_exact_dev) {
   using ST = DecStage<T, B>;
   constexpr int VN = DVec<T>::N;          // elements per 16-byte vector
   constexpr int Q = kGroup / VN;          // vectors per lane per chunk
@@ -240,15 +245,22 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   __shared__ __align__(8) unsigned long long bars[kTmaWarps][kStages];
   __shared__ Seg s_segs[kSmemSegs];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (model) {                       // sync-free path: scalars from the device
+    if (model->status != 0) return;
+    geo.k = model->k;
+  }
+  if (n_exact_dev) geo.n_exact = *n_exact_dev;
   const bool seg_smem = geo.nseg <= kSmemSegs;
-  if (seg_smem)
+  if (!segs)
+    for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = sp.s[i];
+  else if (seg_smem)
     for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = segs[i];
   if (lane == 0) {
     for (int st = 0; st < kStages; ++st) mbar_init(&bars[wid][st], 1);
     mbar_fence_init();
   }
   __syncthreads();
-  const Seg* SG = seg_smem ? s_segs : segs;
+  const Seg* SG = (seg_smem || !segs) ? s_segs : segs;
   uint8_t* wst = dsm + (size_t)wid * kStages * ST::kBytes;
   const uint32_t sentinel = (1u << B) - 1u;
   const uint32_t k = (uint32_t)geo.k;
@@ -291,6 +303,83 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
       const uint8_t* src = chunk_src<B>(packed, geo, t.d);
       for (int i = lane; i < 32 * B; i += 32) sb[ST::kBase + i] = (uint32_t)i < t.d.nbytes ? __ldg(src + i) : 0;
       __syncwarp();
+    }
+    if (t.base_tma && out_al) {
+      // fast path: the whole chunk lies inside the segment and its block, so
+      // no element needs a bounds test; ranks only if the warp has sentinels
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const V w = *reinterpret_cast<const V*>(sb + 16 * lane + 512 * q);
+        const T* tw = reinterpret_cast<const T*>(&w);
+#pragma unroll
+        for (int v = 0; v < VN; ++v) bv[q][v] = tw[v];
+      }
+      unsigned smask = 0, badmask = 0, cnt_pk = 0;
+      uint32_t code[Q][VN];
+      T ov[Q][VN];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        unsigned c = 0;
+#pragma unroll
+        for (int v = 0; v < VN; ++v) {
+          const uint32_t cd = code_at<B>(sb + ST::kBase, VN * lane + 32 * VN * q + v);
+          code[q][v] = cd;
+          const bool snt = cd == sentinel;
+          smask |= (snt ? 1u : 0u) << (q * VN + v);
+          badmask |= (!snt && cd >= k ? 1u : 0u) << (q * VN + v);
+          c += snt;
+          ov[q][v] = apply_center<T>(__ldg(centers_g + min(cd, k - 1)), to_f64(bv[q][v]));
+        }
+        cnt_pk |= c << (8 * q);
+      }
+      if (__any_sync(0xffffffffu, smask != 0)) {
+        unsigned incl = cnt_pk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        const unsigned excl = incl - cnt_pk;
+        unsigned long long before_q = 0;
+        unsigned exhausted = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          unsigned long long pos = chunk_off + before_q + ((excl >> (8 * q)) & 255u);
+          before_q += (tot >> (8 * q)) & 255u;
+#pragma unroll
+          for (int v = 0; v < VN; ++v)
+            if (smask >> (q * VN + v) & 1u) {
+              if (pos < geo.n_exact) ov[q][v] = exact[pos];
+              else exhausted = 1;
+              ++pos;
+            }
+        }
+        if (exhausted) atomicOr(&err->exhausted, 1u);
+        const unsigned in_s = __reduce_add_sync(0xffffffffu, __popc(smask));
+        if (lane == 0) atomicAdd(&info[t.seg].n_sentinel, (unsigned long long)in_s);
+      }
+      if (badmask) {
+        unsigned maxbad = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+          for (int v = 0; v < VN; ++v)
+            if (badmask >> (q * VN + v) & 1u) maxbad = max(maxbad, code[q][v]);
+        atomicOr(&err->bad_index, 1u);
+        atomicMax(&err->max_bad_index, maxbad);
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        *reinterpret_cast<V*>(out + t.oi0 + VN * lane + 32 * VN * q) = *reinterpret_cast<const V*>(&ov[q][0]);
+      if (t.first && lane == 0) info[t.seg].inc_before = chunk_off;
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        const uint64_t nx = it + (uint64_t)kStages * nw;
+        if (nx < geo.nitems) issue(st, nx);
+      }
+      continue;
     }
     if (t.base_tma) {
 #pragma unroll
@@ -432,10 +521,11 @@ static DecodePlan decode_plan(const uint64_t* st, const uint64_t* ct, int nseg, 
 }
 
 template <typename T, int B>
-static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, uint32_t* counts,
-                          unsigned long long* offsets, void* scan_ws, const unsigned long long* prefix_rel,
-                          const double* centers, const void* exact, const void* base, void* out,
-                          nmk_segment_info* info, nmk_decode_err* err, cudaStream_t s) {
+static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, const SegParams& sp,
+                          uint32_t* counts, unsigned long long* offsets, void* scan_ws,
+                          const unsigned long long* prefix_rel, const double* centers, const void* exact,
+                          const void* base, void* out, nmk_segment_info* info, nmk_decode_err* err,
+                          const nmk_model* model, const unsigned long long* n_exact_dev, cudaStream_t s) {
   const int sms = sm_count_d();
   const uint64_t g1 = (geo.nchunks + 7) / 8;
   const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
@@ -453,20 +543,21 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   uint64_t grid = (uint64_t)sms * per_sm;
   const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;
   if (grid > need) grid = need;
-  k_dec_chunks<T, B><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, offsets, prefix_rel, centers,
+  k_dec_chunks<T, B><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, sp, offsets, prefix_rel, centers,
                                                                 (const T*)exact, (const T*)base, (T*)out, info,
-                                                                err);
+                                                                err, model, n_exact_dev);
 }
 
 template <typename T>
-static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, uint32_t* counts,
-                           unsigned long long* offsets, void* scan_ws, const unsigned long long* prefix_rel,
-                           const double* centers, const void* exact, const void* base, void* out,
-                           nmk_segment_info* info, nmk_decode_err* err, cudaStream_t s) {
+static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& geo, const Seg* segs,
+                           const SegParams& sp, uint32_t* counts, unsigned long long* offsets, void* scan_ws,
+                           const unsigned long long* prefix_rel, const double* centers, const void* exact,
+                           const void* base, void* out, nmk_segment_info* info, nmk_decode_err* err,
+                           const nmk_model* model, const unsigned long long* n_exact_dev, cudaStream_t s) {
   switch (bits) {
 #define NMK_DEC_CASE(BB)                                                                                    \
-  case BB: launch_decode<T, BB>(packed, geo, segs, counts, offsets, scan_ws, prefix_rel, centers, exact, base, \
-                                out, info, err, s); break;
+  case BB: launch_decode<T, BB>(packed, geo, segs, sp, counts, offsets, scan_ws, prefix_rel, centers, exact, \
+                                base, out, info, err, model, n_exact_dev, s); break;
     NMK_DEC_CASE(2) NMK_DEC_CASE(3) NMK_DEC_CASE(4) NMK_DEC_CASE(5) NMK_DEC_CASE(6) NMK_DEC_CASE(7)
     NMK_DEC_CASE(8) NMK_DEC_CASE(9) NMK_DEC_CASE(10) NMK_DEC_CASE(11) NMK_DEC_CASE(12) NMK_DEC_CASE(13)
     NMK_DEC_CASE(14) NMK_DEC_CASE(15) NMK_DEC_CASE(16) NMK_DEC_CASE(17) NMK_DEC_CASE(18) NMK_DEC_CASE(19)
@@ -488,13 +579,12 @@ extern "C" size_t nmk_decode_ws_bytes(const uint64_t* h_seg_start, const uint64_
   return decode_plan(h_seg_start, h_seg_count, nseg, epb, first_block).total;
 }
 
-extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
-                          uint64_t epb, uint64_t n_total, const unsigned long long* prefix_rel,
-                          const double* centers, int k, const void* exact, uint64_t n_exact, const void* base,
-                          void* out, int dtype, const uint64_t* h_seg_start, const uint64_t* h_seg_count,
-                          const uint64_t* h_seg_out, int nseg, nmk_segment_info* seg_info,
-                          nmk_decode_err* err, void* ws, size_t ws_bytes, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits, uint64_t epb,
+                       uint64_t n_total, const unsigned long long* prefix_rel, const double* centers, int k,
+                       const nmk_model* model, const void* exact, uint64_t n_exact,
+                       const unsigned long long* n_exact_dev, const void* base, void* out, int dtype,
+                       const uint64_t* h_seg_start, const uint64_t* h_seg_count, const uint64_t* h_seg_out, int nseg,
+                       nmk_segment_info* seg_info, nmk_decode_err* err, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (nseg < 1 || !h_seg_start || !h_seg_count || !h_seg_out || !seg_info || !err || !ws)
     return set_error(NMK_ERR_ARG, "nmk_decode: bad argument");
   if (bits < 2 || bits > 30 || epb == 0 || k < 1) return set_error(NMK_ERR_ARG, "nmk_decode: bad geometry");
@@ -531,7 +621,14 @@ extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t
   cudaMemsetAsync(err, 0, sizeof(nmk_decode_err), s);
   // a pageable H2D cudaMemcpyAsync returns after staging the source, so the
   // host table can be released immediately (no stream synchronisation)
-  cudaMemcpyAsync(dsegs, hs, sizeof(Seg) * (size_t)nseg, cudaMemcpyHostToDevice, s);
+  SegParams sp{};
+  const bool by_value = model != nullptr && nseg <= NMK_DEV_MAX_SEG;
+  if (by_value) {
+    for (int i = 0; i < nseg; ++i) sp.s[i] = hs[i];
+    dsegs = nullptr;   // no host->device copy: graph-capturable
+  } else {
+    cudaMemcpyAsync(dsegs, hs, sizeof(Seg) * (size_t)nseg, cudaMemcpyHostToDevice, s);
+  }
   free(hs);
   DecodeGeom geo{};
   geo.epb = epb;
@@ -546,8 +643,32 @@ extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t
   geo.nseg = nseg;
   geo.k = k;
   if (dtype == NMK_F64)
-    return dispatch_decode<double>(bits, packed, geo, dsegs, counts, offsets, w + p.off_scan, prefix_rel, centers,
-                                   exact, base, out, seg_info, err, s);
-  return dispatch_decode<float>(bits, packed, geo, dsegs, counts, offsets, w + p.off_scan, prefix_rel, centers,
-                                exact, base, out, seg_info, err, s);
+    return dispatch_decode<double>(bits, packed, geo, dsegs, sp, counts, offsets, w + p.off_scan, prefix_rel,
+                                   centers, exact, base, out, seg_info, err, model, n_exact_dev, s);
+  return dispatch_decode<float>(bits, packed, geo, dsegs, sp, counts, offsets, w + p.off_scan, prefix_rel, centers,
+                                exact, base, out, seg_info, err, model, n_exact_dev, s);
+}
+
+extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
+                          uint64_t epb, uint64_t n_total, const unsigned long long* prefix_rel,
+                          const double* centers, int k, const void* exact, uint64_t n_exact, const void* base,
+                          void* out, int dtype, const uint64_t* h_seg_start, const uint64_t* h_seg_count,
+                          const uint64_t* h_seg_out, int nseg, nmk_segment_info* seg_info,
+                          nmk_decode_err* err, void* ws, size_t ws_bytes, void* stream) {
+  return decode_impl(packed, block_stride, first_block, bits, epb, n_total, prefix_rel, centers, k, nullptr, exact,
+                     n_exact, nullptr, base, out, dtype, h_seg_start, h_seg_count, h_seg_out, nseg, seg_info, err, ws,
+                     ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
+                              uint64_t epb, uint64_t n_total, const unsigned long long* prefix_rel,
+                              const double* centers, const nmk_model* model, const void* exact,
+                              const unsigned long long* n_exact, const void* base, void* out, int dtype,
+                              const uint64_t* h_seg_start, const uint64_t* h_seg_count, const uint64_t* h_seg_out,
+                              int nseg, nmk_segment_info* seg_info, nmk_decode_err* err, void* ws, size_t ws_bytes,
+                              void* stream) {
+  if (!model || !n_exact) return set_error(NMK_ERR_ARG, "nmk_decode_dev: model and n_exact required");
+  return decode_impl(packed, block_stride, first_block, bits, epb, n_total, prefix_rel, centers, 1, model, exact, 0,
+                     n_exact, base, out, dtype, h_seg_start, h_seg_count, h_seg_out, nseg, seg_info, err, ws, ws_bytes,
+                     (cudaStream_t)stream);
 }

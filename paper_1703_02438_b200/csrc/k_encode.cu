@@ -228,22 +228,37 @@ __global__ void __launch_bounds__(kEncThreads, 4)
 k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
          double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
-         uint32_t* __restrict__ counts) {
+         uint32_t* __restrict__ counts, const nmk_model* __restrict__ model, bool smem_ok) {
   __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
   __shared__ uint16_t lut[kLutCells];
   __shared__ double s_lo, s_scale;
   __shared__ bool s_use;
-  extern __shared__ __align__(16) double cuts_s[];
+  extern __shared__ __align__(16) double cutsp[];   // [-inf, cuts..., +inf, +inf]
 
+  if (model) {   // sync-free path: the model scalars live on the device
+    if (model->status != 0) {   // nothing to encode: leave empty chunks behind
+      for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += gridDim.x * blockDim.x)
+        counts[c] = 0;
+      return;
+    }
+    k = model->k;
+    tol_bin = model->tol_bin;
+  }
   const int ncuts = k - 1;
-  const bool cuts_in_smem = k <= kSmemCuts + 1;
-  if (cuts_in_smem)
-    for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cuts_s[i] = cuts_g[i];
+  const bool cuts_in_smem = smem_ok && k <= kSmemCuts + 1;
+  if (cuts_in_smem) {
+    for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cutsp[i + 1] = cuts_g[i];
+    if (threadIdx.x == 0) {
+      cutsp[0] = __longlong_as_double(0xfff0000000000000LL);
+      cutsp[ncuts + 1] = __longlong_as_double(0x7ff0000000000000LL);
+      cutsp[ncuts + 2] = cutsp[ncuts + 1];   // read (unused) when i == ncuts
+    }
+  }
   __syncthreads();
   if (cuts_in_smem) {
     double lo, sc;
     bool use;
-    build_cut_lut(cuts_s, ncuts, lut, lo, sc, use);
+    build_cut_lut(cutsp + 1, ncuts, lut, lo, sc, use);
     if (threadIdx.x == 0) { s_lo = lo; s_scale = sc; s_use = use; }
   } else if (threadIdx.x == 0) {
     s_lo = 0.0; s_scale = 0.0; s_use = false;
@@ -251,16 +266,21 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
   __syncthreads();
   uint8_t* my = wbytes[threadIdx.x >> 5];
   if (s_use) {
-    // O(1) search: grid cell -> first candidate, exact compares against the
-    // shared-memory cuts settle it (normally zero or one step)
+    // O(1) search: the grid cell gives i = #cuts below the cell's left edge;
+    // with at most one cut per cell the answer is i or i+1, settled by exact
+    // compares against the three candidate cuts (padded with -inf/+inf).
+    // Any other case (rounding at a cell edge, a crowded cell) walks exactly.
     const double lo = s_lo, scale = s_scale;
     encode_chunks<T, B>(base, cur, geo, centers_g, tol_bin, tol, packed, scratch, counts, my,
                         [&](double r) -> uint32_t {
                           int g = __double2int_rz((r - lo) * scale);   // saturating
                           g = min(max(g, 0), kLutCells - 1);
                           int i = lut[g];
-                          while (i < ncuts && cuts_s[i] < r) ++i;
-                          while (i > 0 && cuts_s[i - 1] >= r) --i;
+                          const double a = cutsp[i], m = cutsp[i + 1], z = cutsp[i + 2];
+                          const bool up = m < r;
+                          if (up ? (r <= z) : (a < r)) return (uint32_t)(i + up);
+                          while (i < ncuts && cutsp[i + 1] < r) ++i;
+                          while (i > 0 && cutsp[i] >= r) --i;
                           return (uint32_t)i;
                         });
   } else {
@@ -423,8 +443,9 @@ static EncodeWs encode_ws_layout(uint64_t nchunks, int elem_bytes) {
 template <typename T, int B>
 static void launch_encode(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
                           const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
-                          uint32_t* counts, cudaStream_t s) {
-  const size_t smem = (k <= kSmemCuts + 1 && k > 1) ? (size_t)(k - 1) * 8 : 0;
+                          uint32_t* counts, const nmk_model* model, int k_cap, cudaStream_t s) {
+  const bool smem_ok = k_cap <= kSmemCuts + 1;
+  const size_t smem = smem_ok ? (size_t)(k_cap + 2) * 8 : 0;
   static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(k_encode<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -437,16 +458,17 @@ static void launch_encode(const void* base, const void* cur, const EncodeGeom& g
   uint64_t need = (geo.nchunks + 7) / 8;
   if (grid > need) grid = need;
   k_encode<T, B><<<(unsigned)grid, kEncThreads, smem, s>>>((const T*)base, (const T*)cur, geo, centers, cuts, k,
-                                                           tol_bin, tol, packed, (T*)scratch, counts);
+                                                           tol_bin, tol, packed, (T*)scratch, counts, model, smem_ok);
 }
 
 template <typename T>
 static int dispatch_encode(int bits, const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
                            const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
-                           uint32_t* counts, cudaStream_t s) {
+                           uint32_t* counts, const nmk_model* model, int k_cap, cudaStream_t s) {
   switch (bits) {
-#define NMK_ENC_CASE(BB) \
-  case BB: launch_encode<T, BB>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, s); break;
+#define NMK_ENC_CASE(BB)                                                                                           \
+  case BB: launch_encode<T, BB>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, model, \
+                                k_cap, s); break;
     NMK_ENC_CASE(2) NMK_ENC_CASE(3) NMK_ENC_CASE(4) NMK_ENC_CASE(5) NMK_ENC_CASE(6) NMK_ENC_CASE(7)
     NMK_ENC_CASE(8) NMK_ENC_CASE(9) NMK_ENC_CASE(10) NMK_ENC_CASE(11) NMK_ENC_CASE(12) NMK_ENC_CASE(13)
     NMK_ENC_CASE(14) NMK_ENC_CASE(15) NMK_ENC_CASE(16) NMK_ENC_CASE(17) NMK_ENC_CASE(18) NMK_ENC_CASE(19)
@@ -458,6 +480,13 @@ static int dispatch_encode(int bits, const void* base, const void* cur, const En
   return check_launch("k_encode");
 }
 
+// Shared body of nmk_encode / nmk_encode_dev.
+static int encode_impl(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
+                       int dtype, const double* centers, const double* cuts, int k, const nmk_model* model,
+                       int k_cap, int bits, double tol_bin, double tolerance, uint64_t epb, uint8_t* packed,
+                       uint64_t block_stride, void* exact, unsigned long long* prefix, unsigned long long* n_inc,
+                       void* ws, size_t ws_bytes, cudaStream_t s);
+
 }  // namespace nmk
 
 using namespace nmk;
@@ -467,22 +496,21 @@ extern "C" size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t
   return encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8).total;
 }
 
-extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
-                          int dtype, const double* centers, const double* cuts, int k, int bits, double tol_bin,
-                          double tolerance, uint64_t epb, uint8_t* packed, uint64_t block_stride, void* exact,
-                          unsigned long long* prefix, unsigned long long* n_inc, void* ws, size_t ws_bytes,
-                          void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
+                            int dtype, const double* centers, const double* cuts, int k, const nmk_model* model,
+                            int k_cap, int bits, double tol_bin, double tolerance, uint64_t epb, uint8_t* packed,
+                            uint64_t block_stride, void* exact, unsigned long long* prefix,
+                            unsigned long long* n_inc, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (n_local == 0) {
     cudaMemsetAsync(n_inc, 0, sizeof(unsigned long long), s);
     return check_launch("nmk_encode(empty)");
   }
-  if (!base || !cur || !centers || !packed || !exact || !prefix || !n_inc || !ws || k < 1)
+  if (!base || !cur || !centers || !packed || !exact || !prefix || !n_inc || !ws || k < 1 || k_cap < k)
     return set_error(NMK_ERR_ARG, "nmk_encode: bad argument");
   if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_encode: bad dtype");
-  if (k > 1 && !cuts) return set_error(NMK_ERR_ARG, "nmk_encode: cuts required for k > 1");
+  if (k_cap > 1 && !cuts) return set_error(NMK_ERR_ARG, "nmk_encode: cuts required for k > 1");
   if (bits < 2 || bits > 30) return set_error(NMK_ERR_ARG, "nmk_encode: bits %d outside [2, 30]", bits);
-  if ((uint64_t)k > (1ULL << bits) - 1) return set_error(NMK_ERR_ARG, "nmk_encode: k %d exceeds 2^B-1", k);
+  if ((uint64_t)k_cap > (1ULL << bits) - 1) return set_error(NMK_ERR_ARG, "nmk_encode: k %d exceeds 2^B-1", k_cap);
   if (epb == 0 || elem0 + n_local > n_total) return set_error(NMK_ERR_ARG, "nmk_encode: bad geometry");
   if (block_stride % 16 || block_stride < (epb * bits + 7) / 8)
     return set_error(NMK_ERR_ARG, "nmk_encode: block_stride must be >= ceil(epb*B/8) and a multiple of 16");
@@ -505,9 +533,9 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
   if (c0_in_blk) cudaMemsetAsync(packed, 0, c0_in_blk * (uint64_t)(32 * bits), s);
   int rc = (dtype == NMK_F64)
                ? dispatch_encode<double>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
-                                         scratch, counts, s)
+                                         scratch, counts, model, k_cap, s)
                : dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
-                                        scratch, counts, s);
+                                        scratch, counts, model, k_cap, s);
   if (rc) return rc;
   chunk_scan(counts, et.nchunks, offsets, n_inc, wb + w.off_scan, s);
   unsigned grid = (unsigned)((et.nchunks + 255) / 256);
@@ -517,6 +545,25 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
   else
     k_enc_finalize<float><<<grid, 256, 0, s>>>(geo, counts, offsets, (const float*)scratch, (float*)exact, prefix);
   return check_launch("k_enc_finalize");
+}
+
+extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
+                          int dtype, const double* centers, const double* cuts, int k, int bits, double tol_bin,
+                          double tolerance, uint64_t epb, uint8_t* packed, uint64_t block_stride, void* exact,
+                          unsigned long long* prefix, unsigned long long* n_inc, void* ws, size_t ws_bytes,
+                          void* stream) {
+  return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, k, nullptr, k, bits, tol_bin, tolerance,
+                     epb, packed, block_stride, exact, prefix, n_inc, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
+                              int dtype, const double* centers, const double* cuts, const nmk_model* model,
+                              int k_cap, int bits, double tolerance, uint64_t epb, uint8_t* packed,
+                              uint64_t block_stride, void* exact, unsigned long long* prefix,
+                              unsigned long long* n_inc, void* ws, size_t ws_bytes, void* stream) {
+  if (!model) return set_error(NMK_ERR_ARG, "nmk_encode_dev: model required");
+  return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, 1, model, k_cap, bits, 0.0, tolerance,
+                     epb, packed, block_stride, exact, prefix, n_inc, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 template <int B>

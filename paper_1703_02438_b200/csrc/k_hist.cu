@@ -417,3 +417,130 @@ extern "C" int nmk_hist_merge(unsigned long long* keys, unsigned long long* coun
   k_rle_lengths_dev<<<g2, 256, 0, s>>>(w.run_start, nruns, w.scal, w.incl, counts);
   return check_launch("nmk_hist_merge");
 }
+
+// ---- sync-free dense histogram: the span is decided on the device ---------
+// k_hist_prep turns the (all-reduced) stats into the dense span
+//   nbins = floor(RN(RN(gmax - gmin) / width)) + 1
+// (the same f64 expression the host would evaluate), stores it in
+// stats->reserved (0: no valid ratio, NMK_SPAN_SPARSE: too wide to densify)
+// and zeroes counts[0 .. nbins] (the tripwire slot included).  k_hist_dev
+// then bins with shared-memory replicas when the span fits a fixed 48 KB
+// budget and with global atomics otherwise; no host round trip is needed.
+namespace nmk {
+
+constexpr uint32_t kDevSmemBins = 12 * 1024;   // 48 KB of u32 counters per CTA
+
+__global__ void k_hist_prep(nmk_stats* __restrict__ st, double width, uint64_t cap_bins,
+                            unsigned long long* __restrict__ counts) {
+  __shared__ unsigned long long s_nb;
+  if (threadIdx.x == 0) {
+    unsigned long long nb = 0;
+    if (st->nvalid) {
+      const double span = __ddiv_rn(__dsub_rn(st->gmax, st->gmin), width);
+      nb = (finite64(span) && span < (double)cap_bins) ? (unsigned long long)floor(span) + 1ULL : NMK_SPAN_SPARSE;
+    }
+    s_nb = nb;
+    if (blockIdx.x == 0) st->reserved = nb;
+  }
+  __syncthreads();
+  const unsigned long long nb = s_nb;
+  if (nb == 0 || nb == NMK_SPAN_SPARSE) return;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nb; i += (uint64_t)gridDim.x * blockDim.x)
+    counts[i] = 0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kHistThreads, 4)
+k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n, const nmk_stats* __restrict__ st,
+           double width, unsigned long long* __restrict__ counts, bool vec_ok) {
+  extern __shared__ uint32_t h[];
+  const unsigned long long nb64 = st->reserved;
+  if (nb64 == 0 || nb64 == NMK_SPAN_SPARSE) return;
+  const uint32_t nbins = (uint32_t)nb64;
+  const double gmin = st->gmin;
+  const double inv_w = 1.0 / width;
+  if (nbins <= kDevSmemBins) {
+    int reps = (int)(kDevSmemBins / nbins);
+    if (reps > kHistThreads / 32) reps = kHistThreads / 32;
+    for (uint32_t i = threadIdx.x; i < nbins * (uint32_t)reps; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    uint32_t* my = h + (uint32_t)((threadIdx.x >> 5) % reps) * nbins;
+    uint32_t last = 0xffffffffu, run = 0;
+    for_each_pair<T, 4>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
+      double q;
+      if (!element_ordinal(b, x, gmin, width, inv_w, q)) return;
+      const uint32_t qi = (q < (double)nbins) ? (uint32_t)q : nbins;   // nbins = tripwire
+      if (qi == last) {
+        ++run;
+      } else {
+        if (run) {
+          if (last < nbins) atomicAdd(&my[last], run);
+          else atomicAdd(&counts[nbins], (unsigned long long)run);
+        }
+        last = qi;
+        run = 1;
+      }
+    });
+    if (run) {
+      if (last < nbins) atomicAdd(&my[last], run);
+      else atomicAdd(&counts[nbins], (unsigned long long)run);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) {
+      uint32_t s = 0;
+      for (int r = 0; r < reps; ++r) s += h[r * nbins + i];
+      if (s) atomicAdd(&counts[i], (unsigned long long)s);
+    }
+  } else {
+    uint64_t last = ~0ULL;
+    unsigned long long run = 0;
+    for_each_pair<T, 2>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
+      double q;
+      if (!element_ordinal(b, x, gmin, width, inv_w, q)) return;
+      const uint64_t qi = (q < (double)nbins) ? (uint64_t)q : nbins;
+      if (qi == last) {
+        ++run;
+      } else {
+        if (run) atomicAdd(&counts[last], run);
+        last = qi;
+        run = 1;
+      }
+    });
+    if (run) atomicAdd(&counts[last], run);
+  }
+}
+
+}  // namespace nmk
+
+extern "C" int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins, unsigned long long* counts,
+                             void* stream) {
+  if (!stats || !counts || cap_bins == 0) return set_error(NMK_ERR_ARG, "nmk_hist_prep: bad argument");
+  k_hist_prep<<<sm_count_h() * 2, 256, 0, (cudaStream_t)stream>>>(stats, width, cap_bins, counts);
+  return check_launch("k_hist_prep");
+}
+
+extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, uint64_t n, int dtype, const nmk_stats* stats,
+                                  double width, unsigned long long* counts, void* stream) {
+  if (!base || !cur || !stats || !counts || n == 0) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  const size_t smem = kDevSmemBins * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_hist_dev<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_hist_dev<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  uint64_t want = (n + 8191) / 8192;
+  uint64_t grid = (uint64_t)sm_count_h() * 4;
+  if (want < grid) grid = want ? want : 1;
+  if (dtype == NMK_F64)
+    k_hist_dev<double><<<(unsigned)grid, kHistThreads, smem, s>>>((const double*)base, (const double*)cur, n, stats,
+                                                                  width, counts, aligned);
+  else if (dtype == NMK_F32)
+    k_hist_dev<float><<<(unsigned)grid, kHistThreads, smem, s>>>((const float*)base, (const float*)cur, n, stats,
+                                                                 width, counts, aligned);
+  else
+    return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad dtype");
+  return check_launch("k_hist_dev");
+}

@@ -88,9 +88,17 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     }
     return;
   }
-  BinView bv{keys, counts, nruns ? (uint64_t)*nruns : m_max, st->gmin, width, nullptr};
+  uint64_t Mv = nruns ? (uint64_t)*nruns : m_max;
+  if (!keys && m_max == 0) {   // sync-free path: span decided on the device
+    Mv = st->reserved;
+    if (Mv == NMK_SPAN_SPARSE) {
+      if (tid == 0) { model->status = NMK_ERR_NEEDS_SPARSE; model->k = 0; model->m_selectable = 0; }
+      return;
+    }
+  }
+  BinView bv{keys, counts, Mv, st->gmin, width, nullptr};
   const uint64_t M = bv.m;
-  if (m_max <= kSelCache) {   // every pass below then reads shared memory
+  if ((m_max == 0 && !keys) ? M <= kSelCache : m_max <= kSelCache) {   // passes then read shared memory
     for (uint64_t i = tid; i < M; i += kSelThreads) s_cache[i] = bv.sel_count(i);
     __syncthreads();
     bv.cache = s_cache;
@@ -308,7 +316,7 @@ extern "C" int nmk_select(const unsigned long long* keys, const unsigned long lo
   if (bits >= 0 && (bits < 2 || bits > 30)) return set_error(NMK_ERR_ARG, "nmk_select: bits %d outside [2, 30]", bits);
   if (keys && !nruns) return set_error(NMK_ERR_ARG, "nmk_select: sparse form needs nruns");
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t smem = m_max <= kSelCache ? (size_t)m_max * 8 : 0;
+  const size_t smem = (m_max == 0 && !keys) ? kSelCache * 8 : (m_max <= kSelCache ? (size_t)m_max * 8 : 0);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_select<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelCache * 8));

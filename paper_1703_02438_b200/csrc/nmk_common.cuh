@@ -142,7 +142,7 @@ __device__ __forceinline__ uint32_t lower_bound_cuts(const double* cuts, int ncu
 // guess; two exact compare loops then land on #cuts < r.  The answer is
 // exact whatever the rounding of the cell computation (monotone cuts), the
 // grid only makes it O(1) on average.
-constexpr int kLutCells = 4096;
+constexpr int kLutCells = 8192;
 
 struct CutLut {
   const double* cuts;      // shared memory

@@ -61,6 +61,25 @@ class ProcessGroupComm:
                         nv, 0], dtype=np.int64)
         stats[:4].copy_(torch.from_numpy(out).to(stats.device))
 
+    def allreduce_stats_device(self, stats) -> None:
+        """Same reduction with three device-side all-reduces (no host copy):
+        MIN over gmin, MAX over gmax, SUM over the valid counts."""
+        import torch
+        f = stats[:2].view(torch.float64)
+        self.dist.all_reduce(f[0:1], op=self.dist.ReduceOp.MIN, group=self.group)
+        self.dist.all_reduce(f[1:2], op=self.dist.ReduceOp.MAX, group=self.group)
+        self.dist.all_reduce(stats[2:3], op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def exscan_device(self, n_inc, offset_out, prefix=None, prefix_global=None) -> None:
+        """Exclusive scan of the per-rank incompressible counts on the device:
+        offset_out[0] = sum over lower ranks; prefix_global = prefix + offset."""
+        import torch
+        allv = torch.empty(self.world, dtype=torch.int64, device=n_inc.device)
+        self.dist.all_gather_into_tensor(allv, n_inc.reshape(1), group=self.group)
+        torch.sum(allv[: self.rank], dim=0, keepdim=True, out=offset_out) if self.rank else offset_out.zero_()
+        if prefix is not None and prefix_global is not None:
+            torch.add(prefix, offset_out, out=prefix_global)
+
     def agree_dense(self, dense: bool) -> bool:
         # every rank derives the same span from the same global (gmin, gmax)
         return dense

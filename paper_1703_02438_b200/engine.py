@@ -372,3 +372,154 @@ def decode_encoding(enc: DeviceEncoding, base, out=None, *, ws=None, stream=None
     # zero-fills the packed bytes between the block start and the range.
     return decode(enc.packed, enc.stride, enc.b0, enc.bits, enc.epb, enc.n, enc.prefix, enc.centers,
                   enc.exact, base, [(enc.elem0, enc.n_local, 0)], out, ws=ws, stream=stream, check=check)
+
+
+# ---------------------------------------------------------------------------
+# Sync-free pipeline (explicit B): every decision scalar stays on the device
+# ---------------------------------------------------------------------------
+
+ASYNC_COMM_BINS = 1 << 16     # dense span all-reduced without a host round trip
+
+
+class DevicePipeline:
+    """compress (K1..K4) + full decompress (K5) of one element range with no
+    host synchronisation: the dense span, k, tol_bin and the exact-value count
+    are produced and consumed on the device (nmk_hist_prep / *_dev entry
+    points), all buffers are preallocated, so one step can be enqueued — or
+    captured once in a CUDA graph and replayed.  ``check()`` reads the device
+    scalars once and reports the rare cases that need the general path (span
+    too wide for a dense histogram, empty histogram)."""
+
+    def __init__(self, n_local: int, dtype, tolerance: float, bits: int, block_bytes: int = 1 << 20,
+                 *, elem0: int = 0, n_total: int | None = None, comm=None, ws: Workspace | None = None):
+        torch = _torch()
+        if bits is None or not MIN_BITS <= bits <= MAX_BITS:
+            raise ValueError("the sync-free pipeline needs an explicit B in [2, 30]")
+        self.torch_dtype = dtype
+        self.dt = N.NMK_F64 if dtype == torch.float64 else N.NMK_F32
+        self.np_dtype = np.dtype("<f8") if self.dt == N.NMK_F64 else np.dtype("<f4")
+        self.n_local, self.elem0 = int(n_local), int(elem0)
+        self.n = int(n_total) if n_total is not None else self.n_local
+        self.tol, self.bits, self.block_bytes, self.comm = float(tolerance), int(bits), int(block_bytes), comm
+        self.width = 2.0 * self.tol
+        self.epb = elements_per_block(block_bytes, bits)
+        self.nblocks = -(-self.n // self.epb)
+        self.stride = block_stride(self.epb, bits)
+        self.b0 = self.elem0 // self.epb
+        self.nlb = (self.elem0 + self.n_local - 1) // self.epb - self.b0 + 1
+        self.k_cap = (1 << bits) - 1
+        self.cap_bins = ASYNC_COMM_BINS if comm is not None else DENSE_MAX_BINS
+        ws = ws or Workspace()
+        self.ws = ws
+        lib = N.lib()
+        dev = ws.device
+        self.stats = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(self.cap_bins + 1, dtype=torch.int64, device=dev)
+        self.centers = torch.zeros(self.k_cap, dtype=torch.float64, device=dev)
+        self.cuts = torch.zeros(self.k_cap, dtype=torch.float64, device=dev)
+        self.centers_t = torch.zeros(self.k_cap, dtype=dtype, device=dev)
+        self.model = torch.zeros(ctypes.sizeof(N.NmkModel) // 8, dtype=torch.int64, device=dev)
+        self.packed = torch.empty(self.nlb * self.stride, dtype=torch.uint8, device=dev)
+        self.exact = torch.empty(max(self.n_local, 1), dtype=dtype, device=dev)
+        self.prefix = torch.zeros(self.nlb, dtype=torch.int64, device=dev)
+        self.n_inc = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.inc_offset = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.prefix_global = torch.zeros(self.nlb, dtype=torch.int64, device=dev)
+        self.mm_bytes = lib.nmk_minmax_ws_bytes(self.n_local)
+        self.mm_ws = torch.zeros(self.mm_bytes, dtype=torch.uint8, device=dev)
+        self.e_bytes = lib.nmk_encode_ws_bytes(self.n_local, self.elem0, self.epb, self.dt)
+        self.e_ws = torch.empty(self.e_bytes, dtype=torch.uint8, device=dev)
+        seg = (ctypes.c_uint64 * 1)
+        self.s_start, self.s_count, self.s_out = seg(self.elem0), seg(self.n_local), seg(0)
+        self.d_bytes = lib.nmk_decode_ws_bytes(self.s_start, self.s_count, 1, self.epb, self.b0)
+        self.d_ws = torch.empty(self.d_bytes, dtype=torch.uint8, device=dev)
+        self.seg_info = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.err = torch.zeros(2, dtype=torch.int64, device=dev)
+        if comm is not None:
+            self.gathered_inc = torch.zeros(comm.world, dtype=torch.int64, device=dev)
+
+    # -- enqueue --------------------------------------------------------------
+    def encode(self, base, cur, mark=None):
+        """Enqueue K1..K4 (+ the exchanges).  ``mark(name)`` is called after
+        each phase (e.g. to record CUDA events)."""
+        lib, st = N.lib(), _stream()
+        P = lambda t: t.data_ptr()  # noqa: E731
+        mark = mark or (lambda name: None)
+        N.check(lib.nmk_minmax(P(base), P(cur), self.n_local, self.dt, P(self.stats), P(self.mm_ws), self.mm_bytes,
+                               st))
+        if self.comm is not None:
+            self.comm.allreduce_stats_device(self.stats)
+        mark("K1_minmax")
+        N.check(lib.nmk_hist_prep(P(self.stats), self.width, self.cap_bins, P(self.counts), st))
+        N.check(lib.nmk_hist_dense_dev(P(base), P(cur), self.n_local, self.dt, P(self.stats), self.width,
+                                       P(self.counts), st))
+        if self.comm is not None:
+            self.comm.allreduce_counts(self.counts)
+        mark("K2_histogram")
+        N.check(lib.nmk_select(None, P(self.counts), 0, None, P(self.stats), self.width, self.tol, self.bits, self.n,
+                               self.dt, P(self.centers), P(self.cuts), P(self.centers_t), self.k_cap, P(self.model),
+                               st))
+        mark("K3_select")
+        N.check(lib.nmk_encode_dev(P(base), P(cur), self.n_local, self.elem0, self.n, self.dt, P(self.centers),
+                                   P(self.cuts), P(self.model), self.k_cap, self.bits, self.tol, self.epb,
+                                   P(self.packed), self.stride, P(self.exact), P(self.prefix), P(self.n_inc),
+                                   P(self.e_ws), self.e_bytes, st))
+        mark("K4_encode")
+        if self.comm is not None:
+            # global positions of this rank's exact values / block prefixes;
+            # the local prefix stays as the decoder's rank anchor
+            self.comm.exscan_device(self.n_inc, self.inc_offset, self.prefix, self.prefix_global)
+
+    def decode(self, base, out):
+        lib, st = N.lib(), _stream()
+        P = lambda t: t.data_ptr()  # noqa: E731
+        N.check(lib.nmk_decode_dev(P(self.packed), self.stride, self.b0, self.bits, self.epb, self.n, P(self.prefix),
+                                   P(self.centers), P(self.model), P(self.exact), P(self.n_inc), P(base), P(out),
+                                   self.dt, self.s_start, self.s_count, self.s_out, 1, P(self.seg_info),
+                                   P(self.err), P(self.d_ws), self.d_bytes, st))
+
+    def step(self, base, cur, out, mark=None):
+        self.encode(base, cur, mark)
+        self.decode(base, out)
+        if mark:
+            mark("K5_decode")
+
+    def capture(self, base, cur, out, warmup: int = 1):
+        """Record step() once into a CUDA graph (buffers are fixed)."""
+        torch = _torch()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self.step(base, cur, out)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(base, cur, out)
+        return g
+
+    # -- host view (one synchronisation) --------------------------------------
+    def check(self) -> dict:
+        sv = _read_struct(self.stats, N.NmkStats)
+        model = _read_struct(self.model, N.NmkModel)
+        e = _read_struct(self.err, N.NmkDecodeErr)
+        n_inc = int(self.n_inc.item())
+        trip = int(self.counts[min(int(sv.reserved), self.cap_bins)].item()) \
+            if 0 < sv.reserved <= self.cap_bins else 0
+        return {"status": int(model.status), "bits": int(model.bits), "k": int(model.k), "n_inc": n_inc,
+                "gmin": float(sv.gmin), "gmax": float(sv.gmax), "nvalid": int(sv.nvalid), "nbins": int(sv.reserved),
+                "tripwire": trip, "bad_index": bool(e.bad_index), "exhausted": bool(e.exhausted),
+                "n_sentinel": int(self.seg_info[1].item())}
+
+    def encoding(self) -> DeviceEncoding:
+        """The finished encode as a DeviceEncoding (after check() passed)."""
+        c = self.check()
+        if c["status"] != 0:
+            raise N.NativeError(c["status"], "sync-free pipeline could not complete: rerun engine.encode")
+        k = c["k"]
+        return DeviceEncoding(
+            n=self.n, elem0=self.elem0, n_local=self.n_local, dtype=self.np_dtype, bits=self.bits, k=k,
+            epb=self.epb, nblocks=self.nblocks, b0=self.b0, stride=self.stride, centers=self.centers[:k],
+            centers_t=self.centers_t[:k], packed=self.packed, exact=self.exact[:c["n_inc"]], prefix=self.prefix,
+            n_inc=c["n_inc"], gmin=c["gmin"], gmax=c["gmax"], nvalid=c["nvalid"], hist_form="dense",
+            tol_bin=float(_read_struct(self.model, N.NmkModel).tol_bin))
