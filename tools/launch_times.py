@@ -20,5 +20,5 @@ tot = 0.0
 for k, v in acc.items():
     m = sum(v) / len(v)
     tot += sum(v)
-    print(f"{k[:50]:50s} n={len(v):3d} mean_us={m:9.2f}")
-print(f"total_us={tot:.1f}")
+    print(f"{k[:50]:50s} n={len(v):3d} mean_ns={m:9.0f}")
+print(f"total_ns={tot:.0f}")
