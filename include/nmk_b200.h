@@ -89,10 +89,12 @@ int nmk_version(void);
 int nmk_ratio(const void* base, const void* cur, uint64_t n, int dtype,
               double* ratios, uint8_t* valid, void* stream);
 
-/* -- K1: fused ratio + min/max + valid count (pipeline.py:190-212) -------- */
+/* -- K1: fused ratio + min/max + valid count (pipeline.py:190-212) --------
+ * keys (optional, 16-byte aligned float[n]): per-element f32 ratio key for
+ * the histogram pass (NaN: invalid element, +inf: decide exactly). */
 size_t nmk_minmax_ws_bytes(uint64_t n);
 int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
-               nmk_stats* stats, void* ws, size_t ws_bytes, void* stream);
+               nmk_stats* stats, float* keys, void* ws, size_t ws_bytes, void* stream);
 
 /* -- K2: histogram of floor((r - gmin) / width) over valid r
  *        (binning.py:110-116 via pipeline.py:214-224).
@@ -170,7 +172,9 @@ int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_bloc
  * trip; the host reads stats/model/n_inc once at the end and reruns the
  * general path in the rare cases flagged there (NMK_ERR_NEEDS_SPARSE).
  *  - nmk_hist_prep: dense span from stats into stats->reserved, zero counts.
- *  - nmk_hist_dense_dev: K2 reading the span from stats->reserved.
+ *  - nmk_hist_dense_dev: K2 reading the span from stats->reserved; with
+ *    `keys` from nmk_minmax it reads 4 bytes per element instead of both
+ *    snapshots and re-reads (base, cur) only where a key cannot decide.
  *  - nmk_select with m_max == 0 and keys == NULL reads the span likewise
  *    (and sets model->status = NMK_ERR_NEEDS_SPARSE if it was too wide).
  *  - nmk_encode_dev: K4 reading k and tol_bin from `model`; k_cap bounds k
@@ -181,8 +185,8 @@ int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_bloc
 #define NMK_DEV_MAX_SEG 4
 int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins,
                   unsigned long long* counts, void* stream);
-int nmk_hist_dense_dev(const void* base, const void* cur, uint64_t n, int dtype,
-                       const nmk_stats* stats, double width,
+int nmk_hist_dense_dev(const void* base, const void* cur, const float* keys, uint64_t n,
+                       int dtype, const nmk_stats* stats, double width,
                        unsigned long long* counts, void* stream);
 int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
                    uint64_t n_total, int dtype, const double* centers, const double* cuts,

@@ -59,7 +59,7 @@ SIGNATURES = {
     "nmk_version": (i32, []),
     "nmk_ratio": (i32, [vp, vp, u64, i32, vp, vp, vp]),
     "nmk_minmax_ws_bytes": (sz, [u64]),
-    "nmk_minmax": (i32, [vp, vp, u64, i32, vp, vp, sz, vp]),
+    "nmk_minmax": (i32, [vp, vp, u64, i32, vp, vp, vp, sz, vp]),
     "nmk_hist_dense": (i32, [vp, vp, u64, i32, vp, dbl, u64, vp, vp]),
     "nmk_hist_sparse_ws_bytes": (sz, [u64]),
     "nmk_hist_sparse": (i32, [vp, vp, u64, i32, vp, dbl, vp, vp, vp, vp, sz, vp]),
@@ -73,7 +73,7 @@ SIGNATURES = {
     "nmk_decode": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, i32, vp, u64, vp, vp, i32,
                          u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
     "nmk_hist_prep": (i32, [vp, dbl, u64, vp, vp]),
-    "nmk_hist_dense_dev": (i32, [vp, vp, u64, i32, vp, dbl, vp, vp]),
+    "nmk_hist_dense_dev": (i32, [vp, vp, vp, u64, i32, vp, dbl, vp, vp]),
     "nmk_encode_dev": (i32, [vp, vp, u64, u64, u64, i32, vp, vp, vp, i32, i32, dbl, u64, vp, u64, vp,
                              vp, vp, vp, sz, vp]),
     "nmk_decode_dev": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, i32,

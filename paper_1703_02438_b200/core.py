@@ -128,7 +128,7 @@ def compute_change_ratios(pair: TemporalPair) -> ChangeRatioField:
     nb = lib.nmk_minmax_ws_bytes(pair.n)
     mm = ws.get("minmax", nb, zero=True)
     N.check(lib.nmk_minmax(b.data_ptr(), c.data_ptr(), pair.n, N.dtype_code(pair.dtype), stats.data_ptr(),
-                           mm.data_ptr(), nb, torch.cuda.current_stream().cuda_stream))
+                           None, mm.data_ptr(), nb, torch.cuda.current_stream().cuda_stream))
     sv = engine._read_struct(stats, N.NmkStats)
     if sv.nvalid == 0:
         raise ValueError("no element has a well-defined change ratio")

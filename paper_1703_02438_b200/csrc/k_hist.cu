@@ -74,6 +74,49 @@ __device__ __forceinline__ void for_each_pair(const T* __restrict__ base, const 
   for (uint64_t j = done + tid; j < n; j += nthr) f(to_f64(base[j]), to_f64(cur[j]), j);
 }
 
+// Visit the ordinal of every valid element from its f32 ratio key (K1), with
+// the (base, current) pair re-read only when the key cannot decide it.
+template <typename T, int UNROLL, typename F>
+__device__ __forceinline__ void for_each_key_ordinal(const float* __restrict__ keys, const T* __restrict__ base,
+                                                     const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
+                                                     double width, double inv_w, F&& f) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  const double et_c = key_bound(gmin, gmax, inv_w);
+  auto one = [&](float key, uint64_t j) {
+    if (key != key) return;                                  // invalid element
+    double q;
+    if (!key_ordinal_c(key, gmin, inv_w, et_c, q) &&
+        !element_ordinal(to_f64(base[j]), to_f64(cur[j]), gmin, width, inv_w, q))
+      return;
+    f(q);
+  };
+  const uint64_t nvec = n / 4;
+  const float4* kv = reinterpret_cast<const float4*>(keys);
+  uint64_t i = tid;
+  for (; i + (UNROLL - 1) * nthr < nvec; i += UNROLL * nthr) {
+    float4 w[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) w[u] = __ldcs(kv + i + u * nthr);   // streamed once
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint64_t j = (i + u * nthr) * 4;
+      one(w[u].x, j);
+      one(w[u].y, j + 1);
+      one(w[u].z, j + 2);
+      one(w[u].w, j + 3);
+    }
+  }
+  for (; i < nvec; i += nthr) {
+    const float4 w = __ldcs(kv + i);
+    one(w.x, i * 4);
+    one(w.y, i * 4 + 1);
+    one(w.z, i * 4 + 2);
+    one(w.w, i * 4 + 3);
+  }
+  for (uint64_t j = nvec * 4 + tid; j < n; j += nthr) one(keys[j], j);
+}
+
 // counts[nbins] is an out-of-range tripwire (must stay 0).
 constexpr int kHistThreads = 256;
 
@@ -451,8 +494,8 @@ __global__ void k_hist_prep(nmk_stats* __restrict__ st, double width, uint64_t c
 
 template <typename T>
 __global__ void __launch_bounds__(kHistThreads, 4)
-k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n, const nmk_stats* __restrict__ st,
-           double width, unsigned long long* __restrict__ counts, bool vec_ok) {
+k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* __restrict__ keys, uint64_t n,
+           const nmk_stats* __restrict__ st, double width, unsigned long long* __restrict__ counts, bool vec_ok) {
   extern __shared__ uint32_t h[];
   const unsigned long long nb64 = st->reserved;
   if (nb64 == 0 || nb64 == NMK_SPAN_SPARSE) return;
@@ -466,9 +509,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n, co
     __syncthreads();
     uint32_t* my = h + (uint32_t)((threadIdx.x >> 5) % reps) * nbins;
     uint32_t last = 0xffffffffu, run = 0;
-    for_each_pair<T, 4>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
-      double q;
-      if (!element_ordinal(b, x, gmin, width, inv_w, q)) return;
+    auto add_q = [&](double q) {
       const uint32_t qi = (q < (double)nbins) ? (uint32_t)q : nbins;   // nbins = tripwire
       if (qi == last) {
         ++run;
@@ -480,7 +521,15 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n, co
         last = qi;
         run = 1;
       }
-    });
+    };
+    if (keys) {
+      for_each_key_ordinal<T, 4>(keys, base, cur, n, gmin, st->gmax, width, inv_w, add_q);
+    } else {
+      for_each_pair<T, 4>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
+        double q;
+        if (element_ordinal(b, x, gmin, width, inv_w, q)) add_q(q);
+      });
+    }
     if (run) {
       if (last < nbins) atomicAdd(&my[last], run);
       else atomicAdd(&counts[nbins], (unsigned long long)run);
@@ -494,9 +543,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n, co
   } else {
     uint64_t last = ~0ULL;
     unsigned long long run = 0;
-    for_each_pair<T, 2>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
-      double q;
-      if (!element_ordinal(b, x, gmin, width, inv_w, q)) return;
+    auto add_q = [&](double q) {
       const uint64_t qi = (q < (double)nbins) ? (uint64_t)q : nbins;
       if (qi == last) {
         ++run;
@@ -505,7 +552,15 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n, co
         last = qi;
         run = 1;
       }
-    });
+    };
+    if (keys) {
+      for_each_key_ordinal<T, 2>(keys, base, cur, n, gmin, st->gmax, width, inv_w, add_q);
+    } else {
+      for_each_pair<T, 2>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
+        double q;
+        if (element_ordinal(b, x, gmin, width, inv_w, q)) add_q(q);
+      });
+    }
     if (run) atomicAdd(&counts[last], run);
   }
 }
@@ -519,8 +574,9 @@ extern "C" int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins, 
   return check_launch("k_hist_prep");
 }
 
-extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, uint64_t n, int dtype, const nmk_stats* stats,
-                                  double width, unsigned long long* counts, void* stream) {
+extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, const float* keys, uint64_t n, int dtype,
+                                  const nmk_stats* stats, double width, unsigned long long* counts, void* stream) {
+  if (keys && ((uintptr_t)keys & 15)) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: keys must be 16-byte aligned");
   if (!base || !cur || !stats || !counts || n == 0) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   const bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
@@ -535,11 +591,11 @@ extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, uint64_t n,
   uint64_t grid = (uint64_t)sm_count_h() * 4;
   if (want < grid) grid = want ? want : 1;
   if (dtype == NMK_F64)
-    k_hist_dev<double><<<(unsigned)grid, kHistThreads, smem, s>>>((const double*)base, (const double*)cur, n, stats,
-                                                                  width, counts, aligned);
+    k_hist_dev<double><<<(unsigned)grid, kHistThreads, smem, s>>>((const double*)base, (const double*)cur, keys, n,
+                                                                  stats, width, counts, aligned);
   else if (dtype == NMK_F32)
-    k_hist_dev<float><<<(unsigned)grid, kHistThreads, smem, s>>>((const float*)base, (const float*)cur, n, stats,
-                                                                 width, counts, aligned);
+    k_hist_dev<float><<<(unsigned)grid, kHistThreads, smem, s>>>((const float*)base, (const float*)cur, keys, n,
+                                                                 stats, width, counts, aligned);
   else
     return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad dtype");
   return check_launch("k_hist_dev");

@@ -23,15 +23,17 @@ struct MinMax {
 // One element into the running (min, max, count) over valid ratios
 // (core.py:115-137, pipeline.py:194-197).  The IEEE quotient is only formed
 // when the fast approximation cannot rule the element out as a new extreme.
-__device__ __forceinline__ void mm_visit(MinMax& a, double b, double x) {
+// Returns the element's f32 ratio key for K2 (ratio_key in nmk_common.cuh).
+__device__ __forceinline__ float mm_visit(MinMax& a, double b, double x) {
   double ra, ea;
   if (fast_ratio(b, x, ra, ea)) {
     a.nv += 1;                                          // finite quotient: valid
-    if (__dsub_rn(ra, ea) > a.lo && __dadd_rn(ra, ea) < a.hi) return;
-    const double r = __ddiv_rn(__dsub_rn(x, b), b);
-    a.lo = r < a.lo ? r : a.lo;
-    a.hi = r > a.hi ? r : a.hi;
-    return;
+    if (!(__dsub_rn(ra, ea) > a.lo && __dadd_rn(ra, ea) < a.hi)) {
+      const double r = __ddiv_rn(__dsub_rn(x, b), b);
+      a.lo = r < a.lo ? r : a.lo;
+      a.hi = r > a.hi ? r : a.hi;
+    }
+    return ratio_key(ra);
   }
   bool v;
   const double r = change_ratio(b, x, v);
@@ -39,7 +41,9 @@ __device__ __forceinline__ void mm_visit(MinMax& a, double b, double x) {
     a.nv += 1;
     a.lo = r < a.lo ? r : a.lo;
     a.hi = r > a.hi ? r : a.hi;
+    return ratio_key(r);
   }
+  return __int_as_float(0x7fc00000);   // invalid: quiet NaN
 }
 
 __device__ __forceinline__ MinMax mm_merge(MinMax a, const MinMax& b) {
@@ -47,6 +51,12 @@ __device__ __forceinline__ MinMax mm_merge(MinMax a, const MinMax& b) {
   a.hi = b.hi > a.hi ? b.hi : a.hi;
   a.nv += b.nv;
   return a;
+}
+
+template <int VN>
+__device__ __forceinline__ void store_keys(float* p, const float (&kv)[VN]) {
+  if constexpr (VN == 2) *reinterpret_cast<float2*>(p) = make_float2(kv[0], kv[1]);
+  else *reinterpret_cast<float4*>(p) = make_float4(kv[0], kv[1], kv[2], kv[3]);
 }
 
 template <typename T> struct Vec;
@@ -62,7 +72,7 @@ template <typename T>
 __global__ void __launch_bounds__(kMinmaxThreads, 4)
 k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
          MinMax* __restrict__ partials, unsigned int* __restrict__ ticket,
-         nmk_stats* __restrict__ out, bool vec_ok) {
+         nmk_stats* __restrict__ out, bool vec_ok, float* __restrict__ keys) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
   MinMax acc;
@@ -89,20 +99,27 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
         double bb[VN], cc[VN];
         vec_get(b[u], bb);
         vec_get(c[u], cc);
+        float kv[VN];
 #pragma unroll
-        for (int e = 0; e < VN; ++e) mm_visit(acc, bb[e], cc[e]);
+        for (int e = 0; e < VN; ++e) kv[e] = mm_visit(acc, bb[e], cc[e]);
+        if (keys) store_keys<VN>(keys + (i + u * nthr) * VN, kv);
       }
     }
     for (; i < nvec; i += nthr) {
       double bb[VN], cc[VN];
       vec_get(__ldg(bv + i), bb);
       vec_get(__ldg(cv + i), cc);
+      float kv[VN];
 #pragma unroll
-      for (int e = 0; e < VN; ++e) mm_visit(acc, bb[e], cc[e]);
+      for (int e = 0; e < VN; ++e) kv[e] = mm_visit(acc, bb[e], cc[e]);
+      if (keys) store_keys<VN>(keys + i * VN, kv);
     }
     done = nvec * VN;
   }
-  for (uint64_t j = done + tid; j < n; j += nthr) mm_visit(acc, to_f64(base[j]), to_f64(cur[j]));
+  for (uint64_t j = done + tid; j < n; j += nthr) {
+    const float kv = mm_visit(acc, to_f64(base[j]), to_f64(cur[j]));
+    if (keys) keys[j] = kv;
+  }
   // warp reduce
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -201,7 +218,7 @@ extern "C" size_t nmk_minmax_ws_bytes(uint64_t n) {
 }
 
 extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
-                          nmk_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+                          nmk_stats* stats, float* keys, void* ws, size_t ws_bytes, void* stream) {
   if (n == 0 || !base || !cur || !stats || !ws) return set_error(NMK_ERR_ARG, "nmk_minmax: bad argument");
   if (ws_bytes < nmk_minmax_ws_bytes(n)) return set_error(NMK_ERR_ARG, "nmk_minmax: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
@@ -210,13 +227,13 @@ extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dty
   MinMax* partials = (MinMax*)((char*)ws + 256);
   // The ticket word must be zero on entry: callers zero a fresh workspace
   // once and the kernel's last CTA resets it after every launch.
-  bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  bool aligned = (((uintptr_t)base | (uintptr_t)cur | (uintptr_t)keys) & 15) == 0;
   if (dtype == NMK_F64)
     k_minmax<double><<<grid, kMinmaxThreads, 0, s>>>((const double*)base, (const double*)cur, n,
-                                                     partials, ticket, stats, aligned);
+                                                     partials, ticket, stats, aligned, keys);
   else if (dtype == NMK_F32)
     k_minmax<float><<<grid, kMinmaxThreads, 0, s>>>((const float*)base, (const float*)cur, n,
-                                                    partials, ticket, stats, aligned);
+                                                    partials, ticket, stats, aligned, keys);
   else
     return set_error(NMK_ERR_ARG, "nmk_minmax: bad dtype %d", dtype);
   return check_launch("k_minmax");

@@ -108,6 +108,56 @@ __device__ __forceinline__ bool element_ordinal(double b, double x, double origi
   return true;
 }
 
+// ---- f32 ratio keys (K1 -> K2) -----------------------------------------------
+// K1 stores, per element, key = RN_f32(r) (from ra or the exact r) so the
+// histogram pass reads 4 bytes instead of both snapshots.  |key - r| <=
+// |key| * 2^-23 whenever key is a normal float in [2^-100, 2^100] or exactly
+// zero; other magnitudes are stored as +inf ("use the exact path"), invalid
+// elements as NaN.
+__device__ __forceinline__ float ratio_key(double r) {
+  const double a = fabs(r);
+  if (r == 0.0) return (float)r;
+  if (a < 0x1p-100 || a > 0x1p+100) return __int_as_float(0x7f800000);
+  return __double2float_rn(r);
+}
+
+// Ordinal from a key (K2): true with the exact ordinal when decidable, false
+// when the exact path (IEEE ratio + IEEE bin division) must run.
+__device__ __forceinline__ bool key_ordinal(float key, double origin, double inv_w, double& q) {
+  const double kd = (double)key;
+  const double s = __dsub_rn(kd, origin);
+  const double t = __dmul_rn(s, inv_w);
+  const double et = __dadd_rn(__dmul_rn(__dadd_rn(fabs(kd) * 0x1p-22, fabs(s) * 0x1p-48), inv_w * 1.0000001),
+                              fabs(t) * 0x1p-46);
+  const double fl = floor(t);
+  if (t < 0x1p+50 && __dsub_rn(t, fl) > et && __dsub_rn(__dadd_rn(fl, 1.0), t) > et) {
+    q = __dadd_rn(fl, 0.0);
+    return true;
+  }
+  return false;
+}
+
+// One bound for a whole launch: the per-element bound of key_ordinal is
+// monotone in |key|, |s| and |t|, all of which are bounded by the global
+// (gmin, gmax), so et_c below dominates it for every valid element.
+__device__ __forceinline__ double key_bound(double gmin, double gmax, double inv_w) {
+  const double amax = fmax(fabs(gmin), fabs(gmax)) * (1.0 + 0x1p-20);
+  const double smax = (gmax - gmin) * (1.0 + 0x1p-20) + amax * 0x1p-20;
+  const double tmax = smax * inv_w * (1.0 + 0x1p-20) + 1.0;
+  return (amax * 0x1p-22 + smax * 0x1p-48) * inv_w * 1.0000001 + tmax * 0x1p-46;
+}
+
+__device__ __forceinline__ bool key_ordinal_c(float key, double origin, double inv_w, double et_c, double& q) {
+  const double t = __dmul_rn(__dsub_rn((double)key, origin), inv_w);
+  const double fl = floor(t);
+  const double fr = __dsub_rn(t, fl);
+  if (t < 0x1p+50 && fr > et_c && fr < 1.0 - et_c) {
+    q = __dadd_rn(fl, 0.0);
+    return true;
+  }
+  return false;
+}
+
 // origin + (q + 0.5) * width, add -> mul -> add (binning.py:50-51).
 __device__ __forceinline__ double bin_center(double q, double origin, double width) {
   return __dadd_rn(origin, __dmul_rn(__dadd_rn(q, 0.5), width));

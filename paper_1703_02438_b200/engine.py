@@ -205,7 +205,7 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
     if n_local > 0:
         mm_bytes = lib.nmk_minmax_ws_bytes(n_local)
         mm_ws = ws.get("minmax", mm_bytes, zero=True)
-        N.check(lib.nmk_minmax(_p(base), _p(cur), n_local, dt, _p(stats), _p(mm_ws), mm_bytes, st))
+        N.check(lib.nmk_minmax(_p(base), _p(cur), n_local, dt, _p(stats), None, _p(mm_ws), mm_bytes, st))
     else:
         stats.copy_(torch.tensor([0x7FF0000000000000, -0x10000000000000, 0, 0], dtype=torch.int64))
     if comm is not None:
@@ -414,6 +414,8 @@ class DevicePipeline:
         lib = N.lib()
         dev = ws.device
         self.stats = torch.zeros(4, dtype=torch.int64, device=dev)
+        # K1 -> K2 f32 ratio keys: K2 reads 4 bytes per element, not 2L
+        self.keys = torch.empty(max(self.n_local, 4), dtype=torch.float32, device=dev)
         self.counts = torch.zeros(self.cap_bins + 1, dtype=torch.int64, device=dev)
         self.centers = torch.zeros(self.k_cap, dtype=torch.float64, device=dev)
         self.cuts = torch.zeros(self.k_cap, dtype=torch.float64, device=dev)
@@ -445,14 +447,14 @@ class DevicePipeline:
         lib, st = N.lib(), _stream()
         P = lambda t: t.data_ptr()  # noqa: E731
         mark = mark or (lambda name: None)
-        N.check(lib.nmk_minmax(P(base), P(cur), self.n_local, self.dt, P(self.stats), P(self.mm_ws), self.mm_bytes,
-                               st))
+        N.check(lib.nmk_minmax(P(base), P(cur), self.n_local, self.dt, P(self.stats), P(self.keys), P(self.mm_ws),
+                               self.mm_bytes, st))
         if self.comm is not None:
             self.comm.allreduce_stats_device(self.stats)
         mark("K1_minmax")
         N.check(lib.nmk_hist_prep(P(self.stats), self.width, self.cap_bins, P(self.counts), st))
-        N.check(lib.nmk_hist_dense_dev(P(base), P(cur), self.n_local, self.dt, P(self.stats), self.width,
-                                       P(self.counts), st))
+        N.check(lib.nmk_hist_dense_dev(P(base), P(cur), P(self.keys), self.n_local, self.dt, P(self.stats),
+                                       self.width, P(self.counts), st))
         if self.comm is not None:
             self.comm.allreduce_counts(self.counts)
         mark("K2_histogram")

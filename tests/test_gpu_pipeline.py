@@ -66,6 +66,34 @@ def test_pipeline_matches_general_path(case, graph):
     assert enc.n_inc == o["n_inc"] and _host_blocks(enc) == o["blocks"]
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("E", [1e-3, 1e-4])
+def test_pipeline_keys_exact_at_bin_edges(dtype, E):
+    """K1's f32 ratio keys drive K2; ratios planted within 8 ulps of every bin
+    edge must still land in the oracle's bins (the exact fallback kicks in)."""
+    rng = np.random.default_rng(21)
+    n = 200_000
+    b = rng.uniform(0.5, 2.0, n)
+    c = b * (1.0 + rng.uniform(-0.02, 0.03, n))
+    r, v = O.ratios_of(b.astype(dtype), c.astype(dtype))
+    gmin = float(r[v].min())
+    edges = gmin + np.arange(1, int(0.04 / (2 * E))) * (2 * E)
+    t = rng.choice(edges, n) + np.spacing(np.abs(edges).max()) * rng.integers(-8, 9, n)
+    b2 = rng.uniform(0.5, 2.0, n) * np.where(rng.uniform(size=n) < 0.3, -1.0, 1.0)
+    base = np.concatenate([b, b2]).astype(dtype)
+    cur = np.concatenate([c, b2 * (1.0 + t)]).astype(dtype)
+    bt, ct = torch.from_numpy(base).cuda(), torch.from_numpy(cur).cuda()
+    pipe = engine.DevicePipeline(bt.numel(), bt.dtype, E, 12, 1 << 16)
+    out = torch.empty_like(bt)
+    pipe.step(bt, ct, out)
+    enc = pipe.encoding()
+    o = O.encode(base, cur, E, 12, 1 << 16)
+    assert enc.centers.cpu().numpy().tobytes() == o["centers"].tobytes()
+    assert _host_blocks(enc) == o["blocks"]
+    assert enc.exact.cpu().numpy().tobytes() == o["exact"].tobytes()
+    assert out.cpu().numpy().tobytes() == O.decode(o, base).tobytes()
+
+
 def test_pipeline_flags_wide_span():
     b, c = workloads.outlier_pair(50_000, seed=3)   # 5e8-bin span: sparse path needed
     base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()

@@ -42,7 +42,8 @@ def _full_exchanges(base, cur, E):
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     mm = torch.zeros(lib.nmk_minmax_ws_bytes(n), dtype=torch.uint8, device="cuda")
     dt = engine.torch_dtype_code(base)
-    N.check(lib.nmk_minmax(base.data_ptr(), cur.data_ptr(), n, dt, stats.data_ptr(), mm.data_ptr(), mm.numel(), st))
+    N.check(lib.nmk_minmax(base.data_ptr(), cur.data_ptr(), n, dt, stats.data_ptr(), None, mm.data_ptr(), mm.numel(),
+                           st))
     sv = engine._read_struct(stats, N.NmkStats)
     width = 2.0 * E
     span = (sv.gmax - sv.gmin) / width
