@@ -15,15 +15,9 @@
 
 namespace nmk {
 
-constexpr int kTileThreads = 256;             // threads per encode/decode CTA
-constexpr int kGroup = 8;                     // elements per thread (B bytes out)
-constexpr int kTile = kTileThreads * kGroup;  // elements per tile (2048)
+constexpr int kGroup = 8;   // consecutive elements per lane: 8 codes = B whole bytes
 
 // ---- element types --------------------------------------------------------
-template <typename T> struct Bits;
-template <> struct Bits<float>  { using U = uint32_t; };
-template <> struct Bits<double> { using U = unsigned long long; };
-
 __device__ __forceinline__ double to_f64(float v) { return (double)v; }
 __device__ __forceinline__ double to_f64(double v) { return v; }
 
@@ -121,22 +115,6 @@ __device__ __forceinline__ float ratio_key(double r) {
   return __double2float_rn(r);
 }
 
-// Ordinal from a key (K2): true with the exact ordinal when decidable, false
-// when the exact path (IEEE ratio + IEEE bin division) must run.
-__device__ __forceinline__ bool key_ordinal(float key, double origin, double inv_w, double& q) {
-  const double kd = (double)key;
-  const double s = __dsub_rn(kd, origin);
-  const double t = __dmul_rn(s, inv_w);
-  const double et = __dadd_rn(__dmul_rn(__dadd_rn(fabs(kd) * 0x1p-22, fabs(s) * 0x1p-48), inv_w * 1.0000001),
-                              fabs(t) * 0x1p-46);
-  const double fl = floor(t);
-  if (t < 0x1p+50 && __dsub_rn(t, fl) > et && __dsub_rn(__dadd_rn(fl, 1.0), t) > et) {
-    q = __dadd_rn(fl, 0.0);
-    return true;
-  }
-  return false;
-}
-
 // One bound for a whole launch: the per-element bound of key_ordinal is
 // monotone in |key|, |s| and |t|, all of which are bounded by the global
 // (gmin, gmax), so et_c below dominates it for every valid element.
@@ -188,29 +166,11 @@ __device__ __forceinline__ uint32_t lower_bound_cuts(const double* cuts, int ncu
 
 // ---- O(1) nearest-center search -------------------------------------------
 // A uniform grid of kLutCells cells over [cuts[0], cuts[ncuts-1]] stores, per
-// cell, #cuts below the cell's left edge.  The cell of r gives a starting
-// guess; two exact compare loops then land on #cuts < r.  The answer is
-// exact whatever the rounding of the cell computation (monotone cuts), the
-// grid only makes it O(1) on average.
+// cell, #cuts below the cell's left edge.  The cell of r gives a candidate i;
+// exact compares against cuts i-1, i, i+1 settle #cuts < r (k_encode.cu), with
+// an exact walk when the cell edge rounding or a crowded cell defeats it, so
+// the grid only makes the search O(1), never inexact.
 constexpr int kLutCells = 8192;
-
-struct CutLut {
-  const double* cuts;      // shared memory
-  const uint16_t* lut;     // shared memory, kLutCells entries
-  int ncuts;
-  double lo, scale;
-  bool use_lut;
-
-  __device__ __forceinline__ uint32_t find(double r) const {
-    if (!use_lut) return lower_bound_cuts(cuts, ncuts, r);
-    double f = (r - lo) * scale;
-    f = fmin(fmax(f, 0.0), (double)(kLutCells - 1));
-    int i = lut[(int)f];
-    while (i < ncuts && cuts[i] < r) ++i;
-    while (i > 0 && cuts[i - 1] >= r) --i;
-    return (uint32_t)i;
-  }
-};
 
 // Build the grid over `ncuts` cuts already in shared memory (all threads).
 __device__ __forceinline__ void build_cut_lut(const double* cuts, int ncuts, uint16_t* lut, double& lo,
@@ -233,27 +193,10 @@ __device__ __forceinline__ void build_cut_lut(const double* cuts, int ncuts, uin
   }
 }
 
-// ---- cp.async (LDGSTS) helpers ---------------------------------------------
+// ---- TMA bulk copies + mbarriers (sm_90+/sm_100a) --------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-// 4/8-byte copy with zero fill when !valid (src-size 0 reads nothing)
-template <int N>
-__device__ __forceinline__ void cp_async_zfill(void* s, const void* g, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(s)), "l"(g), "n"(N),
-               "r"(valid ? N : 0) : "memory");
-}
-// 4-byte slot filled with the first `have` (0..4) source bytes, rest zero
-__device__ __forceinline__ void cp_async_bytes4(void* s, const void* g, int have) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(s)), "l"(g), "r"(have) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// ---- TMA bulk copies + mbarriers (sm_90+/sm_100a) --------------------------
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -292,49 +235,6 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Element stage: thread t's 8 consecutive elements at t*kRow(T) bytes, a row
-// padded by 16 bytes so 128-bit shared loads of 8 threads hit distinct banks.
-template <typename T> struct Stage {
-  static constexpr int kRow = kGroup * (int)sizeof(T) + 16;        // 80 (f64) / 48 (f32)
-  static constexpr int kBytes = kTileThreads * kRow;               // one array of a tile
-  __device__ __forceinline__ static int off(int e) {               // element e of the tile
-    return (e / kGroup) * kRow + (e % kGroup) * (int)sizeof(T);
-  }
-};
-
-// Issue the loads of `src[li0 .. li0 + cnt)` (tile elements e0 .. e0 + cnt)
-// into a Stage array.  Fast path: whole tile, 16-byte aligned.
-template <typename T>
-__device__ __forceinline__ void stage_tile(unsigned char* stage, const T* __restrict__ src, int64_t li_first,
-                                           int e0, int cnt) {
-  constexpr int VN = 16 / (int)sizeof(T);
-  const T* g = src + li_first;  // element e of the tile lives at g[e]
-  if (e0 == 0 && cnt == kTile && (((uintptr_t)g) & 15) == 0) {
-#pragma unroll
-    for (int m = 0; m < kTile / VN / kTileThreads; ++m) {
-      int c = threadIdx.x + m * kTileThreads;   // 16-byte chunk
-      cp_async16(stage + Stage<T>::off(c * VN), g + c * VN);
-    }
-  } else {
-    for (int e = threadIdx.x; e < kTile; e += kTileThreads) {
-      bool ok = e >= e0 && e < e0 + cnt;
-      cp_async_zfill<(int)sizeof(T)>(stage + Stage<T>::off(e), ok ? (const void*)(g + e) : (const void*)src, ok);
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void unstage_group(const unsigned char* stage, T (&v)[kGroup]) {
-  const unsigned char* row = stage + threadIdx.x * Stage<T>::kRow;
-#pragma unroll
-  for (int q = 0; q < (int)(kGroup * sizeof(T)) / 16; ++q) {
-    uint4 w = *reinterpret_cast<const uint4*>(row + 16 * q);
-    const T* tw = reinterpret_cast<const T*>(&w);
-#pragma unroll
-    for (int e = 0; e < 16 / (int)sizeof(T); ++e) v[q * (16 / (int)sizeof(T)) + e] = tw[e];
-  }
-}
-
 // ---- division by a run-time invariant (Granlund-Montgomery) ---------------
 // q = n / d for any 32-bit n with one mul-hi, an add and two shifts.
 struct FastDiv {
@@ -353,48 +253,6 @@ struct FastDiv {
     return (t + ((n - t) >> s1)) >> s2;
   }
 };
-
-// ---- relaxed 64-bit status words for decoupled look-back ------------------
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// status word: [63:62] flag (0 none, 1 aggregate, 2 inclusive), [61:0] value
-constexpr unsigned long long kFlagAgg = 1ULL << 62;
-constexpr unsigned long long kFlagInc = 2ULL << 62;
-constexpr unsigned long long kValMask = (1ULL << 62) - 1;
-
-// Warp-0 decoupled look-back: returns the exclusive prefix of `tile`
-// (tiles < tile_first are not consulted; tile_first seeds its own INCL).
-// Must be called by all 32 lanes of one warp.
-__device__ __forceinline__ unsigned long long lookback(const unsigned long long* status,
-                                                       long long tile, long long tile_first) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long excl = 0;
-  long long base = tile - 1;
-  while (base >= tile_first) {
-    long long t = base - lane;
-    unsigned long long s = kFlagInc;  // lanes before tile_first act as INCL 0
-    if (t >= tile_first) {
-      do { s = ld_relaxed(status + t); } while ((s >> 62) == 0);
-    }
-    unsigned inc_mask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-    unsigned long long v = (s & kValMask);
-    int stop = inc_mask ? (__ffs(inc_mask) - 1) : 32;  // nearest inclusive lane
-    if (lane > stop) v = 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (inc_mask) break;
-    base -= 32;
-  }
-  return excl;
-}
 
 }  // namespace nmk
 
