@@ -10,6 +10,7 @@ Output bytes are identical to the reference's for every input and config.
 
 from __future__ import annotations
 
+import ctypes
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -328,6 +329,116 @@ def decode_host(h: HostEncoding, base, *, elem0: int = 0, count: int | None = No
     out = _d2h_pinned(res.out, "e2e_out").view(h.dtype)
     torch.cuda.current_stream().synchronize()
     return out
+
+
+class StreamCompressor:
+    """Compress + reconstruct a stream of HOST timestep pairs, overlapping the
+    host->device copy of step i+1 with the kernels of step i and the
+    device->host copy of step i-1 (three CUDA streams, ``depth`` device slots).
+
+    ``submit(base, cur)`` takes pinned host tensors and returns a ticket;
+    ``result(ticket)`` waits and returns ``(HostEncoding, reconstruction)``,
+    both views of pinned host buffers owned by the ticket's slot.  Call
+    ``result(t)`` before ``submit`` reuses the slot (``depth`` submissions
+    later).  The kernels are the sync-free device pipeline (explicit B); the
+    exact values (alpha*n of them, unknown at enqueue time) are read back in
+    ``result``."""
+
+    def __init__(self, n: int, dtype, config: PipelineConfig, depth: int = 2, *, elem0: int = 0,
+                 n_total: int | None = None, comm=None):
+        """``n`` elements per step on this rank; with ``comm`` (multi-GPU) the
+        rank holds [elem0, elem0+n) of an ``n_total``-element variable."""
+        import torch
+        _check_strategy(config)
+        if config.bits is None:
+            raise ValueError("StreamCompressor needs an explicit B (PipelineConfig.bits)")
+        N.require_cuda()
+        self.n, self.config, self.depth = int(n), config, int(depth)
+        self.torch_dtype = torch.float64 if np.dtype(dtype).itemsize == 8 else torch.float32
+        self.np_dtype = np.dtype("<f8") if self.torch_dtype == torch.float64 else np.dtype("<f4")
+        self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self.s_x = torch.cuda.Stream()   # exact-value readback: must not queue behind the next step's D2H
+        self.slots = []
+        for _ in range(self.depth):
+            pipe = engine.DevicePipeline(self.n, self.torch_dtype, config.tolerance, config.bits,
+                                         config.block_bytes, elem0=elem0, n_total=n_total, comm=comm,
+                                         ws=engine.Workspace())
+            sl = {
+                "pipe": pipe,
+                "base": torch.empty(self.n, dtype=self.torch_dtype, device="cuda"),
+                "cur": torch.empty(self.n, dtype=self.torch_dtype, device="cuda"),
+                "out": torch.empty(self.n, dtype=self.torch_dtype, device="cuda"),
+                "h_packed": torch.empty(pipe.packed.numel(), dtype=torch.uint8, pin_memory=True),
+                "h_exact": torch.empty(max(self.n // 64, 1), dtype=self.torch_dtype, pin_memory=True),
+                "h_prefix": torch.empty(pipe.prefix.numel(), dtype=torch.int64, pin_memory=True),
+                "h_scal": torch.empty(4 + pipe.model.numel() + 1, dtype=torch.int64, pin_memory=True),
+                "h_centers": torch.empty(pipe.k_cap, dtype=self.torch_dtype, pin_memory=True),
+                "h_out": torch.empty(self.n, dtype=self.torch_dtype, pin_memory=True),
+                "ev_in": torch.cuda.Event(), "ev_cmp": torch.cuda.Event(), "ev_out": torch.cuda.Event(),
+                "busy": False,
+            }
+            self.slots.append(sl)
+        self.count = 0
+
+    def submit(self, base, cur) -> int:
+        import torch
+        t = self.count
+        sl = self.slots[t % self.depth]
+        if sl["busy"]:
+            sl["ev_out"].synchronize()          # slot reuse: its last D2H must be done
+        sl["busy"] = True
+        with torch.cuda.stream(self.s_h2d):
+            self.s_h2d.wait_event(sl["ev_cmp"])  # device inputs no longer read
+            sl["base"].copy_(base, non_blocking=True)
+            sl["cur"].copy_(cur, non_blocking=True)
+            sl["ev_in"].record(self.s_h2d)
+        with torch.cuda.stream(self.s_cmp):
+            self.s_cmp.wait_event(sl["ev_in"])
+            self.s_cmp.wait_event(sl["ev_out"])  # previous D2H of this slot's outputs
+            sl["pipe"].step(sl["base"], sl["cur"], sl["out"])
+            sl["ev_cmp"].record(self.s_cmp)
+        with torch.cuda.stream(self.s_d2h):
+            self.s_d2h.wait_event(sl["ev_cmp"])
+            p = sl["pipe"]
+            sl["h_packed"].copy_(p.packed, non_blocking=True)
+            sl["h_prefix"].copy_(p.prefix, non_blocking=True)
+            sl["h_scal"][:4].copy_(p.stats, non_blocking=True)
+            sl["h_scal"][4:4 + p.model.numel()].copy_(p.model, non_blocking=True)
+            sl["h_scal"][-1:].copy_(p.n_inc, non_blocking=True)
+            sl["h_centers"].copy_(p.centers_t, non_blocking=True)
+            sl["h_out"].copy_(sl["out"], non_blocking=True)
+            sl["ev_out"].record(self.s_d2h)
+        self.count += 1
+        return t
+
+    def result(self, ticket: int):
+        import torch
+        sl = self.slots[ticket % self.depth]
+        sl["ev_out"].synchronize()
+        p = sl["pipe"]
+        scal = sl["h_scal"].numpy()
+        n_inc = int(scal[-1])
+        if n_inc > sl["h_exact"].numel():
+            sl["h_exact"] = torch.empty(n_inc, dtype=self.torch_dtype, pin_memory=True)
+        if n_inc:
+            with torch.cuda.stream(self.s_x):
+                sl["h_exact"][:n_inc].copy_(p.exact[:n_inc], non_blocking=True)
+            self.s_x.synchronize()
+        self.last_d2h_bytes = (p.packed.numel() + n_inc * self.np_dtype.itemsize + p.prefix.numel() * 8
+                               + (4 + p.model.numel() + 1) * 8 + p.k_cap * self.np_dtype.itemsize
+                               + self.n * self.np_dtype.itemsize)
+        model = N.NmkModel.from_buffer_copy(scal[4:4 + p.model.numel()].tobytes()[: ctypes.sizeof(N.NmkModel)])
+        if model.status != 0:
+            raise PipelineError("binning", f"sync-free pipeline status {model.status}: use compress_pair")
+        k = int(model.k)
+        enc = HostEncoding(self.n, self.np_dtype, p.bits, k, p.epb, p.nblocks, p.stride, p.b0,
+                           sl["h_packed"].numpy(), sl["h_exact"].numpy()[:n_inc],
+                           sl["h_prefix"].numpy().view(np.uint64), sl["h_centers"].numpy()[:k], n_inc)
+        return enc, sl["h_out"].numpy()
+
+    def h2d_bytes(self) -> int:
+        """Host->device bytes per step (both snapshots)."""
+        return 2 * self.n * self.np_dtype.itemsize
 
 
 def compress_series(snapshots, config: PipelineConfig, name: str = "var0"):

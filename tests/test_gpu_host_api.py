@@ -1,0 +1,70 @@
+"""Host-buffer entry points (what the e2e benchmark times): encode_host /
+decode_host and the overlapped StreamCompressor must give the oracle's bytes
+and reconstruction for every step of a stream."""
+
+import numpy as np
+import pytest
+
+import nmk_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1703_02438_b200 import pipeline, workloads  # noqa: E402
+
+
+def _blocks(h):
+    return [bytes(h.block(b)) for b in range(h.b0, h.b0 + len(h.prefix))]
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg5_f32"])
+def test_encode_decode_host_match_oracle(case):
+    if case == "cfg1":
+        b, c = workloads.cfg1_host(1 << 18, seed=11); E, bits, bb = 1e-3, 8, 1 << 14
+    else:
+        b, c = workloads.uniform_pair(150_001, seed=12, dtype=np.float32, spread=0.2); E, bits, bb = 1e-3, 10, 1 << 13
+    cfg = pipeline.PipelineConfig(tolerance=E, bits=bits, block_bytes=bb)
+    h = pipeline.encode_host(b, c, cfg)
+    o = O.encode(b, c, E, bits, bb)
+    assert h.n_inc == o["n_inc"] and h.k == len(o["centers"])
+    assert _blocks(h) == o["blocks"]
+    assert h.exact.tobytes() == o["exact"].tobytes()
+    assert h.prefix.tobytes() == o["prefix"].astype(np.uint64).tobytes()
+    assert h.centers.tobytes() == o["centers"].astype(h.centers.dtype).tobytes()
+    out = pipeline.decode_host(h, b)
+    assert out.tobytes() == O.decode(o, b).tobytes()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_stream_compressor_matches_oracle(dtype, depth):
+    n, steps, E, bits, bb = 200_003, 5, 1e-3, 8, 1 << 14
+    series = workloads.drift_series(n, steps + 1, seed=13, dtype=dtype)
+    cfg = pipeline.PipelineConfig(tolerance=E, bits=bits, block_bytes=bb)
+    sc = pipeline.StreamCompressor(n, dtype, cfg, depth=depth)
+    host = [torch.from_numpy(np.ascontiguousarray(s)).pin_memory() for s in series]
+    tickets, got = [], []
+    for i in range(steps):
+        tickets.append(sc.submit(host[i], host[i + 1]))
+        if len(tickets) == depth:      # consume before the slot is reused
+            t = tickets.pop(0)
+            h, rec = sc.result(t)
+            got.append((t, _blocks(h), h.exact.copy(), h.prefix.copy(), rec.copy()))
+    for t in tickets:
+        h, rec = sc.result(t)
+        got.append((t, _blocks(h), h.exact.copy(), h.prefix.copy(), rec.copy()))
+    assert [g[0] for g in got] == list(range(steps))
+    for t, blocks, exact, prefix, rec in got:
+        b, c = series[t], series[t + 1]
+        o = O.encode(b, c, E, bits, bb)
+        assert blocks == o["blocks"]
+        assert exact.tobytes() == o["exact"].tobytes()
+        assert prefix.tobytes() == o["prefix"].astype(np.uint64).tobytes()
+        assert rec.tobytes() == O.decode(o, b).tobytes()
+
+
+def test_stream_compressor_requires_bits():
+    with pytest.raises(ValueError):
+        pipeline.StreamCompressor(1000, np.float64, pipeline.PipelineConfig())
