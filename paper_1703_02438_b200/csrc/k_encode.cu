@@ -144,13 +144,125 @@ __device__ __forceinline__ uint32_t classify(T bt, T xt, Find&& find, const doub
   return (near && rt) ? idx : sentinel;
 }
 
-// The chunk loop, instantiated once per nearest-center search flavour.
-template <typename T, int B, typename Find>
+// The exact classification with a binary search over the cuts in global
+// memory: the fallback of the direct-grid mode (out of line, rarely taken).
+template <typename T>
+__device__ __noinline__ uint32_t classify_exact(T bt, T xt, const double* __restrict__ cuts_g, int ncuts,
+                                                const double* __restrict__ centers_g, double tol_bin, double tol,
+                                                uint32_t sentinel) {
+  return classify<T>(bt, xt,
+                     [&](double r) -> uint32_t {
+                       int a = 0, z = ncuts;
+                       while (a < z) {
+                         int mid = (a + z) >> 1;
+                         if (__ldg(cuts_g + mid) < r) a = mid + 1; else z = mid;
+                       }
+                       return (uint32_t)a;
+                     },
+                     centers_g, tol_bin, tol, sentinel);
+}
+
+// ---- direct-grid mode ---------------------------------------------------------
+// The selected centers sit in the middles of histogram bins of width
+// w = 2*tol_bin.  Lay a grid of cells of width w with origin o = c_0 - w/2;
+// center i lies within D cells of the middle of cell q_i (D measured at set-up,
+// covering quantisation to T and rounding).  For an element whose position
+// u = (r - o)/w is inside cell q with margin m > D + (cut rounding):
+//   * q = q_j selected:  both neighbouring cuts lie outside the cell, so
+//     searchsorted(cuts, r) = j, and |r - c_j| < w/2 = tol_bin  -> code j if
+//     the round-trip filter passes;
+//   * q not selected:    every center is > w/2 away -> sentinel.
+// u is estimated from the division-free ratio (|ra - r| <= |ra| 2^-44), the
+// margin m bounds that error over the table's range; anything closer to a
+// cell edge takes the exact path (classify_exact).  So the codes are the
+// exact path's codes bit for bit, with a table lookup instead of a search.
+struct DirectGrid {
+  double o, iw, m, m_hi, tplus;   // origin, 1/w, margin, 1-margin, span+1
+  int span;
+  bool far_ok;                    // |t| < 2^40 outside the table is decisive
+};
+
+// All threads: builds tab[0..span) (0xFFFF = no center) and centers_s[0..k)
+// and returns true when the mode applies (block-uniform).
+__device__ __forceinline__ bool setup_direct(const double* __restrict__ centers_g, int k, double tol_bin,
+                                             uint16_t* tab, double* centers_s, DirectGrid& g, int* s_fail,
+                                             unsigned long long* s_dmax, int* s_span) {
+  if (threadIdx.x == 0) { *s_fail = 0; *s_dmax = 0ULL; *s_span = 0; }
+  __syncthreads();
+  const double w = __dmul_rn(2.0, tol_bin);
+  const double iw = __ddiv_rn(1.0, w);
+  const double o = __dsub_rn(__ldg(centers_g), tol_bin);
+  const bool ok0 = k >= 1 && k <= kLutCells && tol_bin > 0.0 && finite64(w) && finite64(iw) && finite64(o);
+  if (ok0) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const double c = __ldg(centers_g + i);
+      centers_s[i] = c;
+      const double p = __dmul_rn(__dsub_rn(c, o), iw);
+      const double q = floor(p);
+      const double d = fabs(__dsub_rn(p, __dadd_rn(q, 0.5)));
+      bool ok = p >= 0.0 && p < (double)kLutCells && d <= 0.25;
+      if (ok && i > 0) {
+        const double pp = floor(__dmul_rn(__dsub_rn(__ldg(centers_g + i - 1), o), iw));
+        ok = pp < q;
+      }
+      if (!ok) *s_fail = 1;
+      else atomicMax(s_dmax, (unsigned long long)__double_as_longlong(d));   // d >= 0: bits are ordered
+      if (ok && i == k - 1) *s_span = (int)q + 1;
+    }
+  }
+  __syncthreads();
+  if (!ok0 || *s_fail) return false;
+  const int span = *s_span;
+  for (int i = threadIdx.x; i < span; i += blockDim.x) tab[i] = 0xFFFF;
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    tab[(int)floor(__dmul_rn(__dsub_rn(centers_s[i], o), iw))] = (uint16_t)i;
+  // margin: ratio error over the table's range (|ra| <= A), rounding of t
+  // and of the cuts, the measured center offsets D and their own rounding
+  const double A = fabs(o) + (span + 2.0) * w;
+  const double D = __longlong_as_double((long long)*s_dmax);
+  g.m = (A * iw * 0x1p-44 + A * iw * 0x1p-50 + (span + 2.0) * 0x1p-48) * 1.01 + D + 0x1p-40;
+  g.m_hi = 1.0 - g.m;
+  g.o = o;
+  g.iw = iw;
+  g.span = span;
+  g.tplus = (double)span + 1.0;
+  g.far_ok = fabs(o) * iw < 0x1p+40;
+  __syncthreads();
+  return g.m < 0.02;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t classify_direct(T bt, T xt, const DirectGrid& g, const uint16_t* tab,
+                                                    const double* centers_s, double tol, uint32_t sentinel,
+                                                    const double* __restrict__ cuts_g, int ncuts,
+                                                    const double* __restrict__ centers_g, double tol_bin) {
+  const double bd = to_f64(bt), xd = to_f64(xt);
+  double ra, ea;
+  if (fast_ratio(bd, xd, ra, ea)) {
+    const double t = __dmul_rn(__dsub_rn(ra, g.o), g.iw);
+    if (t > -1.0 && t < g.tplus) {
+      const double fl = floor(t);
+      const double fr = __dsub_rn(t, fl);
+      if (fr > g.m && fr < g.m_hi) {
+        const int qi = (int)fl;
+        const uint32_t idx = (unsigned)qi < (unsigned)g.span ? tab[qi] : 0xFFFFu;
+        if (idx == 0xFFFFu) return sentinel;
+        return roundtrip_ok<T>(centers_s[idx], bd, xd, tol) ? idx : sentinel;
+      }
+    } else if (g.far_ok && fabs(t) < 0x1p+40) {
+      return sentinel;
+    }
+  }
+  return classify_exact<T>(bt, xt, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel);
+}
+
+// The chunk loop, instantiated once per classification flavour.
+template <typename T, int B, typename Cls>
 __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const T* __restrict__ cur,
-                                              const EncodeGeom& geo, const double* __restrict__ centers_g,
-                                              double tol_bin, double tol, uint8_t* __restrict__ packed,
+                                              const EncodeGeom& geo, uint8_t* __restrict__ packed,
                                               T* __restrict__ scratch, uint32_t* __restrict__ counts,
-                                              uint8_t* my, Find&& find) {
+                                              uint8_t* my, Cls&& cls) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t sentinel = (1u << B) - 1u;
   const uint64_t local_end = geo.elem0 + geo.n_local;
@@ -177,7 +289,7 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
       load8<T>(cur + li, xv);
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
-        code[e] = classify<T>(bv[e], xv[e], find, centers_g, tol_bin, tol, sentinel);
+        code[e] = cls(bv[e], xv[e]);
         inc_mask |= (code[e] == sentinel ? 1u : 0u) << e;
       }
     } else {
@@ -187,7 +299,7 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
         const bool in = j >= lo && j < hi;
         bv[e] = in ? __ldg(base + (li + e)) : T(0);
         xv[e] = in ? __ldg(cur + (li + e)) : T(0);
-        code[e] = in ? classify<T>(bv[e], xv[e], find, centers_g, tol_bin, tol, sentinel) : 0u;
+        code[e] = in ? cls(bv[e], xv[e]) : 0u;
         inc_mask |= (in && code[e] == sentinel ? 1u : 0u) << e;
       }
     }
@@ -230,10 +342,12 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
          uint32_t* __restrict__ counts, const nmk_model* __restrict__ model, bool smem_ok) {
   __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
-  __shared__ uint16_t lut[kLutCells];
+  __shared__ uint16_t lut[kLutCells];   // cut grid (search mode) or cell -> center (direct mode)
   __shared__ double s_lo, s_scale;
   __shared__ bool s_use;
-  extern __shared__ __align__(16) double cutsp[];   // [-inf, cuts..., +inf, +inf]
+  __shared__ int s_fail, s_span;
+  __shared__ unsigned long long s_dmax;
+  extern __shared__ __align__(16) double cutsp[];   // [-inf, cuts..., +inf, +inf] or centers
 
   if (model) {   // sync-free path: the model scalars live on the device
     if (model->status != 0) {   // nothing to encode: leave empty chunks behind
@@ -245,8 +359,17 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
     tol_bin = model->tol_bin;
   }
   const int ncuts = k - 1;
+  const uint32_t sentinel = (1u << B) - 1u;
+  uint8_t* my = wbytes[threadIdx.x >> 5];
   const bool cuts_in_smem = smem_ok && k <= kSmemCuts + 1;
   if (cuts_in_smem) {
+    DirectGrid g;
+    if (setup_direct(centers_g, k, tol_bin, lut, cutsp, g, &s_fail, &s_dmax, &s_span)) {
+      encode_chunks<T, B>(base, cur, geo, packed, scratch, counts, my, [&](T b, T x) -> uint32_t {
+        return classify_direct<T>(b, x, g, lut, cutsp, tol, sentinel, cuts_g, ncuts, centers_g, tol_bin);
+      });
+      return;
+    }
     for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cutsp[i + 1] = cuts_g[i];
     if (threadIdx.x == 0) {
       cutsp[0] = __longlong_as_double(0xfff0000000000000LL);
@@ -264,35 +387,38 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
     s_lo = 0.0; s_scale = 0.0; s_use = false;
   }
   __syncthreads();
-  uint8_t* my = wbytes[threadIdx.x >> 5];
   if (s_use) {
     // O(1) search: the grid cell gives i = #cuts below the cell's left edge;
     // with at most one cut per cell the answer is i or i+1, settled by exact
     // compares against the three candidate cuts (padded with -inf/+inf).
     // Any other case (rounding at a cell edge, a crowded cell) walks exactly.
     const double lo = s_lo, scale = s_scale;
-    encode_chunks<T, B>(base, cur, geo, centers_g, tol_bin, tol, packed, scratch, counts, my,
-                        [&](double r) -> uint32_t {
-                          int g = __double2int_rz((r - lo) * scale);   // saturating
-                          g = min(max(g, 0), kLutCells - 1);
-                          int i = lut[g];
-                          const double a = cutsp[i], m = cutsp[i + 1], z = cutsp[i + 2];
-                          const bool up = m < r;
-                          if (up ? (r <= z) : (a < r)) return (uint32_t)(i + up);
-                          while (i < ncuts && cutsp[i + 1] < r) ++i;
-                          while (i > 0 && cutsp[i] >= r) --i;
-                          return (uint32_t)i;
-                        });
+    auto find = [&](double r) -> uint32_t {
+      int g = __double2int_rz((r - lo) * scale);   // saturating
+      g = min(max(g, 0), kLutCells - 1);
+      int i = lut[g];
+      const double a = cutsp[i], m = cutsp[i + 1], z = cutsp[i + 2];
+      const bool up = m < r;
+      if (up ? (r <= z) : (a < r)) return (uint32_t)(i + up);
+      while (i < ncuts && cutsp[i + 1] < r) ++i;
+      while (i > 0 && cutsp[i] >= r) --i;
+      return (uint32_t)i;
+    };
+    encode_chunks<T, B>(base, cur, geo, packed, scratch, counts, my, [&](T b, T x) -> uint32_t {
+      return classify<T>(b, x, find, centers_g, tol_bin, tol, sentinel);
+    });
   } else {
-    encode_chunks<T, B>(base, cur, geo, centers_g, tol_bin, tol, packed, scratch, counts, my,
-                        [&](double r) -> uint32_t {
-                          int a = 0, z = ncuts;
-                          while (a < z) {
-                            int mid = (a + z) >> 1;
-                            if (__ldg(cuts_g + mid) < r) a = mid + 1; else z = mid;
-                          }
-                          return (uint32_t)a;
-                        });
+    auto find = [&](double r) -> uint32_t {
+      int a = 0, z = ncuts;
+      while (a < z) {
+        int mid = (a + z) >> 1;
+        if (__ldg(cuts_g + mid) < r) a = mid + 1; else z = mid;
+      }
+      return (uint32_t)a;
+    };
+    encode_chunks<T, B>(base, cur, geo, packed, scratch, counts, my, [&](T b, T x) -> uint32_t {
+      return classify<T>(b, x, find, centers_g, tol_bin, tol, sentinel);
+    });
   }
 }
 

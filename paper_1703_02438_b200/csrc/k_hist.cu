@@ -12,6 +12,8 @@
 //           planted-outlier test): emit the canonical bit pattern of the
 //           non-negative double ordinal (invalid -> UINT64_MAX), radix sort,
 //           run-length encode.  Output = np.unique(ords, return_counts=True).
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/block/block_reduce.cuh>
@@ -79,11 +81,17 @@ __device__ __forceinline__ void for_each_pair(const T* __restrict__ base, const 
 template <typename T, int UNROLL, typename F>
 __device__ __forceinline__ void for_each_key_ordinal(const float* __restrict__ keys, const T* __restrict__ base,
                                                      const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
-                                                     double width, double inv_w, F&& f) {
+                                                     double width, double inv_w, uint32_t nbins, F&& f) {
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   const double et_c = key_bound(gmin, gmax, inv_w);
+  const KeyGrid32 g32 = key_grid32(gmin, gmax, inv_w, nbins);
   auto one = [&](float key, uint64_t j) {
+    uint32_t qi;
+    if (key_ordinal32(key, g32, qi)) {                       // all-f32 common case
+      f(qi);
+      return;
+    }
     if (key != key) return;                                  // invalid element
     double q;
     if (!key_ordinal_c(key, gmin, inv_w, et_c, q) &&
@@ -492,8 +500,140 @@ __global__ void k_hist_prep(nmk_stats* __restrict__ st, double width, uint64_t c
     counts[i] = 0;
 }
 
+// ---- key histogram with warp-held hot bins -----------------------------------
+// Ratio fields are heavy-headed (most elements fall in one or two bins), so
+// each warp holds two "hot" bins whose counts live in per-lane registers
+// (a compare and a predicated add each).  Every key that is not a sure hit
+// -- an f32-undecided key or a different bin -- is deferred: its bit is set
+// in a per-lane mask and, after the tile, re-read from the shared-memory
+// stage and counted through the full ordinal (f32 -> f64 key -> exact
+// (base, cur)) with one shared-memory atomic into the warp's replica (slot
+// nbins = out-of-range tripwire).  When more than 1/8 of a tile misses the
+// hot pair the warp promotes the last missing ordinal (the evicted bin's
+// count is reduced across the warp and flushed).  Keys stream through a
+// per-warp ring of TMA bulk copies (kKeyStages x 1 KB), so loads for later
+// tiles are in flight while a tile is counted.
+constexpr uint32_t kNoBin = 0xffffffffu;
+constexpr int kKeyTile = 256;      // keys per warp tile (1 KB)
+constexpr int kKeyStages = 4;
+constexpr uint32_t kKeySmemBins = 8 * 1024;   // replicas of nbins + 1 counters (32 KB)
+
 template <typename T>
-__global__ void __launch_bounds__(kHistThreads, 4)
+__device__ __noinline__ uint32_t key_ordinal_slow(float key, const T* __restrict__ base, const T* __restrict__ cur,
+                                                  uint64_t j, double gmin, double width, double inv_w,
+                                                  double et_c, uint32_t nbins) {
+  if (key != key) return kNoBin;   // invalid element
+  double q;
+  if (!key_ordinal_c(key, gmin, inv_w, et_c, q) &&
+      !element_ordinal(to_f64(base[j]), to_f64(cur[j]), gmin, width, inv_w, q))
+    return kNoBin;
+  return q < (double)nbins ? (uint32_t)q : nbins;   // nbins = tripwire
+}
+
+template <typename T>
+__device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, const T* __restrict__ base,
+                                              const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
+                                              double width, double inv_w, uint32_t nbins, uint32_t* my,
+                                              float* stage, unsigned long long* bars) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const double et_c = key_bound(gmin, gmax, inv_w);
+  const KeyGrid32 g32 = key_grid32(gmin, gmax, inv_w, nbins);
+  uint32_t hot1 = kNoBin - 1, hot2 = kNoBin - 2;   // never real ordinals
+  uint32_t c1 = 0, c2 = 0, miss = 0, last_miss = kNoBin;
+  // full ordinal of one key (f32 -> f64 key -> exact pair)
+  auto ord = [&](float key, uint64_t j) -> uint32_t {
+    uint32_t qi;
+    if (key_ordinal32(key, g32, qi)) return qi;
+    double q;
+    if (key == key && key_ordinal_c(key, gmin, inv_w, et_c, q)) return q < (double)nbins ? (uint32_t)q : nbins;
+    return key_ordinal_slow<T>(key, base, cur, j, gmin, width, inv_w, et_c, nbins);
+  };
+  auto visit = [&](uint32_t qi) {
+    if (qi == hot1) {
+      ++c1;
+    } else if (qi == hot2) {
+      ++c2;
+    } else if (qi != kNoBin) {
+      atomicAdd(&my[qi], 1u);   // qi <= nbins
+      ++miss;
+      last_miss = qi;
+    }
+  };
+  auto flush = [&](uint32_t hot, uint32_t c) {
+    const uint32_t tot = __reduce_add_sync(FULL, c);
+    if (lane == 0 && tot && hot <= nbins) atomicAdd(&my[hot], tot);
+  };
+  const uint64_t ntiles = n / kKeyTile;
+  const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  if (lane == 0) {
+    for (int st = 0; st < kKeyStages; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](int st, uint64_t t) {   // lane 0 only
+    mbar_arrive_tx(&bars[st], kKeyTile * 4);
+    tma_load_1d(stage + st * kKeyTile, keys + t * kKeyTile, kKeyTile * 4, &bars[st]);
+  };
+  if (lane == 0)
+    for (int st = 0; st < kKeyStages; ++st)
+      if (wg + st * nw < ntiles) issue(st, wg + st * nw);
+  for (uint64_t kk = 0;; ++kk) {   // warp-uniform
+    const uint64_t t = wg + kk * nw;
+    if (t >= ntiles) break;
+    const int st = (int)(kk % kKeyStages);
+    mbar_wait(&bars[st], (unsigned)((kk / kKeyStages) & 1));
+    const float* sk = stage + st * kKeyTile;
+    const float4 w0 = reinterpret_cast<const float4*>(sk)[lane];
+    const float4 w1 = reinterpret_cast<const float4*>(sk)[32 + lane];
+    const float kv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    uint32_t defer = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      uint32_t qi;
+      const bool ok = key_ordinal32(kv[e], g32, qi);
+      const bool h1 = ok && qi == hot1, h2 = ok && qi == hot2;
+      c1 += h1 ? 1u : 0u;
+      c2 += h2 ? 1u : 0u;
+      defer |= (h1 || h2) ? 0u : (1u << e);
+    }
+    while (defer) {   // this lane's non-hit keys, re-read from the stage
+      const int e = __ffs(defer) - 1;
+      defer &= defer - 1;
+      const int idx = ((e >> 2) * 32 + lane) * 4 + (e & 3);
+      visit(ord(sk[idx], t * kKeyTile + idx));
+    }
+    // adapt: promote the most recent miss when the hot pair covers too little
+    if (__reduce_add_sync(FULL, miss) > (unsigned)(kKeyTile / 8)) {
+      const unsigned have = __ballot_sync(FULL, last_miss < nbins);
+      if (have) {
+        const uint32_t cand = __shfl_sync(FULL, last_miss, __ffs(have) - 1);
+        if (cand != hot1 && cand != hot2) {
+          flush(hot2, c2);
+          hot2 = hot1;
+          c2 = c1;
+          hot1 = cand;
+          c1 = 0;
+        }
+      }
+    }
+    miss = 0;
+    __syncwarp();
+    if (lane == 0) {   // refill this stage
+      fence_proxy_async_smem();
+      const uint64_t nx = t + (uint64_t)kKeyStages * nw;
+      if (nx < ntiles) issue(st, nx);
+    }
+  }
+  // tail: the last n % kKeyTile keys, one element per lane per round
+  for (uint64_t j = ntiles * kKeyTile + wg * 32 + lane; j < n; j += nw * 32) visit(ord(keys[j], j));
+  flush(hot1, c1);
+  flush(hot2, c2);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kHistThreads, 3)
 k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* __restrict__ keys, uint64_t n,
            const nmk_stats* __restrict__ st, double width, unsigned long long* __restrict__ counts, bool vec_ok) {
   extern __shared__ uint32_t h[];
@@ -503,14 +643,33 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
   const double gmin = st->gmin;
   const double inv_w = 1.0 / width;
   if (nbins <= kDevSmemBins) {
+    if (keys && nbins < kKeySmemBins) {   // replicas of nbins + 1 slots (tripwire last)
+      __shared__ unsigned long long s_bars[kHistThreads / 32][kKeyStages];
+      const uint32_t nb1 = nbins + 1;
+      int reps = (int)(kKeySmemBins / nb1);
+      if (reps > kHistThreads / 32) reps = kHistThreads / 32;
+      for (uint32_t i = threadIdx.x; i < nb1 * (uint32_t)reps; i += blockDim.x) h[i] = 0;
+      __syncthreads();
+      const int wid = threadIdx.x >> 5;
+      float* stage = reinterpret_cast<float*>(h + kKeySmemBins) + wid * kKeyStages * kKeyTile;
+      hist_keys_hot<T>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins, h + (uint32_t)(wid % reps) * nb1,
+                       stage, s_bars[wid]);
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < nb1; i += blockDim.x) {
+        uint32_t s = 0;
+        for (int r = 0; r < reps; ++r) s += h[r * nb1 + i];
+        if (s) atomicAdd(&counts[i], (unsigned long long)s);
+      }
+      return;
+    }
     int reps = (int)(kDevSmemBins / nbins);
     if (reps > kHistThreads / 32) reps = kHistThreads / 32;
     for (uint32_t i = threadIdx.x; i < nbins * (uint32_t)reps; i += blockDim.x) h[i] = 0;
     __syncthreads();
     uint32_t* my = h + (uint32_t)((threadIdx.x >> 5) % reps) * nbins;
     uint32_t last = 0xffffffffu, run = 0;
-    auto add_q = [&](double q) {
-      const uint32_t qi = (q < (double)nbins) ? (uint32_t)q : nbins;   // nbins = tripwire
+    auto add_q = [&](auto q) {   // float (f32 key path) or double ordinal
+      const uint32_t qi = (q < (decltype(q))nbins) ? (uint32_t)q : nbins;   // nbins = tripwire
       if (qi == last) {
         ++run;
       } else {
@@ -523,7 +682,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
       }
     };
     if (keys) {
-      for_each_key_ordinal<T, 4>(keys, base, cur, n, gmin, st->gmax, width, inv_w, add_q);
+      for_each_key_ordinal<T, 4>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins, add_q);
     } else {
       for_each_pair<T, 4>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
         double q;
@@ -543,8 +702,8 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
   } else {
     uint64_t last = ~0ULL;
     unsigned long long run = 0;
-    auto add_q = [&](double q) {
-      const uint64_t qi = (q < (double)nbins) ? (uint64_t)q : nbins;
+    auto add_q = [&](auto q) {
+      const uint64_t qi = (q < (decltype(q))nbins) ? (uint64_t)q : nbins;
       if (qi == last) {
         ++run;
       } else {
@@ -554,7 +713,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
       }
     };
     if (keys) {
-      for_each_key_ordinal<T, 2>(keys, base, cur, n, gmin, st->gmax, width, inv_w, add_q);
+      for_each_key_ordinal<T, 2>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins, add_q);
     } else {
       for_each_pair<T, 2>(base, cur, n, vec_ok, [&](double b, double x, uint64_t) {
         double q;
@@ -580,15 +739,23 @@ extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, const float
   if (!base || !cur || !stats || !counts || n == 0) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   const bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
-  const size_t smem = kDevSmemBins * 4;
+  // 48 KB of counters for the pair paths; the key path uses 32 KB of
+  // counters + the per-warp TMA key stages in the same allocation
+  const size_t smem = std::max<size_t>(kDevSmemBins * 4, kKeySmemBins * 4 + (kHistThreads / 32) * kKeyStages * kKeyTile * 4);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_hist_dev<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_hist_dev<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  // one resident wave: the grid-stride loops split the work evenly over it
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist_dev<double>, kHistThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
   uint64_t want = (n + 8191) / 8192;
-  uint64_t grid = (uint64_t)sm_count_h() * 4;
+  uint64_t grid = (uint64_t)sm_count_h() * per_sm;
   if (want < grid) grid = want ? want : 1;
   if (dtype == NMK_F64)
     k_hist_dev<double><<<(unsigned)grid, kHistThreads, smem, s>>>((const double*)base, (const double*)cur, keys, n,

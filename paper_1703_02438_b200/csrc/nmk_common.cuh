@@ -136,6 +136,48 @@ __device__ __forceinline__ bool key_ordinal_c(float key, double origin, double i
   return false;
 }
 
+// ---- all-f32 ordinal from a key (the K2 common case) -------------------------
+// th = RN32(key * iw32 + c32) (one FMA) with iw32 = RN32(1/w) and
+// c32 = RN32(-gmin/w - 0.5) estimates u - 1/2, u = (r - gmin)/w.  With
+// A >= |key|, |gmin|; T >= |u| + 1 (every valid r lies in [gmin, gmax]):
+//   |th - (u - 1/2)| <= |key - r| iw + |key| |iw32 - 1/w| + |c32 - c| + |th| 2^-24
+//                    <= A iw (2^-23 + 2^-24) + (|gmin| iw + 1/2) 2^-24 + T 2^-24
+// and the f64 reference t* = RN(RN(r - gmin)/w) is within T 2^-50 of u; e
+// below is the sum, x1.05.  fl = RN_int(th) comes from the 1.5*2^23 magic
+// add (exact for |th| < 2^22) and d = th - fl is exact, so |d| < 1/2 - e
+// proves floor(t*) = fl.  The ordinal is the integer in m's mantissa.  NaN
+// keys (invalid) and +inf keys (exact path) fail the test; when the bound
+// is too loose the grid is switched off (hi < 0: every key fails).
+struct KeyGrid32 {
+  float iw32, c32, hi;
+  uint32_t nbins;
+};
+
+__device__ __forceinline__ KeyGrid32 key_grid32(double gmin, double gmax, double inv_w, uint32_t nbins) {
+  KeyGrid32 g;
+  const double A = fmax(fabs(gmin), fabs(gmax)) * (1.0 + 0x1p-20);
+  const double T = (gmax - gmin) * inv_w * (1.0 + 0x1p-20) + 2.0;
+  const double G = fabs(gmin) * inv_w;
+  const double e = (A * inv_w * (0x1p-23 + 0x1p-24) + (G + 0.5) * (0x1p-24 + 0x1p-48) + T * (0x1p-24 + 0x1p-50) +
+                    0x1p-40) * 1.05;
+  const bool on = e < 0.05 && T < 0x1p+21 && G < 0x1p+21 && A < 0x1p+100 && inv_w < 0x1p+100;
+  g.iw32 = __double2float_rn(inv_w);
+  g.c32 = __double2float_rn(-gmin * inv_w - 0.5);
+  g.hi = on ? __double2float_rz(0.5 - e) : -1.0f;
+  g.nbins = nbins;
+  return g;
+}
+
+// true (and qi = the exact ordinal, < nbins) when the f32 arithmetic decides
+__device__ __forceinline__ bool key_ordinal32(float key, const KeyGrid32& g, uint32_t& qi) {
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+  const float th = __fmaf_rn(key, g.iw32, g.c32);
+  const float m = __fadd_rn(th, kMagic);
+  const float d = __fsub_rn(th, __fsub_rn(m, kMagic));
+  qi = (uint32_t)(__float_as_int(m) - 0x4B400000);
+  return fabsf(d) < g.hi && qi < g.nbins;
+}
+
 // origin + (q + 0.5) * width, add -> mul -> add (binning.py:50-51).
 __device__ __forceinline__ double bin_center(double q, double origin, double width) {
   return __dadd_rn(origin, __dmul_rn(__dadd_rn(q, 0.5), width));

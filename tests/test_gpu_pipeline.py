@@ -22,7 +22,21 @@ def _host_blocks(enc):
     return [packed[i * enc.stride: i * enc.stride + int(lens[i])].tobytes() for i in range(nlb)]
 
 
-@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg5_b10", "cfg5_b12_e4", "f32"])
+def _special_mix(n, seed, dtype, spread, shift=0.0):
+    """Ragged n, ratios spread over many bins, plus zeros / NaN / inf."""
+    rng = np.random.default_rng(seed)
+    b = rng.uniform(0.5, 2.0, n) * np.where(rng.uniform(size=n) < 0.4, -1.0, 1.0)
+    c = b * (1.0 + shift + rng.uniform(-spread, spread, n))
+    m = rng.uniform(size=n)
+    c[m < 0.01] = np.nan
+    b[(m >= 0.01) & (m < 0.02)] = 0.0
+    c[(m >= 0.015) & (m < 0.02)] = 0.0
+    c[(m >= 0.02) & (m < 0.025)] = np.inf
+    return b.astype(dtype), c.astype(dtype)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg5_b10", "cfg5_b12_e4", "f32", "many_bins", "many_bins_f32",
+                                  "offset_f32", "offset_f32_far", "ragged_small"])
 @pytest.mark.parametrize("graph", [False, True])
 def test_pipeline_matches_general_path(case, graph):
     if case == "cfg1":
@@ -33,9 +47,19 @@ def test_pipeline_matches_general_path(case, graph):
         b, c = workloads.cfg5_host(1 << 19, seed=4); E, bits, bb = 1e-3, 10, 1 << 16
     elif case == "cfg5_b12_e4":
         b, c = workloads.cfg5_host(1 << 19, seed=5); E, bits, bb = 1e-4, 12, 1 << 17
-    else:
+    elif case == "f32":
         s = workloads.cfg3_host(shape=(4, 96, 192), steps=2, seed=3)
         b, c = s[0], s[1]; E, bits, bb = 5e-3, 10, 1 << 15
+    elif case == "many_bins":     # ~6000 bins, hot bins never cover a tile
+        b, c = _special_mix(1_000_003, 31, np.float64, 0.3); E, bits, bb = 5e-5, 12, 1 << 16
+    elif case == "many_bins_f32":
+        b, c = _special_mix(777_777, 32, np.float32, 0.1); E, bits, bb = 2e-5, 11, 1 << 15
+    elif case == "offset_f32":    # centers away from 0: f32 quantisation offsets (direct grid)
+        b, c = _special_mix(500_001, 33, np.float32, 0.01, shift=3.0); E, bits, bb = 5e-5, 9, 1 << 14
+    elif case == "offset_f32_far":   # offsets too large for the direct grid: cut search
+        b, c = _special_mix(500_001, 35, np.float32, 0.002, shift=30.0); E, bits, bb = 1e-5, 9, 1 << 14
+    else:
+        b, c = _special_mix(1_001, 34, np.float64, 0.01); E, bits, bb = 1e-3, 6, 4096
     base = torch.from_numpy(b).cuda()
     cur = torch.from_numpy(c).cuda()
     ref = engine.encode(base, cur, E, bits, bb)
@@ -67,14 +91,15 @@ def test_pipeline_matches_general_path(case, graph):
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("E", [1e-3, 1e-4])
-def test_pipeline_keys_exact_at_bin_edges(dtype, E):
-    """K1's f32 ratio keys drive K2; ratios planted within 8 ulps of every bin
-    edge must still land in the oracle's bins (the exact fallback kicks in)."""
+@pytest.mark.parametrize("E,shift", [(1e-3, 0.0), (1e-4, 0.0), (1e-4, 2.5), (5e-5, -0.7), (2e-3, 40.0)])
+def test_pipeline_keys_exact_at_bin_edges(dtype, E, shift):
+    """K1's f32 ratio keys drive K2 (all-f32 ordinals with an f64 and an
+    exact fallback); ratios planted within 8 ulps of every bin edge, around
+    zero and around an offset, must still land in the oracle's bins."""
     rng = np.random.default_rng(21)
     n = 200_000
     b = rng.uniform(0.5, 2.0, n)
-    c = b * (1.0 + rng.uniform(-0.02, 0.03, n))
+    c = b * (1.0 + shift + rng.uniform(-0.02, 0.03, n))
     r, v = O.ratios_of(b.astype(dtype), c.astype(dtype))
     gmin = float(r[v].min())
     edges = gmin + np.arange(1, int(0.04 / (2 * E))) * (2 * E)
