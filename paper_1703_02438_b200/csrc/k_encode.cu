@@ -164,47 +164,89 @@ __device__ __noinline__ uint32_t classify_exact(T bt, T xt, const double* __rest
 
 // ---- direct-grid mode ---------------------------------------------------------
 // The selected centers sit in the middles of histogram bins of width
-// w = 2*tol_bin.  Lay a grid of cells of width w with origin o = c_0 - w/2;
+// w = 2*tol_bin.  Lay a grid of cells of width w with origin c_0 - w/2;
 // center i lies within D cells of the middle of cell q_i (D measured at set-up,
 // covering quantisation to T and rounding).  For an element whose position
-// u = (r - o)/w is inside cell q with margin m > D + (cut rounding):
+// u = (r - c_0)/w + 1/2 is inside cell q with margin m > D + (cut rounding):
 //   * q = q_j selected:  both neighbouring cuts lie outside the cell, so
 //     searchsorted(cuts, r) = j, and |r - c_j| < w/2 = tol_bin  -> code j if
 //     the round-trip filter passes;
 //   * q not selected:    every center is > w/2 away -> sentinel.
-// u is estimated from the division-free ratio (|ra - r| <= |ra| 2^-44), the
-// margin m bounds that error over the table's range; anything closer to a
-// cell edge takes the exact path (classify_exact).  So the codes are the
-// exact path's codes bit for bit, with a table lookup instead of a search.
+// u is estimated from the division-free ratio (|ra - r| <= |ra| 2^-49) as
+// t' = (ra - c_0)/w ~ u - 1/2, whose nearest integer (magic-number rounding)
+// is the cell; the margin m bounds the error over the table's range, and
+// cells beyond it are sentinels while the error stays below half a cell
+// (|t'| < 2^30, |c_0|/w < 2^40).
+// Anything closer to a cell edge takes the exact path (classify_exact), so
+// the codes are the exact path's codes bit for bit.
 struct DirectGrid {
-  double o, iw, m, m_hi, tplus;   // origin, 1/w, margin, 1-margin, span+1
-  int span;
-  bool far_ok;                    // |t| < 2^40 outside the table is decisive
+  double c0, iw, hm;       // first center, 1/w, 1/2 - margin
+  uint32_t tab_s, opc_s;   // shared addresses: cell+1 -> center, center -> RN(1 + c)
+  uint32_t span2;          // table entries: cells -1 .. span
+  bool far_ok;             // |t'| < 2^30 outside the table is decisive
 };
 
-// All threads: builds tab[0..span) (0xFFFF = no center) and centers_s[0..k)
-// and returns true when the mode applies (block-uniform).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// opaque copies: keep launch constants in registers instead of letting the
+// compiler re-derive them (e.g. shared addresses from the CTA id) per element
+__device__ __forceinline__ double opaque(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// Division-free ratio for the direct grid.  The reciprocal seed is trusted
+// only when its first residual |1 - b*y0| < 2^-16 (which also rejects b = 0,
+// subnormal, huge, inf and NaN b); two Newton steps then give y within
+// 2^-51 of 1/b, so |ra - r| <= |ra| * 2^-49 (+ 2^-1070 if ra is subnormal).
+__device__ __forceinline__ double ratio_seeded(double b, double x, bool& ok) {
+  const double y0 = rcp_approx(b);
+  const double e0 = __fma_rn(-b, y0, 1.0);
+  ok = fabs(e0) < 0x1p-16;
+  double y = __fma_rn(y0, e0, y0);
+  const double e1 = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(y, e1, y);
+  return __dmul_rn(__dsub_rn(x, b), y);
+}
+
+constexpr uint32_t kNoCenter = 0xffffffffu;
+
+// All threads: builds tab[0..span+2) (cell q at q+1, kNoCenter = none) and
+// opc[0..k) = RN(1 + c_i); returns true when the mode applies (block-uniform).
 __device__ __forceinline__ bool setup_direct(const double* __restrict__ centers_g, int k, double tol_bin,
-                                             uint16_t* tab, double* centers_s, DirectGrid& g, int* s_fail,
+                                             uint32_t* tab, double* opc, DirectGrid& g, int* s_fail,
                                              unsigned long long* s_dmax, int* s_span) {
   if (threadIdx.x == 0) { *s_fail = 0; *s_dmax = 0ULL; *s_span = 0; }
   __syncthreads();
   const double w = __dmul_rn(2.0, tol_bin);
   const double iw = __ddiv_rn(1.0, w);
-  const double o = __dsub_rn(__ldg(centers_g), tol_bin);
-  const bool ok0 = k >= 1 && k <= kLutCells && tol_bin > 0.0 && finite64(w) && finite64(iw) && finite64(o);
+  const double c0 = __ldg(centers_g);
+  const bool ok0 = k >= 1 && k <= kLutCells - 2 && tol_bin > 0.0 && finite64(w) && finite64(iw) && finite64(c0);
+  // cell of center i: p = (c_i - c_0)/w + 1/2, q = floor(p), offset |p - q - 1/2|
+  auto cell = [&](double c, double& p) { p = __dadd_rn(__dmul_rn(__dsub_rn(c, c0), iw), 0.5); return floor(p); };
   if (ok0) {
     for (int i = threadIdx.x; i < k; i += blockDim.x) {
       const double c = __ldg(centers_g + i);
-      centers_s[i] = c;
-      const double p = __dmul_rn(__dsub_rn(c, o), iw);
-      const double q = floor(p);
+      opc[i] = __dadd_rn(1.0, c);   // the decoder's (1 + c) (core.py:202-205)
+      double p, pp;
+      const double q = cell(c, p);
       const double d = fabs(__dsub_rn(p, __dadd_rn(q, 0.5)));
-      bool ok = p >= 0.0 && p < (double)kLutCells && d <= 0.25;
-      if (ok && i > 0) {
-        const double pp = floor(__dmul_rn(__dsub_rn(__ldg(centers_g + i - 1), o), iw));
-        ok = pp < q;
-      }
+      bool ok = p >= 0.0 && p < (double)(kLutCells - 2) && d <= 0.25;
+      if (ok && i > 0) ok = cell(__ldg(centers_g + i - 1), pp) < q;
       if (!ok) *s_fail = 1;
       else atomicMax(s_dmax, (unsigned long long)__double_as_longlong(d));   // d >= 0: bits are ordered
       if (ok && i == k - 1) *s_span = (int)q + 1;
@@ -213,44 +255,52 @@ __device__ __forceinline__ bool setup_direct(const double* __restrict__ centers_
   __syncthreads();
   if (!ok0 || *s_fail) return false;
   const int span = *s_span;
-  for (int i = threadIdx.x; i < span; i += blockDim.x) tab[i] = 0xFFFF;
+  for (int i = threadIdx.x; i < span + 2; i += blockDim.x) tab[i] = kNoCenter;
   __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x)
-    tab[(int)floor(__dmul_rn(__dsub_rn(centers_s[i], o), iw))] = (uint16_t)i;
-  // margin: ratio error over the table's range (|ra| <= A), rounding of t
-  // and of the cuts, the measured center offsets D and their own rounding
-  const double A = fabs(o) + (span + 2.0) * w;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double p;
+    tab[(int)cell(__ldg(centers_g + i), p) + 1] = (uint32_t)i;
+  }
+  // margin (cells): ratio error over the table's range (|ra| <= A, relative
+  // 2^-49 taken as 2^-44, plus the subnormal floor), rounding of t' and of
+  // the cell computation, of the cuts, the measured center offsets D
+  const double A = fabs(c0) + (span + 2.0) * w;
   const double D = __longlong_as_double((long long)*s_dmax);
-  g.m = (A * iw * 0x1p-44 + A * iw * 0x1p-50 + (span + 2.0) * 0x1p-48) * 1.01 + D + 0x1p-40;
-  g.m_hi = 1.0 - g.m;
-  g.o = o;
+  const double m = (A * iw * 0x1p-44 + A * iw * 0x1p-50 + (span + 2.0) * 0x1p-48 + iw * 0x1p-1000) * 1.01 + D +
+                   0x1p-40;
+  g.hm = opaque(0.5 - m);
+  g.c0 = c0;
   g.iw = iw;
-  g.span = span;
-  g.tplus = (double)span + 1.0;
-  g.far_ok = fabs(o) * iw < 0x1p+40;
+  g.span2 = (uint32_t)span + 2;
+  g.far_ok = fabs(c0) * iw < 0x1p+40;
+  g.tab_s = opaque(smem_u32(tab));
+  g.opc_s = opaque(smem_u32(opc));
   __syncthreads();
-  return g.m < 0.02;
+  return m < 0.02;
 }
 
 template <typename T>
-__device__ __forceinline__ uint32_t classify_direct(T bt, T xt, const DirectGrid& g, const uint16_t* tab,
-                                                    const double* centers_s, double tol, uint32_t sentinel,
+__device__ __forceinline__ uint32_t classify_direct(T bt, T xt, const DirectGrid& g, double tol, uint32_t sentinel,
                                                     const double* __restrict__ cuts_g, int ncuts,
                                                     const double* __restrict__ centers_g, double tol_bin) {
+  constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: adds round to an integer
   const double bd = to_f64(bt), xd = to_f64(xt);
-  double ra, ea;
-  if (fast_ratio(bd, xd, ra, ea)) {
-    const double t = __dmul_rn(__dsub_rn(ra, g.o), g.iw);
-    if (t > -1.0 && t < g.tplus) {
-      const double fl = floor(t);
-      const double fr = __dsub_rn(t, fl);
-      if (fr > g.m && fr < g.m_hi) {
-        const int qi = (int)fl;
-        const uint32_t idx = (unsigned)qi < (unsigned)g.span ? tab[qi] : 0xFFFFu;
-        if (idx == 0xFFFFu) return sentinel;
-        return roundtrip_ok<T>(centers_s[idx], bd, xd, tol) ? idx : sentinel;
+  bool ok;
+  const double ra = ratio_seeded(bd, xd, ok);
+  const double t = __dmul_rn(__dsub_rn(ra, g.c0), g.iw);   // ~ u - 1/2
+  const double mm = __dadd_rn(t, kMagic);
+  const double dd = __dsub_rn(t, __dsub_rn(mm, kMagic));   // t - RN_int(t), exact
+  const uint32_t q1 = (uint32_t)__double2loint(mm) + 1u;   // cell + 1 (low word of the magic sum)
+  if (ok && fabs(t) < 0x1p+30) {   // the low word holds the cell exactly
+    if (q1 < g.span2) {   // cells -1 .. span: the table decides with the margin
+      if (fabs(dd) < g.hm) {
+        const uint32_t idx = lds_u32(g.tab_s + 4 * q1);
+        if (idx == kNoCenter) return sentinel;
+        // round-trip filter (pipeline.py:143-160) with the stored RN(1 + c)
+        const double rec = to_f64(narrow<T>(__dmul_rn(lds_f64(g.opc_s + 8 * idx), bd)));
+        return fabs(__dsub_rn(rec, xd)) <= __dmul_rn(tol, fabs(bd)) ? idx : sentinel;
       }
-    } else if (g.far_ok && fabs(t) < 0x1p+40) {
+    } else if (g.far_ok) {   // two or more cells outside: no center within w/2
       return sentinel;
     }
   }
@@ -304,20 +354,23 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
       }
     }
     // warp-level compaction of the incompressible values into the chunk's
-    // scratch window (element order)
-    const unsigned cnt = __popc(inc_mask);
-    unsigned incl = cnt;
+    // scratch window (element order); most chunks have none
+    unsigned total = 0;
+    if (__any_sync(0xffffffffu, inc_mask != 0)) {
+      const unsigned cnt = __popc(inc_mask);
+      unsigned incl = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    if (inc_mask) {
-      T* w = scratch + (uint64_t)c * kChunk + (incl - cnt);
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      total = __shfl_sync(0xffffffffu, incl, 31);
+      if (inc_mask) {
+        T* w = scratch + (uint64_t)c * kChunk + (incl - cnt);
 #pragma unroll
-      for (int e = 0; e < kGroup; ++e)
-        if (inc_mask >> e & 1u) *w++ = xv[e];   // raw bits (NaN payloads kept)
+        for (int e = 0; e < kGroup; ++e)
+          if (inc_mask >> e & 1u) *w++ = xv[e];   // raw bits (NaN payloads kept)
+      }
     }
     if (lane == 0) counts[c] = total;
     // packed bytes: stage per warp, then 16-byte stores clipped to the block
@@ -342,7 +395,8 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
          uint32_t* __restrict__ counts, const nmk_model* __restrict__ model, bool smem_ok) {
   __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
-  __shared__ uint16_t lut[kLutCells];   // cut grid (search mode) or cell -> center (direct mode)
+  __shared__ uint32_t lut32[kLutCells];   // cell -> center (direct mode) or, as u16, the cut grid
+  uint16_t* lut = reinterpret_cast<uint16_t*>(lut32);
   __shared__ double s_lo, s_scale;
   __shared__ bool s_use;
   __shared__ int s_fail, s_span;
@@ -364,9 +418,9 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
   const bool cuts_in_smem = smem_ok && k <= kSmemCuts + 1;
   if (cuts_in_smem) {
     DirectGrid g;
-    if (setup_direct(centers_g, k, tol_bin, lut, cutsp, g, &s_fail, &s_dmax, &s_span)) {
+    if (setup_direct(centers_g, k, tol_bin, lut32, cutsp, g, &s_fail, &s_dmax, &s_span)) {
       encode_chunks<T, B>(base, cur, geo, packed, scratch, counts, my, [&](T b, T x) -> uint32_t {
-        return classify_direct<T>(b, x, g, lut, cutsp, tol, sentinel, cuts_g, ncuts, centers_g, tol_bin);
+        return classify_direct<T>(b, x, g, tol, sentinel, cuts_g, ncuts, centers_g, tol_bin);
       });
       return;
     }
