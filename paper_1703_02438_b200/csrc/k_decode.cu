@@ -198,6 +198,36 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* pk, int e) {
   }
 }
 
+// The VN consecutive codes of elements e0 .. e0+VN-1 (MSB-first) from one
+// 64-bit window when they fit (VN*B <= 33), else one code at a time.
+template <int B, int VN>
+__device__ __forceinline__ void codes_at(const uint8_t* pk, int e0, uint32_t (&cd)[VN]) {
+  if constexpr (B == 8 && VN == 2) {
+    const uint32_t two = *reinterpret_cast<const uint16_t*>(pk + e0);   // e0 even
+    cd[0] = two & 255u;
+    cd[1] = two >> 8;
+  } else if constexpr (B == 8 && VN == 4) {
+    const uint32_t four = *reinterpret_cast<const uint32_t*>(pk + e0);  // e0 % 4 == 0
+#pragma unroll
+    for (int v = 0; v < 4; ++v) cd[v] = (four >> (8 * v)) & 255u;
+  } else if constexpr (VN * B <= 33) {
+    const int bit = e0 * B;
+    const int w = (bit >> 5) << 2;
+    const uint32_t a = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w), 0, 0x0123);
+    const uint32_t z = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w + 4), 0, 0x0123);
+    const unsigned long long x = ((unsigned long long)a << 32) | z;
+    const int off = bit & 31;
+#pragma unroll
+    for (int v = 0; v < VN; ++v) cd[v] = (uint32_t)(x >> (64 - off - (v + 1) * B)) & ((1u << B) - 1u);
+  } else {
+#pragma unroll
+    for (int v = 0; v < VN; ++v) cd[v] = code_at<B>(pk, e0 + v);
+  }
+}
+
+// (1 + c) per code, in shared memory for small code books
+constexpr int kOpcMax = 2048;
+
 struct DItem {
   int seg;
   DChunk d;
@@ -250,6 +280,9 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ __align__(8) unsigned long long bars[kTmaWarps][kStages];
   __shared__ Seg s_segs[kSmemSegs];
+  __shared__ DItem s_items[kTmaWarps][kStages];   // geometry of each staged chunk (written at issue)
+  constexpr bool kOpcSmem = ((1 << B) - 1) <= kOpcMax;
+  double* s_opc = reinterpret_cast<double*>(dsm + DecStage<T, B>::kSmem);   // [2^B - 1] when kOpcSmem
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (model) {                       // sync-free path: scalars from the device
     if (model->status != 0) return;
@@ -265,6 +298,10 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     for (int st = 0; st < kStages; ++st) mbar_init(&bars[wid][st], 1);
     mbar_fence_init();
   }
+  if constexpr (kOpcSmem) {   // decoder arithmetic (1 + c) (core.py:202-205); codes >= k are errors
+    for (int i = threadIdx.x; i < (1 << B) - 1; i += kTmaThreads)
+      s_opc[i] = __dadd_rn(1.0, __ldg(centers_g + min(i, geo.k - 1)));
+  }
   __syncthreads();
   const Seg* SG = (seg_smem || !segs) ? s_segs : segs;
   uint8_t* wst = dsm + (size_t)wid * kStages * ST::kBytes;
@@ -275,6 +312,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
 
   auto issue = [&](int st, uint64_t it) {       // lane 0 only
     const DItem t = decode_item<T, B>(it, geo, SG, base);
+    s_items[wid][st] = t;
     uint8_t* sb = wst + st * ST::kBytes;
     mbar_arrive_tx(&bars[wid][st], (t.base_tma ? ST::kBase : 0) + (t.pk_tma ? ST::kPk : 0));
     if (t.base_tma) tma_load_1d(sb, base + t.oi0, ST::kBase, &bars[wid][st]);
@@ -283,13 +321,14 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   if (lane == 0)
     for (int st = 0; st < kStages; ++st)
       if (gw + st * nw < geo.nitems) issue(st, gw + st * nw);
+  __syncwarp();
 
   for (uint64_t kk = 0;; ++kk) {
     const uint64_t it = gw + kk * nw;
     if (it >= geo.nitems) break;
     const int st = (int)(kk % kStages);
     uint8_t* sb = wst + st * ST::kBytes;
-    const DItem t = decode_item<T, B>(it, geo, SG, base);
+    const DItem t = s_items[wid][st];
     // the chunk's rank anchor (codec.py:231-236: prefix of the segment's first
     // block + sentinels counted since); only loaded where a rank is needed
     auto chunk_offset = [&]() -> unsigned long long {
@@ -321,27 +360,50 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
 #pragma unroll
         for (int v = 0; v < VN; ++v) bv[q][v] = tw[v];
       }
-      unsigned smask = 0, badmask = 0, cnt_pk = 0;
       uint32_t code[Q][VN];
       T ov[Q][VN];
+      bool lsnt = false;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        unsigned c = 0;
+        codes_at<B, VN>(sb + ST::kBase, VN * lane + 32 * VN * q, code[q]);
 #pragma unroll
         for (int v = 0; v < VN; ++v) {
-          const uint32_t cd = code_at<B>(sb + ST::kBase, VN * lane + 32 * VN * q + v);
-          code[q][v] = cd;
-          const bool snt = cd == sentinel;
-          smask |= (snt ? 1u : 0u) << (q * VN + v);
-          badmask |= (!snt && cd >= k ? 1u : 0u) << (q * VN + v);
-          c += snt;
-          ov[q][v] = apply_center<T>(__ldg(centers_g + min(cd, k - 1)), to_f64(bv[q][v]));
+          const uint32_t cd = code[q][v];
+          lsnt |= cd == sentinel;
+          if constexpr (kOpcSmem)
+            ov[q][v] = narrow<T>(__dmul_rn(s_opc[min(cd, (uint32_t)(1 << B) - 2u)], to_f64(bv[q][v])));
+          else
+            ov[q][v] = apply_center<T>(__ldg(centers_g + min(cd, k - 1)), to_f64(bv[q][v]));
         }
-        cnt_pk |= c << (8 * q);
       }
-      const bool any_sent = __any_sync(0xffffffffu, smask != 0);
+      // ids in [k, sentinel) are errors; impossible with a full code book
+      unsigned maxbad = 0;
+      bool anybad = false;
+      if (k < sentinel) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+          for (int v = 0; v < VN; ++v)
+            if (code[q][v] - k < sentinel - k) {
+              anybad = true;
+              maxbad = max(maxbad, code[q][v]);
+            }
+      }
+      const bool any_sent = __any_sync(0xffffffffu, lsnt);
       const unsigned long long chunk_off = (any_sent || t.first) ? chunk_offset() : 0ULL;
       if (any_sent) {
+        unsigned smask = 0, cnt_pk = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          unsigned c = 0;
+#pragma unroll
+          for (int v = 0; v < VN; ++v) {
+            const bool snt = code[q][v] == sentinel;
+            smask |= (snt ? 1u : 0u) << (q * VN + v);
+            c += snt;
+          }
+          cnt_pk |= c << (8 * q);
+        }
         unsigned incl = cnt_pk;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -368,13 +430,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         const unsigned in_s = __reduce_add_sync(0xffffffffu, __popc(smask));
         if (lane == 0) atomicAdd(&info[t.seg].n_sentinel, (unsigned long long)in_s);
       }
-      if (badmask) {
-        unsigned maxbad = 0;
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-#pragma unroll
-          for (int v = 0; v < VN; ++v)
-            if (badmask >> (q * VN + v) & 1u) maxbad = max(maxbad, code[q][v]);
+      if (anybad) {
         atomicOr(&err->bad_index, 1u);
         atomicMax(&err->max_bad_index, maxbad);
       }
@@ -541,7 +597,7 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
   k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   chunk_scan(counts, geo.nchunks, offsets, nullptr, scan_ws, s);
-  const size_t smem = DecStage<T, B>::kSmem;
+  const size_t smem = DecStage<T, B>::kSmem + (((1 << B) - 1) <= kOpcMax ? (size_t)((1 << B) - 1) * 8 : 0);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_dec_chunks<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
