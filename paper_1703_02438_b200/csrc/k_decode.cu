@@ -162,6 +162,49 @@ k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __rest
   }
 }
 
+// Byte-aligned code widths (B = 8, 16): one thread per chunk, 16-byte loads
+// and SIMD compares (a sentinel is an all-ones byte / halfword), so each
+// thread keeps the chunk's 32*B bytes in flight instead of B per lane.
+template <int B>
+__device__ __forceinline__ unsigned sentinels_in_word(uint32_t w) {
+  if constexpr (B == 8) return __popc(__vcmpeq4(w, 0xffffffffu)) >> 3;
+  else return __popc(__vcmpeq2(w, 0xffffffffu)) >> 4;
+}
+
+template <int B>
+__global__ void __launch_bounds__(kDecThreads)
+k_dec_count_wide(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
+  static_assert(B == 8 || B == 16, "byte-aligned codes only");
+  const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
+  const uint32_t nthr = gridDim.x * blockDim.x;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += nthr) {
+    const DChunk d = dchunk<B>(geo, g0 + c);
+    const uint8_t* src = chunk_src<B>(packed, geo, d);   // 16-byte aligned
+    const uint32_t nvec = d.nbytes / 16;
+    const uint4* v4 = reinterpret_cast<const uint4*>(src);
+    unsigned n = 0;
+    if (nvec == 2 * B) {   // full chunk
+#pragma unroll 8
+      for (uint32_t i = 0; i < 2 * B; ++i) {
+        const uint4 v = __ldg(v4 + i);
+        n += sentinels_in_word<B>(v.x) + sentinels_in_word<B>(v.y) + sentinels_in_word<B>(v.z) +
+             sentinels_in_word<B>(v.w);
+      }
+    } else {
+      for (uint32_t i = 0; i < nvec; ++i) {
+        const uint4 v = __ldg(v4 + i);
+        n += sentinels_in_word<B>(v.x) + sentinels_in_word<B>(v.y) + sentinels_in_word<B>(v.z) +
+             sentinels_in_word<B>(v.w);
+      }
+      for (uint32_t i = nvec * 16; i < d.nbytes; i += B / 8) {
+        if constexpr (B == 8) n += src[i] == 0xff;
+        else n += (src[i] & src[i + 1]) == 0xff;
+      }
+    }
+    counts[c] = n;
+  }
+}
+
 // ---- 3. reconstruct: per-warp TMA pipeline ---------------------------------
 // Each warp owns kStages shared-memory stages.  Lane 0 keeps kStages chunks in
 // flight with 1-D bulk copies (the chunk's base values + its packed bytes),
@@ -593,10 +636,16 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
                           const void* base, void* out, nmk_segment_info* info, nmk_decode_err* err,
                           const nmk_model* model, const unsigned long long* n_exact_dev, cudaStream_t s) {
   const int sms = sm_count_d();
-  const uint64_t g1 = (geo.nchunks + 7) / 8;
-  const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
-  k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
-  chunk_scan(counts, geo.nchunks, offsets, nullptr, scan_ws, s);
+  if constexpr (B == 8 || B == 16) {
+    const uint64_t g1 = (geo.nchunks + kDecThreads - 1) / kDecThreads;
+    const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
+    k_dec_count_wide<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
+  } else {
+    const uint64_t g1 = (geo.nchunks + 7) / 8;
+    const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
+    k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
+  }
+  chunk_scan(counts, geo.nchunks, offsets, scan_ws, s);
   const size_t smem = DecStage<T, B>::kSmem + (((1 << B) - 1) <= kOpcMax ? (size_t)((1 << B) - 1) * 8 : 0);
   static bool attr = false;
   if (!attr) {

@@ -482,8 +482,10 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsigned long long* __restrict__ offsets,
-               const T* __restrict__ scratch, T* __restrict__ exact, unsigned long long* __restrict__ prefix) {
+               const T* __restrict__ scratch, T* __restrict__ exact, unsigned long long* __restrict__ prefix,
+               unsigned long long* __restrict__ n_inc) {
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_inc = offsets[geo.nchunks];
   const uint32_t cpb = (uint32_t)geo.cpb;
   const uint32_t nthr = gridDim.x * blockDim.x;
   for (uint32_t c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); c0 < (uint32_t)geo.nchunks; c0 += nthr) {
@@ -613,7 +615,7 @@ static EncodeWs encode_ws_layout(uint64_t nchunks, int elem_bytes) {
   EncodeWs w{};
   w.off_counts = 0;
   w.off_offsets = al256(nchunks * 4);
-  w.off_total = w.off_offsets + al256(nchunks * 8);
+  w.off_total = w.off_offsets + al256(nchunks * 8 + 8);   // offsets[nchunks] = total
   w.off_scan = w.off_total + 256;
   w.off_scratch = w.off_scan + al256(chunk_scan_ws_bytes(nchunks));
   w.total = w.off_scratch + al256(nchunks * kChunk * (size_t)elem_bytes);
@@ -717,13 +719,15 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
                : dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
                                         scratch, counts, model, k_cap, s);
   if (rc) return rc;
-  chunk_scan(counts, et.nchunks, offsets, n_inc, wb + w.off_scan, s);
+  chunk_scan(counts, et.nchunks, offsets, wb + w.off_scan, s);
   unsigned grid = (unsigned)((et.nchunks + 255) / 256);
   if (grid > (unsigned)sm_count_e() * 8) grid = sm_count_e() * 8;
   if (dtype == NMK_F64)
-    k_enc_finalize<double><<<grid, 256, 0, s>>>(geo, counts, offsets, (const double*)scratch, (double*)exact, prefix);
+    k_enc_finalize<double><<<grid, 256, 0, s>>>(geo, counts, offsets, (const double*)scratch, (double*)exact, prefix,
+                                                n_inc);
   else
-    k_enc_finalize<float><<<grid, 256, 0, s>>>(geo, counts, offsets, (const float*)scratch, (float*)exact, prefix);
+    k_enc_finalize<float><<<grid, 256, 0, s>>>(geo, counts, offsets, (const float*)scratch, (float*)exact, prefix,
+                                               n_inc);
   return check_launch("k_enc_finalize");
 }
 

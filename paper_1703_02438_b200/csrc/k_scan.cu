@@ -3,83 +3,45 @@
 // Used by K4 (incompressible counts per 256-element chunk -> positions in the
 // compacted exact-value list and the per-block prefix table, pipeline.py:257-
 // 276) and by K5 (sentinel counts per chunk -> rank of every sentinel in the
-// exact list, codec.py:231-236).  Three small launches over 4 bytes per 256
-// elements: per-CTA sums, one-CTA scan of the sums, per-CTA rescan.
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
+// exact list, codec.py:231-236).  One single-pass decoupled look-back scan
+// (CUB) over n + 1 items, the last one reading as 0, so offsets[n] is the
+// total: 4 bytes read and 8 written per 256 elements, no second pass.
+#include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "nmk_common.cuh"
 #include "nmk_scan.cuh"
 
 namespace nmk {
 
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;
-
-__global__ void __launch_bounds__(kScanThreads)
-k_scan_reduce(const uint32_t* __restrict__ counts, uint64_t n, unsigned long long* __restrict__ partial) {
-  typedef cub::BlockReduce<unsigned long long, kScanThreads> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-  unsigned long long s = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    uint64_t j = base + (uint64_t)i * kScanThreads + threadIdx.x;
-    if (j < n) s += counts[j];
+struct CountAt {
+  const uint32_t* counts;
+  uint64_t n;
+  __host__ __device__ unsigned long long operator()(uint64_t i) const {
+    return i < n ? (unsigned long long)counts[i] : 0ULL;
   }
-  unsigned long long t = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+};
+
+using CountIter = thrust::transform_iterator<CountAt, thrust::counting_iterator<uint64_t>>;
+
+static size_t scan_temp_bytes(uint64_t n) {
+  size_t bytes = 0;
+  CountIter it(thrust::counting_iterator<uint64_t>(0), CountAt{nullptr, n});
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (unsigned long long*)nullptr, (int64_t)(n + 1));
+  return bytes;
 }
 
-__global__ void __launch_bounds__(1024)
-k_scan_top(unsigned long long* __restrict__ partial, uint64_t np, unsigned long long* __restrict__ total) {
-  typedef cub::BlockScan<unsigned long long, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  unsigned long long run = 0;
-  for (uint64_t c0 = 0; c0 < np; c0 += 1024) {
-    uint64_t j = c0 + threadIdx.x;
-    unsigned long long v = j < np ? partial[j] : 0ULL, ex, agg;
-    BS(tmp).ExclusiveSum(v, ex, agg);
-    __syncthreads();
-    if (j < np) partial[j] = run + ex;
-    run += agg;
-  }
-  if (threadIdx.x == 0 && total) *total = run;
-}
+size_t chunk_scan_ws_bytes(uint64_t n) { return scan_temp_bytes(n) + 256; }
 
-__global__ void __launch_bounds__(kScanThreads)
-k_scan_apply(const uint32_t* __restrict__ counts, uint64_t n, const unsigned long long* __restrict__ partial,
-             unsigned long long* __restrict__ offsets) {
-  typedef cub::BlockScan<unsigned long long, kScanThreads> BS;
-  __shared__ typename BS::TempStorage tmp;
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-  unsigned long long v[kScanItems], s = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    v[i] = (base + i < n) ? counts[base + i] : 0u;
-    s += v[i];
+void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets, void* ws, cudaStream_t s) {
+  if (n == 0) {
+    cudaMemsetAsync(offsets, 0, sizeof(unsigned long long), s);
+    return;
   }
-  unsigned long long ex;
-  BS(tmp).ExclusiveSum(s, ex);
-  unsigned long long run = partial[blockIdx.x] + ex;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    if (base + i < n) offsets[base + i] = run;
-    run += v[i];
-  }
-}
-
-size_t chunk_scan_ws_bytes(uint64_t n) { return ((n + kScanTile - 1) / kScanTile + 1) * 8 + 256; }
-
-void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets, unsigned long long* total,
-                void* ws, cudaStream_t s) {
-  if (n == 0) return;
-  const uint64_t np = (n + kScanTile - 1) / kScanTile;
-  unsigned long long* partial = (unsigned long long*)ws;
-  k_scan_reduce<<<(unsigned)np, kScanThreads, 0, s>>>(counts, n, partial);
-  k_scan_top<<<1, 1024, 0, s>>>(partial, np, total);
-  k_scan_apply<<<(unsigned)np, kScanThreads, 0, s>>>(counts, n, partial, offsets);
+  size_t bytes = scan_temp_bytes(n);
+  CountIter it(thrust::counting_iterator<uint64_t>(0), CountAt{counts, n});
+  cub::DeviceScan::ExclusiveSum(ws, bytes, it, offsets, (int64_t)(n + 1), s);
 }
 
 }  // namespace nmk
