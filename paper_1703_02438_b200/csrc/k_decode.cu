@@ -221,7 +221,8 @@ template <typename T, int B>
 struct DecStage {
   static constexpr int kBase = kDChunk * (int)sizeof(T);   // 2048 (f64) / 1024 (f32)
   static constexpr int kPk = 32 * B;                        // a multiple of 16
-  static constexpr int kBytes = kBase + kPk + 16;           // +16: 8-byte code windows
+  static constexpr int kAux = kBase + kPk + 16;             // +16: 8-byte code windows
+  static constexpr int kBytes = kAux + 32;                  // rank anchors (4 x u64)
   static constexpr size_t kSmem = (size_t)kTmaWarps * kStages * kBytes;
 };
 
@@ -277,7 +278,7 @@ struct DItem {
   uint32_t lo_rel, hi_rel;   // in-segment elements of the chunk: [lo_rel, hi_rel)
   int64_t oi0;               // base/out index of the chunk's first element
   uint32_t anchor;           // block (relative) of the segment's first chunk
-  bool first;                // the segment's first chunk
+  bool first, last;          // the segment's first / last chunk
   bool base_tma, pk_tma;
 };
 
@@ -302,6 +303,7 @@ __device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo,
   const int64_t hi = lo + (int64_t)sg.count;
   t.lo_rel = (uint32_t)(lo < 0 ? 0 : lo);
   t.hi_rel = (uint32_t)(hi > (int64_t)t.d.valid ? (int64_t)t.d.valid : hi);
+  t.last = hi <= (int64_t)t.d.valid;
   t.oi0 = (int64_t)sg.out - lo;
   t.anchor = geo.fd_cpb.div((uint32_t)sg.gfirst) - (uint32_t)geo.first_block;
   t.base_tma = t.lo_rel == 0 && t.hi_rel == kDChunk && ((uintptr_t)(base + t.oi0) & 15) == 0;
@@ -309,6 +311,22 @@ __device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo,
   return t;
 }
 
+// 8-byte asynchronous copy into shared memory, and an mbarrier arrival once
+// this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Per stage: lane 0 issues the chunk's base values and packed bytes as TMA
+// bulk copies plus four 8-byte cp.async copies of its rank anchors
+// (offsets[c], offsets[c+1], the anchor block's first offset and prefix);
+// the stage's mbarrier (2 arrivals: expect_tx + the cp.async group) completes
+// when all of them landed, so no global load sits on a warp's critical path
+// except the exact values, which are fetched right after the wait (one per
+// lane, coalesced) and handed to the sentinels by shuffle.
 template <typename T, int B>
 __global__ void __launch_bounds__(kTmaThreads, NMK_TMA_MINB)
 k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs, SegParams sp,
@@ -320,6 +338,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   constexpr int VN = DVec<T>::N;          // elements per 16-byte vector
   constexpr int Q = kGroup / VN;          // vectors per lane per chunk
   using V = typename DVec<T>::V;
+  const unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ __align__(8) unsigned long long bars[kTmaWarps][kStages];
   __shared__ Seg s_segs[kSmemSegs];
@@ -338,7 +357,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   else if (seg_smem)
     for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = segs[i];
   if (lane == 0) {
-    for (int st = 0; st < kStages; ++st) mbar_init(&bars[wid][st], 1);
+    for (int st = 0; st < kStages; ++st) mbar_init(&bars[wid][st], 2);
     mbar_fence_init();
   }
   if constexpr (kOpcSmem) {   // decoder arithmetic (1 + c) (core.py:202-205); codes >= k are errors
@@ -360,6 +379,12 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     mbar_arrive_tx(&bars[wid][st], (t.base_tma ? ST::kBase : 0) + (t.pk_tma ? ST::kPk : 0));
     if (t.base_tma) tma_load_1d(sb, base + t.oi0, ST::kBase, &bars[wid][st]);
     if (t.pk_tma) tma_load_1d(sb + ST::kBase, chunk_src<B>(packed, geo, t.d), ST::kPk, &bars[wid][st]);
+    const uint32_t aux = smem_u32(sb + ST::kAux);
+    cp_async8(aux, offsets + t.d.crel);
+    cp_async8(aux + 8, offsets + t.d.crel + 1);
+    cp_async8(aux + 16, offsets + (uint64_t)t.anchor * geo.cpb);
+    cp_async8(aux + 24, prefix_rel + t.anchor);
+    cp_async_arrive(&bars[wid][st]);
   };
   if (lane == 0)
     for (int st = 0; st < kStages; ++st)
@@ -372,11 +397,6 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     const int st = (int)(kk % kStages);
     uint8_t* sb = wst + st * ST::kBytes;
     const DItem t = s_items[wid][st];
-    // the chunk's rank anchor (codec.py:231-236: prefix of the segment's first
-    // block + sentinels counted since); only loaded where a rank is needed
-    auto chunk_offset = [&]() -> unsigned long long {
-      return prefix_rel[t.anchor] + (offsets[t.d.crel] - offsets[t.anchor * geo.cpb]);
-    };
     T bv[Q][VN];
     if (!t.base_tma) {
 #pragma unroll
@@ -388,6 +408,11 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         }
     }
     mbar_wait(&bars[wid][st], (unsigned)((kk / kStages) & 1));
+    // the chunk's rank anchor (codec.py:231-236: prefix of the segment's first
+    // block + sentinels counted since) and its sentinel count
+    const unsigned long long* ax = reinterpret_cast<const unsigned long long*>(sb + ST::kAux);
+    const unsigned long long chunk_off = ax[3] + (ax[0] - ax[2]);
+    const uint32_t nsent = (uint32_t)(ax[1] - ax[0]);
     if (!t.pk_tma) {
       const uint8_t* src = chunk_src<B>(packed, geo, t.d);
       for (int i = lane; i < 32 * B; i += 32) sb[ST::kBase + i] = (uint32_t)i < t.d.nbytes ? __ldg(src + i) : 0;
@@ -395,7 +420,11 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     }
     if (t.base_tma && out_al) {
       // fast path: the whole chunk lies inside the segment and its block, so
-      // no element needs a bounds test; ranks only if the warp has sentinels
+      // no element needs a bounds test.  Exact values first (latency hides
+      // behind the arithmetic): lane j holds the chunk's j-th one.
+      const bool few = nsent <= 32;
+      T exv = T(0);
+      if (nsent && few && lane < (int)nsent && chunk_off + lane < geo.n_exact) exv = exact[chunk_off + lane];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const V w = *reinterpret_cast<const V*>(sb + 16 * lane + 512 * q);
@@ -405,14 +434,12 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
       }
       uint32_t code[Q][VN];
       T ov[Q][VN];
-      bool lsnt = false;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         codes_at<B, VN>(sb + ST::kBase, VN * lane + 32 * VN * q, code[q]);
 #pragma unroll
         for (int v = 0; v < VN; ++v) {
           const uint32_t cd = code[q][v];
-          lsnt |= cd == sentinel;
           if constexpr (kOpcSmem)
             ov[q][v] = narrow<T>(__dmul_rn(s_opc[min(cd, (uint32_t)(1 << B) - 2u)], to_f64(bv[q][v])));
           else
@@ -420,9 +447,9 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         }
       }
       // ids in [k, sentinel) are errors; impossible with a full code book
-      unsigned maxbad = 0;
-      bool anybad = false;
       if (k < sentinel) {
+        unsigned maxbad = 0;
+        bool anybad = false;
 #pragma unroll
         for (int q = 0; q < Q; ++q)
 #pragma unroll
@@ -431,10 +458,12 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
               anybad = true;
               maxbad = max(maxbad, code[q][v]);
             }
+        if (anybad) {
+          atomicOr(&err->bad_index, 1u);
+          atomicMax(&err->max_bad_index, maxbad);
+        }
       }
-      const bool any_sent = __any_sync(0xffffffffu, lsnt);
-      const unsigned long long chunk_off = (any_sent || t.first) ? chunk_offset() : 0ULL;
-      if (any_sent) {
+      if (nsent) {   // warp-uniform (from the count pass)
         unsigned smask = 0, cnt_pk = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -450,37 +479,46 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         unsigned incl = cnt_pk;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          const unsigned y = __shfl_up_sync(FULL, incl, o);
           if (lane >= o) incl += y;
         }
-        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        const unsigned tot = __shfl_sync(FULL, incl, 31);
         const unsigned excl = incl - cnt_pk;
-        unsigned long long before_q = 0;
-        unsigned exhausted = 0;
+        unsigned before_q = 0, exhausted = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          unsigned long long pos = chunk_off + before_q + ((excl >> (8 * q)) & 255u);
+          unsigned r = before_q + ((excl >> (8 * q)) & 255u);   // rank within the chunk
           before_q += (tot >> (8 * q)) & 255u;
 #pragma unroll
-          for (int v = 0; v < VN; ++v)
-            if (smask >> (q * VN + v) & 1u) {
-              if (pos < geo.n_exact) ov[q][v] = exact[pos];
+          for (int v = 0; v < VN; ++v) {
+            const bool snt = smask >> (q * VN + v) & 1u;
+            if (few) {
+              const T got = __shfl_sync(FULL, exv, (int)(r & 31u));
+              if (snt) {
+                if (chunk_off + r < geo.n_exact) ov[q][v] = got;
+                else exhausted = 1;
+              }
+            } else if (snt) {
+              if (chunk_off + r < geo.n_exact) ov[q][v] = exact[chunk_off + r];
               else exhausted = 1;
-              ++pos;
             }
+            r += snt ? 1u : 0u;
+          }
         }
         if (exhausted) atomicOr(&err->exhausted, 1u);
-        const unsigned in_s = __reduce_add_sync(0xffffffffu, __popc(smask));
-        if (lane == 0) atomicAdd(&info[t.seg].n_sentinel, (unsigned long long)in_s);
-      }
-      if (anybad) {
-        atomicOr(&err->bad_index, 1u);
-        atomicMax(&err->max_bad_index, maxbad);
       }
 #pragma unroll
       for (int q = 0; q < Q; ++q)
         *reinterpret_cast<V*>(out + t.oi0 + VN * lane + 32 * VN * q) = *reinterpret_cast<const V*>(&ov[q][0]);
-      if (t.first && lane == 0) info[t.seg].inc_before = chunk_off;
+      // segment bookkeeping: inc_before = rank at the segment start, and
+      // n_sentinel = rank(end) - rank(start), added by the last / first chunk
+      if (lane == 0) {
+        if (t.first) {
+          info[t.seg].inc_before = chunk_off;
+          atomicAdd(&info[t.seg].n_sentinel, 0ULL - chunk_off);
+        }
+        if (t.last) atomicAdd(&info[t.seg].n_sentinel, chunk_off + nsent);
+      }
       __syncwarp();
       if (lane == 0) {
         fence_proxy_async_smem();
@@ -498,10 +536,9 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         for (int v = 0; v < VN; ++v) bv[q][v] = tw[v];
       }
     }
-    const unsigned long long chunk_off = chunk_offset();
     // codes and masks; element order is (q, lane, v)
     uint32_t code[Q][VN];
-    unsigned smask = 0, inmask = 0, cnt_pk = 0, ahead = 0;
+    unsigned smask = 0, inmask = 0, cnt_pk = 0, ahead = 0, upto = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       unsigned c = 0;
@@ -514,6 +551,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
           smask |= 1u << bitp;
           ++c;
           ahead += e < t.lo_rel;
+          upto += e < t.hi_rel;
         }
         if (e >= t.lo_rel && e < t.hi_rel) inmask |= 1u << bitp;
       }
@@ -523,10 +561,10 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     unsigned incl = cnt_pk;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
       if (lane >= o) incl += y;
     }
-    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    const unsigned tot = __shfl_sync(FULL, incl, 31);
     const unsigned excl = incl - cnt_pk;
     T ov[Q][VN];
     unsigned bad = 0, maxbad = 0, exhausted = 0;
@@ -572,11 +610,15 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
       atomicMax(&err->max_bad_index, maxbad);
     }
     if (exhausted) atomicOr(&err->exhausted, 1u);
-    const unsigned in_s = __reduce_add_sync(0xffffffffu, __popc(smask & inmask));
-    if (lane == 0 && in_s) atomicAdd(&info[t.seg].n_sentinel, (unsigned long long)in_s);
-    if (t.first) {
-      const unsigned ah = __reduce_add_sync(0xffffffffu, ahead);
-      if (lane == 0) info[t.seg].inc_before = chunk_off + ah;
+    if (t.first || t.last) {
+      const unsigned ah = __reduce_add_sync(FULL, ahead), up = __reduce_add_sync(FULL, upto);
+      if (lane == 0) {
+        if (t.first) {
+          info[t.seg].inc_before = chunk_off + ah;
+          atomicAdd(&info[t.seg].n_sentinel, 0ULL - (chunk_off + ah));
+        }
+        if (t.last) atomicAdd(&info[t.seg].n_sentinel, chunk_off + up);
+      }
     }
     // stage consumed: refill it kStages chunks ahead
     __syncwarp();

@@ -169,13 +169,15 @@ __device__ __forceinline__ KeyGrid32 key_grid32(double gmin, double gmax, double
 }
 
 // true (and qi = the exact ordinal, < nbins) when the f32 arithmetic decides
+// (nbins must be the dense span of the same gmin, gmax, width)
 __device__ __forceinline__ bool key_ordinal32(float key, const KeyGrid32& g, uint32_t& qi) {
   constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
   const float th = __fmaf_rn(key, g.iw32, g.c32);
   const float m = __fadd_rn(th, kMagic);
   const float d = __fsub_rn(th, __fsub_rn(m, kMagic));
   qi = (uint32_t)(__float_as_int(m) - 0x4B400000);
-  return fabsf(d) < g.hi && qi < g.nbins;
+  // decided => qi = floor(t*) <= floor(RN((gmax - gmin)/w)) = nbins - 1
+  return fabsf(d) < g.hi;
 }
 
 // origin + (q + 0.5) * width, add -> mul -> add (binning.py:50-51).
