@@ -38,7 +38,7 @@ METRIC = "compress+decompress GB/s of input (n*L per timestep / (t_compress + t_
 CONFIG_NAME = "cfg2: 512^3 fp64 8^3-block field, E=1e-3, B=8, top-k, 1 MiB index blocks"
 # k_minmax, k_hist_prep, k_hist_dev, k_select, k_encode, k_scan_{reduce,top,apply},
 # k_enc_finalize, k_dec_count, k_scan_{reduce,top,apply}, k_dec_chunks
-GPU_LAUNCHES_PER_STEP = 14
+GPU_LAUNCHES_PER_STEP = 12   # K1, prep, K2, K3, K4, scan x2, finalize | count, scan x2, K5 (ncu launch list)
 
 
 def parse():
@@ -243,7 +243,7 @@ def main():
 
     # per-phase device times: a separate instrumented pass (events between phases)
     phases = {}
-    for _ in range(3):
+    for _ in range(max(args.steps, 3)):
         evs = [("start", torch.cuda.Event(enable_timing=True))]
         evs[0][1].record(stream)
 
@@ -258,24 +258,47 @@ def main():
             phases.setdefault(nm, []).append(e0.elapsed_time(e1))
     mean = {k: sum(v) / len(v) for k, v in phases.items()}
 
-    class _Enc:  # geometry for the roofline arithmetic
-        n_inc = chk["n_inc"]
-        k = chk["k"]
-        prefix = pipe.prefix
-        stride = pipe.stride
-    enc = _Enc()
-    nb_local = enc.prefix.numel()
-    k4_bytes = n_local * (2 * L + BITS / 8) + enc.n_inc * L + 8 * nb_local
-    k5_bytes = n_local * (2 * L + BITS / 8) + enc.n_inc * L
-    k1_bytes = k2_bytes = 2 * n_local * L
+    # roofline arithmetic per phase.  alg = SURVEY.md 8(d) algorithmic bytes
+    # (the reference's three-pass schedule); moved = what this design reads
+    # and writes (K1 also writes 4-byte ratio keys so K2 reads 4 B instead of
+    # 2L; K5 adds the B/8 sentinel-count pass).
+    n_inc, nb_local = chk["n_inc"], pipe.prefix.numel()
+    pk = n_local * BITS / 8
+    rf = {
+        "K1_minmax": (2 * L * n_local, 2 * L * n_local + 4 * n_local, "k_minmax"),
+        "K2_histogram": (2 * L * n_local, 4 * n_local, "k_hist_dev"),
+        "K4_encode": (2 * L * n_local + pk + n_inc * L + 8 * nb_local,) * 2 + ("k_encode",),
+        "K5_decode": (2 * L * n_local + pk + n_inc * L, 2 * L * n_local + 2 * pk + n_inc * L, "k_dec_chunks"),
+    }
     peak, peak_src = peaks()
-    k4_gbs = k4_bytes / (mean["K4_encode"] / 1e3) / 1e9
-    k5_gbs = k5_bytes / (mean["K5_decode"] / 1e3) / 1e9
-    traffic = None
+    traffic_map = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("k_encode_dram_bytes_per_launch")
+            traffic_map = json.load(f).get("dram_bytes_per_launch", {})
+    roof_all = {}
+    for ph, (alg, moved, kern) in rf.items():
+        sec = mean[ph] / 1e3
+        roof_all[ph] = {"kernel": kern, "ms": mean[ph], "alg_bytes": alg, "moved_bytes": moved,
+                        "gbs": alg / sec / 1e9, "frac": alg / sec / 1e9 / peak,
+                        "moved_gbs": moved / sec / 1e9, "moved_frac": moved / sec / 1e9 / peak}
+    roof_all["K3_select"] = {"ms": mean["K3_select"], "note": "single CTA over the histogram (latency-bound)"}
+    roof_all["K4_encode"]["note"] = "includes the chunk-count scan and the finalize pass"
+    roof_all["K5_decode"]["note"] = "includes the sentinel-count pass (+B/8 bytes/element) and its scan"
+    step_alg = sum(v[0] for v in rf.values())
+    step_moved = sum(v[1] for v in rf.values())
+    roof_all["step"] = {"alg_bytes": step_alg, "moved_bytes": step_moved, "ms": ms_step,
+                        "frac": step_alg / (ms_step / 1e3) / 1e9 / peak,
+                        "moved_frac": step_moved / (ms_step / 1e3) / 1e9 / peak,
+                        "note": "graph-replayed step; alg = SURVEY 8(d) compress 6L+B/8+aL + decompress 2L+B/8+aL"}
+    roof_all["timing"] = (f"phase times: CUDA events between phases on the launch stream, mean of "
+                          f"{max(args.steps, 3)} eager steps after the timed graph replays")
+    dom = max(("K1_minmax", "K2_histogram", "K4_encode", "K5_decode"), key=lambda k: mean[k])
+    d = roof_all[dom]
+    roofline = {"bound": "hbm", "kernel": f"{d['kernel']} ({dom.split('_')[0]}, the longest phase)",
+                "achieved": d["gbs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
+                "traffic": traffic_map.get(d["kernel"]), "alg_bytes_per_launch": d["alg_bytes"],
+                "moved_bytes_per_launch": d["moved_bytes"], "moved_frac": d["moved_frac"], "peak_source": peak_src}
     compress_ms = mean["K1_minmax"] + mean["K2_histogram"] + mean["K3_select"] + mean["K4_encode"]
 
     e2e = None
@@ -330,27 +353,13 @@ def main():
             "config": {"workload": CONFIG_NAME, "n_per_gpu": n_local, "n_total": n_total,
                        "parallelism": f"dp{world} (contiguous element shards)",
                        "l2": "inputs 2 GiB/GPU > 126 MB L2 (no flush needed)",
-                       "k": enc.k, "alpha": enc.n_inc / n_local, "hist_form": "dense",
+                       "k": chk["k"], "alpha": n_inc / n_local, "hist_form": "dense",
                        "execution": "sync-free device pipeline" + (" replayed as one CUDA graph" if use_graph else "")},
             "compress": {"ms": compress_ms, "gbs_per_gpu": n_local * L / (compress_ms / 1e3) / 1e9},
             "decompress": {"ms": mean["K5_decode"], "gbs_per_gpu": n_local * L / (mean["K5_decode"] / 1e3) / 1e9},
             "phase_ms": mean,
-            "roofline": {"bound": "hbm", "kernel": "k_encode (K4)", "achieved": k4_gbs, "peak": peak,
-                         "unit": "GB/s", "frac": k4_gbs / peak, "traffic": traffic,
-                         "alg_bytes_per_launch": k4_bytes, "peak_source": peak_src},
-            "roofline_all": {
-                "K1_minmax": {"alg_bytes": k1_bytes, "ms": mean["K1_minmax"],
-                              "gbs": k1_bytes / (mean["K1_minmax"] / 1e3) / 1e9,
-                              "frac": k1_bytes / (mean["K1_minmax"] / 1e3) / 1e9 / peak},
-                "K2_histogram": {"alg_bytes": k2_bytes, "ms": mean["K2_histogram"],
-                                 "gbs": k2_bytes / (mean["K2_histogram"] / 1e3) / 1e9,
-                                 "frac": k2_bytes / (mean["K2_histogram"] / 1e3) / 1e9 / peak},
-                "K3_select": {"ms": mean["K3_select"]},
-                "K4_encode": {"alg_bytes": k4_bytes, "ms": mean["K4_encode"], "gbs": k4_gbs,
-                              "frac": k4_gbs / peak, "note": "includes chunk-count scan + finalize"},
-                "K5_decode": {"alg_bytes": k5_bytes, "ms": mean["K5_decode"], "gbs": k5_gbs, "frac": k5_gbs / peak,
-                              "note": "includes the sentinel-count pass (+B/8 bytes/element) and its scan"},
-                "note": "phase times from an event-instrumented pass; the headline value is the graph replay"},
+            "roofline": roofline,
+            "roofline_all": roof_all,
             "e2e": e2e,
             "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
             "cpu_baseline": cpu,
