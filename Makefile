@@ -10,7 +10,7 @@ LIB := paper_1703_02438_b200/libnmkgpu.so
 
 all: $(LIB)
 
-build/%.o: paper_1703_02438_b200/csrc/%.cu paper_1703_02438_b200/csrc/nmk_common.cuh paper_1703_02438_b200/csrc/nmk_scan.cuh include/nmk_b200.h
+build/%.o: paper_1703_02438_b200/csrc/%.cu $(wildcard paper_1703_02438_b200/csrc/*.cuh) include/nmk_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 

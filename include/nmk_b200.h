@@ -138,13 +138,16 @@ int nmk_select(const unsigned long long* keys, const unsigned long long* counts,
  * block_stride >= ceil(epb*bits/8) and a multiple of 16.
  * exact: n_local elements of capacity; prefix: local prefix per local block
  * (entry for a block whose start precedes elem0 is left untouched);
- * n_inc: device u64 total of local incompressible values. */
+ * n_inc: device u64 total of local incompressible values.
+ * recon (nullable, n_local elements of dtype): also write the decoder's
+ * reconstruction of every local element -- T((1+c)*base) or the exact value
+ * -- bit-identical to nmk_decode's output (compress_series). */
 size_t nmk_encode_ws_bytes(uint64_t n_local, uint64_t elem0, uint64_t epb, int dtype);
 int nmk_encode(const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
                uint64_t n_total, int dtype, const double* centers, const double* cuts,
                int k, int bits, double tol_bin, double tolerance, uint64_t epb,
                uint8_t* packed, uint64_t block_stride, void* exact,
-               unsigned long long* prefix, unsigned long long* n_inc,
+               unsigned long long* prefix, unsigned long long* n_inc, void* recon,
                void* ws, size_t ws_bytes, void* stream);
 
 /* -- K5: fused unpack + sentinel scan + reconstruct, batched over segments
@@ -192,7 +195,7 @@ int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t
                    uint64_t n_total, int dtype, const double* centers, const double* cuts,
                    const nmk_model* model, int k_cap, int bits, double tolerance, uint64_t epb,
                    uint8_t* packed, uint64_t block_stride, void* exact,
-                   unsigned long long* prefix, unsigned long long* n_inc,
+                   unsigned long long* prefix, unsigned long long* n_inc, void* recon,
                    void* ws, size_t ws_bytes, void* stream);
 int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint64_t first_block,
                    int bits, uint64_t epb, uint64_t n_total,

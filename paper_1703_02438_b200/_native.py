@@ -68,14 +68,14 @@ SIGNATURES = {
     "nmk_select": (i32, [vp, vp, u64, vp, vp, dbl, dbl, i32, u64, i32, vp, vp, vp, u64, vp, vp]),
     "nmk_encode_ws_bytes": (sz, [u64, u64, u64, i32]),
     "nmk_encode": (i32, [vp, vp, u64, u64, u64, i32, vp, vp, i32, i32, dbl, dbl, u64, vp, u64, vp,
-                         vp, vp, vp, sz, vp]),
+                         vp, vp, vp, vp, sz, vp]),
     "nmk_decode_ws_bytes": (sz, [u64p, u64p, i32, u64, u64]),
     "nmk_decode": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, i32, vp, u64, vp, vp, i32,
                          u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
     "nmk_hist_prep": (i32, [vp, dbl, u64, vp, vp]),
     "nmk_hist_dense_dev": (i32, [vp, vp, vp, u64, i32, vp, dbl, vp, vp]),
     "nmk_encode_dev": (i32, [vp, vp, u64, u64, u64, i32, vp, vp, vp, i32, i32, dbl, u64, vp, u64, vp,
-                             vp, vp, vp, sz, vp]),
+                             vp, vp, vp, vp, sz, vp]),
     "nmk_decode_dev": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, i32,
                              u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
     "nmk_pack": (i32, [vp, u64, i32, vp, vp]),

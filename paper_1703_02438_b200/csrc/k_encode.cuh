@@ -1,0 +1,551 @@
+// k_encode.cuh — K4 kernels and their launchers (templates).  The
+// instantiations for each index length B are spread over k_encode_b*.cu so
+// the 2 dtypes x 29 B x {plain, fused reconstruction} kernels compile in
+// parallel; k_encode.cu holds the dispatch, finalize and the C-ABI.
+#pragma once
+
+// k_encode.cu — K4: fused classify + round-trip filter + B-bit packing +
+// stable compaction of the incompressible values.
+//
+// One pass over both snapshots replaces phases 3a, 3b and 4a of
+// compress_pair (pkg/src/nmk/pipeline.py:232-288):
+//   nearest_center + compressible_mask (binning.py:287-301, 350-359),
+//   _roundtrip_filter (pipeline.py:143-160), the sentinel substitution,
+//   the element-order compaction current[~flags] and the per-block
+//   incompressible prefix (pipeline.py:257-276), and pack_block MSB-first
+//   (codec.py:83-92) into the block layout of codec.BlockLayout (codec.py:28-59).
+//
+// Work unit: a CHUNK of 256 elements = one warp x 8 consecutive elements per
+// lane, laid on the grid of index blocks (chunks never straddle a block), so
+// each lane's 8 codes are exactly B whole bytes of its block and a chunk's
+// 32*B bytes start 16-byte aligned.  Warps run independently (no block-wide
+// barrier): a chunk writes its packed bytes, its incompressible count and
+// its incompressible values into its own 256-slot scratch window.  A short
+// finalize pass (k_scan.cu + k_enc_finalize) turns the counts into positions,
+// moves the (rare) values into the compacted list and fills the per-block
+// prefix table.
+#include "nmk_common.cuh"
+#include "nmk_scan.cuh"
+
+namespace nmk {
+
+constexpr int kChunk = 32 * kGroup;   // 256 elements per warp chunk
+constexpr int kEncThreads = 256;      // 8 warps per CTA
+constexpr int kSmemCuts = 4096;       // cuts in shared memory up to this many
+
+template <int B>
+__device__ __forceinline__ void pack8(const uint32_t (&code)[kGroup], uint8_t* dst) {
+  // MSB-first bit string of 8 codes = B bytes; B is a compile-time constant
+  // so every shift below resolves statically.
+  uint8_t out[B];
+  unsigned long long acc = 0;
+  int nacc = 0, ob = 0;
+#pragma unroll
+  for (int e = 0; e < kGroup; ++e) {
+    acc = (acc << B) | code[e];
+    nacc += B;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (nacc >= 8) {
+        out[ob++] = (uint8_t)(acc >> (nacc - 8));
+        nacc -= 8;
+      }
+    }
+  }
+  // widest aligned store the byte offset lane*B allows
+  if constexpr (B % 16 == 0) {
+#pragma unroll
+    for (int w = 0; w < B / 16; ++w) {
+      uint4 v;
+      uint32_t* p = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        p[q] = out[w * 16 + q * 4] | (out[w * 16 + q * 4 + 1] << 8) | (out[w * 16 + q * 4 + 2] << 16) |
+               ((uint32_t)out[w * 16 + q * 4 + 3] << 24);
+      reinterpret_cast<uint4*>(dst)[w] = v;
+    }
+  } else if constexpr (B % 8 == 0) {
+#pragma unroll
+    for (int w = 0; w < B / 8; ++w) {
+      uint2 v;
+      v.x = out[w * 8] | (out[w * 8 + 1] << 8) | (out[w * 8 + 2] << 16) | ((uint32_t)out[w * 8 + 3] << 24);
+      v.y = out[w * 8 + 4] | (out[w * 8 + 5] << 8) | (out[w * 8 + 6] << 16) | ((uint32_t)out[w * 8 + 7] << 24);
+      reinterpret_cast<uint2*>(dst)[w] = v;
+    }
+  } else if constexpr (B % 4 == 0) {
+#pragma unroll
+    for (int w = 0; w < B / 4; ++w)
+      reinterpret_cast<uint32_t*>(dst)[w] =
+          out[w * 4] | (out[w * 4 + 1] << 8) | (out[w * 4 + 2] << 16) | ((uint32_t)out[w * 4 + 3] << 24);
+  } else if constexpr (B % 2 == 0) {
+#pragma unroll
+    for (int w = 0; w < B / 2; ++w)
+      reinterpret_cast<uint16_t*>(dst)[w] = (uint16_t)(out[w * 2] | (out[w * 2 + 1] << 8));
+  } else {
+#pragma unroll
+    for (int w = 0; w < B; ++w) dst[w] = out[w];
+  }
+}
+
+struct EncodeGeom {
+  uint64_t n_local, elem0, n_total, epb, cpb, g0, nchunks, b0, stride;
+  FastDiv fd_cpb;   // chunk id -> block
+};
+
+// Chunk c of this range: block, in-block chunk index and element spans.
+struct ChunkSpan {
+  uint64_t b, ci, blk_start, blk_end, lo, hi, chunk_lo;
+};
+
+__device__ __forceinline__ ChunkSpan chunk_span(const EncodeGeom& geo, uint64_t c) {
+  ChunkSpan s;
+  const uint64_t g = geo.g0 + c;
+  s.b = g / geo.cpb;
+  s.ci = g - s.b * geo.cpb;
+  s.blk_start = s.b * geo.epb;
+  s.blk_end = s.blk_start + geo.epb;
+  if (s.blk_end > geo.n_total) s.blk_end = geo.n_total;
+  s.chunk_lo = s.blk_start + s.ci * kChunk;
+  uint64_t chunk_hi = s.chunk_lo + kChunk;
+  if (chunk_hi > s.blk_end) chunk_hi = s.blk_end;
+  const uint64_t local_end = geo.elem0 + geo.n_local;
+  s.lo = s.chunk_lo > geo.elem0 ? s.chunk_lo : geo.elem0;
+  s.hi = chunk_hi < local_end ? chunk_hi : local_end;
+  return s;
+}
+
+template <typename T> struct EVec;
+template <> struct EVec<double> { using V = double2; static constexpr int N = 2; };
+template <> struct EVec<float>  { using V = float4;  static constexpr int N = 4; };
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* __restrict__ p, T (&v)[kGroup]) {
+  using V = typename EVec<T>::V;
+  constexpr int VN = EVec<T>::N;
+#pragma unroll
+  for (int q = 0; q < kGroup / VN; ++q) {
+    V w = __ldg(reinterpret_cast<const V*>(p) + q);
+    const T* t = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) v[q * VN + e] = t[e];
+  }
+}
+
+// Per-element classification: returns the code (idx or sentinel).
+template <typename T, typename Find>
+__device__ __forceinline__ uint32_t classify(T bt, T xt, Find&& find, const double* __restrict__ centers,
+                                             double tol_bin, double tol, uint32_t sentinel) {
+  const double bd = to_f64(bt), xd = to_f64(xt);
+  // core.py:129-136: finite(r) already implies finite(b) and finite(x)
+  double r = __ddiv_rn(__dsub_rn(xd, bd), bd);
+  bool valid = finite64(r);
+  if (!valid) {
+    valid = (bd == 0.0 && xd == 0.0);
+    r = 0.0;
+  }
+  const uint32_t idx = find(r);
+  const double c = __ldg(centers + idx);
+  const bool near = valid && (fabs(__dsub_rn(r, c)) <= tol_bin);
+  const bool rt = roundtrip_ok<T>(c, bd, xd, tol);   // branch-free
+  return (near && rt) ? idx : sentinel;
+}
+
+// The exact classification with a binary search over the cuts in global
+// memory: the fallback of the direct-grid mode (out of line, rarely taken).
+template <typename T>
+__device__ __noinline__ uint32_t classify_exact(T bt, T xt, const double* __restrict__ cuts_g, int ncuts,
+                                                const double* __restrict__ centers_g, double tol_bin, double tol,
+                                                uint32_t sentinel) {
+  return classify<T>(bt, xt,
+                     [&](double r) -> uint32_t {
+                       int a = 0, z = ncuts;
+                       while (a < z) {
+                         int mid = (a + z) >> 1;
+                         if (__ldg(cuts_g + mid) < r) a = mid + 1; else z = mid;
+                       }
+                       return (uint32_t)a;
+                     },
+                     centers_g, tol_bin, tol, sentinel);
+}
+
+// ---- direct-grid mode ---------------------------------------------------------
+// The selected centers sit in the middles of histogram bins of width
+// w = 2*tol_bin.  Lay a grid of cells of width w with origin c_0 - w/2;
+// center i lies within D cells of the middle of cell q_i (D measured at set-up,
+// covering quantisation to T and rounding).  For an element whose position
+// u = (r - c_0)/w + 1/2 is inside cell q with margin m > D + (cut rounding):
+//   * q = q_j selected:  both neighbouring cuts lie outside the cell, so
+//     searchsorted(cuts, r) = j, and |r - c_j| < w/2 = tol_bin  -> code j if
+//     the round-trip filter passes;
+//   * q not selected:    every center is > w/2 away -> sentinel.
+// u is estimated from the division-free ratio (|ra - r| <= |ra| 2^-49) as
+// t' = (ra - c_0)/w ~ u - 1/2, whose nearest integer (magic-number rounding)
+// is the cell; the margin m bounds the error over the table's range, and
+// cells beyond it are sentinels while the error stays below half a cell
+// (|t'| < 2^30, |c_0|/w < 2^40).
+// Anything closer to a cell edge takes the exact path (classify_exact), so
+// the codes are the exact path's codes bit for bit.
+struct DirectGrid {
+  double c0, iw, hm;       // first center, 1/w, 1/2 - margin
+  uint32_t tab_s, opc_s;   // shared addresses: cell+1 -> center, center -> RN(1 + c)
+  uint32_t span2;          // table entries: cells -1 .. span
+  bool far_ok;             // |t'| < 2^30 outside the table is decisive
+};
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// opaque copies: keep launch constants in registers instead of letting the
+// compiler re-derive them (e.g. shared addresses from the CTA id) per element
+__device__ __forceinline__ double opaque(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// Division-free ratio for the direct grid.  The reciprocal seed is trusted
+// only when its first residual |1 - b*y0| < 2^-16 (which also rejects b = 0,
+// subnormal, huge, inf and NaN b); two Newton steps then give y within
+// 2^-51 of 1/b, so |ra - r| <= |ra| * 2^-49 (+ 2^-1070 if ra is subnormal).
+__device__ __forceinline__ double ratio_seeded(double b, double x, bool& ok) {
+  const double y0 = rcp_approx(b);
+  const double e0 = __fma_rn(-b, y0, 1.0);
+  ok = fabs(e0) < 0x1p-16;
+  double y = __fma_rn(y0, e0, y0);
+  const double e1 = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(y, e1, y);
+  return __dmul_rn(__dsub_rn(x, b), y);
+}
+
+constexpr uint32_t kNoCenter = 0xffffffffu;
+
+// All threads: builds tab[0..span+2) (cell q at q+1, kNoCenter = none) and
+// opc[0..k) = RN(1 + c_i); returns true when the mode applies (block-uniform).
+__device__ __forceinline__ bool setup_direct(const double* __restrict__ centers_g, int k, double tol_bin,
+                                             uint32_t* tab, double* opc, DirectGrid& g, int* s_fail,
+                                             unsigned long long* s_dmax, int* s_span) {
+  if (threadIdx.x == 0) { *s_fail = 0; *s_dmax = 0ULL; *s_span = 0; }
+  __syncthreads();
+  const double w = __dmul_rn(2.0, tol_bin);
+  const double iw = __ddiv_rn(1.0, w);
+  const double c0 = __ldg(centers_g);
+  const bool ok0 = k >= 1 && k <= kLutCells - 2 && tol_bin > 0.0 && finite64(w) && finite64(iw) && finite64(c0);
+  // cell of center i: p = (c_i - c_0)/w + 1/2, q = floor(p), offset |p - q - 1/2|
+  auto cell = [&](double c, double& p) { p = __dadd_rn(__dmul_rn(__dsub_rn(c, c0), iw), 0.5); return floor(p); };
+  if (ok0) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const double c = __ldg(centers_g + i);
+      opc[i] = __dadd_rn(1.0, c);   // the decoder's (1 + c) (core.py:202-205)
+      double p, pp;
+      const double q = cell(c, p);
+      const double d = fabs(__dsub_rn(p, __dadd_rn(q, 0.5)));
+      bool ok = p >= 0.0 && p < (double)(kLutCells - 2) && d <= 0.25;
+      if (ok && i > 0) ok = cell(__ldg(centers_g + i - 1), pp) < q;
+      if (!ok) *s_fail = 1;
+      else atomicMax(s_dmax, (unsigned long long)__double_as_longlong(d));   // d >= 0: bits are ordered
+      if (ok && i == k - 1) *s_span = (int)q + 1;
+    }
+  }
+  __syncthreads();
+  if (!ok0 || *s_fail) return false;
+  const int span = *s_span;
+  for (int i = threadIdx.x; i < span + 2; i += blockDim.x) tab[i] = kNoCenter;
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double p;
+    tab[(int)cell(__ldg(centers_g + i), p) + 1] = (uint32_t)i;
+  }
+  // margin (cells): ratio error over the table's range (|ra| <= A, relative
+  // 2^-49 taken as 2^-44, plus the subnormal floor), rounding of t' and of
+  // the cell computation, of the cuts, the measured center offsets D
+  const double A = fabs(c0) + (span + 2.0) * w;
+  const double D = __longlong_as_double((long long)*s_dmax);
+  const double m = (A * iw * 0x1p-44 + A * iw * 0x1p-50 + (span + 2.0) * 0x1p-48 + iw * 0x1p-1000) * 1.01 + D +
+                   0x1p-40;
+  g.hm = opaque(0.5 - m);
+  g.c0 = c0;
+  g.iw = iw;
+  g.span2 = (uint32_t)span + 2;
+  g.far_ok = fabs(c0) * iw < 0x1p+40;
+  g.tab_s = opaque(smem_u32(tab));
+  g.opc_s = opaque(smem_u32(opc));
+  __syncthreads();
+  return m < 0.02;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t classify_direct(T bt, T xt, const DirectGrid& g, double tol, uint32_t sentinel,
+                                                    const double* __restrict__ cuts_g, int ncuts,
+                                                    const double* __restrict__ centers_g, double tol_bin) {
+  constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: adds round to an integer
+  const double bd = to_f64(bt), xd = to_f64(xt);
+  bool ok;
+  const double ra = ratio_seeded(bd, xd, ok);
+  const double t = __dmul_rn(__dsub_rn(ra, g.c0), g.iw);   // ~ u - 1/2
+  const double mm = __dadd_rn(t, kMagic);
+  const double dd = __dsub_rn(t, __dsub_rn(mm, kMagic));   // t - RN_int(t), exact
+  const uint32_t q1 = (uint32_t)__double2loint(mm) + 1u;   // cell + 1 (low word of the magic sum)
+  if (ok && fabs(t) < 0x1p+30) {   // the low word holds the cell exactly
+    if (q1 < g.span2) {   // cells -1 .. span: the table decides with the margin
+      if (fabs(dd) < g.hm) {
+        const uint32_t idx = lds_u32(g.tab_s + 4 * q1);
+        if (idx == kNoCenter) return sentinel;
+        // round-trip filter (pipeline.py:143-160) with the stored RN(1 + c)
+        const double rec = to_f64(narrow<T>(__dmul_rn(lds_f64(g.opc_s + 8 * idx), bd)));
+        return fabs(__dsub_rn(rec, xd)) <= __dmul_rn(tol, fabs(bd)) ? idx : sentinel;
+      }
+    } else if (g.far_ok) {   // two or more cells outside: no center within w/2
+      return sentinel;
+    }
+  }
+  return classify_exact<T>(bt, xt, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel);
+}
+
+// The chunk loop, instantiated once per classification flavour.
+template <typename T, int B, bool kRecon, typename Cls, typename Rec>
+__device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const T* __restrict__ cur,
+                                              const EncodeGeom& geo, uint8_t* __restrict__ packed,
+                                              T* __restrict__ scratch, uint32_t* __restrict__ counts,
+                                              uint8_t* my, T* __restrict__ recon, Cls&& cls, Rec&& rec_of) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t sentinel = (1u << B) - 1u;
+  const uint64_t local_end = geo.elem0 + geo.n_local;
+  const bool ptr_al = (((uintptr_t)base | (uintptr_t)cur | (kRecon ? (uintptr_t)recon : 0)) & 15) == 0;
+  // chunk ids fit 32 bits (n < 2^40): cheap block / in-block split
+  const uint32_t cpb = (uint32_t)geo.cpb;
+  const uint32_t nw = gridDim.x * (kEncThreads / 32);
+  for (uint32_t c = blockIdx.x * (kEncThreads / 32) + wid; c < (uint32_t)geo.nchunks; c += nw) {
+    const uint32_t g = (uint32_t)geo.g0 + c;
+    const uint32_t b = geo.fd_cpb.div(g), ci = g - b * cpb;
+    const uint64_t blk_start = (uint64_t)b * geo.epb;
+    const uint64_t blk_end = min(blk_start + geo.epb, geo.n_total);
+    const uint64_t chunk_lo = blk_start + (uint64_t)ci * kChunk;
+    const uint64_t lo = max(chunk_lo, geo.elem0), hi = min(blk_end, local_end);
+    const uint64_t grp_lo = chunk_lo + (uint64_t)lane * kGroup;
+    const bool full = chunk_lo >= geo.elem0 && chunk_lo + kChunk <= hi;  // warp-uniform
+    T bv[kGroup], xv[kGroup];
+    uint32_t code[kGroup];
+    unsigned inc_mask = 0;
+    const int64_t li = (int64_t)grp_lo - (int64_t)geo.elem0;
+    constexpr int VN = EVec<T>::N;
+    if (full && ptr_al && (li % VN) == 0) {
+      load8<T>(base + li, bv);
+      load8<T>(cur + li, xv);
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e) {
+        code[e] = cls(bv[e], xv[e]);
+        inc_mask |= (code[e] == sentinel ? 1u : 0u) << e;
+      }
+      if constexpr (kRecon) {   // the decoder's values, written by the encoder
+        using V = typename EVec<T>::V;
+#pragma unroll
+        for (int q = 0; q < kGroup / VN; ++q) {
+          V w;
+          T* t = reinterpret_cast<T*>(&w);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) {
+            const int ee = q * VN + e;
+            t[e] = code[ee] == sentinel ? xv[ee] : rec_of(code[ee], bv[ee]);
+          }
+          reinterpret_cast<V*>(recon + li)[q] = w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e) {
+        const uint64_t j = grp_lo + e;
+        const bool in = j >= lo && j < hi;
+        bv[e] = in ? __ldg(base + (li + e)) : T(0);
+        xv[e] = in ? __ldg(cur + (li + e)) : T(0);
+        code[e] = in ? cls(bv[e], xv[e]) : 0u;
+        inc_mask |= (in && code[e] == sentinel ? 1u : 0u) << e;
+        if constexpr (kRecon)
+          if (in) recon[li + e] = code[e] == sentinel ? xv[e] : rec_of(code[e], bv[e]);
+      }
+    }
+    // warp-level compaction of the incompressible values into the chunk's
+    // scratch window (element order); most chunks have none
+    unsigned total = 0;
+    if (__any_sync(0xffffffffu, inc_mask != 0)) {
+      const unsigned cnt = __popc(inc_mask);
+      unsigned incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      total = __shfl_sync(0xffffffffu, incl, 31);
+      if (inc_mask) {
+        T* w = scratch + (uint64_t)c * kChunk + (incl - cnt);
+#pragma unroll
+        for (int e = 0; e < kGroup; ++e)
+          if (inc_mask >> e & 1u) *w++ = xv[e];   // raw bits (NaN payloads kept)
+      }
+    }
+    if (lane == 0) counts[c] = total;
+    // packed bytes: stage per warp, then 16-byte stores clipped to the block
+    pack8<B>(code, my + lane * B);
+    __syncwarp();
+    const uint64_t blk_bytes = ((blk_end - blk_start) * B + 7) / 8;
+    const uint64_t off = (uint64_t)ci * (32 * B);
+    const uint32_t nbytes = (uint32_t)min(blk_bytes > off ? blk_bytes - off : 0, (uint64_t)(32 * B));
+    uint8_t* dst = packed + (uint64_t)(b - geo.b0) * geo.stride + off;
+    const uint32_t nvec = nbytes / 16;
+    for (uint32_t i = lane; i < nvec; i += 32)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(my)[i];
+    for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) dst[i] = my[i];
+    __syncwarp();
+  }
+}
+
+template <typename T, int B, bool kRecon>
+__global__ void __launch_bounds__(kEncThreads, 4)
+k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
+         const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
+         double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
+         uint32_t* __restrict__ counts, const nmk_model* __restrict__ model, bool smem_ok, T* __restrict__ recon) {
+  __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
+  __shared__ uint32_t lut32[kLutCells];   // cell -> center (direct mode) or, as u16, the cut grid
+  uint16_t* lut = reinterpret_cast<uint16_t*>(lut32);
+  __shared__ double s_lo, s_scale;
+  __shared__ bool s_use;
+  __shared__ int s_fail, s_span;
+  __shared__ unsigned long long s_dmax;
+  extern __shared__ __align__(16) double cutsp[];   // [-inf, cuts..., +inf, +inf] or centers
+
+  if (model) {   // sync-free path: the model scalars live on the device
+    if (model->status != 0) {   // nothing to encode: leave empty chunks behind
+      for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += gridDim.x * blockDim.x)
+        counts[c] = 0;
+      return;
+    }
+    k = model->k;
+    tol_bin = model->tol_bin;
+  }
+  const int ncuts = k - 1;
+  const uint32_t sentinel = (1u << B) - 1u;
+  uint8_t* my = wbytes[threadIdx.x >> 5];
+  const bool cuts_in_smem = smem_ok && k <= kSmemCuts + 1;
+  if (cuts_in_smem) {
+    DirectGrid g;
+    if (setup_direct(centers_g, k, tol_bin, lut32, cutsp, g, &s_fail, &s_dmax, &s_span)) {
+      encode_chunks<T, B, kRecon>(
+          base, cur, geo, packed, scratch, counts, my, recon,
+          [&](T b, T x) -> uint32_t { return classify_direct<T>(b, x, g, tol, sentinel, cuts_g, ncuts, centers_g, tol_bin); },
+          [&](uint32_t cd, T b) -> T { return narrow<T>(__dmul_rn(lds_f64(g.opc_s + 8 * cd), to_f64(b))); });
+      return;
+    }
+    for (int i = threadIdx.x; i < ncuts; i += kEncThreads) cutsp[i + 1] = cuts_g[i];
+    if (threadIdx.x == 0) {
+      cutsp[0] = __longlong_as_double(0xfff0000000000000LL);
+      cutsp[ncuts + 1] = __longlong_as_double(0x7ff0000000000000LL);
+      cutsp[ncuts + 2] = cutsp[ncuts + 1];   // read (unused) when i == ncuts
+    }
+  }
+  __syncthreads();
+  if (cuts_in_smem) {
+    double lo, sc;
+    bool use;
+    build_cut_lut(cutsp + 1, ncuts, lut, lo, sc, use);
+    if (threadIdx.x == 0) { s_lo = lo; s_scale = sc; s_use = use; }
+  } else if (threadIdx.x == 0) {
+    s_lo = 0.0; s_scale = 0.0; s_use = false;
+  }
+  __syncthreads();
+  if (s_use) {
+    // O(1) search: the grid cell gives i = #cuts below the cell's left edge;
+    // with at most one cut per cell the answer is i or i+1, settled by exact
+    // compares against the three candidate cuts (padded with -inf/+inf).
+    // Any other case (rounding at a cell edge, a crowded cell) walks exactly.
+    const double lo = s_lo, scale = s_scale;
+    auto find = [&](double r) -> uint32_t {
+      int g = __double2int_rz((r - lo) * scale);   // saturating
+      g = min(max(g, 0), kLutCells - 1);
+      int i = lut[g];
+      const double a = cutsp[i], m = cutsp[i + 1], z = cutsp[i + 2];
+      const bool up = m < r;
+      if (up ? (r <= z) : (a < r)) return (uint32_t)(i + up);
+      while (i < ncuts && cutsp[i + 1] < r) ++i;
+      while (i > 0 && cutsp[i] >= r) --i;
+      return (uint32_t)i;
+    };
+    encode_chunks<T, B, kRecon>(
+        base, cur, geo, packed, scratch, counts, my, recon,
+        [&](T b, T x) -> uint32_t { return classify<T>(b, x, find, centers_g, tol_bin, tol, sentinel); },
+        [&](uint32_t cd, T b) -> T { return apply_center<T>(__ldg(centers_g + cd), to_f64(b)); });
+  } else {
+    auto find = [&](double r) -> uint32_t {
+      int a = 0, z = ncuts;
+      while (a < z) {
+        int mid = (a + z) >> 1;
+        if (__ldg(cuts_g + mid) < r) a = mid + 1; else z = mid;
+      }
+      return (uint32_t)a;
+    };
+    encode_chunks<T, B, kRecon>(
+        base, cur, geo, packed, scratch, counts, my, recon,
+        [&](T b, T x) -> uint32_t { return classify<T>(b, x, find, centers_g, tol_bin, tol, sentinel); },
+        [&](uint32_t cd, T b) -> T { return apply_center<T>(__ldg(centers_g + cd), to_f64(b)); });
+  }
+}
+
+static int sm_count_e() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <typename T, int B, bool kRecon>
+static void launch_encode_k(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
+                            const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
+                            uint32_t* counts, const nmk_model* model, int k_cap, void* recon, cudaStream_t s) {
+  const bool smem_ok = k_cap <= kSmemCuts + 1;
+  const size_t smem = smem_ok ? (size_t)(k_cap + 2) * 8 : 0;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_encode<T, B, kRecon>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode<T, B, kRecon>, kEncThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)sm_count_e() * per_sm;
+  uint64_t need = (geo.nchunks + 7) / 8;
+  if (grid > need) grid = need;
+  k_encode<T, B, kRecon><<<(unsigned)grid, kEncThreads, smem, s>>>((const T*)base, (const T*)cur, geo, centers,
+                                                                   cuts, k, tol_bin, tol, packed, (T*)scratch, counts,
+                                                                   model, smem_ok, (T*)recon);
+}
+
+// the fused reconstruction is a separate instantiation: the plain encode
+// keeps its register budget
+template <typename T, int B>
+void launch_encode(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
+                          const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
+                          uint32_t* counts, const nmk_model* model, int k_cap, void* recon, cudaStream_t s) {
+  if (recon)
+    launch_encode_k<T, B, true>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, model, k_cap,
+                                recon, s);
+  else
+    launch_encode_k<T, B, false>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, model,
+                                 k_cap, nullptr, s);
+}
+
+}  // namespace nmk

@@ -171,11 +171,13 @@ class _PhaseClock:
 
 def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: int = 1 << 20,
            *, elem0: int = 0, n_total: int | None = None, comm=None, ws: Workspace | None = None,
-           stream=None, timing: bool = False) -> DeviceEncoding:
+           stream=None, timing: bool = False, recon=None) -> DeviceEncoding:
     """Run K1..K4 on device tensors ``base``/``cur`` (1-D, same dtype, CUDA).
 
     ``elem0``/``n_total`` place this range inside a longer global stream (a
     multi-GPU shard); ``comm`` (see distributed.py) performs the exchanges.
+    ``recon`` (a tensor like ``cur``) receives K4's reconstruction of every
+    element, bit-identical to decoding the result.
     """
     torch = _torch()
     if base.device.type != "cuda" or cur.device.type != "cuda":
@@ -300,9 +302,12 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
     if n_local > 0:
         e_bytes = lib.nmk_encode_ws_bytes(n_local, elem0, epb, dt)
         e_ws = ws.get("encode_ws", e_bytes)
+        if recon is not None and (recon.shape != cur.shape or recon.dtype != cur.dtype or not recon.is_cuda):
+            raise ValueError("recon must be a CUDA tensor like current")
         N.check(lib.nmk_encode(_p(base), _p(cur), n_local, elem0, n, dt, _p(centers), _p(cuts), k, B,
                                float(model.tol_bin), float(tolerance), epb, _p(packed), stride, _p(exact),
-                               _p(prefix), _p(n_inc_t), _p(e_ws), e_bytes, st))
+                               _p(prefix), _p(n_inc_t), _p(recon) if recon is not None else None, _p(e_ws),
+                               e_bytes, st))
     else:
         n_inc_t.zero_()
     clock.mark("assign_index")
@@ -441,9 +446,10 @@ class DevicePipeline:
             self.gathered_inc = torch.zeros(comm.world, dtype=torch.int64, device=dev)
 
     # -- enqueue --------------------------------------------------------------
-    def encode(self, base, cur, mark=None):
+    def encode(self, base, cur, mark=None, recon=None):
         """Enqueue K1..K4 (+ the exchanges).  ``mark(name)`` is called after
-        each phase (e.g. to record CUDA events)."""
+        each phase (e.g. to record CUDA events); ``recon`` receives K4's
+        reconstruction (= the decode of this encoding)."""
         lib, st = N.lib(), _stream()
         P = lambda t: t.data_ptr()  # noqa: E731
         mark = mark or (lambda name: None)
@@ -465,7 +471,7 @@ class DevicePipeline:
         N.check(lib.nmk_encode_dev(P(base), P(cur), self.n_local, self.elem0, self.n, self.dt, P(self.centers),
                                    P(self.cuts), P(self.model), self.k_cap, self.bits, self.tol, self.epb,
                                    P(self.packed), self.stride, P(self.exact), P(self.prefix), P(self.n_inc),
-                                   P(self.e_ws), self.e_bytes, st))
+                                   P(recon) if recon is not None else None, P(self.e_ws), self.e_bytes, st))
         mark("K4_encode")
         if self.comm is not None:
             # global positions of this rank's exact values / block prefixes;

@@ -182,9 +182,10 @@ def _check_strategy(config: PipelineConfig) -> None:
             f"strategy {config.strategy!r} is outside the B200 hot path (top_k binning only)")
 
 
-def _encode_device(base_d, cur_d, config: PipelineConfig, timing: bool = True):
+def _encode_device(base_d, cur_d, config: PipelineConfig, timing: bool = True, recon=None):
     try:
-        return engine.encode(base_d, cur_d, config.tolerance, config.bits, config.block_bytes, timing=timing)
+        return engine.encode(base_d, cur_d, config.tolerance, config.bits, config.block_bytes, timing=timing,
+                             recon=recon)
     except N.NativeError as exc:
         if exc.code == N.NMK_ERR_EMPTY_HIST:
             raise PipelineError("binning", "empty histogram") from exc
@@ -445,9 +446,10 @@ def compress_series(snapshots, config: PipelineConfig, name: str = "var0"):
     """Compress a snapshot chain (pipeline.py:343-372).
 
     Snapshot i is encoded against the reconstruction of snapshot i-1.  The
-    reconstruction never leaves the GPU: it is decoded from the packed stream
-    K4 just wrote (the same bytes the host variable holds), so the result is
-    identical to the reference's decompress-then-encode loop.
+    reconstruction never leaves the GPU: K4 writes it while encoding (the
+    decoder's arithmetic on the same codes and exact values), so
+    the chain equals the reference's decompress-then-encode loop without a
+    decode pass per step.
     """
     _check_strategy(config)
     snapshots = [np.ascontiguousarray(s) for s in snapshots]
@@ -462,14 +464,13 @@ def compress_series(snapshots, config: PipelineConfig, name: str = "var0"):
     TemporalPair(snapshots[0], snapshots[1])  # dtype / shape validation
     N.require_cuda()
     first = snapshots[0].copy()
+    import torch
     recon = to_device(first, "h2d_base")
+    nxt = torch.empty_like(recon)
     variables = []
     for i, snap in enumerate(snapshots[1:], start=1):
         cur = to_device(snap, "h2d_cur")
-        enc = _encode_device(recon, cur, config, timing=False)
+        enc = _encode_device(recon, cur, config, timing=False, recon=nxt)
         variables.append(assemble_variable(enc, config, f"{name}.{i:04d}"))
-        res = engine.decode_encoding(enc, recon)
-        if res.bad_index or res.exhausted:  # pragma: no cover - internal invariant
-            raise PipelineError("decode", "device reconstruction failed")
-        recon = res.out
+        recon, nxt = nxt, recon
     return first, variables

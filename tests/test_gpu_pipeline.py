@@ -62,10 +62,13 @@ def test_pipeline_matches_general_path(case, graph):
         b, c = _special_mix(1_001, 34, np.float64, 0.01); E, bits, bb = 1e-3, 6, 4096
     base = torch.from_numpy(b).cuda()
     cur = torch.from_numpy(c).cuda()
-    ref = engine.encode(base, cur, E, bits, bb)
+    rec_general = torch.full_like(cur, float("nan"))
+    ref = engine.encode(base, cur, E, bits, bb, recon=rec_general)
     ref_blocks, ref_exact = _host_blocks(ref), ref.exact.cpu().numpy().copy()
     ref_prefix = ref.prefix.cpu().numpy().copy()
     ref_out = engine.decode_encoding(ref, base).out.cpu().numpy()
+    # K4's fused reconstruction is the decoder's output, bit for bit
+    assert rec_general.cpu().numpy().tobytes() == ref_out.tobytes()
     pipe = engine.DevicePipeline(base.numel(), base.dtype, E, bits, bb)
     out = torch.empty_like(base)
     if graph:
@@ -88,6 +91,10 @@ def test_pipeline_matches_general_path(case, graph):
     # and against the oracle
     o = O.encode(b, c, E, bits, bb)
     assert enc.n_inc == o["n_inc"] and _host_blocks(enc) == o["blocks"]
+    # sync-free encode with the fused reconstruction
+    rec = torch.full_like(cur, float("nan"))
+    pipe.encode(base, cur, recon=rec)
+    assert rec.cpu().numpy().tobytes() == ref_out.tobytes()
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])

@@ -48,7 +48,7 @@ def test_workspace_queries_need_no_device():
 def test_argument_errors_are_reported_without_device():
     lib = N.load()
     rc = lib.nmk_encode(None, None, 10, 0, 10, N.NMK_F64, None, None, 1, 8, 1e-3, 1e-3, 16, None, 16,
-                        None, None, None, None, 0, None)
+                        None, None, None, None, None, 0, None)
     assert rc == N.NMK_ERR_ARG
     assert b"bad argument" in lib.nmk_last_error()
 
