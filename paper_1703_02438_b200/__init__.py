@@ -9,8 +9,9 @@ fallback: without the library or a CUDA device the entry points raise
 """
 
 from ._native import NativeError, NativeUnavailable
-from .codec import BlockLayout, CodecError, decode_all_indices, pack_block, partial_decode, unpack_block
-from .container import CompressedVariable, ContainerError, read_file, write_file
+from .codec import (BlockLayout, CodecError, decode_all_indices, pack_block, partial_decode, partial_decode_file,
+                    unpack_block)
+from .container import CompressedVariable, ContainerError, VariableHandle, read_file, scan_file, write_file
 from .core import (ChangeRatioField, TemporalPair, Tolerance, compute_change_ratios, ratio_arrays,
                    reconstruct)
 from .pipeline import (PhaseTimings, PipelineConfig, PipelineError, compress_pair, compress_series,
@@ -22,6 +23,6 @@ __all__ = [
     "BlockLayout", "ChangeRatioField", "CodecError", "CompressedVariable", "ContainerError",
     "NativeError", "NativeUnavailable", "PhaseTimings", "PipelineConfig", "PipelineError",
     "TemporalPair", "Tolerance", "compress_pair", "compress_series", "compute_change_ratios",
-    "decode_all_indices", "decompress", "pack_block", "partial_decode", "ratio_arrays",
-    "read_file", "reconstruct", "unpack_block", "write_file",
+    "decode_all_indices", "decompress", "pack_block", "partial_decode", "partial_decode_file", "ratio_arrays",
+    "read_file", "reconstruct", "scan_file", "unpack_block", "VariableHandle", "write_file",
 ]

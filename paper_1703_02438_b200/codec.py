@@ -165,12 +165,14 @@ def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_off
     pre = np.asarray(prefix, dtype=np.uint64)[first:first + nb].astype(np.int64)
     base_inc = int(pre[0])
     d_prefix_rel = torch.from_numpy(pre - base_inc).to(dev)
-    d_centers = torch.from_numpy(np.ascontiguousarray(centers64, dtype=np.float64)).to(dev)
-    ex = np.ascontiguousarray(exact[max(base_inc - exact_offset, 0):])
+    d_centers = torch.tensor(np.asarray(centers64, dtype=np.float64), device=dev)   # copies (read-only ok)
+    ex = np.array(exact[max(base_inc - exact_offset, 0):], copy=True)
     if base_inc < exact_offset:
         raise ValueError("exact values start after the covering block")
     d_exact = torch.from_numpy(ex).to(dev) if ex.size else torch.empty(0, dtype=_tdt(base.dtype), device=dev)
-    d_base = torch.from_numpy(np.ascontiguousarray(base)).to(dev)
+    base = np.asarray(base)
+    d_base = (torch.from_numpy(base) if base.flags.writeable and base.flags.c_contiguous
+              else torch.from_numpy(np.array(base, copy=True))).to(dev)
     res = engine.decode(d_packed, stride, first, bits, epb, n, d_prefix_rel, d_centers, d_exact, d_base,
                         [(start, count, 0)])
     need = int(res.n_sentinel[0])
@@ -224,6 +226,28 @@ def partial_decode(variable, start: int, count: int, base_reconstructed) -> np.n
     return _decode_range(variable, start, count, base_reconstructed,
                          lambda b: _block_bytes_of(variable, b),
                          lambda lo: (variable.incompressible_table[lo:], lo))
+
+
+def partial_decode_file(handle, start: int, count: int, base_reconstructed) -> np.ndarray:
+    """Like ``partial_decode`` straight from an on-disk variable
+    (codec.py:261-278): only the covering blocks' DEFLATE bytes and the exact
+    values those blocks reference are read from the file."""
+    variable = handle.variable
+    offsets = variable.index_offsets
+    epb = variable.elements_per_block
+
+    def block_bytes(b: int) -> bytes:
+        lo = int(offsets[b])
+        hi = int(offsets[b + 1]) if b + 1 < len(offsets) else handle.index_table_len
+        return handle.read_index_range(lo, hi)
+
+    def inc_slice(lo: int):
+        last = (start + count - 1) // epb if count else start // epb
+        hi = int(variable.incompressible_prefix[last + 1]) if last + 1 < variable.nblocks \
+            else variable.n_incompressible
+        return handle.read_incompressible_range(lo, max(hi - lo, 0)), lo
+
+    return _decode_range(variable, start, count, base_reconstructed, block_bytes, inc_slice)
 
 
 def decode_block_indices(variable, ordinal: int) -> np.ndarray:

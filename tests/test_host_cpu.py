@@ -88,6 +88,40 @@ def test_container_round_trip(tmp_path):
     assert container.to_bytes([w]) == container.to_bytes([v])
 
 
+def test_scan_file_reads_metadata_and_byte_ranges(tmp_path):
+    """container.scan_file / VariableHandle (container.py:273-347): bodies stay
+    on disk, byte ranges read back exactly, bounds and truncation raise."""
+    vs = []
+    for i, (nb, n_inc) in enumerate(((2, 1), (3, 4))):
+        vs.append(container.CompressedVariable(
+            name=f"v{i}", dtype_code=i % 2, n=8 * nb, bits=4, tolerance=1e-3, elements_per_block=8, nblocks=nb,
+            n_incompressible=n_inc, centers=np.array([0.0, 0.5]), index_offsets=np.arange(nb, dtype=np.uint64) * 3,
+            incompressible_prefix=np.array([0] + [1] * (nb - 1), dtype=np.uint64),
+            index_table=bytes(range(3 * nb + 2)), incompressible_table=np.arange(n_inc, dtype=np.float64) + 7))
+    p = tmp_path / "two.nmk"
+    size = container.write_file(p, vs)
+    hs = container.scan_file(p)
+    assert [h.variable.name for h in hs] == ["v0", "v1"]
+    assert sum(h.record_size() for h in hs) == size - 10
+    for h, v in zip(hs, vs):
+        assert len(h.variable.index_table) == 0 and h.index_table_len == len(v.index_table)
+        assert h.read_index_range(1, 4) == v.index_table[1:4]
+        got = h.read_incompressible_range(1, v.n_incompressible - 1)
+        assert got.tobytes() == v.incompressible_table.astype(v.numpy_dtype)[1:].tobytes()
+        assert container.to_bytes([h.load()]) == container.to_bytes([v])
+        with pytest.raises(container.InvariantError):
+            h.read_index_range(0, h.index_table_len + 1)
+        with pytest.raises(container.InvariantError):
+            h.read_incompressible_range(0, v.n_incompressible + 1)
+    data = p.read_bytes()
+    (tmp_path / "cut.nmk").write_bytes(data[:-3])
+    with pytest.raises(container.TruncatedFileError):
+        container.scan_file(tmp_path / "cut.nmk")
+    (tmp_path / "magic.nmk").write_bytes(b"XXXX" + data[4:])
+    with pytest.raises(container.BadMagicError):
+        container.scan_file(tmp_path / "magic.nmk")
+
+
 def test_workloads_are_seeded():
     a = workloads.cfg1_host(1000, seed=3)
     b = workloads.cfg1_host(1000, seed=3)
