@@ -169,6 +169,20 @@ int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_bloc
                nmk_segment_info* seg_info, nmk_decode_err* err,
                void* ws, size_t ws_bytes, void* stream);
 
+/* -- optional lossless stage on the GPU (codec.compress_block, codec.py:108-116)
+ * Raw RFC 1951 stream per index block: block b's packed bytes (block_len,
+ * last_len for the final block) at packed + b * block_stride.  Segments of
+ * seg_bytes (multiple of 16, 64..65535) are LZ77 + fixed-Huffman coded
+ * independently and joined by byte-aligning empty stored blocks, so any
+ * inflater reproduces the input.  out (capacity nmk_deflate_bound) receives
+ * the streams back to back; block_off[0..nblocks] (device) their offsets,
+ * block_off[nblocks] = total bytes.  Not byte-equal to zlib's output. */
+size_t nmk_deflate_ws_bytes(uint64_t nblocks, uint64_t block_len, uint32_t seg_bytes);
+uint64_t nmk_deflate_bound(uint64_t nblocks, uint64_t block_len, uint32_t seg_bytes);
+int nmk_deflate(const uint8_t* packed, uint64_t block_stride, uint64_t nblocks, uint64_t block_len,
+                uint64_t last_len, uint32_t seg_bytes, uint8_t* out, unsigned long long* block_off,
+                void* ws, size_t ws_bytes, void* stream);
+
 /* -- sync-free (graph-capturable) variants ---------------------------------
  * Every decision scalar stays on the device, so a whole compress + decompress
  * step can be enqueued (or captured in a CUDA graph) without a host round

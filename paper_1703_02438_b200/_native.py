@@ -27,6 +27,7 @@ NMK_F64 = 1
 
 u64 = ctypes.c_uint64
 i32 = ctypes.c_int
+u32 = ctypes.c_uint32
 dbl = ctypes.c_double
 vp = ctypes.c_void_p
 sz = ctypes.c_size_t
@@ -78,6 +79,9 @@ SIGNATURES = {
                              vp, vp, vp, vp, sz, vp]),
     "nmk_decode_dev": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, i32,
                              u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
+    "nmk_deflate_ws_bytes": (sz, [u64, u64, u32]),
+    "nmk_deflate_bound": (u64, [u64, u64, u32]),
+    "nmk_deflate": (i32, [vp, u64, u64, u64, u64, u32, vp, vp, vp, sz, vp]),
     "nmk_pack": (i32, [vp, u64, i32, vp, vp]),
     "nmk_unpack": (i32, [vp, u64, i32, vp, vp]),
 }

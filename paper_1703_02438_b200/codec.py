@@ -116,6 +116,35 @@ def compress_block(packed: bytes, level: int = DEFAULT_DEFLATE_LEVEL) -> bytes:
         raise CodecError(f"deflate failed: {exc}") from exc
 
 
+def gpu_deflate_blocks(packed_dev, stride: int, lengths, seg_bytes: int = 8192) -> list[bytes]:
+    """Raw DEFLATE of every packed block on the GPU (k_deflate.cu): block b
+    is ``packed_dev[b*stride : b*stride + lengths[b]]`` (all blocks but the
+    last have equal length).  Inflates (zlib or any inflater) to the packed
+    bytes; not byte-equal to zlib's stream (opt-in: PipelineConfig.deflate)."""
+    import torch
+    from . import engine
+    lengths = [int(x) for x in lengths]
+    nb = len(lengths)
+    if nb == 0:
+        return []
+    if any(x != lengths[0] for x in lengths[:-1]) or lengths[-1] > lengths[0] or lengths[-1] < 1:
+        raise CodecError("gpu deflate: blocks must share one length (the last may be shorter)")
+    lib = N.lib()
+    dev = packed_dev.device
+    ws_bytes = lib.nmk_deflate_ws_bytes(nb, lengths[0], seg_bytes)
+    bound = lib.nmk_deflate_bound(nb, lengths[0], seg_bytes)
+    if not ws_bytes or not bound:
+        raise CodecError(f"gpu deflate: unsupported segment size {seg_bytes}")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    out = torch.empty(bound, dtype=torch.uint8, device=dev)
+    off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
+    N.check(lib.nmk_deflate(packed_dev.data_ptr(), stride, nb, lengths[0], lengths[-1], seg_bytes, out.data_ptr(),
+                            off.data_ptr(), ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream))
+    o = off.cpu().numpy()
+    data = out[: int(o[-1])].cpu().numpy().tobytes()
+    return [data[int(o[b]): int(o[b + 1])] for b in range(nb)]
+
+
 def decompress_block(data: bytes) -> bytes:
     """Inflate one raw deflate stream produced by :func:`compress_block`."""
     try:

@@ -45,6 +45,10 @@ class PipelineConfig:
     bits: int | None = None
     block_bytes: int = codec.DEFAULT_BLOCK_BYTES
     deflate_level: int = codec.DEFAULT_DEFLATE_LEVEL
+    # lossless stage: "host" = stdlib zlib exactly as the reference (default,
+    # byte-identical .nmk files); "gpu" = k_deflate.cu (valid raw DEFLATE,
+    # different bytes; deflate_level is ignored)
+    deflate: str = "host"
 
     def __post_init__(self) -> None:
         if self.workers < 1:
@@ -57,6 +61,8 @@ class PipelineConfig:
             raise ValueError(f"bits must be in [{MIN_BITS}, {MAX_BITS}]")
         if not 0 <= self.deflate_level <= 9:
             raise ValueError("deflate level must be in 0..9")
+        if self.deflate not in ("host", "gpu"):
+            raise ValueError(f"deflate must be 'host' or 'gpu', got {self.deflate!r}")
         Tolerance(self.tolerance)
 
 
@@ -157,16 +163,29 @@ def assemble_variable(enc: engine.DeviceEncoding, config: PipelineConfig, name: 
                       timings: PhaseTimings | None = None) -> container.CompressedVariable:
     """Device encoding -> CompressedVariable (pipeline.py:290-324)."""
     t0 = time.perf_counter()
-    blocks, exact, prefix, centers = _encoding_to_host(enc)
-    t1 = time.perf_counter()
-    deflated = _deflate(blocks, config)
+    if config.deflate == "gpu":
+        # the packed stream never comes to the host: only the DEFLATE output
+        try:
+            deflated = codec.gpu_deflate_blocks(enc.packed, enc.stride, enc.block_lengths())
+        except N.NativeError as exc:
+            raise PipelineError("zlib", str(exc)) from exc
+        tz = time.perf_counter()
+        exact = _to_host(enc.exact, "d2h_exact").view(enc.dtype) if enc.n_inc else np.zeros(0, dtype=enc.dtype)
+        prefix = enc.prefix.cpu().numpy().view(np.uint64).copy()
+        centers = enc.centers_t.cpu().numpy().astype(enc.dtype, copy=False).copy()
+        t1 = time.perf_counter()
+        zlib_s, pack_s = tz - t0, t1 - tz
+    else:
+        blocks, exact, prefix, centers = _encoding_to_host(enc)
+        t1 = time.perf_counter()
+        deflated = _deflate(blocks, config)
+        pack_s, zlib_s = t1 - t0, time.perf_counter() - t1
     sizes = np.fromiter((len(b) for b in deflated), dtype=np.uint64, count=len(deflated))
     offsets = np.zeros(len(deflated), dtype=np.uint64)
     np.cumsum(sizes[:-1], out=offsets[1:])
-    t2 = time.perf_counter()
     if timings is not None:
-        timings.bits_packing += t1 - t0
-        timings.zlib += t2 - t1
+        timings.bits_packing += pack_s
+        timings.zlib += zlib_s
     variable = container.CompressedVariable(
         name=name, dtype_code=container.dtype_code_for(enc.dtype), n=enc.n, bits=enc.bits,
         tolerance=float(config.tolerance), elements_per_block=enc.epb, nblocks=enc.nblocks,

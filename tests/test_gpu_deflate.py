@@ -1,0 +1,100 @@
+"""The optional GPU lossless stage (k_deflate.cu): every stream
+it emits is a valid raw DEFLATE stream that zlib inflates back to the packed
+bytes exactly; .nmk files written with it decompress through the unchanged
+host inflate path to the same values as the default (zlib) stage."""
+
+import zlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1703_02438_b200 import codec, container, engine, pipeline, workloads  # noqa: E402
+from paper_1703_02438_b200.core import TemporalPair  # noqa: E402
+
+
+def _inflate(data: bytes) -> bytes:
+    d = zlib.decompressobj(-zlib.MAX_WBITS)
+    out = d.decompress(data) + d.flush()
+    assert d.eof and not d.unused_data
+    return out
+
+
+def _blocks_on_device(blocks, stride):
+    buf = np.zeros(len(blocks) * stride, dtype=np.uint8)
+    for i, b in enumerate(blocks):
+        buf[i * stride: i * stride + len(b)] = np.frombuffer(b, dtype=np.uint8)
+    return torch.from_numpy(buf).cuda()
+
+
+def _patterns(rng, n):
+    yield rng.integers(0, 256, n, dtype=np.uint8).tobytes()                      # incompressible
+    yield bytes(n)                                                                # one long run
+    yield (np.arange(n) % 7).astype(np.uint8).tobytes()                          # short period
+    x = np.full(n, 127, dtype=np.uint8)                                           # index-stream-like
+    pos = rng.choice(n, n // 50, replace=False)
+    x[pos] = rng.integers(0, 255, pos.size)
+    yield x.tobytes()
+    yield np.repeat(rng.integers(0, 256, n // 300 + 1, dtype=np.uint8), 300)[:n].tobytes()
+
+
+@pytest.mark.parametrize("seg", [64, 1024, 8192, 65520])
+@pytest.mark.parametrize("n,last", [(1, 1), (100_000, 100_000), (70_000, 12_345), (4096, 17)])
+def test_streams_inflate_exactly(seg, n, last):
+    rng = np.random.default_rng(seg + n)
+    for data in _patterns(rng, n):
+        nb = 3 if last != n else 1
+        blocks = [data] * (nb - 1) + [data[:last]]
+        stride = (n + 15) // 16 * 16
+        out = codec.gpu_deflate_blocks(_blocks_on_device(blocks, stride), stride, [len(b) for b in blocks], seg)
+        assert len(out) == nb
+        for o, b in zip(out, blocks):
+            assert _inflate(o) == b
+
+
+def test_compression_of_real_index_streams():
+    """cfg2 packed stream: inflates exactly and compresses within 2x of zlib."""
+    base, cur = workloads.cfg2_device(256, seed=0)
+    enc = engine.encode(base, cur, 1e-3, 8)
+    lens = enc.block_lengths()
+    gpu = codec.gpu_deflate_blocks(enc.packed, enc.stride, lens)
+    packed = enc.packed.cpu().numpy()
+    tot_gpu = tot_zlib = 0
+    for b, (g, ln) in enumerate(zip(gpu, lens)):
+        raw = packed[b * enc.stride: b * enc.stride + int(ln)].tobytes()
+        assert _inflate(g) == raw
+        tot_gpu += len(g)
+        tot_zlib += len(codec.compress_block(raw))
+    assert tot_gpu < 2.0 * tot_zlib, (tot_gpu, tot_zlib)
+    assert tot_gpu < 0.25 * int(sum(lens))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_pipeline_gpu_deflate_round_trip(tmp_path, dtype):
+    b, c = workloads.cfg5_host(200_003, seed=71)
+    b, c = b.astype(dtype), c.astype(dtype)
+    host_cfg = pipeline.PipelineConfig(tolerance=1e-3, bits=10, block_bytes=1 << 14)
+    gpu_cfg = pipeline.PipelineConfig(tolerance=1e-3, bits=10, block_bytes=1 << 14, deflate="gpu")
+    v_host, _ = pipeline.compress_pair(TemporalPair(b, c), host_cfg, name="h")
+    v_gpu, t = pipeline.compress_pair(TemporalPair(b, c), gpu_cfg, name="g")
+    assert t.zlib >= 0.0
+    # same model and exact values; same index stream after inflate
+    assert v_gpu.centers.tobytes() == v_host.centers.tobytes()
+    assert v_gpu.incompressible_table.tobytes() == v_host.incompressible_table.tobytes()
+    assert (codec.decode_all_indices(v_gpu) == codec.decode_all_indices(v_host)).all()
+    path = tmp_path / "g.nmk"
+    container.write_file(path, [v_gpu])
+    (w,) = container.read_file(path)
+    assert pipeline.decompress(w, b).tobytes() == pipeline.decompress(v_host, b).tobytes()
+    h = container.scan_file(path)[0]
+    s, n = 20_000, 50_000
+    assert codec.partial_decode_file(h, s, n, b[s:s + n]).tobytes() == pipeline.decompress(v_host, b)[s:s + n].tobytes()
+
+
+def test_config_rejects_unknown_engine():
+    with pytest.raises(ValueError):
+        pipeline.PipelineConfig(deflate="cpu")
