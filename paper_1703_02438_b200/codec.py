@@ -116,7 +116,7 @@ def compress_block(packed: bytes, level: int = DEFAULT_DEFLATE_LEVEL) -> bytes:
         raise CodecError(f"deflate failed: {exc}") from exc
 
 
-def gpu_deflate_blocks(packed_dev, stride: int, lengths, seg_bytes: int = 8192) -> list[bytes]:
+def gpu_deflate_blocks(packed_dev, stride: int, lengths, seg_bytes: int = 16384) -> list[bytes]:
     """Raw DEFLATE of every packed block on the GPU (k_deflate.cu): block b
     is ``packed_dev[b*stride : b*stride + lengths[b]]`` (all blocks but the
     last have equal length).  Inflates (zlib or any inflater) to the packed

@@ -3,8 +3,8 @@
 //
 // Each index block (pipeline.py:290-304: one raw RFC 1951 stream per block)
 // is cut into segments of seg_bytes.  One thread compresses one segment:
-// greedy LZ77 over the segment (3-byte hash, one candidate per bucket, 32-bit
-// compare-extend, window = the segment), a counting pass builds the
+// LZ77 over the segment (3-byte hash, 4-way buckets, run candidate, one-step
+// lazy evaluation, window = the segment), a counting pass builds the
 // segment's own length-limited Huffman codes, and the emitting pass writes a
 // dynamic-Huffman block (BTYPE = 10) -- or the fixed code (BTYPE = 01) when
 // that is not larger.  The segment's block is then closed with the end-of-block
@@ -23,9 +23,10 @@
 
 namespace nmk {
 
-constexpr int kDefThreads = 64;                  // 64 KB of hash tables per CTA
-constexpr int kDefHashBits = 9;                  // 512 buckets x u16 per thread
+constexpr int kDefThreads = 32;                  // 64 KB of hash tables per CTA (3 CTAs / SM)
+constexpr int kDefHashBits = 8;                  // 256 buckets x 4 ways (u16 positions in a u64) per thread
 constexpr int kDefHash = 1 << kDefHashBits;
+constexpr uint64_t kEmptyBucket = ~0ULL;         // four 0xffff slots
 constexpr int kMinMatch = 3, kMaxMatch = 258;
 
 // worst case of one segment: the fixed code (chosen whenever the dynamic one
@@ -101,10 +102,15 @@ __device__ __forceinline__ void dist_symbol(uint32_t dist, uint32_t& code, uint3
 // Greedy LZ77 over one segment: distance-1 candidate (runs) and one hash
 // candidate, 32-bit compare-extend; deterministic, so the counting pass and
 // the emitting pass make identical decisions.
+// LZ77 over one segment: candidates are the previous byte (runs) and the
+// four most recent positions of the 3-byte hash bucket (a u64 holding four
+// u16 positions, newest in the low bits); one-step lazy evaluation defers a
+// short match when the next position matches longer.  Deterministic, so the
+// counting pass and the emitting pass make identical decisions.
 template <typename Lit, typename Match>
-__device__ __forceinline__ void lz77(const uint8_t* __restrict__ src, uint32_t n, uint16_t* ht, Lit&& lit,
+__device__ __forceinline__ void lz77(const uint8_t* __restrict__ src, uint32_t n, uint64_t* ht, Lit&& lit,
                                      Match&& match) {
-  for (int i = 0; i < kDefHash; ++i) ht[i] = 0xffff;
+  for (int i = 0; i < kDefHash; ++i) ht[i] = kEmptyBucket;
   auto word_at = [&](uint32_t i) -> uint32_t {   // bytes past n read as 0
     uint32_t v = 0;
     if (i + 4 <= n) {
@@ -114,34 +120,70 @@ __device__ __forceinline__ void lz77(const uint8_t* __restrict__ src, uint32_t n
     }
     return v;
   };
-  uint32_t i = 0;
-  while (i < n) {
-    uint32_t best = 0, dist = 0;
-    if (i + kMinMatch <= n) {
-      const uint32_t h = hash3(word_at(i));
-      const uint32_t cand = ht[h];
-      ht[h] = (uint16_t)i;
-      const uint32_t cands[2] = {i >= 1 ? i - 1 : 0xffffffffu, cand != 0xffff ? cand : 0xffffffffu};
-#pragma unroll
-      for (int ci = 0; ci < 2; ++ci) {
-        const uint32_t j = cands[ci];
-        if (j == 0xffffffffu || j >= i || i - j > 32768u) continue;   // RFC 1951 window
-        const uint32_t maxl = min((uint32_t)kMaxMatch, n - i);
-        uint32_t l = 0;
-        while (l + 4 <= maxl && word_at(j + l) == word_at(i + l)) l += 4;
-        while (l < maxl && src[j + l] == src[i + l]) ++l;
-        if (l > best) { best = l; dist = i - j; }
-      }
+  auto extend = [&](uint32_t j, uint32_t i) -> uint32_t {
+    const uint32_t maxl = min((uint32_t)kMaxMatch, n - i);
+    uint32_t l = 0;
+    while (l + 4 <= maxl && word_at(j + l) == word_at(i + l)) l += 4;
+    while (l < maxl && src[j + l] == src[i + l]) ++l;
+    return l;
+  };
+  // longest match at i (0 if none); inserts i into its bucket
+  auto find = [&](uint32_t i, uint32_t& dist) -> uint32_t {
+    uint32_t best = 0;
+    if (i + kMinMatch > n) return 0;
+    const uint32_t h = hash3(word_at(i));
+    const uint64_t bucket = ht[h];
+    ht[h] = (bucket << 16) | i;
+    if (i >= 1) {
+      best = extend(i - 1, i);
+      dist = 1;
     }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t j = (uint32_t)(bucket >> (16 * w)) & 0xffffu;
+      if (j == 0xffffu || j + 1 >= i || i - j > 32768u) continue;   // j = i-1 already tried; RFC 1951 window
+      const uint32_t l = extend(j, i);
+      if (l > best) { best = l; dist = i - j; }
+    }
+    return best;
+  };
+  auto insert = [&](uint32_t p) {
+    if (p + kMinMatch <= n) {
+      const uint32_t h = hash3(word_at(p));
+      ht[h] = (ht[h] << 16) | p;
+    }
+  };
+  uint32_t i = 0;
+  uint32_t dist = 0;
+  uint32_t best = find(0, dist);
+  while (i < n) {
     if (best >= kMinMatch) {
-      match(best, dist);
-      const uint32_t end = i + best;
-      for (uint32_t p = i + 1; p < end && p + kMinMatch <= n && p < i + 8; ++p) ht[hash3(word_at(p))] = (uint16_t)p;
-      i = end;
+      if (best < 32 && i + 1 < n) {   // lazy: a longer match one byte later wins
+        uint32_t d2 = 0;
+        const uint32_t b2 = find(i + 1, d2);
+        if (b2 > best) {
+          lit(src[i]);
+          ++i;
+          best = b2;
+          dist = d2;
+          continue;
+        }
+        // i+1 is inserted already; emit the match at i
+        match(best, dist);
+        const uint32_t end = i + best;
+        for (uint32_t p = i + 2; p < end && p < i + 8; ++p) insert(p);
+        i = end;
+      } else {
+        match(best, dist);
+        const uint32_t end = i + best;
+        for (uint32_t p = i + 1; p < end && p < i + 8; ++p) insert(p);
+        i = end;
+      }
     } else {
       lit(src[i]);
       ++i;
     }
+    if (i < n) best = find(i, dist);
   }
 }
 
@@ -223,9 +265,9 @@ __global__ void __launch_bounds__(kDefThreads)
 k_deflate_segments(const uint8_t* __restrict__ packed, uint64_t stride, uint64_t nblocks, uint64_t block_len,
                    uint64_t last_len, uint32_t seg_bytes, uint32_t segs_per_block, uint8_t* __restrict__ scratch,
                    uint32_t* __restrict__ seg_len) {
-  extern __shared__ uint16_t s_hash[];   // kDefThreads x kDefHash
+  extern __shared__ uint64_t s_hash[];   // kDefThreads x kDefHash buckets
   const uint64_t nseg = nblocks * segs_per_block;
-  uint16_t* ht = s_hash + (size_t)threadIdx.x * kDefHash;
+  uint64_t* ht = s_hash + (size_t)threadIdx.x * kDefHash;
   for (uint64_t sg = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
        sg += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = sg / segs_per_block;
@@ -424,7 +466,7 @@ extern "C" int nmk_deflate(const uint8_t* packed, uint64_t block_stride, uint64_
   uint8_t* scratch = (uint8_t*)(wb + p.off_scratch);
   uint32_t* seg_len = (uint32_t*)(wb + p.off_len);
   unsigned long long* offsets = (unsigned long long*)(wb + p.off_offsets);
-  const size_t smem = (size_t)kDefThreads * kDefHash * sizeof(uint16_t);
+  const size_t smem = (size_t)kDefThreads * kDefHash * sizeof(uint64_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_deflate_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

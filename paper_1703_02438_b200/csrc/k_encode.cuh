@@ -31,6 +31,9 @@ namespace nmk {
 
 constexpr int kChunk = 32 * kGroup;   // 256 elements per warp chunk
 constexpr int kEncThreads = 256;      // 8 warps per CTA
+#ifndef NMK_ENC_MINB
+#define NMK_ENC_MINB 4   // 64 registers: measured best (3 -> 85 regs is slower)
+#endif
 constexpr int kSmemCuts = 4096;       // cuts in shared memory up to this many
 
 template <int B>
@@ -411,7 +414,7 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
 }
 
 template <typename T, int B, bool kRecon>
-__global__ void __launch_bounds__(kEncThreads, 4)
+__global__ void __launch_bounds__(kEncThreads, NMK_ENC_MINB)
 k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
          double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
