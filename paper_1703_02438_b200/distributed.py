@@ -62,19 +62,33 @@ class ProcessGroupComm:
         stats[:4].copy_(torch.from_numpy(out).to(stats.device))
 
     def allreduce_stats_device(self, stats) -> None:
-        """Same reduction with three device-side all-reduces (no host copy):
-        MIN over gmin, MAX over gmax, SUM over the valid counts."""
+        """Same reduction without a host copy: one all-gather of the 32-byte
+        records, then MIN over gmin, MAX over gmax and SUM over the valid
+        counts on the device (one collective instead of three)."""
         import torch
-        f = stats[:2].view(torch.float64)
-        self.dist.all_reduce(f[0:1], op=self.dist.ReduceOp.MIN, group=self.group)
-        self.dist.all_reduce(f[1:2], op=self.dist.ReduceOp.MAX, group=self.group)
-        self.dist.all_reduce(stats[2:3], op=self.dist.ReduceOp.SUM, group=self.group)
+        g = self._stats_buf(stats)
+        self.dist.all_gather_into_tensor(g, stats[:4].contiguous(), group=self.group)
+        g2 = g.view(self.world, 4)
+        f = g2[:, :2].contiguous().view(torch.float64)
+        torch.amin(f[:, 0], dim=0, keepdim=True, out=stats[0:1].view(torch.float64))
+        torch.amax(f[:, 1], dim=0, keepdim=True, out=stats[1:2].view(torch.float64))
+        torch.sum(g2[:, 2], dim=0, keepdim=True, out=stats[2:3])
+
+    def _stats_buf(self, stats):
+        import torch
+        buf = getattr(self, "_sbuf", None)
+        if buf is None or buf.device != stats.device:
+            buf = torch.empty(self.world * 4, dtype=torch.int64, device=stats.device)
+            self._sbuf = buf
+        return buf
 
     def exscan_device(self, n_inc, offset_out, prefix=None, prefix_global=None) -> None:
         """Exclusive scan of the per-rank incompressible counts on the device:
         offset_out[0] = sum over lower ranks; prefix_global = prefix + offset."""
         import torch
-        allv = torch.empty(self.world, dtype=torch.int64, device=n_inc.device)
+        allv = getattr(self, "_nbuf", None)
+        if allv is None or allv.device != n_inc.device:
+            allv = self._nbuf = torch.empty(self.world, dtype=torch.int64, device=n_inc.device)
         self.dist.all_gather_into_tensor(allv, n_inc.reshape(1), group=self.group)
         torch.sum(allv[: self.rank], dim=0, keepdim=True, out=offset_out) if self.rank else offset_out.zero_()
         if prefix is not None and prefix_global is not None:

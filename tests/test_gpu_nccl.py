@@ -79,3 +79,24 @@ def test_general_encode_over_nccl(nccl_world1):
     assert n_inc == o["n_inc"] and blocks == o["blocks"]
     assert exact.tobytes() == o["exact"].tobytes()
     assert prefix.tobytes() == np.asarray(o["prefix"], dtype=np.uint64).tobytes()
+
+
+def test_device_pipeline_graph_with_nccl_exchanges(nccl_world1):
+    """The bench captures the multi-GPU step (kernels + NCCL exchanges) as one
+    CUDA graph: replays must equal the eager step."""
+    b, c = workloads.cfg1_host(1 << 18, seed=44)
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(base.numel(), base.dtype, 1e-3, 8, 1 << 15, elem0=0, n_total=base.numel(),
+                                 comm=nccl_world1)
+    out_e = torch.empty_like(base)
+    pipe.step(base, cur, out_e)
+    ref_blocks = _blocks(pipe.encoding())
+    out_g = torch.empty_like(base)
+    g = pipe.capture(base, cur, out_g)
+    out_g.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert pipe.check()["status"] == 0
+    assert _blocks(pipe.encoding()) == ref_blocks
+    assert out_g.cpu().numpy().tobytes() == out_e.cpu().numpy().tobytes()
