@@ -13,7 +13,16 @@
 namespace nmk {
 
 constexpr int kMinmaxThreads = 256;
-constexpr int kMinmaxUnroll = 4;
+#ifndef NMK_MM_UNROLL
+#define NMK_MM_UNROLL 4
+#endif
+#ifndef NMK_MM_MINB
+#define NMK_MM_MINB 4
+#endif
+#ifndef NMK_MM_CTAS
+#define NMK_MM_CTAS 8
+#endif
+constexpr int kMinmaxUnroll = NMK_MM_UNROLL;
 
 struct MinMax {
   double lo, hi;
@@ -69,7 +78,7 @@ __device__ __forceinline__ void vec_get(const float4& v, double* o) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kMinmaxThreads, 4)
+__global__ void __launch_bounds__(kMinmaxThreads, NMK_MM_MINB)
 k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
          MinMax* __restrict__ partials, unsigned int* __restrict__ ticket,
          nmk_stats* __restrict__ out, bool vec_ok, float* __restrict__ keys) {
@@ -204,7 +213,7 @@ static int sm_count() {
 
 static unsigned minmax_grid(uint64_t n) {
   uint64_t want = (n + 4095) / 4096;  // >= 4096 elements per CTA
-  uint64_t cap = (uint64_t)sm_count() * 8;
+  uint64_t cap = (uint64_t)sm_count() * NMK_MM_CTAS;
   if (want < 1) want = 1;
   return (unsigned)(want < cap ? want : cap);
 }

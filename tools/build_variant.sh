@@ -3,7 +3,7 @@
 #   tools/build_variant.sh NAME -DNMK_KEY_TILE=512 ...   -> variants/NAME.so
 set -e
 name=$1; shift
-dir=build_variants/$name
+dir=/tmp/nmk_build_variants/$name
 mkdir -p "$dir" variants
 objs=()
 for f in paper_1703_02438_b200/csrc/*.cu; do
