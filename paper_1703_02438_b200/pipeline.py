@@ -374,6 +374,7 @@ class StreamCompressor:
             raise ValueError("StreamCompressor needs an explicit B (PipelineConfig.bits)")
         N.require_cuda()
         self.n, self.config, self.depth = int(n), config, int(depth)
+        self.elem0, self.n_total, self.comm = int(elem0), (int(n_total) if n_total is not None else int(n)), comm
         self.torch_dtype = torch.float64 if np.dtype(dtype).itemsize == 8 else torch.float32
         self.np_dtype = np.dtype("<f8") if self.torch_dtype == torch.float64 else np.dtype("<f4")
         self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
@@ -448,13 +449,47 @@ class StreamCompressor:
                                + (4 + p.model.numel() + 1) * 8 + p.k_cap * self.np_dtype.itemsize
                                + self.n * self.np_dtype.itemsize)
         model = N.NmkModel.from_buffer_copy(scal[4:4 + p.model.numel()].tobytes()[: ctypes.sizeof(N.NmkModel)])
+        if model.status == N.NMK_ERR_NEEDS_SPARSE:
+            return self._general_path(sl)
         if model.status != 0:
-            raise PipelineError("binning", f"sync-free pipeline status {model.status}: use compress_pair")
+            raise PipelineError("binning", f"sync-free pipeline status {model.status}")
         k = int(model.k)
         enc = HostEncoding(self.n, self.np_dtype, p.bits, k, p.epb, p.nblocks, p.stride, p.b0,
                            sl["h_packed"].numpy(), sl["h_exact"].numpy()[:n_inc],
                            sl["h_prefix"].numpy().view(np.uint64), sl["h_centers"].numpy()[:k], n_inc)
         return enc, sl["h_out"].numpy()
+
+    def _general_path(self, sl):
+        """A span too wide for the dense device histogram: rerun this slot's
+        step (its device inputs are intact until the slot is resubmitted)
+        through engine.encode's sort-based path, with K4's fused
+        reconstruction standing in for the decode."""
+        import torch
+        p = sl["pipe"]
+        with torch.cuda.stream(self.s_x):
+            try:
+                enc = engine.encode(sl["base"], sl["cur"], self.config.tolerance, self.config.bits,
+                                    self.config.block_bytes, elem0=self.elem0, n_total=self.n_total, comm=self.comm,
+                                    recon=sl["out"])
+            except N.NativeError as exc:
+                raise PipelineError("binning", str(exc)) from exc
+            nb = enc.prefix.numel() * enc.stride
+            sl["h_packed"][:nb].copy_(enc.packed[:nb], non_blocking=True)
+            if enc.n_inc > sl["h_exact"].numel():
+                sl["h_exact"] = torch.empty(enc.n_inc, dtype=self.torch_dtype, pin_memory=True)
+            if enc.n_inc:
+                sl["h_exact"][: enc.n_inc].copy_(enc.exact, non_blocking=True)
+            sl["h_prefix"][: enc.prefix.numel()].copy_(enc.prefix, non_blocking=True)
+            sl["h_centers"][: enc.k].copy_(enc.centers_t, non_blocking=True)
+            sl["h_out"].copy_(sl["out"], non_blocking=True)
+        self.s_x.synchronize()
+        self.last_d2h_bytes = nb + enc.n_inc * self.np_dtype.itemsize + enc.prefix.numel() * 8 + \
+            enc.k * self.np_dtype.itemsize + self.n * self.np_dtype.itemsize
+        h = HostEncoding(self.n, self.np_dtype, enc.bits, enc.k, enc.epb, enc.nblocks, enc.stride, enc.b0,
+                         sl["h_packed"].numpy(), sl["h_exact"].numpy()[: enc.n_inc],
+                         sl["h_prefix"].numpy().view(np.uint64), sl["h_centers"].numpy()[: enc.k], enc.n_inc)
+        assert p.stride == enc.stride and p.epb == enc.epb
+        return h, sl["h_out"].numpy()
 
     def h2d_bytes(self) -> int:
         """Host->device bytes per step (both snapshots)."""

@@ -68,3 +68,16 @@ def test_stream_compressor_matches_oracle(dtype, depth):
 def test_stream_compressor_requires_bits():
     with pytest.raises(ValueError):
         pipeline.StreamCompressor(1000, np.float64, pipeline.PipelineConfig())
+
+
+def test_stream_compressor_falls_back_for_wide_spans():
+    """A 5e8-bin span cannot use the dense device histogram: the step reruns
+    through the sort-based general path and still equals the oracle."""
+    b, c = workloads.outlier_pair(60_000, seed=81)
+    cfg = pipeline.PipelineConfig(tolerance=1e-3, bits=4, block_bytes=1 << 12)
+    sc = pipeline.StreamCompressor(b.size, np.float64, cfg, depth=2)
+    hb, hc = torch.from_numpy(b).pin_memory(), torch.from_numpy(c).pin_memory()
+    h, rec = sc.result(sc.submit(hb, hc))
+    o = O.encode(b, c, 1e-3, 4, 1 << 12)
+    assert _blocks(h) == o["blocks"] and h.exact.tobytes() == o["exact"].tobytes()
+    assert rec.tobytes() == O.decode(o, b).tobytes()
