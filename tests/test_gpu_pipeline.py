@@ -146,3 +146,22 @@ def test_pipeline_degenerate():
     chk = pipe.check()
     assert chk["status"] == 0 and chk["k"] == 1 and chk["n_inc"] == 10_000
     assert torch.equal(out, cur)
+
+
+@pytest.mark.parametrize("n", [1, 3, 8, 255, 256, 257, 511, 4097, 70_001])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_pipeline_small_and_ragged(n, dtype):
+    """Sizes below / around the chunk (256), key tile (512) and vector widths."""
+    b, c = workloads.cfg5_host(n, seed=n)
+    b, c = b.astype(dtype), c.astype(dtype)
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(n, base.dtype, 1e-3, 8, 4096)
+    out = torch.empty_like(base)
+    pipe.step(base, cur, out)
+    chk = pipe.check()
+    assert chk["status"] == 0 and not chk["bad_index"] and not chk["exhausted"]
+    o = O.encode(b, c, 1e-3, 8, 4096)
+    enc = pipe.encoding()
+    assert _host_blocks(enc) == o["blocks"]
+    assert enc.exact.cpu().numpy().tobytes() == o["exact"].tobytes()
+    assert out.cpu().numpy().tobytes() == O.decode(o, b).tobytes()
