@@ -211,6 +211,20 @@ int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t
                    uint8_t* packed, uint64_t block_stride, void* exact,
                    unsigned long long* prefix, unsigned long long* n_inc, void* recon,
                    void* ws, size_t ws_bytes, void* stream);
+/* K4 keyed mode: as nmk_encode_dev, classifying from nmk_minmax's f32 ratio
+ * keys (16-byte aligned float[n_local]) against the histogram bins of
+ * `stats` (gmin, gmax, dense span from nmk_hist_prep) and `width` (= 2E), so
+ * it reads 4 bytes per element; (base, cur) are re-read only where a key
+ * cannot decide, for the incompressible values and for `recon`.  Falls back
+ * to reading both snapshots when the centers are not on the bin grid.
+ * Replaces the same reference phases as nmk_encode (pipeline.py:232-288). */
+int nmk_encode_keyed_dev(const float* keys, const nmk_stats* stats, double width,
+                         const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
+                         uint64_t n_total, int dtype, const double* centers, const double* cuts,
+                         const nmk_model* model, int k_cap, int bits, double tolerance, uint64_t epb,
+                         uint8_t* packed, uint64_t block_stride, void* exact,
+                         unsigned long long* prefix, unsigned long long* n_inc, void* recon,
+                         void* ws, size_t ws_bytes, void* stream);
 int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint64_t first_block,
                    int bits, uint64_t epb, uint64_t n_total,
                    const unsigned long long* prefix_rel, const double* centers,

@@ -27,10 +27,10 @@ namespace nmk {
 #define NMK_ENC_EXTERN(BB)                                                                                      \
   extern template void launch_encode<double, BB>(const void*, const void*, const EncodeGeom&, const double*,      \
                                                  const double*, int, double, double, uint8_t*, void*, uint32_t*, \
-                                                 const nmk_model*, int, void*, cudaStream_t);                     \
+                                                 const nmk_model*, int, void*, const EncodeKeys&, cudaStream_t);                     \
   extern template void launch_encode<float, BB>(const void*, const void*, const EncodeGeom&, const double*,       \
                                                 const double*, int, double, double, uint8_t*, void*, uint32_t*,  \
-                                                const nmk_model*, int, void*, cudaStream_t);
+                                                const nmk_model*, int, void*, const EncodeKeys&, cudaStream_t);
 NMK_ENC_EXTERN(2) NMK_ENC_EXTERN(3) NMK_ENC_EXTERN(4) NMK_ENC_EXTERN(5) NMK_ENC_EXTERN(6) NMK_ENC_EXTERN(7)
 NMK_ENC_EXTERN(8) NMK_ENC_EXTERN(9) NMK_ENC_EXTERN(10) NMK_ENC_EXTERN(11) NMK_ENC_EXTERN(12) NMK_ENC_EXTERN(13)
 NMK_ENC_EXTERN(14) NMK_ENC_EXTERN(15) NMK_ENC_EXTERN(16) NMK_ENC_EXTERN(17) NMK_ENC_EXTERN(18) NMK_ENC_EXTERN(19)
@@ -39,17 +39,30 @@ NMK_ENC_EXTERN(26) NMK_ENC_EXTERN(27) NMK_ENC_EXTERN(28) NMK_ENC_EXTERN(29) NMK_
 #undef NMK_ENC_EXTERN
 
 // Finalize: chunk offsets -> compacted exact list + per-block prefix.
-// One thread per chunk for the bookkeeping; chunks with more than a few
-// incompressible values are copied by the whole warp, one chunk at a time.
+// One thread per chunk for the bookkeeping.  The values come either from
+// the chunk's scratch window (k_encode: chunks with more than a few values
+// are copied by the whole warp, one chunk at a time) or, after
+// k_encode_keyed (*keyed_done), straight from `cur` at the positions of the
+// chunk's 256-bit mask (one byte per lane of the encoding warp).
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsigned long long* __restrict__ offsets,
                const T* __restrict__ scratch, T* __restrict__ exact, unsigned long long* __restrict__ prefix,
-               unsigned long long* __restrict__ n_inc) {
+               unsigned long long* __restrict__ n_inc, const T* __restrict__ cur,
+               const uint32_t* __restrict__ keyed_done) {
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_inc = offsets[geo.nchunks];
+  const bool gather = keyed_done && *keyed_done;
+  const uint8_t* masks = reinterpret_cast<const uint8_t*>(scratch);
   const uint32_t cpb = (uint32_t)geo.cpb;
   const uint32_t nthr = gridDim.x * blockDim.x;
+  // local index of element 0 of lane l's group in chunk c: chunk_lo - elem0 + 8 l
+  auto chunk_li = [&](uint32_t c) -> int64_t {
+    const uint32_t g = (uint32_t)geo.g0 + c;
+    const uint32_t b = geo.fd_cpb.div(g);
+    return (int64_t)((uint64_t)b * geo.epb + (uint64_t)(g - b * cpb) * kChunk) - (int64_t)geo.elem0;
+  };
+  const unsigned big_at = gather ? 32u : 4u;
   for (uint32_t c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); c0 < (uint32_t)geo.nchunks; c0 += nthr) {
     const uint32_t c = c0 + lane;
     const bool in = c < (uint32_t)geo.nchunks;
@@ -59,17 +72,47 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
       const uint32_t g = (uint32_t)geo.g0 + c;
       const uint32_t b = geo.fd_cpb.div(g);
       if (g == b * cpb && (uint64_t)b * geo.epb >= geo.elem0) prefix[b - geo.b0] = off;
-      if (n <= 4)
-        for (unsigned i = 0; i < n; ++i) exact[off + i] = scratch[(uint64_t)c * kChunk + i];
+      if (n && n <= big_at) {
+        if (gather) {
+          const uint4* mp = reinterpret_cast<const uint4*>(masks + (uint64_t)c * 32);
+          const uint4 m0 = mp[0], m1 = mp[1];
+          const uint32_t mw[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+          const int64_t li = chunk_li(c);
+          unsigned long long o = off;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            for (uint32_t m = mw[q]; m; m &= m - 1u) {   // bit 8 l + e of the mask = element 8 l + e
+              const int bit = __ffs(m) - 1;
+              exact[o++] = cur[li + q * 32 + bit];
+            }
+        } else {
+          for (unsigned i = 0; i < n; ++i) exact[off + i] = scratch[(uint64_t)c * kChunk + i];
+        }
+      }
     }
-    unsigned big = __ballot_sync(0xffffffffu, n > 4);
+    unsigned big = __ballot_sync(0xffffffffu, n > big_at);
     while (big) {
       const int src = __ffs(big) - 1;
       big &= big - 1;
       const unsigned nn = __shfl_sync(0xffffffffu, n, src);
       const unsigned long long oo = __shfl_sync(0xffffffffu, off, src);
-      const uint64_t cs = (uint64_t)(c0 + src) * kChunk;
-      for (unsigned i = lane; i < nn; i += 32) exact[oo + i] = scratch[cs + i];
+      const uint32_t cb = c0 + src;
+      if (gather) {   // lane l handles its byte of the mask: warp scan for the output slot
+        const unsigned m = masks[(uint64_t)cb * 32 + lane];
+        const unsigned cnt = __popc(m);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int64_t li = chunk_li(cb) + lane * kGroup;
+        unsigned long long o = oo + (incl - cnt);
+        for (unsigned mm = m; mm; mm &= mm - 1u) exact[o++] = cur[li + __ffs(mm) - 1];
+      } else {
+        const uint64_t cs = (uint64_t)cb * kChunk;
+        for (unsigned i = lane; i < nn; i += 32) exact[oo + i] = scratch[cs + i];
+      }
     }
   }
 }
@@ -176,11 +219,12 @@ static EncodeWs encode_ws_layout(uint64_t nchunks, int elem_bytes) {
 template <typename T>
 static int dispatch_encode(int bits, const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
                            const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
-                           uint32_t* counts, const nmk_model* model, int k_cap, void* recon, cudaStream_t s) {
+                           uint32_t* counts, const nmk_model* model, int k_cap, void* recon, const EncodeKeys& kx,
+                           cudaStream_t s) {
   switch (bits) {
 #define NMK_ENC_CASE(BB)                                                                                           \
   case BB: launch_encode<T, BB>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, model, \
-                                k_cap, recon, s); break;
+                                k_cap, recon, kx, s); break;
     NMK_ENC_CASE(2) NMK_ENC_CASE(3) NMK_ENC_CASE(4) NMK_ENC_CASE(5) NMK_ENC_CASE(6) NMK_ENC_CASE(7)
     NMK_ENC_CASE(8) NMK_ENC_CASE(9) NMK_ENC_CASE(10) NMK_ENC_CASE(11) NMK_ENC_CASE(12) NMK_ENC_CASE(13)
     NMK_ENC_CASE(14) NMK_ENC_CASE(15) NMK_ENC_CASE(16) NMK_ENC_CASE(17) NMK_ENC_CASE(18) NMK_ENC_CASE(19)
@@ -197,7 +241,7 @@ static int encode_impl(const void* base, const void* cur, uint64_t n_local, uint
                        int dtype, const double* centers, const double* cuts, int k, const nmk_model* model,
                        int k_cap, int bits, double tol_bin, double tolerance, uint64_t epb, uint8_t* packed,
                        uint64_t block_stride, void* exact, unsigned long long* prefix, unsigned long long* n_inc,
-                       void* recon, void* ws, size_t ws_bytes, cudaStream_t s);
+                       void* recon, const EncodeKeys& kx, void* ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace nmk
 
@@ -212,7 +256,8 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
                             int dtype, const double* centers, const double* cuts, int k, const nmk_model* model,
                             int k_cap, int bits, double tol_bin, double tolerance, uint64_t epb, uint8_t* packed,
                             uint64_t block_stride, void* exact, unsigned long long* prefix,
-                            unsigned long long* n_inc, void* recon, void* ws, size_t ws_bytes, cudaStream_t s) {
+                            unsigned long long* n_inc, void* recon, const EncodeKeys& kx, void* ws, size_t ws_bytes,
+                            cudaStream_t s) {
   if (n_local == 0) {
     cudaMemsetAsync(n_inc, 0, sizeof(unsigned long long), s);
     return check_launch("nmk_encode(empty)");
@@ -232,10 +277,25 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
   EncodeChunks et = encode_chunks(n_local, elem0, epb);
   if (epb >= (1ULL << 31) || (n_total + kChunk - 1) / kChunk >= (1ULL << 32))
     return set_error(NMK_ERR_ARG, "nmk_encode: block or stream too large for 32-bit chunk indexing");
-  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride, FastDiv{}};
+  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride, FastDiv{}, 0, 0, false};
   geo.fd_cpb.init((uint32_t)et.cpb);
+  {
+    auto chunk_lo = [&](uint64_t c) {   // first element of local chunk c
+      const uint64_t g = et.g0 + c, b = g / et.cpb;
+      return b * epb + (g - b * et.cpb) * kChunk;
+    };
+    const uint64_t local_end = elem0 + n_local;
+    geo.c_first = chunk_lo(0) == elem0 ? 0u : 1u;
+    const uint64_t last = et.nchunks - 1;
+    geo.c_last = (uint32_t)(chunk_lo(last) + kChunk <= local_end ? last : (last ? last - 1 : 0));
+    if (et.nchunks == 1 && chunk_lo(0) + kChunk > local_end) geo.c_first = 1;   // no whole chunk
+    geo.key_al = elem0 % 4 == 0 && epb % 4 == 0;
+  }
   EncodeWs w = encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8);
   char* wb = (char*)ws;
+  EncodeKeys kxw = kx;
+  kxw.done = (uint32_t*)(wb + w.off_total + 128);   // keyed-mode flag (k_encode_keyed -> k_encode, finalize)
+  const bool keyed = kx.keys && model && k_cap <= kSmemCuts + 1;   // launch_encode_k's condition
   uint32_t* counts = (uint32_t*)(wb + w.off_counts);
   unsigned long long* offsets = (unsigned long long*)(wb + w.off_offsets);
   void* scratch = wb + w.off_scratch;
@@ -245,19 +305,19 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
   if (c0_in_blk) cudaMemsetAsync(packed, 0, c0_in_blk * (uint64_t)(32 * bits), s);
   int rc = (dtype == NMK_F64)
                ? dispatch_encode<double>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
-                                         scratch, counts, model, k_cap, recon, s)
+                                         scratch, counts, model, k_cap, recon, kxw, s)
                : dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
-                                        scratch, counts, model, k_cap, recon, s);
+                                        scratch, counts, model, k_cap, recon, kxw, s);
   if (rc) return rc;
   chunk_scan(counts, et.nchunks, offsets, wb + w.off_scan, s);
   unsigned grid = (unsigned)((et.nchunks + 255) / 256);
   if (grid > (unsigned)sm_count_e() * 8) grid = sm_count_e() * 8;
   if (dtype == NMK_F64)
     k_enc_finalize<double><<<grid, 256, 0, s>>>(geo, counts, offsets, (const double*)scratch, (double*)exact, prefix,
-                                                n_inc);
+                                                n_inc, (const double*)cur, keyed ? kxw.done : nullptr);
   else
     k_enc_finalize<float><<<grid, 256, 0, s>>>(geo, counts, offsets, (const float*)scratch, (float*)exact, prefix,
-                                               n_inc);
+                                               n_inc, (const float*)cur, keyed ? kxw.done : nullptr);
   return check_launch("k_enc_finalize");
 }
 
@@ -267,7 +327,8 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
                           unsigned long long* prefix, unsigned long long* n_inc, void* recon, void* ws,
                           size_t ws_bytes, void* stream) {
   return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, k, nullptr, k, bits, tol_bin, tolerance,
-                     epb, packed, block_stride, exact, prefix, n_inc, recon, ws, ws_bytes, (cudaStream_t)stream);
+                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{nullptr, nullptr, 0.0, nullptr}, ws,
+                     ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total,
@@ -277,7 +338,21 @@ extern "C" int nmk_encode_dev(const void* base, const void* cur, uint64_t n_loca
                               unsigned long long* n_inc, void* recon, void* ws, size_t ws_bytes, void* stream) {
   if (!model) return set_error(NMK_ERR_ARG, "nmk_encode_dev: model required");
   return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, 1, model, k_cap, bits, 0.0, tolerance,
-                     epb, packed, block_stride, exact, prefix, n_inc, recon, ws, ws_bytes, (cudaStream_t)stream);
+                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{nullptr, nullptr, 0.0, nullptr}, ws,
+                     ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int nmk_encode_keyed_dev(const float* keys, const nmk_stats* stats, double width, const void* base,
+                                    const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total, int dtype,
+                                    const double* centers, const double* cuts, const nmk_model* model, int k_cap,
+                                    int bits, double tolerance, uint64_t epb, uint8_t* packed, uint64_t block_stride,
+                                    void* exact, unsigned long long* prefix, unsigned long long* n_inc, void* recon,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  if (!model || !keys || !stats) return set_error(NMK_ERR_ARG, "nmk_encode_keyed_dev: model, keys and stats required");
+  if ((uintptr_t)keys & 15) return set_error(NMK_ERR_ARG, "nmk_encode_keyed_dev: keys must be 16-byte aligned");
+  return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, 1, model, k_cap, bits, 0.0, tolerance,
+                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{keys, stats, width, nullptr}, ws,
+                     ws_bytes, (cudaStream_t)stream);
 }
 
 template <int B>

@@ -90,9 +90,21 @@ __device__ __forceinline__ void pack8(const uint32_t (&code)[kGroup], uint8_t* d
   }
 }
 
+// K1's f32 ratio keys for the keyed mode (keys == nullptr: read the snapshots)
+struct EncodeKeys {
+  const float* keys;
+  const nmk_stats* st;   // gmin, gmax, dense span (stats->reserved)
+  double width;          // histogram width 2E
+  uint32_t* done;        // device flag: 1 when the keyed kernel did the work
+};
+
 struct EncodeGeom {
   uint64_t n_local, elem0, n_total, epb, cpb, g0, nchunks, b0, stride;
   FastDiv fd_cpb;   // chunk id -> block
+  // keyed K4: chunks c_first..c_last are wholly inside [elem0, elem0 + n_local);
+  // key_al: every chunk start is a multiple of 4 elements from elem0
+  uint32_t c_first, c_last;
+  bool key_al;
 };
 
 // Chunk c of this range: block, in-block chunk index and element spans.
@@ -316,6 +328,236 @@ __device__ __forceinline__ uint32_t classify_direct(T bt, T xt, const DirectGrid
   return classify_exact<T>(bt, xt, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel);
 }
 
+// ---- keyed mode: classification from K1's f32 ratio keys ---------------------
+// When K1 stored the keys (DevicePipeline, engine.encode), K4 reads 4 bytes
+// per element instead of both snapshots (k_encode_keyed).  The cells are the
+// histogram bins (origin gmin, width w = 2E); u = (r - gmin)/w.
+//  * f32 test (classify_key / classify_key2, FFMA2/FADD2): th = RN32(key*iw32
+//    + c32) estimates u - 1/2 - q_ref, q_ref the bin of r = 0, and
+//      |th - (u - 1/2 - q_ref)| <= |th| 2^-23 + |key| iw 2^-22 + C0
+//    per element (setup_keyed), so |d| + that bound < 1/2 - margin, with
+//    d = th - RN_int(th), places u inside bin floor(u) farther than the
+//    margin from its edges.  Small ratios (the bulk) get a tiny bound.
+//  * f64 test (classify_key64) for the few keys the f32 test leaves open;
+//    then the exact path from (b, x) for +inf keys and the rest.
+// Each selected center lies within D of its bin's middle (measured at
+// set-up); the margin adds D, the cut rounding and the round-trip term, so:
+//   * bin selected (center j):  |r - c_j| < E - delta, both cuts around c_j
+//     lie farther than that, so searchsorted gives j, the near test passes,
+//     and the round-trip filter passes: with b in the safe range (K1 stores a
+//     finite key only then, or for b = x = 0) the decoder's value satisfies
+//     |T((1+c)b) - x| <= |b| (|c - r| + delta) with
+//       delta = 4(1 + A) 2^-52 + 2E 2^-52 [+ (1 + A + E) 2^-23 + 2^-48 for f32],
+//     A >= |c|, |r| (IEEE error of the sub, div, add, mul, narrowing and of
+//     RN(E|b|); subnormal results absorbed by |b| >= 2^-900 / 2^-100);
+//   * bin not selected: every center is more than w/2 away -> sentinel.
+// NaN keys are invalid elements (sentinel).  So the codes are the exact
+// path's codes bit for bit.  Incompressible positions go out as a 256-bit
+// mask per chunk; k_enc_finalize gathers their values from `cur`.
+constexpr uint32_t kKeySlow = 0x80000000u;   // not a code: decide again (f64 key test, exact path)
+constexpr uint32_t kIncFlag = 0x40000000u;   // tags the sentinel in the keyed table (codes < 2^30)
+
+struct KeyedGrid {
+  unsigned long long iw2, c2;   // (iw32, iw32) and (c32, c32) as f32x2
+  float iw32, c32, hi4;
+  float ka;         // RU32(iw 2^-22): the key-error term of the per-element bound
+  uint32_t q0m1;    // ordinal of the first center - 1 (table row 0)
+  uint32_t rowbase; // magic-sum bits -> table row
+  uint32_t span2;   // table rows: ordinals q0-1 .. q_last+1
+  uint32_t tab_s, opc_s;
+  uint32_t kd_s;    // shared double[3]: gmin, 1/w, 1/2 - margin (f64 key test)
+};
+
+// All threads: tab[row] = code of ordinal q0 - 1 + row (center index, or the
+// sentinel tagged with kIncFlag), opc[i] = RN(1 + c_i); true when the mode
+// applies (block-uniform).
+template <typename T>
+__device__ __forceinline__ bool setup_keyed(const double* __restrict__ centers_g, int k,
+                                            const nmk_stats* __restrict__ st, double width, double tol,
+                                            double tol_bin, uint32_t sentinel, uint32_t* tab, double* opc,
+                                            KeyedGrid& g, int* s_fail, unsigned long long* s_dmax, int* s_q,
+                                            double* s_kd) {
+  if (threadIdx.x == 0) { *s_fail = 0; *s_dmax = 0ULL; s_q[0] = 0; s_q[1] = 0; }
+  __syncthreads();
+  const double gmin = st->gmin, gmax = st->gmax;
+  const unsigned long long nb = st->reserved;
+  const double inv_w = __ddiv_rn(1.0, width);
+  const bool ok0 = k >= 1 && nb >= 1 && nb < (1ULL << 21) && tol > 0.0 && tol < 0x1p+20 && tol_bin == tol &&
+                   width == __dmul_rn(2.0, tol) && finite64(gmin) && finite64(gmax) && finite64(inv_w);
+  auto pos = [&](double c) { return __dmul_rn(__dsub_rn(c, gmin), inv_w); };   // (c - gmin)/w
+  if (ok0) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const double c = __ldg(centers_g + i);
+      opc[i] = __dadd_rn(1.0, c);   // the decoder's (1 + c) (core.py:202-205)
+      const double p = pos(c);
+      const double q = floor(p);
+      const double d = fabs(__dsub_rn(p, __dadd_rn(q, 0.5)));
+      bool ok = p >= 0.0 && p < (double)nb && d <= 0.25;   // false for NaN
+      if (ok && i > 0) ok = floor(pos(__ldg(centers_g + i - 1))) < q;
+      if (!ok) *s_fail = 1;
+      else atomicMax(s_dmax, (unsigned long long)__double_as_longlong(d));
+      if (ok && i == 0) s_q[0] = (int)q;
+      if (ok && i == k - 1) s_q[1] = (int)q;
+    }
+  }
+  __syncthreads();
+  if (!ok0 || *s_fail) return false;
+  const int q0 = s_q[0], span2 = s_q[1] - q0 + 3;
+  if (span2 > kLutCells) return false;
+  for (int i = threadIdx.x; i < span2; i += blockDim.x) tab[i] = sentinel | kIncFlag;
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) tab[(int)floor(pos(__ldg(centers_g + i))) - q0 + 1] = (uint32_t)i;
+  const double A = fmax(fmax(fabs(gmin), fabs(gmax)), fmax(fabs(__ldg(centers_g)), fabs(__ldg(centers_g + k - 1))));
+  const double D = __longlong_as_double((long long)*s_dmax);
+  constexpr bool kF32 = sizeof(T) == 4;
+  const double delta = (4.0 * (1.0 + A) + 2.0 * tol) * 0x1p-52 + (kF32 ? (1.0 + A + tol) * 0x1p-23 + 0x1p-48 : 0x1p-170);
+  // margin terms (cells): the round trip, cut / center-position rounding
+  const double mp = D + (delta * inv_w + A * inv_w * 0x1p-50 + (nb + 2.0) * 0x1p-48 + 0x1p-40) * 1.01;
+  // f32 test, origin moved to the bin of r = 0 (q_ref) so the constants and
+  // the FMA are small where the ratios are:  th = RN32(key*iw32 + c32) with
+  // c' = -gmin/w - 1/2 - q_ref (|c'| <= 1/2), and per element
+  //   |th - (u - 1/2 - q_ref)| <= |th| 2^-23 + |key| iw 2^-22 + C0
+  // (FMA rounding, |key - r| <= |key| 2^-23, |iw32 - 1/w|, RN32 of c').
+  const double G = fabs(gmin) * inv_w;
+  const double cd = -gmin * inv_w - 0.5;
+  const double qref = rint(cd);
+  const double cp = cd - qref;   // exact (Sterbenz)
+  const double C0 = fabs(cp) * 0x1p-24 + G * 0x1p-50 + 0x1p-40;
+  const double hiT = 0.5 - mp - C0 - 0x1p-23;   // 2^-23: the f32 rounding of the bound itself
+  const bool on = G < 0x1p+30 && A * inv_w < 0x1p+40 && inv_w < 0x1p+100 && A < 0x1p+100 && hiT > 0.25;
+  if (threadIdx.x == 0) {
+    s_kd[0] = gmin;
+    s_kd[1] = inv_w;
+    s_kd[2] = 0.5 - mp;
+  }
+  g.kd_s = opaque(smem_u32(s_kd));
+  g.iw32 = __double2float_rn(inv_w);
+  g.c32 = __double2float_rn(cp);
+  g.ka = __double2float_ru(inv_w * 0x1p-22);
+  g.iw2 = ((unsigned long long)__float_as_uint(g.iw32) << 32) | __float_as_uint(g.iw32);
+  g.c2 = ((unsigned long long)__float_as_uint(g.c32) << 32) | __float_as_uint(g.c32);
+  g.hi4 = on ? __double2float_rz(hiT) : -1.0f;
+  g.q0m1 = (uint32_t)(q0 - 1);
+  g.rowbase = 0x4B400000u + (uint32_t)(q0 - 1 - (long long)qref);   // magic-sum bits -> table row
+  g.span2 = (uint32_t)span2;
+  g.tab_s = opaque(smem_u32(tab));
+  g.opc_s = opaque(smem_u32(opc));
+  __syncthreads();
+  return g.hi4 > 0.0f;
+}
+
+// Branch-free: rows outside the table are clamped onto its last row (ordinal
+// q_last + 1, never a center: the tagged sentinel); a key outside the
+// margin, NaN included, gives kKeySlow.
+__device__ __forceinline__ uint32_t classify_key(float key, const KeyedGrid& g) {
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+  const float th = __fmaf_rn(key, g.iw32, g.c32);
+  const float m = __fadd_rn(th, kMagic);
+  const float d = __fsub_rn(th, __fsub_rn(m, kMagic));
+  const uint32_t row = min((uint32_t)__float_as_int(m) - g.rowbase, g.span2 - 1u);
+  const uint32_t code = lds_u32(g.tab_s + 4 * row);
+  const float sb = __fmaf_rn(fabsf(th), 0x1p-23f, __fmaf_rn(fabsf(key), g.ka, fabsf(d)));   // |d| + bound
+  return sb < g.hi4 ? code : kKeySlow;
+}
+
+// classify_key for two keys at once: the f32 arithmetic in f32x2 form
+// (FFMA2 / FADD2, each lane IEEE round-to-nearest like the scalar ops), the
+// bound test per key.
+// Returns the two table codes; `bad` collects keys outside the margin (NaN
+// included), which the caller re-decides.
+__device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGrid& g, uint32_t& ca, uint32_t& cb,
+                                              bool& bad) {
+  constexpr unsigned long long kMagic2 = 0x4B4000004B400000ULL;   // (1.5 * 2^23, 1.5 * 2^23)
+  const unsigned long long k2 = ((unsigned long long)__float_as_uint(kb) << 32) | __float_as_uint(ka);
+  unsigned long long th, m, t, d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(th) : "l"(k2), "l"(g.iw2), "l"(g.c2));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(th), "l"(kMagic2));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(m), "l"(kMagic2));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(th), "l"(t));
+  const uint32_t ra = min((uint32_t)m - g.rowbase, g.span2 - 1u);
+  const uint32_t rb = min((uint32_t)(m >> 32) - g.rowbase, g.span2 - 1u);
+  ca = lds_u32(g.tab_s + 4 * ra);
+  cb = lds_u32(g.tab_s + 4 * rb);
+  const float sa = __fmaf_rn(fabsf(__uint_as_float((uint32_t)th)), 0x1p-23f,
+                             __fmaf_rn(fabsf(ka), g.ka, fabsf(__uint_as_float((uint32_t)d))));
+  const float sb = __fmaf_rn(fabsf(__uint_as_float((uint32_t)(th >> 32))), 0x1p-23f,
+                             __fmaf_rn(fabsf(kb), g.ka, fabsf(__uint_as_float((uint32_t)(d >> 32)))));
+  bad |= !(sa < g.hi4);
+  bad |= !(sb < g.hi4);
+}
+
+// Second tier for keys the f32 test left undecided (near a bin edge by the
+// launch-wide bound, which is loose for the small ratios of a dominant bin):
+// t = RN(RN(key - gmin) / w) in f64 with the per-element bound
+//   |t - u| <= et = |key| iw 2^-22 + |t| 2^-49 + 2^-60
+// (|key - r| <= |key| 2^-23, three roundings of t), so with f = t - floor(t),
+// |f - 1/2| < 1/2 - margin - et puts u in bin floor(t) with the margin of
+// setup_keyed.  +inf keys (exact path) give NaN and fail.
+__device__ __forceinline__ uint32_t classify_key64(float key, const KeyedGrid& g) {
+  const double gmin = lds_f64(g.kd_s), iw = lds_f64(g.kd_s + 8), half_m = lds_f64(g.kd_s + 16);
+  const double t = __dmul_rn(__dsub_rn((double)key, gmin), iw);
+  const double fl = floor(t);
+  const double f = __dsub_rn(t, fl);
+  const double et = fabs((double)key) * iw * 0x1p-22 + fabs(t) * 0x1p-49 + 0x1p-60;
+  if (!(fabs(__dsub_rn(f, 0.5)) < __dsub_rn(half_m, et)) || !(t < 0x1p+31)) return kKeySlow;
+  const uint32_t row = min((uint32_t)(long long)fl - g.q0m1, g.span2 - 1u);
+  return lds_u32(g.tab_s + 4 * row);
+}
+
+// Packed bytes of one chunk: each lane's 8 codes are B bytes at lane * B;
+// whole chunks store them directly, a chunk clipped by its block's end
+// stages them per warp and stores the block's bytes only.
+template <int B>
+__device__ __forceinline__ void chunk_pack(const EncodeGeom& geo, uint32_t b, uint32_t ci, uint64_t blk_start,
+                                           uint64_t blk_end, const uint32_t (&code)[kGroup], uint8_t* my,
+                                           uint8_t* __restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t blk_bytes = ((blk_end - blk_start) * B + 7) / 8;
+  const uint64_t off = (uint64_t)ci * (32 * B);
+  uint8_t* dst = packed + (uint64_t)(b - geo.b0) * geo.stride + off;
+  if (blk_bytes >= off + 32 * B) {
+    pack8<B>(code, dst + lane * B);
+    return;
+  }
+  const uint32_t nbytes = (uint32_t)(blk_bytes > off ? blk_bytes - off : 0);
+  pack8<B>(code, my + lane * B);
+  __syncwarp();
+  const uint32_t nvec = nbytes / 16;
+  for (uint32_t i = lane; i < nvec; i += 32)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(my)[i];
+  for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) dst[i] = my[i];
+  __syncwarp();
+}
+
+// Chunk epilogue of the snapshot-reading flavours: warp-level compaction of
+// the incompressible values (already in registers) into the chunk's scratch
+// window (element order; most chunks have none), the chunk count, and the
+// packed bytes.
+template <typename T, int B, typename XOf>
+__device__ __forceinline__ void chunk_finish(const EncodeGeom& geo, uint32_t c, uint32_t b, uint32_t ci,
+                                             uint64_t blk_start, uint64_t blk_end, const uint32_t (&code)[kGroup],
+                                             unsigned inc_mask, XOf&& x_of, T* __restrict__ scratch,
+                                             uint32_t* __restrict__ counts, uint8_t* my, uint8_t* __restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  unsigned total = 0;
+  if (__any_sync(0xffffffffu, inc_mask != 0)) {
+    const unsigned cnt = __popc(inc_mask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    total = __shfl_sync(0xffffffffu, incl, 31);
+    T* w = scratch + (uint64_t)c * kChunk + (incl - cnt);
+#pragma unroll
+    for (int e = 0; e < kGroup; ++e)
+      if (inc_mask >> e & 1u) *w++ = x_of(e);   // raw bits (NaN payloads kept)
+  }
+  if (lane == 0) counts[c] = total;
+  chunk_pack<B>(geo, b, ci, blk_start, blk_end, code, my, packed);
+}
+
 // The chunk loop, instantiated once per classification flavour.
 template <typename T, int B, bool kRecon, typename Cls, typename Rec>
 __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const T* __restrict__ cur,
@@ -378,38 +620,211 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
           if (in) recon[li + e] = code[e] == sentinel ? xv[e] : rec_of(code[e], bv[e]);
       }
     }
-    // warp-level compaction of the incompressible values into the chunk's
-    // scratch window (element order); most chunks have none
-    unsigned total = 0;
-    if (__any_sync(0xffffffffu, inc_mask != 0)) {
-      const unsigned cnt = __popc(inc_mask);
-      unsigned incl = cnt;
+    chunk_finish<T, B>(geo, c, b, ci, blk_start, blk_end, code, inc_mask, [&](int e) { return xv[e]; }, scratch,
+                       counts, my, packed);
+  }
+}
+
+// The keyed chunk loop: codes from the keys; the snapshots are read only
+// where a key cannot decide (slow), for the incompressible values, and for
+// the fused reconstruction's base values.  Each warp keeps the keys of
+// kKeyStagesE chunks in flight (TMA ring in shared memory).
+#ifndef NMK_ENCK_STAGES
+#define NMK_ENCK_STAGES 4
+#endif
+constexpr int kKeyStagesE = NMK_ENCK_STAGES;
+// dynamic shared memory of k_encode_keyed: opc doubles, then 128-byte aligned key tiles
+__host__ __device__ constexpr size_t keyed_ring_off(int k_cap) { return ((size_t)(k_cap + 2) + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t keyed_smem_bytes(int k_cap) {
+  return keyed_ring_off(k_cap) * 8 + (size_t)(kEncThreads / 32) * kKeyStagesE * kChunk * 4;
+}
+template <typename T, int B, bool kRecon, typename Slow, typename Rec>
+__device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ keys, const T* __restrict__ base,
+                                                    const T* __restrict__ cur, const EncodeGeom& geo,
+                                                    uint8_t* __restrict__ packed, uint8_t* __restrict__ masks,
+                                                    uint32_t* __restrict__ counts, uint8_t* my,
+                                                    T* __restrict__ recon, const KeyedGrid& kg, float* kring,
+                                                    unsigned long long* kbars, Slow&& slow, Rec&& rec_of) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t sentinel = (1u << B) - 1u;
+  const uint64_t local_end = geo.elem0 + geo.n_local;
+  const bool ptr_al = (((uintptr_t)keys | (kRecon ? ((uintptr_t)base | (uintptr_t)recon) : 0)) & 15) == 0;
+  const uint32_t cpb = (uint32_t)geo.cpb;
+  const uint32_t cpb_whole = (uint32_t)(geo.epb / kChunk);   // chunks per block that are never clipped
+  constexpr int VN = EVec<T>::N;
+  // this warp's contiguous run of chunks [cA, cB)
+  const uint32_t nch = (uint32_t)geo.nchunks;
+  const uint32_t nwarps = gridDim.x * (kEncThreads / 32);
+  const uint32_t wg = blockIdx.x * (kEncThreads / 32) + wid;
+  const uint32_t per = nch / nwarps, rem = nch % nwarps;
+  const uint32_t cA = wg * per + min(wg, rem);
+  const uint32_t cB = cA + per + (wg < rem ? 1u : 0u);
+  // chunk cursor, advanced incrementally (no division in the loop)
+  struct Cur {
+    uint32_t c, b, ci;
+    uint64_t lo;   // first element of the chunk
+  };
+  auto at = [&](uint32_t c) {
+    Cur k;
+    const uint32_t g = (uint32_t)geo.g0 + c;
+    k.c = c;
+    k.b = geo.fd_cpb.div(g);
+    k.ci = g - k.b * cpb;
+    k.lo = (uint64_t)k.b * geo.epb + (uint64_t)k.ci * kChunk;
+    return k;
+  };
+  auto next = [&](Cur& k) {
+    ++k.c;
+    if (++k.ci == cpb) {
+      k.ci = 0;
+      ++k.b;
+      k.lo = (uint64_t)k.b * geo.epb;
+    } else {
+      k.lo += kChunk;
+    }
+  };
+  // warp-uniform: a whole chunk of this range, inside its block, key vectors aligned
+  // chunks [c_first, c_last] lie wholly inside this range (geo, host-computed)
+  const bool al_all = ptr_al && geo.key_al;
+  auto fast_of = [&](const Cur& k) {
+    return k.c >= geo.c_first && k.c <= geo.c_last && k.ci < cpb_whole &&
+           (al_all || (ptr_al && ((k.lo - geo.elem0) & 3) == 0));
+  };
+  auto run = [&](const Cur& k, bool fast, const float4& k0, const float4& k1) {
+    uint32_t code[kGroup];
+    unsigned live = 0xffu;
+    const uint64_t grp_lo = k.lo + (uint64_t)lane * kGroup;
+    const int64_t li = (int64_t)grp_lo - (int64_t)geo.elem0;
+    uint64_t blk_start = 0, blk_end = 0;
+    if (fast) {
+      bool bad = false;
+      classify_key2(k0.x, k0.y, kg, code[0], code[1], bad);
+      classify_key2(k0.z, k0.w, kg, code[2], code[3], bad);
+      classify_key2(k1.x, k1.y, kg, code[4], code[5], bad);
+      classify_key2(k1.z, k1.w, kg, code[6], code[7], bad);
+      if (__any_sync(0xffffffffu, bad) && bad) {   // mark this lane's undecided keys
+        const float kk[kGroup] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+        for (int e = 0; e < kGroup; ++e) code[e] = classify_key(kk[e], kg);
       }
-      total = __shfl_sync(0xffffffffu, incl, 31);
-      if (inc_mask) {
-        T* w = scratch + (uint64_t)c * kChunk + (incl - cnt);
+    } else {
+      blk_start = (uint64_t)k.b * geo.epb;
+      blk_end = min(blk_start + geo.epb, geo.n_total);
+      const uint64_t lo = max(k.lo, geo.elem0), hi = min(blk_end, local_end);
+      live = 0u;
 #pragma unroll
-        for (int e = 0; e < kGroup; ++e)
-          if (inc_mask >> e & 1u) *w++ = xv[e];   // raw bits (NaN payloads kept)
+      for (int e = 0; e < kGroup; ++e) {
+        const uint64_t j = grp_lo + e;
+        const bool in = j >= lo && j < hi;
+        live |= (in ? 1u : 0u) << e;
+        code[e] = in ? classify_key(keys[li + e], kg) : 0u;
       }
     }
-    if (lane == 0) counts[c] = total;
-    // packed bytes: stage per warp, then 16-byte stores clipped to the block
-    pack8<B>(code, my + lane * B);
+    uint32_t any = 0;
+#pragma unroll
+    for (int e = 0; e < kGroup; ++e) any |= code[e];
+    const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kIncFlag));
+    if (flags & kKeySlow) {   // rare: NaN key, f64 key test, exact path
+      if (any & kKeySlow) {
+#pragma unroll
+        for (int e = 0; e < kGroup; ++e) {
+          if (code[e] & kKeySlow) {
+            const float key = __ldg(keys + li + e);
+            uint32_t v = key != key ? (sentinel | kIncFlag) : classify_key64(key, kg);
+            if (v == kKeySlow) {
+              v = slow(__ldg(base + li + e), __ldg(cur + li + e));
+              v |= v == sentinel ? kIncFlag : 0u;
+            }
+            code[e] = v;
+          }
+        }
+      }
+      any = 0;
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e) any |= code[e];
+    }
+    // incompressible elements: the chunk's count and its 256-bit position
+    // mask (one byte per lane); k_enc_finalize gathers the values from cur
+    unsigned total = 0;
+    if (__any_sync(0xffffffffu, any & kIncFlag)) {
+      unsigned inc_mask = 0;
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e) {
+        inc_mask |= ((code[e] >> 30) & 1u) << e;
+        code[e] &= ~kIncFlag;
+      }
+      inc_mask &= live;
+      total = __reduce_add_sync(0xffffffffu, (unsigned)__popc(inc_mask));
+      masks[(uint64_t)k.c * 32 + lane] = (uint8_t)inc_mask;
+    }
+    if (lane == 0) counts[k.c] = total;
+    if constexpr (kRecon) {   // the decoder's values
+      if (fast) {
+        T bv[kGroup];
+        load8<T>(base + li, bv);
+        using V = typename EVec<T>::V;
+#pragma unroll
+        for (int q = 0; q < kGroup / VN; ++q) {
+          V w;
+          T* t = reinterpret_cast<T*>(&w);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) {
+            const int ee = q * VN + e;
+            t[e] = code[ee] == sentinel ? __ldg(cur + li + ee) : rec_of(code[ee], bv[ee]);
+          }
+          reinterpret_cast<V*>(recon + li)[q] = w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < kGroup; ++e)
+          if (live >> e & 1u)
+            recon[li + e] = code[e] == sentinel ? __ldg(cur + li + e) : rec_of(code[e], __ldg(base + li + e));
+      }
+    }
+    if (fast) {   // whole chunk inside its block: each lane stores its B bytes
+      pack8<B>(code, packed + (uint64_t)(k.b - geo.b0) * geo.stride + (uint64_t)k.ci * (32 * B) + lane * B);
+    } else {
+      chunk_pack<B>(geo, k.b, k.ci, blk_start, blk_end, code, my, packed);
+    }
+  };
+  // per-warp ring of kKeyStagesE chunk key tiles (1 KB each) filled by TMA
+  // bulk copies; chunks that are not whole read their keys directly in run()
+  float* ring = kring + (size_t)wid * kKeyStagesE * kChunk;
+  unsigned long long* bars = kbars + wid * kKeyStagesE;
+  if (lane == 0) {
+    for (int st = 0; st < kKeyStagesE; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (cA >= cB) return;
+  Cur cp = at(cA), pf = cp;
+  auto issue = [&](int st) {   // warp-uniform; lane 0 issues the copy of chunk pf
+    if (pf.c < cB && fast_of(pf) && lane == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_tx(&bars[st], kChunk * 4);
+      tma_load_1d(ring + st * kChunk, keys + (pf.lo - geo.elem0), kChunk * 4, &bars[st]);
+    }
+    next(pf);
+  };
+#pragma unroll
+  for (int st = 0; st < kKeyStagesE; ++st) issue(st);
+  uint32_t ph = 0;   // per-stage mbarrier phase bits
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  int st = 0;
+  for (; cp.c < cB; next(cp)) {
+    const bool fast = fast_of(cp);
+    float4 k0 = z4, k1 = z4;
+    if (fast) {
+      mbar_wait(&bars[st], (ph >> st) & 1u);
+      ph ^= 1u << st;
+      const float4* src = reinterpret_cast<const float4*>(ring + st * kChunk) + lane * 2;
+      k0 = src[0];
+      k1 = src[1];
+    }
     __syncwarp();
-    const uint64_t blk_bytes = ((blk_end - blk_start) * B + 7) / 8;
-    const uint64_t off = (uint64_t)ci * (32 * B);
-    const uint32_t nbytes = (uint32_t)min(blk_bytes > off ? blk_bytes - off : 0, (uint64_t)(32 * B));
-    uint8_t* dst = packed + (uint64_t)(b - geo.b0) * geo.stride + off;
-    const uint32_t nvec = nbytes / 16;
-    for (uint32_t i = lane; i < nvec; i += 32)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(my)[i];
-    for (uint32_t i = nvec * 16 + lane; i < nbytes; i += 32) dst[i] = my[i];
-    __syncwarp();
+    issue(st);   // refill the stage just read
+    run(cp, fast, k0, k1);
+    st = st + 1 == kKeyStagesE ? 0 : st + 1;
   }
 }
 
@@ -418,7 +833,8 @@ __global__ void __launch_bounds__(kEncThreads, NMK_ENC_MINB)
 k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
          const double* __restrict__ centers_g, const double* __restrict__ cuts_g, int k,
          double tol_bin, double tol, uint8_t* __restrict__ packed, T* __restrict__ scratch,
-         uint32_t* __restrict__ counts, const nmk_model* __restrict__ model, bool smem_ok, T* __restrict__ recon) {
+         uint32_t* __restrict__ counts, const nmk_model* __restrict__ model, bool smem_ok, T* __restrict__ recon,
+         const uint32_t* __restrict__ done) {
   __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
   __shared__ uint32_t lut32[kLutCells];   // cell -> center (direct mode) or, as u16, the cut grid
   uint16_t* lut = reinterpret_cast<uint16_t*>(lut32);
@@ -428,6 +844,7 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
   __shared__ unsigned long long s_dmax;
   extern __shared__ __align__(16) double cutsp[];   // [-inf, cuts..., +inf, +inf] or centers
 
+  if (done && *done) return;   // k_encode_keyed already encoded this range
   if (model) {   // sync-free path: the model scalars live on the device
     if (model->status != 0) {   // nothing to encode: leave empty chunks behind
       for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += gridDim.x * blockDim.x)
@@ -504,6 +921,50 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
   }
 }
 
+// K4 keyed mode as its own kernel (own register budget).  Every CTA runs the
+// same set-up; when the mode does not apply (centers off the bin grid, span
+// too wide, bound too loose) it writes done = 0 and returns, and k_encode,
+// launched right after, does the work; otherwise done = 1 and k_encode exits.
+#ifndef NMK_ENCK_MINB
+#define NMK_ENCK_MINB 3
+#endif
+template <typename T, int B, bool kRecon>
+__global__ void __launch_bounds__(kEncThreads, NMK_ENCK_MINB)
+k_encode_keyed(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
+               const double* __restrict__ centers_g, const double* __restrict__ cuts_g, double tol,
+               uint8_t* __restrict__ packed, T* __restrict__ scratch, uint32_t* __restrict__ counts,
+               const nmk_model* __restrict__ model, int k_cap, T* __restrict__ recon, EncodeKeys kx) {
+  __shared__ __align__(16) uint8_t wbytes[kEncThreads / 32][32 * B + 16];
+  __shared__ uint32_t tab[kLutCells];   // ordinal row -> code
+  __shared__ int s_fail, s_q[2];
+  __shared__ unsigned long long s_dmax;
+  __shared__ double s_kd[3];
+  __shared__ __align__(8) unsigned long long kbars[(kEncThreads / 32) * kKeyStagesE];
+  extern __shared__ __align__(128) double opc[];   // RN(1 + c_i) [k_cap + 2], then the key ring
+  float* kring = reinterpret_cast<float*>(opc + keyed_ring_off(k_cap));
+  const uint32_t sentinel = (1u << B) - 1u;
+  if (model->status != 0) {   // nothing to encode: leave empty chunks behind
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += gridDim.x * blockDim.x)
+      counts[c] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *kx.done = 1u;
+    return;
+  }
+  const int k = model->k;
+  const double tol_bin = model->tol_bin;
+  KeyedGrid kg;
+  const bool ok = k <= k_cap && k <= kSmemCuts + 1 &&
+                  setup_keyed<T>(centers_g, k, kx.st, kx.width, tol, tol_bin, sentinel, tab, opc, kg, &s_fail,
+                                 &s_dmax, s_q, s_kd);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *kx.done = ok ? 1u : 0u;
+  if (!ok) return;
+  const int ncuts = k - 1;
+  encode_chunks_keyed<T, B, kRecon>(
+      kx.keys, base, cur, geo, packed, reinterpret_cast<uint8_t*>(scratch), counts, wbytes[threadIdx.x >> 5], recon,
+      kg, kring, kbars,
+      [&](T b, T x) -> uint32_t { return classify_exact<T>(b, x, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel); },
+      [&](uint32_t cd, T b) -> T { return narrow<T>(__dmul_rn(lds_f64(kg.opc_s + 8 * cd), to_f64(b))); });
+}
+
 static int sm_count_e() {
   static int sms = 0;
   if (!sms) {
@@ -518,7 +979,8 @@ static int sm_count_e() {
 template <typename T, int B, bool kRecon>
 static void launch_encode_k(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
                             const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
-                            uint32_t* counts, const nmk_model* model, int k_cap, void* recon, cudaStream_t s) {
+                            uint32_t* counts, const nmk_model* model, int k_cap, void* recon, const EncodeKeys& kx,
+                            cudaStream_t s) {
   const bool smem_ok = k_cap <= kSmemCuts + 1;
   const size_t smem = smem_ok ? (size_t)(k_cap + 2) * 8 : 0;
   static size_t attr = 0;
@@ -532,9 +994,25 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
   uint64_t grid = (uint64_t)sm_count_e() * per_sm;
   uint64_t need = (geo.nchunks + 7) / 8;
   if (grid > need) grid = need;
-  k_encode<T, B, kRecon><<<(unsigned)grid, kEncThreads, smem, s>>>((const T*)base, (const T*)cur, geo, centers,
-                                                                   cuts, k, tol_bin, tol, packed, (T*)scratch, counts,
-                                                                   model, smem_ok, (T*)recon);
+  if (kx.keys && model && smem_ok) {
+    const size_t smem_k = keyed_smem_bytes(k_cap);
+    static size_t attr_k = 0;
+    if (smem_k > attr_k) {
+      cudaFuncSetAttribute(k_encode_keyed<T, B, kRecon>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
+      attr_k = smem_k;
+    }
+    int per_sm_k = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_k, k_encode_keyed<T, B, kRecon>, kEncThreads, smem_k);
+    if (per_sm_k < 1) per_sm_k = 1;
+    uint64_t grid_k = (uint64_t)sm_count_e() * per_sm_k;
+    if (grid_k > need) grid_k = need;
+    k_encode_keyed<T, B, kRecon><<<(unsigned)grid_k, kEncThreads, smem_k, s>>>(
+        (const T*)base, (const T*)cur, geo, centers, cuts, tol, packed, (T*)scratch, counts, model, k_cap, (T*)recon,
+        kx);
+  }
+  k_encode<T, B, kRecon><<<(unsigned)grid, kEncThreads, smem, s>>>(
+      (const T*)base, (const T*)cur, geo, centers, cuts, k, tol_bin, tol, packed, (T*)scratch, counts, model, smem_ok,
+      (T*)recon, (kx.keys && model && smem_ok) ? kx.done : nullptr);
 }
 
 // the fused reconstruction is a separate instantiation: the plain encode
@@ -542,13 +1020,14 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
 template <typename T, int B>
 void launch_encode(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
                           const double* cuts, int k, double tol_bin, double tol, uint8_t* packed, void* scratch,
-                          uint32_t* counts, const nmk_model* model, int k_cap, void* recon, cudaStream_t s) {
+                          uint32_t* counts, const nmk_model* model, int k_cap, void* recon, const EncodeKeys& kx,
+                          cudaStream_t s) {
   if (recon)
     launch_encode_k<T, B, true>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, model, k_cap,
-                                recon, s);
+                                recon, kx, s);
   else
     launch_encode_k<T, B, false>(base, cur, geo, centers, cuts, k, tol_bin, tol, packed, scratch, counts, model,
-                                 k_cap, nullptr, s);
+                                 k_cap, nullptr, kx, s);
 }
 
 }  // namespace nmk

@@ -32,7 +32,11 @@ struct MinMax {
 // One element into the running (min, max, count) over valid ratios
 // (core.py:115-137, pipeline.py:194-197).  The IEEE quotient is only formed
 // when the fast approximation cannot rule the element out as a new extreme.
-// Returns the element's f32 ratio key for K2 (ratio_key in nmk_common.cuh).
+// Returns the element's f32 ratio key for K2 and K4 (ratio_key in
+// nmk_common.cuh): finite only when b = x = 0 or b lies in the safe range of
+// key_safe<T> (K4's keyed round-trip proof needs it), else +inf ("decide
+// exactly") for a valid element and NaN for an invalid one.
+template <typename T>
 __device__ __forceinline__ float mm_visit(MinMax& a, double b, double x) {
   double ra, ea;
   if (fast_ratio(b, x, ra, ea)) {
@@ -42,7 +46,7 @@ __device__ __forceinline__ float mm_visit(MinMax& a, double b, double x) {
       a.lo = r < a.lo ? r : a.lo;
       a.hi = r > a.hi ? r : a.hi;
     }
-    return ratio_key(ra);
+    return key_safe<T>(b, x) ? ratio_key(ra) : __int_as_float(0x7f800000);
   }
   bool v;
   const double r = change_ratio(b, x, v);
@@ -50,7 +54,7 @@ __device__ __forceinline__ float mm_visit(MinMax& a, double b, double x) {
     a.nv += 1;
     a.lo = r < a.lo ? r : a.lo;
     a.hi = r > a.hi ? r : a.hi;
-    return ratio_key(r);
+    return (key_safe<T>(b, x) || (b == 0.0 && x == 0.0)) ? ratio_key(r) : __int_as_float(0x7f800000);
   }
   return __int_as_float(0x7fc00000);   // invalid: quiet NaN
 }
@@ -110,7 +114,7 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
         vec_get(c[u], cc);
         float kv[VN];
 #pragma unroll
-        for (int e = 0; e < VN; ++e) kv[e] = mm_visit(acc, bb[e], cc[e]);
+        for (int e = 0; e < VN; ++e) kv[e] = mm_visit<T>(acc, bb[e], cc[e]);
         if (keys) store_keys<VN>(keys + (i + u * nthr) * VN, kv);
       }
     }
@@ -120,13 +124,13 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
       vec_get(__ldg(cv + i), cc);
       float kv[VN];
 #pragma unroll
-      for (int e = 0; e < VN; ++e) kv[e] = mm_visit(acc, bb[e], cc[e]);
+      for (int e = 0; e < VN; ++e) kv[e] = mm_visit<T>(acc, bb[e], cc[e]);
       if (keys) store_keys<VN>(keys + i * VN, kv);
     }
     done = nvec * VN;
   }
   for (uint64_t j = done + tid; j < n; j += nthr) {
-    const float kv = mm_visit(acc, to_f64(base[j]), to_f64(cur[j]));
+    const float kv = mm_visit<T>(acc, to_f64(base[j]), to_f64(cur[j]));
     if (keys) keys[j] = kv;
   }
   // warp reduce

@@ -115,6 +115,18 @@ __device__ __forceinline__ float ratio_key(double r) {
   return __double2float_rn(r);
 }
 
+// Safe range for a finite key (K4 keyed mode, k_encode.cuh): |b| in
+// [2^-900, 2^901) and |x| < 2^901 for f64 inputs, [2^-100, 2^101) and
+// < 2^101 for f32, so the decoder's product (1 + c) b neither overflows nor
+// loses relative accuracy to subnormal rounding.
+template <typename T>
+__device__ __forceinline__ bool key_safe(double b, double x) {
+  constexpr int lo = sizeof(T) == 4 ? 1023 - 100 : 1023 - 900;
+  constexpr int hi = sizeof(T) == 4 ? 1023 + 100 : 1023 + 900;
+  const int eb = (__double2hiint(b) >> 20) & 0x7ff, ex = (__double2hiint(x) >> 20) & 0x7ff;
+  return eb >= lo && eb <= hi && ex <= hi;
+}
+
 // One bound for a whole launch: the per-element bound of key_ordinal is
 // monotone in |key|, |s| and |t|, all of which are bounded by the global
 // (gmin, gmax), so et_c below dominates it for every valid element.

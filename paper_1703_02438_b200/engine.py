@@ -171,8 +171,11 @@ class _PhaseClock:
 
 def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: int = 1 << 20,
            *, elem0: int = 0, n_total: int | None = None, comm=None, ws: Workspace | None = None,
-           stream=None, timing: bool = False, recon=None) -> DeviceEncoding:
+           stream=None, timing: bool = False, recon=None, keyed: bool = True) -> DeviceEncoding:
     """Run K1..K4 on device tensors ``base``/``cur`` (1-D, same dtype, CUDA).
+
+    ``keyed``: K1 stores f32 ratio keys; for a dense histogram K2 and K4 then
+    read 4 bytes per element instead of both snapshots (same bytes out).
 
     ``elem0``/``n_total`` place this range inside a longer global stream (a
     multi-GPU shard); ``comm`` (see distributed.py) performs the exchanges.
@@ -207,7 +210,9 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
     if n_local > 0:
         mm_bytes = lib.nmk_minmax_ws_bytes(n_local)
         mm_ws = ws.get("minmax", mm_bytes, zero=True)
-        N.check(lib.nmk_minmax(_p(base), _p(cur), n_local, dt, _p(stats), None, _p(mm_ws), mm_bytes, st))
+        keys = ws.typed("ratio_keys", n_local + 4, torch.float32) if keyed else None
+        N.check(lib.nmk_minmax(_p(base), _p(cur), n_local, dt, _p(stats), _p(keys) if keyed else None, _p(mm_ws),
+                               mm_bytes, st))
     else:
         stats.copy_(torch.tensor([0x7FF0000000000000, -0x10000000000000, 0, 0], dtype=torch.int64))
     if comm is not None:
@@ -233,7 +238,12 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
         if dense:
             form = "dense"
             counts_t = ws.typed("hist_counts", nbins + 1, torch.int64)
-            if n_local > 0:
+            if n_local > 0 and keyed:
+                # device span (same arithmetic as above) + K2 from the keys
+                N.check(lib.nmk_hist_prep(_p(stats), width, DENSE_MAX_BINS, _p(counts_t), st))
+                N.check(lib.nmk_hist_dense_dev(_p(base), _p(cur), _p(keys), n_local, dt, _p(stats), width,
+                                               _p(counts_t), st))
+            elif n_local > 0:
                 N.check(lib.nmk_hist_dense(_p(base), _p(cur), n_local, dt, _p(stats), width, nbins,
                                            _p(counts_t), st))
             else:
@@ -304,10 +314,16 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
         e_ws = ws.get("encode_ws", e_bytes)
         if recon is not None and (recon.shape != cur.shape or recon.dtype != cur.dtype or not recon.is_cuda):
             raise ValueError("recon must be a CUDA tensor like current")
-        N.check(lib.nmk_encode(_p(base), _p(cur), n_local, elem0, n, dt, _p(centers), _p(cuts), k, B,
-                               float(model.tol_bin), float(tolerance), epb, _p(packed), stride, _p(exact),
-                               _p(prefix), _p(n_inc_t), _p(recon) if recon is not None else None, _p(e_ws),
-                               e_bytes, st))
+        if keyed and form == "dense":
+            N.check(lib.nmk_encode_keyed_dev(_p(keys), _p(stats), width, _p(base), _p(cur), n_local, elem0, n, dt,
+                                             _p(centers), _p(cuts), _p(model_t), min(cap_k, (1 << B) - 1), B, float(tolerance), epb,
+                                             _p(packed), stride, _p(exact), _p(prefix), _p(n_inc_t),
+                                             _p(recon) if recon is not None else None, _p(e_ws), e_bytes, st))
+        else:
+            N.check(lib.nmk_encode(_p(base), _p(cur), n_local, elem0, n, dt, _p(centers), _p(cuts), k, B,
+                                   float(model.tol_bin), float(tolerance), epb, _p(packed), stride, _p(exact),
+                                   _p(prefix), _p(n_inc_t), _p(recon) if recon is not None else None, _p(e_ws),
+                                   e_bytes, st))
     else:
         n_inc_t.zero_()
     clock.mark("assign_index")
@@ -468,10 +484,12 @@ class DevicePipeline:
                                self.dt, P(self.centers), P(self.cuts), P(self.centers_t), self.k_cap, P(self.model),
                                st))
         mark("K3_select")
-        N.check(lib.nmk_encode_dev(P(base), P(cur), self.n_local, self.elem0, self.n, self.dt, P(self.centers),
-                                   P(self.cuts), P(self.model), self.k_cap, self.bits, self.tol, self.epb,
-                                   P(self.packed), self.stride, P(self.exact), P(self.prefix), P(self.n_inc),
-                                   P(recon) if recon is not None else None, P(self.e_ws), self.e_bytes, st))
+        # K4 classifies from the keys (4 bytes per element instead of 2L)
+        N.check(lib.nmk_encode_keyed_dev(P(self.keys), P(self.stats), self.width, P(base), P(cur), self.n_local,
+                                         self.elem0, self.n, self.dt, P(self.centers), P(self.cuts), P(self.model),
+                                         self.k_cap, self.bits, self.tol, self.epb, P(self.packed), self.stride,
+                                         P(self.exact), P(self.prefix), P(self.n_inc),
+                                         P(recon) if recon is not None else None, P(self.e_ws), self.e_bytes, st))
         mark("K4_encode")
         if self.comm is not None:
             # global positions of this rank's exact values / block prefixes;

@@ -1,0 +1,124 @@
+"""K4's keyed mode (classification from K1's f32 ratio keys, k_encode.cuh
+setup_keyed / classify_key) must give the exact path's bits: ratios planted
+at cuts, at c +- E and at bin edges, f32 round-trip rejections, magnitudes
+at the edges of the keys' safe range, and the keyed/unkeyed engines
+compared byte for byte (packed stream, exact values, prefix, recon)."""
+
+import numpy as np
+import pytest
+
+import nmk_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1703_02438_b200 import engine  # noqa: E402
+
+
+def _blocks(enc):
+    nlb = enc.prefix.numel()
+    packed = enc.packed[: nlb * enc.stride].cpu().numpy()
+    lens = enc.block_lengths()
+    return [packed[i * enc.stride: i * enc.stride + int(lens[i])].tobytes() for i in range(nlb)]
+
+
+def _run_all(b, c, E, bits, bb=1 << 16):
+    """oracle vs engine(keyed) vs engine(unkeyed) vs DevicePipeline (keyed)."""
+    o = O.encode(b, c, E, bits, bb)
+    dec = O.decode(o, b).tobytes()
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    outs = []
+    for keyed in (True, False):
+        rec = torch.full_like(cur, float("nan"))
+        enc = engine.encode(base, cur, E, bits, bb, recon=rec, keyed=keyed, ws=engine.Workspace())
+        assert enc.n_inc == o["n_inc"]
+        assert _blocks(enc) == o["blocks"], f"packed stream differs (keyed={keyed})"
+        assert enc.exact.cpu().numpy().tobytes() == o["exact"].tobytes()
+        assert enc.prefix.cpu().numpy().astype(np.uint64).tobytes() == o["prefix"].astype(np.uint64).tobytes()
+        assert rec.cpu().numpy().tobytes() == dec, f"fused reconstruction differs (keyed={keyed})"
+        outs.append(enc)
+    if bits is not None:
+        pipe = engine.DevicePipeline(base.numel(), base.dtype, E, bits, bb)
+        out = torch.empty_like(base)
+        pipe.step(base, cur, out)
+        chk = pipe.check()
+        if chk["status"] == 0:
+            enc = pipe.encoding()
+            assert _blocks(enc) == o["blocks"]
+            assert enc.exact.cpu().numpy().tobytes() == o["exact"].tobytes()
+            assert out.cpu().numpy().tobytes() == dec
+            rec = torch.full_like(cur, float("nan"))
+            pipe.encode(base, cur, recon=rec)
+            assert rec.cpu().numpy().tobytes() == dec
+    return o
+
+
+def _plant(rng, targets, n, dtype, lo=0.5, hi=2.0):
+    t = rng.choice(targets, n)
+    t = t + np.spacing(np.abs(t) + 1e-300) * rng.integers(-8, 9, n)
+    b = rng.uniform(lo, hi, n) * np.where(rng.uniform(size=n) < 0.3, -1.0, 1.0)
+    return b.astype(dtype), (b * (1.0 + t)).astype(dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("E,shift", [(1e-3, 0.0), (1e-4, 0.0), (2e-4, 1.5), (1e-5, -0.3)])
+def test_keyed_cuts_tolerance_and_bin_edges(dtype, E, shift):
+    rng = np.random.default_rng(41)
+    n = 150_000
+    b = rng.lognormal(0.0, 1.0, n)
+    c = b * (1.0 + shift + np.where(rng.uniform(size=n) < 0.8, rng.normal(0, 4 * E, n),
+                                    rng.uniform(-60 * E, 60 * E, n)))
+    b, c = b.astype(dtype), c.astype(dtype)
+    o = O.encode(b, c, E, 8, 1 << 16)
+    cen = o["centers"].astype(np.float64)
+    r, v = O.ratios_of(b, c)
+    gmin = float(r[v].min())
+    edges = gmin + np.arange(1, 200) * (2 * E)
+    targets = np.concatenate([0.5 * (cen[:-1] + cen[1:]), cen + E, cen - E, cen + E * (1 - 1e-9),
+                              cen - E * (1 + 1e-9), cen + E * (1 - 3e-8), edges])
+    pb, px = _plant(rng, targets, n, dtype)
+    _run_all(np.concatenate([b, pb]), np.concatenate([c, px]), E, 8)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e3, 3e5])
+def test_keyed_f32_roundtrip_rejections(scale):
+    """f32 values where T((1+c)b) misses by a rounding: the filter must reject
+    exactly the oracle's elements (pipeline.py:143-160)."""
+    rng = np.random.default_rng(42)
+    n = 200_000
+    E = 2e-6
+    b = (rng.uniform(0.5, 2.0, n) * scale).astype(np.float32)
+    c = (b.astype(np.float64) * (1.0 + rng.normal(0, 3 * E, n))).astype(np.float32)
+    o = _run_all(b, c, E, 10, 1 << 15)
+    assert o["n_inc"] > 0
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_keyed_safe_range_edges(dtype):
+    """Bases and currents straddling the keys' safe range (2^-900..2^901 for
+    f64, 2^-100..2^101 for f32) and b = x = 0 pairs."""
+    rng = np.random.default_rng(43)
+    lo, hi = (-900, 901) if dtype == np.float64 else (-100, 101)
+    n = 60_000
+    e = rng.choice(np.r_[lo - 3:lo + 4, hi - 4:hi + 3, -2:3], n)
+    b = np.ldexp(rng.uniform(1.0, 2.0, n), e) * np.where(rng.uniform(size=n) < 0.5, -1, 1)
+    c = b * (1.0 + np.where(rng.uniform(size=n) < 0.5, rng.normal(0, 0.002, n), rng.uniform(-0.04, 0.04, n)))
+    z = rng.uniform(size=n) < 0.01
+    b[z] = 0.0
+    c[z] = 0.0
+    with np.errstate(over="ignore"):
+        b, c = b.astype(dtype), c.astype(dtype)
+    _run_all(b, c, 1e-3, 8, 1 << 14)
+
+
+def test_keyed_all_invalid_and_tiny():
+    rng = np.random.default_rng(44)
+    b = np.zeros(5000)
+    c = rng.uniform(1, 2, 5000)
+    _run_all(b, c, 1e-3, 4, 4096)            # no valid ratio: degenerate model
+    for n in (1, 7, 300, 1025):
+        b = rng.lognormal(0, 1, n)
+        c = b * (1 + rng.normal(0, 0.002, n))
+        _run_all(b, c, 1e-3, 8, 4096)

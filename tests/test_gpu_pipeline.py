@@ -63,7 +63,7 @@ def test_pipeline_matches_general_path(case, graph):
     base = torch.from_numpy(b).cuda()
     cur = torch.from_numpy(c).cuda()
     rec_general = torch.full_like(cur, float("nan"))
-    ref = engine.encode(base, cur, E, bits, bb, recon=rec_general)
+    ref = engine.encode(base, cur, E, bits, bb, recon=rec_general, keyed=False)   # snapshot-reading K2/K4
     ref_blocks, ref_exact = _host_blocks(ref), ref.exact.cpu().numpy().copy()
     ref_prefix = ref.prefix.cpu().numpy().copy()
     ref_out = engine.decode_encoding(ref, base).out.cpu().numpy()
