@@ -542,6 +542,52 @@ __device__ __noinline__ uint32_t key_ordinal_slow(float key, const T* __restrict
   return q < (double)nbins ? (uint32_t)q : nbins;   // nbins = tripwire
 }
 
+// Hot-bin test in f32 without the magic rounding: th = RN32(key*iw32 + c32)
+// with the origin moved to the bin of r = 0 (q_ref), c32 = RN32(c'),
+// c' = -gmin/w - 1/2 - q_ref, estimates t* - 1/2 - q_ref (t* = the
+// reference's RN(RN(r - gmin)/w)) within
+//   e(th, key) = |th| 2^-24 + |key| iw 2^-22 + |c'| 2^-24 + |t*| 2^-52.
+// For hot bin h the test |th - (h - q_ref)| < hi_h, with e bounded over bin
+// h (|th| <= |h - q_ref| + 1/2, |key| <= max |r| over the bin, + slack),
+// proves floor(t*) = h.  The difference th - (h - q_ref) is exact when below
+// 1/2 (Sterbenz) and rounds monotonically otherwise.
+struct HotGrid {
+  double gmin, w, iw, qref, cabs, G;
+  float iw32, c32;
+};
+
+__device__ __forceinline__ HotGrid hot_grid(double gmin, double width, double inv_w) {
+  HotGrid g;
+  g.gmin = gmin;
+  g.w = width;
+  g.iw = inv_w;
+  g.G = fabs(gmin) * inv_w;
+  const double cd = -gmin * inv_w - 0.5;
+  g.qref = rint(cd);
+  const double cp = cd - g.qref;   // exact (Sterbenz)
+  g.cabs = fabs(cp);
+  g.iw32 = __double2float_rn(inv_w);
+  g.c32 = __double2float_rn(cp);
+  return g;
+}
+
+// (h - q_ref as f32, threshold); threshold -1 never matches
+__device__ __forceinline__ void hot_params(uint32_t h, uint32_t nbins, const HotGrid& g, float& hc, float& hi) {
+  hc = 0.0f;
+  hi = -1.0f;
+  if (h >= nbins || !(g.G < 0x1p+30) || !(g.iw < 0x1p+100)) return;
+  const double hcd = (double)h - g.qref;
+  if (fabs(hcd) >= 0x1p+22) return;
+  const double rlo = g.gmin + (double)h * g.w, rhi = g.gmin + ((double)h + 1.0) * g.w;
+  const double K = fmax(fabs(rlo), fabs(rhi)) * (1.0 + 0x1p-20) + g.w * 0x1p-10;
+  const double e = (fabs(hcd) + 0.5) * (0x1p-24 + 0x1p-52) * (1.0 + 0x1p-20) + K * g.iw * 0x1p-22 +
+                   g.cabs * 0x1p-24 + g.G * 0x1p-50 + 0x1p-40;
+  const double t = 0.5 - e - 0x1p-24;
+  if (!(K < 0x1p+100) || !(t > 0.25)) return;
+  hc = (float)hcd;   // exact
+  hi = __double2float_rz(t);
+}
+
 template <typename T>
 __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, const T* __restrict__ base,
                                               const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
@@ -551,7 +597,18 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
   const int lane = threadIdx.x & 31;
   const double et_c = key_bound(gmin, gmax, inv_w);
   const KeyGrid32 g32 = key_grid32(gmin, gmax, inv_w, nbins);
+  const HotGrid hg = hot_grid(gmin, width, inv_w);
+  const unsigned long long iw2 = ((unsigned long long)__float_as_uint(hg.iw32) << 32) | __float_as_uint(hg.iw32);
+  const unsigned long long c2c = ((unsigned long long)__float_as_uint(hg.c32) << 32) | __float_as_uint(hg.c32);
   uint32_t hot1 = kNoBin - 1, hot2 = kNoBin - 2;   // never real ordinals
+  float h1c = 0.f, h2c = 0.f, hi1 = -1.f, hi2 = -1.f;
+  unsigned long long n1c2 = 0, n2c2 = 0;            // (-h1c, -h1c), (-h2c, -h2c) as f32x2
+  auto set_hot = [&]() {
+    hot_params(hot1, nbins, hg, h1c, hi1);
+    hot_params(hot2, nbins, hg, h2c, hi2);
+    n1c2 = ((unsigned long long)__float_as_uint(-h1c) << 32) | __float_as_uint(-h1c);
+    n2c2 = ((unsigned long long)__float_as_uint(-h2c) << 32) | __float_as_uint(-h2c);
+  };
   uint32_t c1 = 0, c2 = 0, miss = 0, last_miss = kNoBin;
   // full ordinal of one key (f32 -> f64 key -> exact pair)
   auto ord = [&](float key, uint64_t j) -> uint32_t {
@@ -576,6 +633,20 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     const uint32_t tot = __reduce_add_sync(FULL, c);
     if (lane == 0 && tot && hot <= nbins) atomicAdd(&my[hot], tot);
   };
+  // two keys against the hot pair: predicated counts, defer bits for the rest
+  auto hot2keys = [&](float ka, float kb, int e, uint32_t& defer) {
+    const unsigned long long k2 = ((unsigned long long)__float_as_uint(kb) << 32) | __float_as_uint(ka);
+    unsigned long long th, a, b;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(th) : "l"(k2), "l"(iw2), "l"(c2c));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a) : "l"(th), "l"(n1c2));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(b) : "l"(th), "l"(n2c2));
+    const bool a0 = fabsf(__uint_as_float((uint32_t)a)) < hi1, a1 = fabsf(__uint_as_float((uint32_t)(a >> 32))) < hi1;
+    const bool b0 = fabsf(__uint_as_float((uint32_t)b)) < hi2, b1 = fabsf(__uint_as_float((uint32_t)(b >> 32))) < hi2;
+    c1 += (a0 ? 1u : 0u) + (a1 ? 1u : 0u);
+    c2 += (b0 ? 1u : 0u) + (b1 ? 1u : 0u);
+    defer |= ((a0 || b0) ? 0u : 1u) << e;
+    defer |= ((a1 || b1) ? 0u : 2u) << e;
+  };
   const uint64_t ntiles = n / kKeyTile;
   const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -597,21 +668,12 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     const int st = (int)(kk % kKeyStages);
     mbar_wait(&bars[st], (unsigned)((kk / kKeyStages) & 1));
     const float* sk = stage + st * kKeyTile;
-    float kv[kKeyPerLane];
+    uint32_t defer = 0;
 #pragma unroll
     for (int u = 0; u < kKeyPerLane / 4; ++u) {
       const float4 w = reinterpret_cast<const float4*>(sk)[u * 32 + lane];
-      kv[4 * u] = w.x; kv[4 * u + 1] = w.y; kv[4 * u + 2] = w.z; kv[4 * u + 3] = w.w;
-    }
-    uint32_t defer = 0;
-#pragma unroll
-    for (int e = 0; e < kKeyPerLane; ++e) {
-      uint32_t qi;
-      const bool ok = key_ordinal32(kv[e], g32, qi);
-      const bool h1 = ok && qi == hot1, h2 = ok && qi == hot2;
-      c1 += h1 ? 1u : 0u;
-      c2 += h2 ? 1u : 0u;
-      defer |= (h1 || h2) ? 0u : (1u << e);
+      hot2keys(w.x, w.y, 4 * u, defer);
+      hot2keys(w.z, w.w, 4 * u + 2, defer);
     }
     while (defer) {   // this lane's non-hit keys, re-read from the stage
       const int e = __ffs(defer) - 1;
@@ -630,6 +692,7 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
           c2 = c1;
           hot1 = cand;
           c1 = 0;
+          set_hot();
         }
       }
     }

@@ -122,3 +122,43 @@ def test_keyed_all_invalid_and_tiny():
         b = rng.lognormal(0, 1, n)
         c = b * (1 + rng.normal(0, 0.002, n))
         _run_all(b, c, 1e-3, 8, 4096)
+
+
+def _dense_counts(pipe, nbins):
+    return pipe.counts[: nbins + 1].cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("E,shift,sigma", [(1e-3, 0.0, 3e-4), (1e-3, 2e-4, 2e-4), (1e-4, 0.0, 1e-4),
+                                           (5e-3, 0.7, 1e-3)])
+def test_keyed_histogram_hot_bins_exact(dtype, E, shift, sigma):
+    """K2's hot-bin f32 test (k_hist.cu hot_params) against the oracle's
+    np.unique histogram: a dominant narrow bin whose edge sits near the bulk
+    of the ratios, planted ratios within a few ulps of its edges, outliers."""
+    rng = np.random.default_rng(45)
+    n = 400_000
+    b = rng.uniform(0.5, 2.0, n) * np.where(rng.uniform(size=n) < 0.3, -1.0, 1.0)
+    r = shift + rng.normal(0, sigma, n)
+    out = rng.uniform(size=n) < 0.03
+    r[out] = rng.laplace(0, 0.1, out.sum())
+    c = b * (1.0 + r)
+    b, c = b.astype(dtype), c.astype(dtype)
+    rr, v = O.ratios_of(b, c)
+    gmin = float(rr[v].min())
+    e0 = gmin + np.floor((shift - gmin) / (2 * E)) * (2 * E)      # edges around the bulk
+    edges = e0 + np.arange(-3, 4) * (2 * E)
+    pb, px = _plant(rng, edges, 100_000, dtype)
+    base = np.concatenate([b, pb]).astype(dtype)
+    cur = np.concatenate([c, px]).astype(dtype)
+    bt, ct = torch.from_numpy(base).cuda(), torch.from_numpy(cur).cuda()
+    pipe = engine.DevicePipeline(bt.numel(), bt.dtype, E, 10, 1 << 16)
+    out_t = torch.empty_like(bt)
+    pipe.step(bt, ct, out_t)
+    chk = pipe.check()
+    assert chk["status"] == 0 and chk["tripwire"] == 0
+    rr, v = O.ratios_of(base, cur)
+    keys, counts = O.histogram(rr[v], chk["gmin"], 2 * E)
+    dense = np.zeros(chk["nbins"], dtype=np.int64)
+    dense[keys.astype(np.int64)] = counts
+    got = _dense_counts(pipe, chk["nbins"])
+    np.testing.assert_array_equal(got[: chk["nbins"]], dense)
