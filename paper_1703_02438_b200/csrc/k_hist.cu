@@ -609,7 +609,10 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     n1c2 = ((unsigned long long)__float_as_uint(-h1c) << 32) | __float_as_uint(-h1c);
     n2c2 = ((unsigned long long)__float_as_uint(-h2c) << 32) | __float_as_uint(-h2c);
   };
-  uint32_t c1 = 0, c2 = 0, miss = 0, last_miss = kNoBin;
+  uint32_t c2 = 0, miss = 0, last_miss = kNoBin;
+  // hot-pair counts: c2 = hot2 hits of the f32 test; hot1 hits are derived,
+  // c1 = tested - ndef - c2 + c1x; c1x / c2x: deferred keys resolving to hot1 / hot2
+  uint32_t tested = 0, ndef = 0, c1x = 0, c2x = 0;
   // full ordinal of one key (f32 -> f64 key -> exact pair)
   auto ord = [&](float key, uint64_t j) -> uint32_t {
     uint32_t qi;
@@ -620,9 +623,9 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
   };
   auto visit = [&](uint32_t qi) {
     if (qi == hot1) {
-      ++c1;
+      ++c1x;
     } else if (qi == hot2) {
-      ++c2;
+      ++c2x;
     } else if (qi != kNoBin) {
       atomicAdd(&my[qi], 1u);   // qi <= nbins
       ++miss;
@@ -633,19 +636,32 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     const uint32_t tot = __reduce_add_sync(FULL, c);
     if (lane == 0 && tot && hot <= nbins) atomicAdd(&my[hot], tot);
   };
-  // two keys against the hot pair: predicated counts, defer bits for the rest
+  // two keys against the hot pair.  Per key: a hot2 hit is counted, a key in
+  // neither hot bin sets its defer bit; hot1 hits are not counted one by one
+  // but derived at flush time: c1 = tested - deferred - c2 + c1x (c1x: deferred
+  // keys whose full ordinal turned out to be hot1).
   auto hot2keys = [&](float ka, float kb, int e, uint32_t& defer) {
     const unsigned long long k2 = ((unsigned long long)__float_as_uint(kb) << 32) | __float_as_uint(ka);
     unsigned long long th, a, b;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(th) : "l"(k2), "l"(iw2), "l"(c2c));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a) : "l"(th), "l"(n1c2));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(b) : "l"(th), "l"(n2c2));
-    const bool a0 = fabsf(__uint_as_float((uint32_t)a)) < hi1, a1 = fabsf(__uint_as_float((uint32_t)(a >> 32))) < hi1;
-    const bool b0 = fabsf(__uint_as_float((uint32_t)b)) < hi2, b1 = fabsf(__uint_as_float((uint32_t)(b >> 32))) < hi2;
-    c1 += (a0 ? 1u : 0u) + (a1 ? 1u : 0u);
-    c2 += (b0 ? 1u : 0u) + (b1 ? 1u : 0u);
-    defer |= ((a0 || b0) ? 0u : 1u) << e;
-    defer |= ((a1 || b1) ? 0u : 2u) << e;
+    asm("{\n\t.reg .pred p1, p2, q1, q2;\n\t"
+        "setp.lt.f32 p1, %3, %5;\n\t"       // key a in hot2
+        "setp.lt.f32 q1, %2, %4;\n\t"       // key a in hot1
+        "or.pred q1, q1, p1;\n\t"
+        "@p1 add.u32 %0, %0, 1;\n\t"
+        "@!q1 or.b32 %1, %1, %8;\n\t"
+        "setp.lt.f32 p2, %7, %5;\n\t"       // key b in hot2
+        "setp.lt.f32 q2, %6, %4;\n\t"       // key b in hot1
+        "or.pred q2, q2, p2;\n\t"
+        "@p2 add.u32 %0, %0, 1;\n\t"
+        "@!q2 or.b32 %1, %1, %9;\n\t"
+        "}"
+        : "+r"(c2), "+r"(defer)
+        : "f"(fabsf(__uint_as_float((uint32_t)a))), "f"(fabsf(__uint_as_float((uint32_t)b))), "f"(hi1), "f"(hi2),
+          "f"(fabsf(__uint_as_float((uint32_t)(a >> 32)))), "f"(fabsf(__uint_as_float((uint32_t)(b >> 32)))),
+          "r"(1u << e), "r"(2u << e));
   };
   const uint64_t ntiles = n / kKeyTile;
   const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -675,6 +691,8 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
       hot2keys(w.x, w.y, 4 * u, defer);
       hot2keys(w.z, w.w, 4 * u + 2, defer);
     }
+    tested += kKeyPerLane;
+    ndef += __popc(defer);
     while (defer) {   // this lane's non-hit keys, re-read from the stage
       const int e = __ffs(defer) - 1;
       defer &= defer - 1;
@@ -687,11 +705,11 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
       if (have) {
         const uint32_t cand = __shfl_sync(FULL, last_miss, __ffs(have) - 1);
         if (cand != hot1 && cand != hot2) {
-          flush(hot2, c2);
+          flush(hot1, tested - ndef - c2 + c1x);
+          flush(hot2, c2 + c2x);
           hot2 = hot1;
-          c2 = c1;
           hot1 = cand;
-          c1 = 0;
+          tested = ndef = c1x = c2x = c2 = 0;
           set_hot();
         }
       }
@@ -706,8 +724,8 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
   }
   // tail: the last n % kKeyTile keys, one element per lane per round
   for (uint64_t j = ntiles * kKeyTile + wg * 32 + lane; j < n; j += nw * 32) visit(ord(keys[j], j));
-  flush(hot1, c1);
-  flush(hot2, c2);
+  flush(hot1, tested - ndef - c2 + c1x);
+  flush(hot2, c2 + c2x);
 }
 
 template <typename T>
