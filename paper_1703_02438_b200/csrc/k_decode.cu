@@ -162,9 +162,10 @@ k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __rest
   }
 }
 
-// Byte-aligned code widths (B = 8, 16): one thread per chunk, 16-byte loads
-// and SIMD compares (a sentinel is an all-ones byte / halfword), so each
-// thread keeps the chunk's 32*B bytes in flight instead of B per lane.
+// Byte-aligned code widths (B = 8, 16): a half-warp per chunk, 16-byte
+// coalesced loads (a warp reads two chunks' 2 x 32B bytes per instruction,
+// kDecPairs pairs in flight) and SIMD compares (a sentinel is an all-ones
+// byte / halfword), reduced over the half-warp.
 template <int B>
 __device__ __forceinline__ unsigned sentinels_in_word(uint32_t w) {
   if constexpr (B == 8) return __popc(__vcmpeq4(w, 0xffffffffu)) >> 3;
@@ -172,36 +173,63 @@ __device__ __forceinline__ unsigned sentinels_in_word(uint32_t w) {
 }
 
 template <int B>
+__device__ __forceinline__ unsigned sentinels_in_vec(const uint4& v) {
+  return sentinels_in_word<B>(v.x) + sentinels_in_word<B>(v.y) + sentinels_in_word<B>(v.z) +
+         sentinels_in_word<B>(v.w);
+}
+
+constexpr int kDecPairs = 4;   // chunk pairs per warp iteration
+
+template <int B>
 __global__ void __launch_bounds__(kDecThreads)
 k_dec_count_wide(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
   static_assert(B == 8 || B == 16, "byte-aligned codes only");
+  constexpr int kPer = (32 * B / 16) / 16;   // 16-byte vectors per lane per chunk (1 or 2)
+  const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
   const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
-  const uint32_t nthr = gridDim.x * blockDim.x;
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += nthr) {
-    const DChunk d = dchunk<B>(geo, g0 + c);
-    const uint8_t* src = chunk_src<B>(packed, geo, d);   // 16-byte aligned
-    const uint32_t nvec = d.nbytes / 16;
-    const uint4* v4 = reinterpret_cast<const uint4*>(src);
-    unsigned n = 0;
-    if (nvec == 2 * B) {   // full chunk
-#pragma unroll 8
-      for (uint32_t i = 0; i < 2 * B; ++i) {
-        const uint4 v = __ldg(v4 + i);
-        n += sentinels_in_word<B>(v.x) + sentinels_in_word<B>(v.y) + sentinels_in_word<B>(v.z) +
-             sentinels_in_word<B>(v.w);
-      }
-    } else {
-      for (uint32_t i = 0; i < nvec; ++i) {
-        const uint4 v = __ldg(v4 + i);
-        n += sentinels_in_word<B>(v.x) + sentinels_in_word<B>(v.y) + sentinels_in_word<B>(v.z) +
-             sentinels_in_word<B>(v.w);
-      }
-      for (uint32_t i = nvec * 16; i < d.nbytes; i += B / 8) {
-        if constexpr (B == 8) n += src[i] == 0xff;
-        else n += (src[i] & src[i + 1]) == 0xff;
+  const uint32_t nch = (uint32_t)geo.nchunks;
+  const uint32_t nwarps = gridDim.x * (kDecThreads / 32);
+  const uint32_t step = nwarps * 2 * kDecPairs;
+  for (uint32_t c0 = (blockIdx.x * (kDecThreads / 32) + (threadIdx.x >> 5)) * 2 * kDecPairs; c0 < nch; c0 += step) {
+    uint4 w[kDecPairs][kPer];
+    uint32_t nb[kDecPairs];
+#pragma unroll
+    for (int u = 0; u < kDecPairs; ++u) {
+      const uint32_t c = c0 + 2 * u + half;
+      nb[u] = 0;
+      if (c < nch) {
+        const DChunk d = dchunk<B>(geo, g0 + c);
+        const uint4* v4 = reinterpret_cast<const uint4*>(chunk_src<B>(packed, geo, d));   // 16-byte aligned
+        nb[u] = d.nbytes;
+#pragma unroll
+        for (int p = 0; p < kPer; ++p) {
+          const uint32_t o = (uint32_t)(sub + 16 * p) * 16;
+          w[u][p] = o + 16 <= d.nbytes ? __ldg(v4 + sub + 16 * p) : make_uint4(0, 0, 0, 0);
+        }
       }
     }
-    counts[c] = n;
+#pragma unroll
+    for (int u = 0; u < kDecPairs; ++u) {
+      const uint32_t c = c0 + 2 * u + half;
+      unsigned n = 0;
+#pragma unroll
+      for (int p = 0; p < kPer; ++p) {
+        const uint32_t o = (uint32_t)(sub + 16 * p) * 16;
+        if (o + 16 <= nb[u]) {
+          n += sentinels_in_vec<B>(w[u][p]);
+        } else if (o < nb[u]) {   // the block's last, clipped vector
+          const DChunk d = dchunk<B>(geo, g0 + c);
+          const uint8_t* src = chunk_src<B>(packed, geo, d);
+          for (uint32_t i = o; i < nb[u]; i += B / 8) {
+            if constexpr (B == 8) n += src[i] == 0xff;
+            else n += (src[i] & src[i + 1]) == 0xff;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);   // within the half-warp
+      if (sub == 0 && c < nch) counts[c] = n;
+    }
   }
 }
 
@@ -679,7 +707,8 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
                           const nmk_model* model, const unsigned long long* n_exact_dev, cudaStream_t s) {
   const int sms = sm_count_d();
   if constexpr (B == 8 || B == 16) {
-    const uint64_t g1 = (geo.nchunks + kDecThreads - 1) / kDecThreads;
+    const uint64_t per_cta = (uint64_t)(kDecThreads / 32) * 2 * kDecPairs;
+    const uint64_t g1 = (geo.nchunks + per_cta - 1) / per_cta;
     const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
     k_dec_count_wide<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   } else {

@@ -630,13 +630,13 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
 // the fused reconstruction's base values.  Each warp keeps the keys of
 // kKeyStagesE chunks in flight (TMA ring in shared memory).
 #ifndef NMK_ENCK_STAGES
-#define NMK_ENCK_STAGES 4
+#define NMK_ENCK_STAGES 2   // stages of two chunks' keys (2 KB) per warp
 #endif
 constexpr int kKeyStagesE = NMK_ENCK_STAGES;
 // dynamic shared memory of k_encode_keyed: opc doubles, then 128-byte aligned key tiles
 __host__ __device__ constexpr size_t keyed_ring_off(int k_cap) { return ((size_t)(k_cap + 2) + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t keyed_smem_bytes(int k_cap) {
-  return keyed_ring_off(k_cap) * 8 + (size_t)(kEncThreads / 32) * kKeyStagesE * kChunk * 4;
+  return keyed_ring_off(k_cap) * 8 + (size_t)(kEncThreads / 32) * kKeyStagesE * 2 * kChunk * 4;
 }
 template <typename T, int B, bool kRecon, typename Slow, typename Rec>
 __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ keys, const T* __restrict__ base,
@@ -787,9 +787,11 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       chunk_pack<B>(geo, k.b, k.ci, blk_start, blk_end, code, my, packed);
     }
   };
-  // per-warp ring of kKeyStagesE chunk key tiles (1 KB each) filled by TMA
-  // bulk copies; chunks that are not whole read their keys directly in run()
-  float* ring = kring + (size_t)wid * kKeyStagesE * kChunk;
+  // per-warp ring of kKeyStagesE tiles, each the keys of two consecutive
+  // chunks (2 KB), filled by TMA bulk copies.  A pair is staged when both
+  // chunks are fast and in the same block; other chunks go one at a time
+  // with their keys read directly.
+  float* ring = kring + (size_t)wid * kKeyStagesE * 2 * kChunk;
   unsigned long long* bars = kbars + wid * kKeyStagesE;
   if (lane == 0) {
     for (int st = 0; st < kKeyStagesE; ++st) mbar_init(&bars[st], 1);
@@ -797,33 +799,55 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   }
   __syncwarp();
   if (cA >= cB) return;
+  auto pair_of = [&](const Cur& k) {   // warp-uniform
+    return k.c + 1 < cB && k.c + 1 <= geo.c_last && k.ci + 1 < cpb_whole && fast_of(k);
+  };
   Cur cp = at(cA), pf = cp;
-  auto issue = [&](int st) {   // warp-uniform; lane 0 issues the copy of chunk pf
-    if (pf.c < cB && fast_of(pf) && lane == 0) {
+  auto issue = [&](int st) {   // warp-uniform; lane 0 issues the copy of pair pf
+    if (pf.c >= cB) return;
+    const bool pr = pair_of(pf);
+    if (pr && lane == 0) {
       fence_proxy_async_smem();
-      mbar_arrive_tx(&bars[st], kChunk * 4);
-      tma_load_1d(ring + st * kChunk, keys + (pf.lo - geo.elem0), kChunk * 4, &bars[st]);
+      mbar_arrive_tx(&bars[st], 2 * kChunk * 4);
+      tma_load_1d(ring + st * 2 * kChunk, keys + (pf.lo - geo.elem0), 2 * kChunk * 4, &bars[st]);
     }
     next(pf);
+    if (pr) next(pf);
   };
 #pragma unroll
   for (int st = 0; st < kKeyStagesE; ++st) issue(st);
   uint32_t ph = 0;   // per-stage mbarrier phase bits
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   int st = 0;
-  for (; cp.c < cB; next(cp)) {
-    const bool fast = fast_of(cp);
-    float4 k0 = z4, k1 = z4;
-    if (fast) {
+  while (cp.c < cB) {
+    const bool pr = pair_of(cp);
+    float4 a0 = z4, a1 = z4, b0 = z4, b1 = z4;
+    if (pr) {
       mbar_wait(&bars[st], (ph >> st) & 1u);
       ph ^= 1u << st;
-      const float4* src = reinterpret_cast<const float4*>(ring + st * kChunk) + lane * 2;
-      k0 = src[0];
-      k1 = src[1];
+      const float4* src = reinterpret_cast<const float4*>(ring + st * 2 * kChunk) + lane * 2;
+      a0 = src[0];
+      a1 = src[1];
+      b0 = src[64];
+      b1 = src[65];
     }
     __syncwarp();
     issue(st);   // refill the stage just read
-    run(cp, fast, k0, k1);
+    if (pr) {
+      run(cp, true, a0, a1);
+      next(cp);
+      run(cp, true, b0, b1);
+      next(cp);
+    } else {
+      const bool fast = fast_of(cp);
+      if (fast) {
+        const float4* src = reinterpret_cast<const float4*>(keys + (cp.lo - geo.elem0)) + lane * 2;
+        a0 = __ldg(src);
+        a1 = __ldg(src + 1);
+      }
+      run(cp, fast, a0, a1);
+      next(cp);
+    }
     st = st + 1 == kKeyStagesE ? 0 : st + 1;
   }
 }

@@ -4,44 +4,140 @@
 // compacted exact-value list and the per-block prefix table, pipeline.py:257-
 // 276) and by K5 (sentinel counts per chunk -> rank of every sentinel in the
 // exact list, codec.py:231-236).  One single-pass decoupled look-back scan
-// (CUB) over n + 1 items, the last one reading as 0, so offsets[n] is the
-// total: 4 bytes read and 8 written per 256 elements, no second pass.
-#include <cub/device/device_scan.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
-
+// over n + 1 items (the last one reads as 0, so offsets[n] is the total):
+// 4 bytes read and 8 written per 256 elements.  Tiles of 8192 items go to
+// CTAs in blockIdx order; each CTA publishes its tile aggregate, then looks
+// back over its predecessors' (flag, value) words until it meets an
+// inclusive prefix.  The tile-status words are zeroed by a memset node in
+// front of the kernel, so no state survives between launches.
 #include "nmk_common.cuh"
 #include "nmk_scan.cuh"
 
 namespace nmk {
 
-struct CountAt {
-  const uint32_t* counts;
-  uint64_t n;
-  __host__ __device__ unsigned long long operator()(uint64_t i) const {
-    return i < n ? (unsigned long long)counts[i] : 0ULL;
-  }
-};
+constexpr int kScanThreads = 256;
+constexpr int kScanRounds = 8;                                    // uint4 per lane
+constexpr int kScanWarpItems = 32 * 4 * kScanRounds;              // 1024 contiguous counts per warp
+constexpr int kScanTile = (kScanThreads / 32) * kScanWarpItems;   // 8192 per CTA (few tiles: short look-back)
+constexpr unsigned long long kFlagAgg = 1ULL << 62;    // tile aggregate published
+constexpr unsigned long long kFlagPre = 2ULL << 62;    // inclusive prefix published
+constexpr unsigned long long kValMask = (1ULL << 62) - 1;
 
-using CountIter = thrust::transform_iterator<CountAt, thrust::counting_iterator<uint64_t>>;
-
-static size_t scan_temp_bytes(uint64_t n) {
-  size_t bytes = 0;
-  CountIter it(thrust::counting_iterator<uint64_t>(0), CountAt{nullptr, n});
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (unsigned long long*)nullptr, (int64_t)(n + 1));
-  return bytes;
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-size_t chunk_scan_ws_bytes(uint64_t n) { return scan_temp_bytes(n) + 256; }
+// Each warp owns 1024 contiguous items; in round q lane l holds items
+// w0 + 128 q + 4 l .. + 3 (coalesced 512-byte loads, 1 KB stores).
+__global__ void __launch_bounds__(kScanThreads)
+k_chunk_scan(const uint32_t* __restrict__ counts, uint64_t n, unsigned long long* __restrict__ offsets,
+             unsigned long long* __restrict__ status) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t tile = blockIdx.x;
+  const uint64_t w0 = tile * kScanTile + (uint64_t)wid * kScanWarpItems;
+  const bool vec = ((reinterpret_cast<uintptr_t>(counts) & 15) == 0);
+  uint4 v[kScanRounds];
+  uint32_t ex[kScanRounds];        // lane's exclusive offset inside the round
+  unsigned long long wsum = 0;     // warp running total (uniform)
+  unsigned long long rbase[kScanRounds];
+#pragma unroll
+  for (int q = 0; q < kScanRounds; ++q) {
+    const uint64_t i = w0 + (uint64_t)q * 128 + (uint64_t)lane * 4;
+    if (vec && i + 4 <= n) {
+      v[q] = __ldcs(reinterpret_cast<const uint4*>(counts + i));
+    } else {   // item n (and beyond) reads 0
+      v[q].x = i < n ? counts[i] : 0u;
+      v[q].y = i + 1 < n ? counts[i + 1] : 0u;
+      v[q].z = i + 2 < n ? counts[i + 2] : 0u;
+      v[q].w = i + 3 < n ? counts[i + 3] : 0u;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kScanRounds; ++q) {
+    const uint32_t sq = v[q].x + v[q].y + v[q].z + v[q].w;   // < 2^32: counts are <= 256 each
+    uint32_t incl = sq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    ex[q] = incl - sq;
+    rbase[q] = wsum;
+    wsum += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __shared__ unsigned long long s_warp[kScanThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  if (lane == 0) s_warp[wid] = wsum;
+  __syncthreads();
+  unsigned long long wbase = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    const unsigned long long x = s_warp[w];
+    wbase += w < wid ? x : 0ULL;
+    agg += x;
+  }
+  // look-back (warp 0): lane j inspects tile - 1 - j - 32 r
+  if (wid == 0) {
+    unsigned long long prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_status(status, kFlagPre | agg);
+    } else {
+      if (lane == 0) st_status(status + tile, kFlagAgg | agg);
+      int64_t base = (int64_t)tile - 1;
+      while (true) {
+        const int64_t t = base - lane;
+        unsigned long long s = t >= 0 ? ld_status(status + t) : kFlagPre;   // before tile 0: prefix 0
+        // wait until every inspected predecessor has published something
+        while (__any_sync(0xffffffffu, s == 0)) {
+          if (s == 0) s = ld_status(status + t);
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (s & kFlagPre) != 0);
+        const int stop = pre ? __ffs(pre) - 1 : 32;   // first (nearest) inclusive prefix
+        unsigned long long part = (lane <= stop && t >= 0) ? (s & kValMask) : 0ULL;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        prefix += part;
+        if (pre) break;
+        base -= 32;
+      }
+      if (lane == 0) st_status(status + tile, kFlagPre | (prefix + agg));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  const unsigned long long wstart = s_prefix + wbase;
+#pragma unroll
+  for (int q = 0; q < kScanRounds; ++q) {
+    const uint64_t i = w0 + (uint64_t)q * 128 + (uint64_t)lane * 4;
+    const unsigned long long o0 = wstart + rbase[q] + ex[q];
+    const unsigned long long o1 = o0 + v[q].x, o2 = o1 + v[q].y, o3 = o2 + v[q].z;
+    if (i + 4 <= n + 1) {   // offsets holds n + 1 entries
+      if ((i & 1) == 0) {
+        reinterpret_cast<ulonglong2*>(offsets + i)[0] = make_ulonglong2(o0, o1);
+        reinterpret_cast<ulonglong2*>(offsets + i)[1] = make_ulonglong2(o2, o3);
+      } else {
+        offsets[i] = o0; offsets[i + 1] = o1; offsets[i + 2] = o2; offsets[i + 3] = o3;
+      }
+    } else {
+      if (i <= n) offsets[i] = o0;
+      if (i + 1 <= n) offsets[i + 1] = o1;
+      if (i + 2 <= n) offsets[i + 2] = o2;
+    }
+  }
+}
+
+size_t chunk_scan_ws_bytes(uint64_t n) { return ((n + 1 + kScanTile - 1) / kScanTile) * 8 + 256; }
 
 void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets, void* ws, cudaStream_t s) {
-  if (n == 0) {
-    cudaMemsetAsync(offsets, 0, sizeof(unsigned long long), s);
-    return;
-  }
-  size_t bytes = scan_temp_bytes(n);
-  CountIter it(thrust::counting_iterator<uint64_t>(0), CountAt{counts, n});
-  cub::DeviceScan::ExclusiveSum(ws, bytes, it, offsets, (int64_t)(n + 1), s);
+  const uint64_t ntiles = (n + 1 + kScanTile - 1) / kScanTile;
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(ws);
+  cudaMemsetAsync(status, 0, ntiles * 8, s);
+  k_chunk_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(counts, n, offsets, status);
 }
 
 }  // namespace nmk
