@@ -36,9 +36,10 @@ BITS = 8
 SIDE = 512
 METRIC = "compress+decompress GB/s of input (n*L per timestep / (t_compress + t_decompress))"
 CONFIG_NAME = "cfg2: 512^3 fp64 8^3-block field, E=1e-3, B=8, top-k, 1 MiB index blocks"
-# k_minmax, k_hist_prep, k_hist_dev, k_select, k_encode, k_scan_{reduce,top,apply},
-# k_enc_finalize, k_dec_count, k_scan_{reduce,top,apply}, k_dec_chunks
-GPU_LAUNCHES_PER_STEP = 12   # K1, prep, K2, K3, K4, scan x2, finalize | count, scan x2, K5 (ncu launch list)
+# k_minmax, k_hist_prep, k_hist_dev, k_select, k_encode_keyed, k_encode (exits when the
+# keyed kernel did the work), k_chunk_scan, k_enc_finalize, k_dec_count_wide, k_chunk_scan,
+# k_dec_chunks
+GPU_LAUNCHES_PER_STEP = 11   # K1, prep, K2, K3, K4 keyed + fallback, scan, finalize | count, scan, K5 (ncu launch list)
 
 
 def parse():
@@ -271,14 +272,18 @@ def main():
 
     # roofline arithmetic per phase.  alg = SURVEY.md 8(d) algorithmic bytes
     # (the reference's three-pass schedule); moved = what this design reads
-    # and writes (K1 also writes 4-byte ratio keys so K2 reads 4 B instead of
-    # 2L; K5 adds the B/8 sentinel-count pass).
+    # and writes: K1 also writes 4-byte ratio keys, so K2 and K4 read 4 B per
+    # element instead of 2L (K4: + packed codes, the incompressible values
+    # gathered and written, chunk counts/offsets); K5 adds the B/8
+    # sentinel-count pass.
     n_inc, nb_local = chk["n_inc"], pipe.prefix.numel()
     pk = n_local * BITS / 8
+    nchunks = -(-n_local // 256)
     rf = {
         "K1_minmax": (2 * L * n_local, 2 * L * n_local + 4 * n_local, "k_minmax"),
         "K2_histogram": (2 * L * n_local, 4 * n_local, "k_hist_dev"),
-        "K4_encode": (2 * L * n_local + pk + n_inc * L + 8 * nb_local,) * 2 + ("k_encode",),
+        "K4_encode": (2 * L * n_local + pk + n_inc * L + 8 * nb_local,
+                      4 * n_local + pk + 2 * n_inc * L + 16 * nchunks + 8 * nb_local, "k_encode_keyed"),
         "K5_decode": (2 * L * n_local + pk + n_inc * L, 2 * L * n_local + 2 * pk + n_inc * L, "k_dec_chunks"),
     }
     peak, peak_src = peaks()

@@ -180,6 +180,8 @@ __device__ __forceinline__ unsigned sentinels_in_vec(const uint4& v) {
 
 constexpr int kDecPairs = 4;   // chunk pairs per warp iteration
 
+// Each warp counts a contiguous run of chunks; half-warp h takes chunks
+// cA + h, cA + h + 2, ... through a cursor advanced without division.
 template <int B>
 __global__ void __launch_bounds__(kDecThreads)
 k_dec_count_wide(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
@@ -189,28 +191,47 @@ k_dec_count_wide(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* _
   const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
   const uint32_t nch = (uint32_t)geo.nchunks;
   const uint32_t nwarps = gridDim.x * (kDecThreads / 32);
-  const uint32_t step = nwarps * 2 * kDecPairs;
-  for (uint32_t c0 = (blockIdx.x * (kDecThreads / 32) + (threadIdx.x >> 5)) * 2 * kDecPairs; c0 < nch; c0 += step) {
+  const uint32_t wg = blockIdx.x * (kDecThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t per = nch / nwarps, rem = nch % nwarps;
+  const uint32_t cA = wg * per + min(wg, rem), cB = cA + per + (wg < rem ? 1u : 0u);
+  if (cA >= cB) return;
+  const uint32_t cpb = geo.cpb;
+  // cursor of this half's next chunk
+  uint32_t c = cA + half;
+  const DChunk d0 = dchunk<B>(geo, g0 + min(c, nch - 1));
+  uint32_t b = d0.b, ci = d0.ci;
+  auto adv2 = [&]() {
+    c += 2;
+    ci += 2;
+    if (ci >= cpb) { ci -= cpb; ++b; }
+  };
+  while (__any_sync(0xffffffffu, c < cB)) {
     uint4 w[kDecPairs][kPer];
-    uint32_t nb[kDecPairs];
+    uint32_t cc[kDecPairs], nb[kDecPairs];
+    const uint8_t* src[kDecPairs];
 #pragma unroll
     for (int u = 0; u < kDecPairs; ++u) {
-      const uint32_t c = c0 + 2 * u + half;
+      cc[u] = c;
       nb[u] = 0;
-      if (c < nch) {
-        const DChunk d = dchunk<B>(geo, g0 + c);
-        const uint4* v4 = reinterpret_cast<const uint4*>(chunk_src<B>(packed, geo, d));   // 16-byte aligned
-        nb[u] = d.nbytes;
+      src[u] = packed + (uint64_t)(b - (uint32_t)geo.first_block) * geo.stride + (uint64_t)ci * (32 * B);
+      if (c < cB) {
+        // bytes of this chunk inside its block (all 32 B unless it is the block's clipped tail)
+        const uint64_t blk_start = (uint64_t)b * geo.epb;
+        const uint64_t rem_el = geo.n_total - blk_start;
+        const uint32_t blk_len = (uint32_t)(rem_el < geo.epb ? rem_el : geo.epb);
+        const uint32_t blk_bytes = (uint32_t)(((uint64_t)blk_len * B + 7) / 8);
+        nb[u] = min((uint32_t)(32 * B), blk_bytes - ci * (32 * B));
+        const uint4* v4 = reinterpret_cast<const uint4*>(src[u]);   // 16-byte aligned
 #pragma unroll
         for (int p = 0; p < kPer; ++p) {
           const uint32_t o = (uint32_t)(sub + 16 * p) * 16;
-          w[u][p] = o + 16 <= d.nbytes ? __ldg(v4 + sub + 16 * p) : make_uint4(0, 0, 0, 0);
+          w[u][p] = o + 16 <= nb[u] ? __ldg(v4 + sub + 16 * p) : make_uint4(0, 0, 0, 0);
         }
       }
+      adv2();
     }
 #pragma unroll
     for (int u = 0; u < kDecPairs; ++u) {
-      const uint32_t c = c0 + 2 * u + half;
       unsigned n = 0;
 #pragma unroll
       for (int p = 0; p < kPer; ++p) {
@@ -218,17 +239,15 @@ k_dec_count_wide(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* _
         if (o + 16 <= nb[u]) {
           n += sentinels_in_vec<B>(w[u][p]);
         } else if (o < nb[u]) {   // the block's last, clipped vector
-          const DChunk d = dchunk<B>(geo, g0 + c);
-          const uint8_t* src = chunk_src<B>(packed, geo, d);
           for (uint32_t i = o; i < nb[u]; i += B / 8) {
-            if constexpr (B == 8) n += src[i] == 0xff;
-            else n += (src[i] & src[i + 1]) == 0xff;
+            if constexpr (B == 8) n += src[u][i] == 0xff;
+            else n += (src[u][i] & src[u][i + 1]) == 0xff;
           }
         }
       }
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);   // within the half-warp
-      if (sub == 0 && c < nch) counts[c] = n;
+      if (sub == 0 && cc[u] < cB) counts[cc[u]] = n;
     }
   }
 }
@@ -709,7 +728,7 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   if constexpr (B == 8 || B == 16) {
     const uint64_t per_cta = (uint64_t)(kDecThreads / 32) * 2 * kDecPairs;
     const uint64_t g1 = (geo.nchunks + per_cta - 1) / per_cta;
-    const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
+    const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 4 ? g1 : (uint64_t)sms * 4);
     k_dec_count_wide<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   } else {
     const uint64_t g1 = (geo.nchunks + 7) / 8;
