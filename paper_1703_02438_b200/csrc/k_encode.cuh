@@ -462,11 +462,9 @@ __device__ __forceinline__ uint32_t classify_key(float key, const KeyedGrid& g) 
 
 // classify_key for two keys at once: the f32 arithmetic in f32x2 form
 // (FFMA2 / FADD2, each lane IEEE round-to-nearest like the scalar ops), the
-// bound test per key.
-// Returns the two table codes; `bad` collects keys outside the margin (NaN
-// included), which the caller re-decides.
-__device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGrid& g, uint32_t& ca, uint32_t& cb,
-                                              bool& bad) {
+// bound test per key.  Keys outside the margin (NaN included) give kKeySlow,
+// which the caller re-decides.
+__device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGrid& g, uint32_t& ca, uint32_t& cb) {
   constexpr unsigned long long kMagic2 = 0x4B4000004B400000ULL;   // (1.5 * 2^23, 1.5 * 2^23)
   const unsigned long long k2 = ((unsigned long long)__float_as_uint(kb) << 32) | __float_as_uint(ka);
   unsigned long long th, m, t, d;
@@ -476,14 +474,14 @@ __device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGri
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(th), "l"(t));
   const uint32_t ra = min((uint32_t)m - g.rowbase, g.span2 - 1u);
   const uint32_t rb = min((uint32_t)(m >> 32) - g.rowbase, g.span2 - 1u);
-  ca = lds_u32(g.tab_s + 4 * ra);
-  cb = lds_u32(g.tab_s + 4 * rb);
+  const uint32_t ta = lds_u32(g.tab_s + 4 * ra);
+  const uint32_t tb = lds_u32(g.tab_s + 4 * rb);
   const float sa = __fmaf_rn(fabsf(__uint_as_float((uint32_t)th)), 0x1p-23f,
                              __fmaf_rn(fabsf(ka), g.ka, fabsf(__uint_as_float((uint32_t)d))));
   const float sb = __fmaf_rn(fabsf(__uint_as_float((uint32_t)(th >> 32))), 0x1p-23f,
                              __fmaf_rn(fabsf(kb), g.ka, fabsf(__uint_as_float((uint32_t)(d >> 32)))));
-  bad |= !(sa < g.hi4);
-  bad |= !(sb < g.hi4);
+  ca = sa < g.hi4 ? ta : kKeySlow;
+  cb = sb < g.hi4 ? tb : kKeySlow;
 }
 
 // Second tier for keys the f32 test left undecided (near a bin edge by the
@@ -659,9 +657,12 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   const uint32_t per = nch / nwarps, rem = nch % nwarps;
   const uint32_t cA = wg * per + min(wg, rem);
   const uint32_t cB = cA + per + (wg < rem ? 1u : 0u);
-  // chunk cursor, advanced incrementally (no division in the loop)
+  const uint32_t cBf = min(cB, geo.c_last + 1u);   // whole chunks of this range end here
+  // chunk cursor, advanced incrementally (no division in the loop).  `left`
+  // counts the pairs still ahead in the current run of whole chunks (same
+  // block, keys aligned), so the common step is a few adds.
   struct Cur {
-    uint32_t c, b, ci;
+    uint32_t c, b, ci, left;
     uint64_t lo;   // first element of the chunk
   };
   auto at = [&](uint32_t c) {
@@ -671,9 +672,10 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     k.b = geo.fd_cpb.div(g);
     k.ci = g - k.b * cpb;
     k.lo = (uint64_t)k.b * geo.epb + (uint64_t)k.ci * kChunk;
+    k.left = 0;
     return k;
   };
-  auto next = [&](Cur& k) {
+  auto next = [&](Cur& k) {   // one chunk
     ++k.c;
     if (++k.ci == cpb) {
       k.ci = 0;
@@ -683,13 +685,106 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       k.lo += kChunk;
     }
   };
-  // warp-uniform: a whole chunk of this range, inside its block, key vectors aligned
-  // chunks [c_first, c_last] lie wholly inside this range (geo, host-computed)
+  auto next_pair = [&](Cur& k) {   // ci + 2 <= cpb_whole <= cpb
+    k.c += 2;
+    --k.left;
+    k.ci += 2;
+    k.lo += 2 * kChunk;
+    if (k.ci == cpb) {
+      k.ci = 0;
+      ++k.b;
+      k.lo = (uint64_t)k.b * geo.epb;
+    }
+  };
   const bool al_all = ptr_al && geo.key_al;
+  // warp-uniform: a whole chunk of this range, inside its block, key vectors aligned
   auto fast_of = [&](const Cur& k) {
     return k.c >= geo.c_first && k.c <= geo.c_last && k.ci < cpb_whole &&
            (al_all || (ptr_al && ((k.lo - geo.elem0) & 3) == 0));
   };
+  // warp-uniform: the current item is a pair of whole chunks (starts a run when needed)
+  auto pair_of = [&](Cur& k) {
+    if (k.left == 0 && k.c + 1 < cBf && k.ci + 1 < cpb_whole && fast_of(k))
+      k.left = min(cBf - k.c, cpb_whole - k.ci) >> 1;
+    return k.left != 0;
+  };
+  // the rare keys: NaN (invalid -> sentinel), the f64 key test, the exact path
+  auto redo = [&](uint32_t& code, int64_t j) {
+    const float key = __ldg(keys + j);
+    uint32_t v = key != key ? (sentinel | kIncFlag) : classify_key64(key, kg);
+    if (v == kKeySlow) {
+      v = slow(__ldg(base + j), __ldg(cur + j));
+      v |= v == sentinel ? kIncFlag : 0u;
+    }
+    code = v;
+  };
+  auto recon8 = [&](int64_t li, const uint32_t (&code)[kGroup]) {   // the decoder's values
+    T bv[kGroup];
+    load8<T>(base + li, bv);
+    using V = typename EVec<T>::V;
+#pragma unroll
+    for (int q = 0; q < kGroup / VN; ++q) {
+      V w;
+      T* t = reinterpret_cast<T*>(&w);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        const int ee = q * VN + e;
+        t[e] = code[ee] == sentinel ? __ldg(cur + li + ee) : rec_of(code[ee], bv[ee]);
+      }
+      reinterpret_cast<V*>(recon + li)[q] = w;
+    }
+  };
+  // a pair of whole chunks (16 keys per lane): one warp reduction decides
+  // whether anything but table codes occurred
+  auto run_pair = [&](const Cur& k, const float4& a0, const float4& a1, const float4& b0, const float4& b1) {
+    uint32_t ca[kGroup], cb[kGroup];
+    classify_key2(a0.x, a0.y, kg, ca[0], ca[1]);
+    classify_key2(a0.z, a0.w, kg, ca[2], ca[3]);
+    classify_key2(a1.x, a1.y, kg, ca[4], ca[5]);
+    classify_key2(a1.z, a1.w, kg, ca[6], ca[7]);
+    classify_key2(b0.x, b0.y, kg, cb[0], cb[1]);
+    classify_key2(b0.z, b0.w, kg, cb[2], cb[3]);
+    classify_key2(b1.x, b1.y, kg, cb[4], cb[5]);
+    classify_key2(b1.z, b1.w, kg, cb[6], cb[7]);
+    const int64_t li = (int64_t)(k.lo - geo.elem0) + lane * kGroup;   // chunk B: li + kChunk
+    uint32_t any = 0;
+#pragma unroll
+    for (int e = 0; e < kGroup; ++e) any |= ca[e] | cb[e];
+    const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kIncFlag));
+    uint32_t tot = 0;
+    if (flags) {
+      if (flags & kKeySlow) {
+        if (any & kKeySlow) {
+#pragma unroll
+          for (int e = 0; e < kGroup; ++e) {
+            if (ca[e] & kKeySlow) redo(ca[e], li + e);
+            if (cb[e] & kKeySlow) redo(cb[e], li + kChunk + e);
+          }
+        }
+      }
+      unsigned ma = 0, mb = 0;
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e) {
+        ma |= ((ca[e] >> 30) & 1u) << e;
+        mb |= ((cb[e] >> 30) & 1u) << e;
+        ca[e] &= ~kIncFlag;
+        cb[e] &= ~kIncFlag;
+      }
+      // both chunks' counts in one reduction (each <= 256)
+      tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(ma) | ((unsigned)__popc(mb) << 16));
+      masks[(uint64_t)k.c * 32 + lane] = (uint8_t)ma;
+      masks[(uint64_t)k.c * 32 + 32 + lane] = (uint8_t)mb;
+    }
+    if (lane < 2) counts[k.c + lane] = lane ? tot >> 16 : tot & 0xffffu;
+    if constexpr (kRecon) {
+      recon8(li, ca);
+      recon8(li + kChunk, cb);
+    }
+    uint8_t* dst = packed + (uint64_t)(k.b - geo.b0) * geo.stride + (uint64_t)k.ci * (32 * B) + lane * B;
+    pack8<B>(ca, dst);
+    pack8<B>(cb, dst + 32 * B);
+  };
+  // a single chunk: whole (keys given) or clipped by its block / this range
   auto run = [&](const Cur& k, bool fast, const float4& k0, const float4& k1) {
     uint32_t code[kGroup];
     unsigned live = 0xffu;
@@ -697,16 +792,10 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     const int64_t li = (int64_t)grp_lo - (int64_t)geo.elem0;
     uint64_t blk_start = 0, blk_end = 0;
     if (fast) {
-      bool bad = false;
-      classify_key2(k0.x, k0.y, kg, code[0], code[1], bad);
-      classify_key2(k0.z, k0.w, kg, code[2], code[3], bad);
-      classify_key2(k1.x, k1.y, kg, code[4], code[5], bad);
-      classify_key2(k1.z, k1.w, kg, code[6], code[7], bad);
-      if (__any_sync(0xffffffffu, bad) && bad) {   // mark this lane's undecided keys
-        const float kk[kGroup] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-#pragma unroll
-        for (int e = 0; e < kGroup; ++e) code[e] = classify_key(kk[e], kg);
-      }
+      classify_key2(k0.x, k0.y, kg, code[0], code[1]);
+      classify_key2(k0.z, k0.w, kg, code[2], code[3]);
+      classify_key2(k1.x, k1.y, kg, code[4], code[5]);
+      classify_key2(k1.z, k1.w, kg, code[6], code[7]);
     } else {
       blk_start = (uint64_t)k.b * geo.epb;
       blk_end = min(blk_start + geo.epb, geo.n_total);
@@ -724,29 +813,15 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) any |= code[e];
     const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kIncFlag));
-    if (flags & kKeySlow) {   // rare: NaN key, f64 key test, exact path
+    unsigned total = 0;
+    if (flags) {
       if (any & kKeySlow) {
 #pragma unroll
-        for (int e = 0; e < kGroup; ++e) {
-          if (code[e] & kKeySlow) {
-            const float key = __ldg(keys + li + e);
-            uint32_t v = key != key ? (sentinel | kIncFlag) : classify_key64(key, kg);
-            if (v == kKeySlow) {
-              v = slow(__ldg(base + li + e), __ldg(cur + li + e));
-              v |= v == sentinel ? kIncFlag : 0u;
-            }
-            code[e] = v;
-          }
-        }
+        for (int e = 0; e < kGroup; ++e)
+          if (code[e] & kKeySlow) redo(code[e], li + e);
       }
-      any = 0;
-#pragma unroll
-      for (int e = 0; e < kGroup; ++e) any |= code[e];
-    }
-    // incompressible elements: the chunk's count and its 256-bit position
-    // mask (one byte per lane); k_enc_finalize gathers the values from cur
-    unsigned total = 0;
-    if (__any_sync(0xffffffffu, any & kIncFlag)) {
+      // incompressible elements: the chunk's count and its 256-bit position
+      // mask (one byte per lane); k_enc_finalize gathers the values from cur
       unsigned inc_mask = 0;
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
@@ -758,22 +833,9 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       masks[(uint64_t)k.c * 32 + lane] = (uint8_t)inc_mask;
     }
     if (lane == 0) counts[k.c] = total;
-    if constexpr (kRecon) {   // the decoder's values
+    if constexpr (kRecon) {
       if (fast) {
-        T bv[kGroup];
-        load8<T>(base + li, bv);
-        using V = typename EVec<T>::V;
-#pragma unroll
-        for (int q = 0; q < kGroup / VN; ++q) {
-          V w;
-          T* t = reinterpret_cast<T*>(&w);
-#pragma unroll
-          for (int e = 0; e < VN; ++e) {
-            const int ee = q * VN + e;
-            t[e] = code[ee] == sentinel ? __ldg(cur + li + ee) : rec_of(code[ee], bv[ee]);
-          }
-          reinterpret_cast<V*>(recon + li)[q] = w;
-        }
+        recon8(li, code);
       } else {
 #pragma unroll
         for (int e = 0; e < kGroup; ++e)
@@ -789,7 +851,7 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   };
   // per-warp ring of kKeyStagesE tiles, each the keys of two consecutive
   // chunks (2 KB), filled by TMA bulk copies.  A pair is staged when both
-  // chunks are fast and in the same block; other chunks go one at a time
+  // chunks are whole and in the same block; other chunks go one at a time
   // with their keys read directly.
   float* ring = kring + (size_t)wid * kKeyStagesE * 2 * kChunk;
   unsigned long long* bars = kbars + wid * kKeyStagesE;
@@ -799,20 +861,19 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   }
   __syncwarp();
   if (cA >= cB) return;
-  auto pair_of = [&](const Cur& k) {   // warp-uniform
-    return k.c + 1 < cB && k.c + 1 <= geo.c_last && k.ci + 1 < cpb_whole && fast_of(k);
-  };
   Cur cp = at(cA), pf = cp;
-  auto issue = [&](int st) {   // warp-uniform; lane 0 issues the copy of pair pf
+  auto issue = [&](int st) {   // warp-uniform; lane 0 issues the copy of item pf
     if (pf.c >= cB) return;
-    const bool pr = pair_of(pf);
-    if (pr && lane == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_tx(&bars[st], 2 * kChunk * 4);
-      tma_load_1d(ring + st * 2 * kChunk, keys + (pf.lo - geo.elem0), 2 * kChunk * 4, &bars[st]);
+    if (pair_of(pf)) {
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_tx(&bars[st], 2 * kChunk * 4);
+        tma_load_1d(ring + st * 2 * kChunk, keys + (pf.lo - geo.elem0), 2 * kChunk * 4, &bars[st]);
+      }
+      next_pair(pf);
+    } else {
+      next(pf);
     }
-    next(pf);
-    if (pr) next(pf);
   };
 #pragma unroll
   for (int st = 0; st < kKeyStagesE; ++st) issue(st);
@@ -820,26 +881,19 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   int st = 0;
   while (cp.c < cB) {
-    const bool pr = pair_of(cp);
-    float4 a0 = z4, a1 = z4, b0 = z4, b1 = z4;
-    if (pr) {
+    if (pair_of(cp)) {
       mbar_wait(&bars[st], (ph >> st) & 1u);
       ph ^= 1u << st;
       const float4* src = reinterpret_cast<const float4*>(ring + st * 2 * kChunk) + lane * 2;
-      a0 = src[0];
-      a1 = src[1];
-      b0 = src[64];
-      b1 = src[65];
-    }
-    __syncwarp();
-    issue(st);   // refill the stage just read
-    if (pr) {
-      run(cp, true, a0, a1);
-      next(cp);
-      run(cp, true, b0, b1);
-      next(cp);
+      const float4 a0 = src[0], a1 = src[1], b0 = src[64], b1 = src[65];
+      __syncwarp();
+      issue(st);   // refill the stage just read
+      run_pair(cp, a0, a1, b0, b1);
+      next_pair(cp);
     } else {
+      issue(st);
       const bool fast = fast_of(cp);
+      float4 a0 = z4, a1 = z4;
       if (fast) {
         const float4* src = reinterpret_cast<const float4*>(keys + (cp.lo - geo.elem0)) + lane * 2;
         a0 = __ldg(src);
@@ -950,7 +1004,7 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
 // too wide, bound too loose) it writes done = 0 and returns, and k_encode,
 // launched right after, does the work; otherwise done = 1 and k_encode exits.
 #ifndef NMK_ENCK_MINB
-#define NMK_ENCK_MINB 3
+#define NMK_ENCK_MINB 2
 #endif
 template <typename T, int B, bool kRecon>
 __global__ void __launch_bounds__(kEncThreads, NMK_ENCK_MINB)
