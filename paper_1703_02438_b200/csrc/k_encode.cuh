@@ -357,6 +357,26 @@ __device__ __forceinline__ uint32_t classify_direct(T bt, T xt, const DirectGrid
 constexpr uint32_t kKeySlow = 0x80000000u;   // not a code: decide again (f64 key test, exact path)
 constexpr uint32_t kIncFlag = 0x40000000u;   // tags the sentinel in the keyed table (codes < 2^30)
 
+// The keyed table holds u16 entries for B <= 15 (codes < 2^15), so twice
+// as many ordinals fit in the same 32 KB; the sentinel's tag is then bit 15.
+#ifndef NMK_T16_MAXB
+#define NMK_T16_MAXB 15
+#endif
+template <bool T16>
+constexpr int kTabCells = T16 ? 2 * kLutCells : kLutCells;
+template <bool T16>
+constexpr int kIncBit = T16 ? 15 : 30;
+template <bool T16>
+__device__ __forceinline__ uint32_t tab_code(uint32_t tab_s, uint32_t row) {
+  if constexpr (T16) {
+    uint32_t t;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(t) : "r"(tab_s + 2 * row));
+    return t;
+  } else {
+    return lds_u32(tab_s + 4 * row);
+  }
+}
+
 struct KeyedGrid {
   unsigned long long iw2, c2;   // (iw32, iw32) and (c32, c32) as f32x2
   float iw32, c32, hi4;
@@ -371,7 +391,7 @@ struct KeyedGrid {
 // All threads: tab[row] = code of ordinal q0 - 1 + row (center index, or the
 // sentinel tagged with kIncFlag), opc[i] = RN(1 + c_i); true when the mode
 // applies (block-uniform).
-template <typename T>
+template <typename T, bool T16>
 __device__ __forceinline__ bool setup_keyed(const double* __restrict__ centers_g, int k,
                                             const nmk_stats* __restrict__ st, double width, double tol,
                                             double tol_bin, uint32_t sentinel, uint32_t* tab, double* opc,
@@ -403,10 +423,18 @@ __device__ __forceinline__ bool setup_keyed(const double* __restrict__ centers_g
   __syncthreads();
   if (!ok0 || *s_fail) return false;
   const int q0 = s_q[0], span2 = s_q[1] - q0 + 3;
-  if (span2 > kLutCells) return false;
-  for (int i = threadIdx.x; i < span2; i += blockDim.x) tab[i] = sentinel | kIncFlag;
+  if (span2 > kTabCells<T16>) return false;
+  uint16_t* tab16 = reinterpret_cast<uint16_t*>(tab);
+  for (int i = threadIdx.x; i < span2; i += blockDim.x) {
+    if constexpr (T16) tab16[i] = (uint16_t)(sentinel | (1u << kIncBit<true>));
+    else tab[i] = sentinel | kIncFlag;
+  }
   __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x) tab[(int)floor(pos(__ldg(centers_g + i))) - q0 + 1] = (uint32_t)i;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const int row = (int)floor(pos(__ldg(centers_g + i))) - q0 + 1;
+    if constexpr (T16) tab16[row] = (uint16_t)i;
+    else tab[row] = (uint32_t)i;
+  }
   const double A = fmax(fmax(fabs(gmin), fabs(gmax)), fmax(fabs(__ldg(centers_g)), fabs(__ldg(centers_g + k - 1))));
   const double D = __longlong_as_double((long long)*s_dmax);
   constexpr bool kF32 = sizeof(T) == 4;
@@ -449,13 +477,14 @@ __device__ __forceinline__ bool setup_keyed(const double* __restrict__ centers_g
 // Branch-free: rows outside the table are clamped onto its last row (ordinal
 // q_last + 1, never a center: the tagged sentinel); a key outside the
 // margin, NaN included, gives kKeySlow.
+template <bool T16>
 __device__ __forceinline__ uint32_t classify_key(float key, const KeyedGrid& g) {
   constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
   const float th = __fmaf_rn(key, g.iw32, g.c32);
   const float m = __fadd_rn(th, kMagic);
   const float d = __fsub_rn(th, __fsub_rn(m, kMagic));
   const uint32_t row = min((uint32_t)__float_as_int(m) - g.rowbase, g.span2 - 1u);
-  const uint32_t code = lds_u32(g.tab_s + 4 * row);
+  const uint32_t code = tab_code<T16>(g.tab_s, row);
   const float sb = __fmaf_rn(fabsf(th), 0x1p-23f, __fmaf_rn(fabsf(key), g.ka, fabsf(d)));   // |d| + bound
   return sb < g.hi4 ? code : kKeySlow;
 }
@@ -464,6 +493,7 @@ __device__ __forceinline__ uint32_t classify_key(float key, const KeyedGrid& g) 
 // (FFMA2 / FADD2, each lane IEEE round-to-nearest like the scalar ops), the
 // bound test per key.  Keys outside the margin (NaN included) give kKeySlow,
 // which the caller re-decides.
+template <bool T16>
 __device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGrid& g, uint32_t& ca, uint32_t& cb) {
   constexpr unsigned long long kMagic2 = 0x4B4000004B400000ULL;   // (1.5 * 2^23, 1.5 * 2^23)
   const unsigned long long k2 = ((unsigned long long)__float_as_uint(kb) << 32) | __float_as_uint(ka);
@@ -474,8 +504,8 @@ __device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGri
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(th), "l"(t));
   const uint32_t ra = min((uint32_t)m - g.rowbase, g.span2 - 1u);
   const uint32_t rb = min((uint32_t)(m >> 32) - g.rowbase, g.span2 - 1u);
-  const uint32_t ta = lds_u32(g.tab_s + 4 * ra);
-  const uint32_t tb = lds_u32(g.tab_s + 4 * rb);
+  const uint32_t ta = tab_code<T16>(g.tab_s, ra);
+  const uint32_t tb = tab_code<T16>(g.tab_s, rb);
   const float sa = __fmaf_rn(fabsf(__uint_as_float((uint32_t)th)), 0x1p-23f,
                              __fmaf_rn(fabsf(ka), g.ka, fabsf(__uint_as_float((uint32_t)d))));
   const float sb = __fmaf_rn(fabsf(__uint_as_float((uint32_t)(th >> 32))), 0x1p-23f,
@@ -491,6 +521,7 @@ __device__ __forceinline__ void classify_key2(float ka, float kb, const KeyedGri
 // (|key - r| <= |key| 2^-23, three roundings of t), so with f = t - floor(t),
 // |f - 1/2| < 1/2 - margin - et puts u in bin floor(t) with the margin of
 // setup_keyed.  +inf keys (exact path) give NaN and fail.
+template <bool T16>
 __device__ __forceinline__ uint32_t classify_key64(float key, const KeyedGrid& g) {
   const double gmin = lds_f64(g.kd_s), iw = lds_f64(g.kd_s + 8), half_m = lds_f64(g.kd_s + 16);
   const double t = __dmul_rn(__dsub_rn((double)key, gmin), iw);
@@ -499,7 +530,7 @@ __device__ __forceinline__ uint32_t classify_key64(float key, const KeyedGrid& g
   const double et = fabs((double)key) * iw * 0x1p-22 + fabs(t) * 0x1p-49 + 0x1p-60;
   if (!(fabs(__dsub_rn(f, 0.5)) < __dsub_rn(half_m, et)) || !(t < 0x1p+31)) return kKeySlow;
   const uint32_t row = min((uint32_t)(long long)fl - g.q0m1, g.span2 - 1u);
-  return lds_u32(g.tab_s + 4 * row);
+  return tab_code<T16>(g.tab_s, row);
 }
 
 // Packed bytes of one chunk: each lane's 8 codes are B bytes at lane * B;
@@ -631,12 +662,33 @@ __device__ __forceinline__ void encode_chunks(const T* __restrict__ base, const 
 #define NMK_ENCK_STAGES 2   // stages of two chunks' keys (2 KB) per warp
 #endif
 constexpr int kKeyStagesE = NMK_ENCK_STAGES;
+// a stage holds a chunk pair's keys plus 4 of slack: a pair whose first key
+// is not 16-byte aligned (blocks of epb % 4 != 0 elements, e.g. B = 12) is
+// copied from the aligned address below it
+constexpr int kStageKeys = 2 * kChunk + 4;
 // dynamic shared memory of k_encode_keyed: opc doubles, then 128-byte aligned key tiles
 __host__ __device__ constexpr size_t keyed_ring_off(int k_cap) { return ((size_t)(k_cap + 2) + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t keyed_smem_bytes(int k_cap) {
-  return keyed_ring_off(k_cap) * 8 + (size_t)(kEncThreads / 32) * kKeyStagesE * 2 * kChunk * 4;
+  return keyed_ring_off(k_cap) * 8 + (size_t)(kEncThreads / 32) * kKeyStagesE * kStageKeys * 4;
 }
-template <typename T, int B, bool kRecon, typename Slow, typename Rec>
+// Lane keys 8 l + shift .. + 7 from a 16-byte aligned shared-memory row p
+// (p = row + 8 l): three aligned vectors, then a warp-uniform shift.
+__device__ __forceinline__ void shifted_keys(const float* p, uint32_t shift, float4& a, float4& b) {
+  const float4 v0 = reinterpret_cast<const float4*>(p)[0], v1 = reinterpret_cast<const float4*>(p)[1],
+               v2 = reinterpret_cast<const float4*>(p)[2];
+  if (shift == 1) {
+    a = make_float4(v0.y, v0.z, v0.w, v1.x);
+    b = make_float4(v1.y, v1.z, v1.w, v2.x);
+  } else if (shift == 2) {
+    a = make_float4(v0.z, v0.w, v1.x, v1.y);
+    b = make_float4(v1.z, v1.w, v2.x, v2.y);
+  } else {
+    a = make_float4(v0.w, v1.x, v1.y, v1.z);
+    b = make_float4(v1.w, v2.x, v2.y, v2.z);
+  }
+}
+
+template <typename T, int B, bool kRecon, bool kAligned, typename Slow, typename Rec>
 __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ keys, const T* __restrict__ base,
                                                     const T* __restrict__ cur, const EncodeGeom& geo,
                                                     uint8_t* __restrict__ packed, uint8_t* __restrict__ masks,
@@ -645,8 +697,12 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
                                                     unsigned long long* kbars, Slow&& slow, Rec&& rec_of) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t sentinel = (1u << B) - 1u;
+  constexpr bool kT16 = B <= NMK_T16_MAXB;
+  constexpr uint32_t kInc = 1u << kIncBit<kT16>;   // tags the sentinel in table codes
   const uint64_t local_end = geo.elem0 + geo.n_local;
-  const bool ptr_al = (((uintptr_t)keys | (kRecon ? ((uintptr_t)base | (uintptr_t)recon) : 0)) & 15) == 0;
+  // keys are 16-byte aligned (nmk_encode_keyed_dev checks); vector access
+  // to base / recon needs them aligned too
+  const bool ptr_al = (((uintptr_t)base | (uintptr_t)recon) & 15) == 0;
   const uint32_t cpb = (uint32_t)geo.cpb;
   const uint32_t cpb_whole = (uint32_t)(geo.epb / kChunk);   // chunks per block that are never clipped
   constexpr int VN = EVec<T>::N;
@@ -696,29 +752,37 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       k.lo = (uint64_t)k.b * geo.epb;
     }
   };
-  const bool al_all = ptr_al && geo.key_al;
-  // warp-uniform: a whole chunk of this range, inside its block, key vectors aligned
-  auto fast_of = [&](const Cur& k) {
-    return k.c >= geo.c_first && k.c <= geo.c_last && k.ci < cpb_whole &&
-           (al_all || (ptr_al && ((k.lo - geo.elem0) & 3) == 0));
-  };
-  // warp-uniform: the current item is a pair of whole chunks (starts a run when needed)
+  // warp-uniform: a whole chunk of this range, inside its block
+  auto fast_of = [&](const Cur& k) { return k.c >= geo.c_first && k.c <= geo.c_last && k.ci < cpb_whole; };
+  // warp-uniform: the current item is a pair of whole chunks (starts a run
+  // when needed).  A misaligned run's copies read up to 4 - shift keys past
+  // the pair, so its last pair must leave them inside this range.
   auto pair_of = [&](Cur& k) {
-    if (k.left == 0 && k.c + 1 < cBf && k.ci + 1 < cpb_whole && fast_of(k))
-      k.left = min(cBf - k.c, cpb_whole - k.ci) >> 1;
+    if (k.left == 0 && k.c + 1 < cBf && k.ci + 1 < cpb_whole && fast_of(k)) {
+      uint32_t avail = min(cBf - k.c, cpb_whole - k.ci) & ~1u;
+      const uint32_t sh = kAligned ? 0u : (uint32_t)(k.lo - geo.elem0) & 3u;
+      if (sh && k.lo + (uint64_t)avail * kChunk + 4 - sh > local_end) avail -= 2;
+      k.left = avail >> 1;
+    }
     return k.left != 0;
   };
   // the rare keys: NaN (invalid -> sentinel), the f64 key test, the exact path
   auto redo = [&](uint32_t& code, int64_t j) {
     const float key = __ldg(keys + j);
-    uint32_t v = key != key ? (sentinel | kIncFlag) : classify_key64(key, kg);
+    uint32_t v = key != key ? (sentinel | kInc) : classify_key64<kT16>(key, kg);
     if (v == kKeySlow) {
       v = slow(__ldg(base + j), __ldg(cur + j));
-      v |= v == sentinel ? kIncFlag : 0u;
+      v |= v == sentinel ? kInc : 0u;
     }
     code = v;
   };
   auto recon8 = [&](int64_t li, const uint32_t (&code)[kGroup]) {   // the decoder's values
+    if (!ptr_al || (li & (VN - 1)) != 0) {
+#pragma unroll
+      for (int e = 0; e < kGroup; ++e)
+        recon[li + e] = code[e] == sentinel ? __ldg(cur + li + e) : rec_of(code[e], __ldg(base + li + e));
+      return;
+    }
     T bv[kGroup];
     load8<T>(base + li, bv);
     using V = typename EVec<T>::V;
@@ -738,19 +802,19 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   // whether anything but table codes occurred
   auto run_pair = [&](const Cur& k, const float4& a0, const float4& a1, const float4& b0, const float4& b1) {
     uint32_t ca[kGroup], cb[kGroup];
-    classify_key2(a0.x, a0.y, kg, ca[0], ca[1]);
-    classify_key2(a0.z, a0.w, kg, ca[2], ca[3]);
-    classify_key2(a1.x, a1.y, kg, ca[4], ca[5]);
-    classify_key2(a1.z, a1.w, kg, ca[6], ca[7]);
-    classify_key2(b0.x, b0.y, kg, cb[0], cb[1]);
-    classify_key2(b0.z, b0.w, kg, cb[2], cb[3]);
-    classify_key2(b1.x, b1.y, kg, cb[4], cb[5]);
-    classify_key2(b1.z, b1.w, kg, cb[6], cb[7]);
+    classify_key2<kT16>(a0.x, a0.y, kg, ca[0], ca[1]);
+    classify_key2<kT16>(a0.z, a0.w, kg, ca[2], ca[3]);
+    classify_key2<kT16>(a1.x, a1.y, kg, ca[4], ca[5]);
+    classify_key2<kT16>(a1.z, a1.w, kg, ca[6], ca[7]);
+    classify_key2<kT16>(b0.x, b0.y, kg, cb[0], cb[1]);
+    classify_key2<kT16>(b0.z, b0.w, kg, cb[2], cb[3]);
+    classify_key2<kT16>(b1.x, b1.y, kg, cb[4], cb[5]);
+    classify_key2<kT16>(b1.z, b1.w, kg, cb[6], cb[7]);
     const int64_t li = (int64_t)(k.lo - geo.elem0) + lane * kGroup;   // chunk B: li + kChunk
     uint32_t any = 0;
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) any |= ca[e] | cb[e];
-    const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kIncFlag));
+    const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kInc));
     uint32_t tot = 0;
     if (flags) {
       if (flags & kKeySlow) {
@@ -765,10 +829,10 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       unsigned ma = 0, mb = 0;
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
-        ma |= ((ca[e] >> 30) & 1u) << e;
-        mb |= ((cb[e] >> 30) & 1u) << e;
-        ca[e] &= ~kIncFlag;
-        cb[e] &= ~kIncFlag;
+        ma |= ((ca[e] >> kIncBit<kT16>) & 1u) << e;
+        mb |= ((cb[e] >> kIncBit<kT16>) & 1u) << e;
+        ca[e] &= ~kInc;
+        cb[e] &= ~kInc;
       }
       // both chunks' counts in one reduction (each <= 256)
       tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(ma) | ((unsigned)__popc(mb) << 16));
@@ -792,10 +856,10 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     const int64_t li = (int64_t)grp_lo - (int64_t)geo.elem0;
     uint64_t blk_start = 0, blk_end = 0;
     if (fast) {
-      classify_key2(k0.x, k0.y, kg, code[0], code[1]);
-      classify_key2(k0.z, k0.w, kg, code[2], code[3]);
-      classify_key2(k1.x, k1.y, kg, code[4], code[5]);
-      classify_key2(k1.z, k1.w, kg, code[6], code[7]);
+      classify_key2<kT16>(k0.x, k0.y, kg, code[0], code[1]);
+      classify_key2<kT16>(k0.z, k0.w, kg, code[2], code[3]);
+      classify_key2<kT16>(k1.x, k1.y, kg, code[4], code[5]);
+      classify_key2<kT16>(k1.z, k1.w, kg, code[6], code[7]);
     } else {
       blk_start = (uint64_t)k.b * geo.epb;
       blk_end = min(blk_start + geo.epb, geo.n_total);
@@ -806,13 +870,13 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
         const uint64_t j = grp_lo + e;
         const bool in = j >= lo && j < hi;
         live |= (in ? 1u : 0u) << e;
-        code[e] = in ? classify_key(keys[li + e], kg) : 0u;
+        code[e] = in ? classify_key<kT16>(keys[li + e], kg) : 0u;
       }
     }
     uint32_t any = 0;
 #pragma unroll
     for (int e = 0; e < kGroup; ++e) any |= code[e];
-    const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kIncFlag));
+    const uint32_t flags = __reduce_or_sync(0xffffffffu, any & (kKeySlow | kInc));
     unsigned total = 0;
     if (flags) {
       if (any & kKeySlow) {
@@ -825,8 +889,8 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       unsigned inc_mask = 0;
 #pragma unroll
       for (int e = 0; e < kGroup; ++e) {
-        inc_mask |= ((code[e] >> 30) & 1u) << e;
-        code[e] &= ~kIncFlag;
+        inc_mask |= ((code[e] >> kIncBit<kT16>) & 1u) << e;
+        code[e] &= ~kInc;
       }
       inc_mask &= live;
       total = __reduce_add_sync(0xffffffffu, (unsigned)__popc(inc_mask));
@@ -853,7 +917,7 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
   // chunks (2 KB), filled by TMA bulk copies.  A pair is staged when both
   // chunks are whole and in the same block; other chunks go one at a time
   // with their keys read directly.
-  float* ring = kring + (size_t)wid * kKeyStagesE * 2 * kChunk;
+  float* ring = kring + (size_t)wid * kKeyStagesE * kStageKeys;
   unsigned long long* bars = kbars + wid * kKeyStagesE;
   if (lane == 0) {
     for (int st = 0; st < kKeyStagesE; ++st) mbar_init(&bars[st], 1);
@@ -866,9 +930,11 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     if (pf.c >= cB) return;
     if (pair_of(pf)) {
       if (lane == 0) {
+        const uint32_t sh = kAligned ? 0u : (uint32_t)(pf.lo - geo.elem0) & 3u;
+        const unsigned bytes = sh ? kStageKeys * 4 : 2 * kChunk * 4;
         fence_proxy_async_smem();
-        mbar_arrive_tx(&bars[st], 2 * kChunk * 4);
-        tma_load_1d(ring + st * 2 * kChunk, keys + (pf.lo - geo.elem0), 2 * kChunk * 4, &bars[st]);
+        mbar_arrive_tx(&bars[st], bytes);
+        tma_load_1d(ring + st * kStageKeys, keys + (pf.lo - geo.elem0 - sh), bytes, &bars[st]);
       }
       next_pair(pf);
     } else {
@@ -884,8 +950,18 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     if (pair_of(cp)) {
       mbar_wait(&bars[st], (ph >> st) & 1u);
       ph ^= 1u << st;
-      const float4* src = reinterpret_cast<const float4*>(ring + st * 2 * kChunk) + lane * 2;
-      const float4 a0 = src[0], a1 = src[1], b0 = src[64], b1 = src[65];
+      const uint32_t sh = kAligned ? 0u : (uint32_t)(cp.lo - geo.elem0) & 3u;   // warp-uniform
+      float4 a0, a1, b0, b1;
+      if (sh == 0) {
+        const float4* src = reinterpret_cast<const float4*>(ring + st * kStageKeys) + lane * 2;
+        a0 = src[0];
+        a1 = src[1];
+        b0 = src[64];
+        b1 = src[65];
+      } else {
+        shifted_keys(ring + st * kStageKeys + lane * 8, sh, a0, a1);
+        shifted_keys(ring + st * kStageKeys + kChunk + lane * 8, sh, b0, b1);
+      }
       __syncwarp();
       issue(st);   // refill the stage just read
       run_pair(cp, a0, a1, b0, b1);
@@ -895,9 +971,14 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
       const bool fast = fast_of(cp);
       float4 a0 = z4, a1 = z4;
       if (fast) {
-        const float4* src = reinterpret_cast<const float4*>(keys + (cp.lo - geo.elem0)) + lane * 2;
-        a0 = __ldg(src);
-        a1 = __ldg(src + 1);
+        const float* kp = keys + (cp.lo - geo.elem0) + lane * 8;
+        if (kAligned || ((cp.lo - geo.elem0) & 3) == 0) {
+          a0 = __ldg(reinterpret_cast<const float4*>(kp));
+          a1 = __ldg(reinterpret_cast<const float4*>(kp) + 1);
+        } else {
+          a0 = make_float4(__ldg(kp), __ldg(kp + 1), __ldg(kp + 2), __ldg(kp + 3));
+          a1 = make_float4(__ldg(kp + 4), __ldg(kp + 5), __ldg(kp + 6), __ldg(kp + 7));
+        }
       }
       run(cp, fast, a0, a1);
       next(cp);
@@ -1031,16 +1112,22 @@ k_encode_keyed(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom
   const double tol_bin = model->tol_bin;
   KeyedGrid kg;
   const bool ok = k <= k_cap && k <= kSmemCuts + 1 &&
-                  setup_keyed<T>(centers_g, k, kx.st, kx.width, tol, tol_bin, sentinel, tab, opc, kg, &s_fail,
+                  setup_keyed<T, (B <= NMK_T16_MAXB)>(centers_g, k, kx.st, kx.width, tol, tol_bin, sentinel, tab, opc, kg, &s_fail,
                                  &s_dmax, s_q, s_kd);
   if (blockIdx.x == 0 && threadIdx.x == 0) *kx.done = ok ? 1u : 0u;
   if (!ok) return;
   const int ncuts = k - 1;
-  encode_chunks_keyed<T, B, kRecon>(
-      kx.keys, base, cur, geo, packed, reinterpret_cast<uint8_t*>(scratch), counts, wbytes[threadIdx.x >> 5], recon,
-      kg, kring, kbars,
-      [&](T b, T x) -> uint32_t { return classify_exact<T>(b, x, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel); },
-      [&](uint32_t cd, T b) -> T { return narrow<T>(__dmul_rn(lds_f64(kg.opc_s + 8 * cd), to_f64(b))); });
+  auto slow = [&](T b, T x) -> uint32_t {
+    return classify_exact<T>(b, x, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel);
+  };
+  auto rec = [&](uint32_t cd, T b) -> T { return narrow<T>(__dmul_rn(lds_f64(kg.opc_s + 8 * cd), to_f64(b))); };
+  // every chunk's keys 16-byte aligned (epb % 4 == 0): the shift logic compiles away
+  if (geo.key_al)
+    encode_chunks_keyed<T, B, kRecon, true>(kx.keys, base, cur, geo, packed, reinterpret_cast<uint8_t*>(scratch),
+                                            counts, wbytes[threadIdx.x >> 5], recon, kg, kring, kbars, slow, rec);
+  else
+    encode_chunks_keyed<T, B, kRecon, false>(kx.keys, base, cur, geo, packed, reinterpret_cast<uint8_t*>(scratch),
+                                             counts, wbytes[threadIdx.x >> 5], recon, kg, kring, kbars, slow, rec);
 }
 
 static int sm_count_e() {

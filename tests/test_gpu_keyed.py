@@ -162,3 +162,32 @@ def test_keyed_histogram_hot_bins_exact(dtype, E, shift, sigma):
     dense[keys.astype(np.int64)] = counts
     got = _dense_counts(pipe, chk["nbins"])
     np.testing.assert_array_equal(got[: chk["nbins"]], dense)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("bits", [12, 13, 11])
+def test_keyed_misaligned_blocks(dtype, bits):
+    """Index blocks of epb % 4 != 0 elements (B = 12: 43690 per 64 KiB block,
+    B = 13 / 11: odd epb) start keys at every shift mod 4: the keyed kernel's
+    shifted pair copies and the unaligned single chunks must match the oracle."""
+    rng = np.random.default_rng(46 + bits)
+    n = 700_001
+    b = rng.lognormal(0.0, 1.0, n)
+    c = b * (1.0 + np.where(rng.uniform(size=n) < 0.9, rng.normal(0, 0.002, n), rng.uniform(-0.05, 0.05, n)))
+    b[rng.uniform(size=n) < 0.003] = 0.0
+    _run_all(b.astype(dtype), c.astype(dtype), 1e-3, bits)
+
+
+def test_keyed_wide_table_u16():
+    """B <= 15 keeps a u16 ordinal table of 16384 rows: selected centers
+    spread over more than 8192 histogram bins (uniform ratios over ~12000
+    bins, B = 12 takes the 4095 fullest) must still take the keyed path and
+    match the oracle."""
+    rng = np.random.default_rng(47)
+    n = 600_000
+    E = 5e-5
+    b = rng.uniform(0.5, 2.0, n)
+    c = b * (1.0 + rng.uniform(-0.6, 0.6, n))
+    o = _run_all(b, c, E, 12)
+    cen = o["centers"]
+    assert (cen[-1] - cen[0]) / (2 * E) > 8192   # the table really is wider than the u32 one
