@@ -516,6 +516,12 @@ __global__ void k_hist_prep(nmk_stats* __restrict__ st, double width, uint64_t c
 // per-warp ring of TMA bulk copies (kKeyStages x 1 KB), so loads for later
 // tiles are in flight while a tile is counted.
 constexpr uint32_t kNoBin = 0xffffffffu;
+#ifndef NMK_PRIV_ATOM
+#define NMK_PRIV_ATOM 1   // A/B: atomicAdd beats the plain read-modify-write by 8 % (cfg4)
+#endif
+#ifndef NMK_HIST_PRIV
+#define NMK_HIST_PRIV 1     // lane-private counters for spans <= 63 bins
+#endif
 #ifndef NMK_KEY_TILE
 #define NMK_KEY_TILE 512   // measured: 512 x 2 stages beats 256 x 4 by 15 % (K2)
 #endif
@@ -728,6 +734,131 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
   flush(hot2, c2 + c2x);
 }
 
+// ---- key histogram with lane-private counters (spans of <= 63 bins) ---------
+// Spread ratio fields (cfg1/cfg4: sigma = one bin, 50 bins; cfg3: ~6 bins)
+// defeat the hot pair above: most keys miss it and the deferral loop runs at
+// the pace of the unluckiest lane.  With a span this small every lane owns a
+// private copy of the whole histogram in shared memory -- u16 counters packed
+// two bins per word, word (q / 2) of lane l at [(q / 2) * 32 + l], so a
+// warp's 32 updates hit 32 distinct banks and need no conflict resolution.
+// Per key: one f32 FMA + magic rounding (key_ordinal32) and one shared add;
+// keys the f32 test cannot decide take the full ordinal (ord) in place.
+// The u16 halves are drained into the CTA's u32 totals before they can
+// overflow (every kPrivDrain tiles: <= 16 * kPrivDrain keys per lane).
+constexpr uint32_t kPrivBins = 64;                  // nbins + 1 (tripwire) <= 64
+constexpr uint32_t kPrivWords = kPrivBins / 2 * 32; // per warp (4 KB)
+constexpr uint32_t kPrivDrain = 256;                // tiles between drains (< 65536 / 16; cheap, and
+                                                    // exercised by the 2^29-element tests)
+
+template <typename T>
+__device__ __forceinline__ void hist_keys_priv(const float* __restrict__ keys, const T* __restrict__ base,
+                                               const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
+                                               double width, double inv_w, uint32_t nbins, uint32_t* priv,
+                                               uint32_t* cta_tot, float* stage, unsigned long long* bars) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const double et_c = key_bound(gmin, gmax, inv_w);
+  const KeyGrid32 g32 = key_grid32(gmin, gmax, inv_w, nbins);
+  for (uint32_t i = lane; i < kPrivWords; i += 32) priv[i] = 0;
+  uint32_t* mine = priv + lane;
+  auto bump = [&](uint32_t qi) {   // qi <= nbins < kPrivBins
+#if NMK_PRIV_ATOM
+    atomicAdd(&mine[(qi >> 1) * 32], 1u << ((qi & 1u) * 16));   // lane-private: never contended
+#else
+    mine[(qi >> 1) * 32] += 1u << ((qi & 1u) * 16);
+#endif
+  };
+  auto slow = [&](float key, uint64_t j) {
+    double q;
+    if (key == key && key_ordinal_c(key, gmin, inv_w, et_c, q)) {
+      bump(q < (double)nbins ? (uint32_t)q : nbins);
+      return;
+    }
+    const uint32_t qi = key_ordinal_slow<T>(key, base, cur, j, gmin, width, inv_w, et_c, nbins);
+    if (qi != kNoBin) bump(qi);
+  };
+  auto drain = [&]() {   // lane l sums word l and word l + 32 over the 32 lanes
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t w = lane + 32u * h;
+      if (w < kPrivBins / 2) {
+        uint32_t lo = 0, hi = 0;
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t v = priv[w * 32 + ((lane + i) & 31)];   // rotated: no bank conflicts
+          lo += v & 0xffffu;
+          hi += v >> 16;
+        }
+        if (lo) atomicAdd(&cta_tot[2 * w], lo);
+        if (hi) atomicAdd(&cta_tot[2 * w + 1], hi);
+      }
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < kPrivWords; i += 32) priv[i] = 0;
+    __syncwarp();
+  };
+  const uint64_t ntiles = n / kKeyTile;
+  const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  if (lane == 0) {
+    for (int st = 0; st < kKeyStages; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](int st, uint64_t t) {   // lane 0 only
+    mbar_arrive_tx(&bars[st], kKeyTile * 4);
+    tma_load_1d(stage + st * kKeyTile, keys + t * kKeyTile, kKeyTile * 4, &bars[st]);
+  };
+  if (lane == 0)
+    for (int st = 0; st < kKeyStages; ++st)
+      if (wg + st * nw < ntiles) issue(st, wg + st * nw);
+  uint32_t since = 0;
+  for (uint64_t kk = 0;; ++kk) {   // warp-uniform
+    const uint64_t t = wg + kk * nw;
+    if (t >= ntiles) break;
+    const int st = (int)(kk % kKeyStages);
+    mbar_wait(&bars[st], (unsigned)((kk / kKeyStages) & 1));
+    const float* sk = stage + st * kKeyTile;
+    uint32_t defer = 0;
+#pragma unroll
+    for (int u = 0; u < kKeyPerLane / 4; ++u) {
+      const float4 w = reinterpret_cast<const float4*>(sk)[u * 32 + lane];
+      const float kv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t qi;
+        if (key_ordinal32(kv[e], g32, qi)) bump(qi);
+        else defer |= 1u << (4 * u + e);
+      }
+    }
+    while (defer) {   // rare: undecided / invalid / out-of-range keys
+      const int e = __ffs(defer) - 1;
+      defer &= defer - 1;
+      const int idx = ((e >> 2) * 32 + lane) * 4 + (e & 3);
+      slow(sk[idx], t * kKeyTile + idx);
+    }
+    __syncwarp();
+    if (lane == 0) {   // refill this stage
+      fence_proxy_async_smem();
+      const uint64_t nx = t + (uint64_t)kKeyStages * nw;
+      if (nx < ntiles) issue(st, nx);
+    }
+    if (++since == kPrivDrain) {
+      drain();
+      since = 0;
+    }
+  }
+  // tail: the last n % kKeyTile keys, one element per lane per round
+  for (uint64_t j = ntiles * kKeyTile + wg * 32 + lane; j < n; j += nw * 32) {
+    const float key = keys[j];
+    uint32_t qi;
+    if (key_ordinal32(key, g32, qi)) bump(qi);
+    else slow(key, j);
+  }
+  drain();
+  (void)FULL;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kHistThreads, 3)
 k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* __restrict__ keys, uint64_t n,
@@ -739,8 +870,22 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
   const double gmin = st->gmin;
   const double inv_w = 1.0 / width;
   if (nbins <= kDevSmemBins) {
+    __shared__ unsigned long long s_bars[kHistThreads / 32][kKeyStages];
+    static_assert(kPrivWords * (kHistThreads / 32) <= kKeySmemBins, "private tables alias the replicas");
+    if (NMK_HIST_PRIV && keys && nbins + 1 <= kPrivBins) {   // lane-private counters (tripwire = slot nbins)
+      __shared__ uint32_t s_tot[kPrivBins];
+      if (threadIdx.x < kPrivBins) s_tot[threadIdx.x] = 0;
+      __syncthreads();
+      const int wid = threadIdx.x >> 5;
+      float* stage = reinterpret_cast<float*>(h + kKeySmemBins) + wid * kKeyStages * kKeyTile;
+      hist_keys_priv<T>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins, h + wid * kPrivWords, s_tot, stage,
+                        s_bars[wid]);
+      __syncthreads();
+      if (threadIdx.x <= nbins && s_tot[threadIdx.x])
+        atomicAdd(&counts[threadIdx.x], (unsigned long long)s_tot[threadIdx.x]);
+      return;
+    }
     if (keys && nbins < kKeySmemBins) {   // replicas of nbins + 1 slots (tripwire last)
-      __shared__ unsigned long long s_bars[kHistThreads / 32][kKeyStages];
       const uint32_t nb1 = nbins + 1;
       int reps = (int)(kKeySmemBins / nb1);
       if (reps > kHistThreads / 32) reps = kHistThreads / 32;
