@@ -23,6 +23,9 @@ constexpr int kMinmaxThreads = 256;
 #define NMK_MM_CTAS 8
 #endif
 constexpr int kMinmaxUnroll = NMK_MM_UNROLL;
+#ifndef NMK_MM_UNROLL32
+#define NMK_MM_UNROLL32 2   // f32: 2 x 16-byte vectors of each snapshot per thread in flight
+#endif
 
 struct MinMax {
   double lo, hi;
@@ -59,6 +62,50 @@ __device__ __forceinline__ float mm_visit(MinMax& a, double b, double x) {
   return __int_as_float(0x7fc00000);   // invalid: quiet NaN
 }
 
+// f32 inputs: the common element is decided in f32 arithmetic.  When |b| is
+// in [2^-60, 2^60) and the computed d = RN32(x - b) has |d| < |b| / 4, the
+// exact difference is below |b| / 4 (1 + 2^-24), so x / b is in (0.74, 1.26),
+// x - b is exact (Sterbenz) and r = RN64(d / b) is finite: the element is
+// valid and key_safe holds.  The key is d / b by a reciprocal seed (max rel.
+// error 2^-22 assumed for rcp.approx) and one FMA Newton correction of the
+// quotient: before the last rounding the relative error is below
+// (2^-22 + 2^-24)^2 < 2^-43, so |key - r| <= |key| (2^-24 + 2^-43 + 2^-52)
+// < |key| 2^-23 -- the key contract of ratio_key (nmk_common.cuh).  No
+// intermediate is subnormal in this range (a nonzero |d| is >= 2^-25 |b| >= 2^-85).
+// The element can only be a new extreme if [key -+ |key| 2^-22] (rounded
+// f32, still containing r) reaches the running extremes, kept as
+// lo32 >= RU32(lo) and hi32 <= RD32(hi) (shared across the warp between
+// iterations: an element above some lane's minimum is never the global one);
+// then the exact f64 quotient is formed.  Everything else takes the f64 path.
+__device__ __forceinline__ float mm_visit32(MinMax& a, float& lo32, float& hi32, float b, float x) {
+  const float ab = fabsf(b);
+  const float d = __fsub_rn(x, b);
+  if (ab >= 0x1p-60f && ab < 0x1p+60f && fabsf(d) < 0.25f * ab) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(b));
+    const float q0 = __fmul_rn(d, y);
+    const float key = __fmaf_rn(__fmaf_rn(-b, q0, d), y, q0);
+    a.nv += 1;
+    const float m = fabsf(key) * 0x1p-22f;
+    if (!(__fsub_rn(key, m) > lo32 && __fadd_rn(key, m) < hi32)) {
+      const double r = __ddiv_rn((double)d, (double)b);
+      if (r < a.lo) {
+        a.lo = r;
+        lo32 = fminf(lo32, __double2float_ru(r));
+      }
+      if (r > a.hi) {
+        a.hi = r;
+        hi32 = fmaxf(hi32, __double2float_rd(r));
+      }
+    }
+    return key;
+  }
+  const float key = mm_visit<float>(a, (double)b, (double)x);
+  lo32 = fminf(lo32, __double2float_ru(a.lo));
+  hi32 = fmaxf(hi32, __double2float_rd(a.hi));
+  return key;
+}
+
 __device__ __forceinline__ MinMax mm_merge(MinMax a, const MinMax& b) {
   a.lo = b.lo < a.lo ? b.lo : a.lo;
   a.hi = b.hi > a.hi ? b.hi : a.hi;
@@ -92,6 +139,7 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
   acc.nv = 0;
   acc.lo = __longlong_as_double(0x7ff0000000000000LL);   // +inf
   acc.hi = __longlong_as_double(0xfff0000000000000LL);   // -inf
+  float lo32 = __int_as_float(0x7f800000), hi32 = __int_as_float(0xff800000);   // f32 path: RU(lo), RD(hi)
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   uint64_t done = 0;
@@ -100,22 +148,39 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
     const V* bv = reinterpret_cast<const V*>(base);
     const V* cv = reinterpret_cast<const V*>(cur);
     uint64_t i = tid;
-    for (; i + (kMinmaxUnroll - 1) * nthr < nvec; i += kMinmaxUnroll * nthr) {
-      V b[kMinmaxUnroll], c[kMinmaxUnroll];
+    constexpr int U = VN == 4 ? NMK_MM_UNROLL32 : kMinmaxUnroll;
+    // warp-uniform trip count (the f32 thresholds are shared by shuffles):
+    // a warp iterates while its last lane is in range, the rest is the tail
+    const uint64_t lane_hi = 31 - (threadIdx.x & 31);
+    for (; i + lane_hi + (U - 1) * nthr < nvec; i += U * nthr) {
+      V b[U], c[U];
 #pragma unroll
-      for (int u = 0; u < kMinmaxUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         b[u] = __ldg(bv + i + u * nthr);
         c[u] = __ldg(cv + i + u * nthr);
       }
 #pragma unroll
-      for (int u = 0; u < kMinmaxUnroll; ++u) {
-        double bb[VN], cc[VN];
-        vec_get(b[u], bb);
-        vec_get(c[u], cc);
+      for (int u = 0; u < U; ++u) {
         float kv[VN];
+        if constexpr (VN == 4) {   // f32
+          const float bf[4] = {b[u].x, b[u].y, b[u].z, b[u].w}, cf[4] = {c[u].x, c[u].y, c[u].z, c[u].w};
 #pragma unroll
-        for (int e = 0; e < VN; ++e) kv[e] = mm_visit<T>(acc, bb[e], cc[e]);
+          for (int e = 0; e < VN; ++e) kv[e] = mm_visit32(acc, lo32, hi32, bf[e], cf[e]);
+        } else {
+          double bb[VN], cc[VN];
+          vec_get(b[u], bb);
+          vec_get(c[u], cc);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) kv[e] = mm_visit<T>(acc, bb[e], cc[e]);
+        }
         if (keys) store_keys<VN>(keys + (i + u * nthr) * VN, kv);
+      }
+      if constexpr (VN == 4) {   // share the f32 thresholds across the warp
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo32 = fminf(lo32, __shfl_xor_sync(0xffffffffu, lo32, o));
+          hi32 = fmaxf(hi32, __shfl_xor_sync(0xffffffffu, hi32, o));
+        }
       }
     }
     for (; i < nvec; i += nthr) {

@@ -191,3 +191,66 @@ def test_keyed_wide_table_u16():
     o = _run_all(b, c, E, 12)
     cen = o["centers"]
     assert (cen[-1] - cen[0]) / (2 * E) > 8192   # the table really is wider than the u32 one
+
+
+def _f32_boundary_pair(rng, n):
+    """f32 pairs around K1's f32 fast path edges (k_ratio.cu mm_visit32):
+    |d| near |b| / 4, |b| near 2^-60 and 2^60, x == b, sign flips, zeros,
+    ratios that straddle the running extremes."""
+    mag = np.exp2(rng.uniform(-64.0, 64.0, n))
+    edge = rng.choice([2.0 ** -60, 2.0 ** 60, 1.0], n) * (1.0 + rng.integers(-3, 4, n) * 2.0 ** -23)
+    b = np.where(rng.uniform(size=n) < 0.3, edge, mag) * np.where(rng.uniform(size=n) < 0.4, -1.0, 1.0)
+    b = b.astype(np.float32)
+    r = rng.choice([0.25, -0.25, 0.0, 1e-3, -1e-3, 0.7, -0.9, 3.0], n)
+    r = r + rng.integers(-4, 5, n) * 2.0 ** -24
+    x = (b.astype(np.float64) * (1.0 + r)).astype(np.float32)
+    x[rng.uniform(size=n) < 0.01] = 0.0
+    b[rng.uniform(size=n) < 0.005] = 0.0
+    return b, x
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_f32_keys_contract_and_extremes(seed):
+    """K1's f32 keys satisfy |key - r| <= |key| 2^-23 (r the reference's f64
+    ratio, core.py:126-136); invalid elements get NaN, keys outside the safe
+    range +inf; gmin / gmax / nvalid equal numpy's exactly."""
+    from paper_1703_02438_b200 import _native as N
+    rng = np.random.default_rng(seed)
+    n = (1 << 18) + 37
+    b, x = _f32_boundary_pair(rng, n)
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(x).cuda()
+    lib = N.lib()
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    keys = torch.empty(n + 4, dtype=torch.float32, device="cuda")
+    wsb = lib.nmk_minmax_ws_bytes(n)
+    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
+    N.check(lib.nmk_minmax(base.data_ptr(), cur.data_ptr(), n, N.NMK_F32, stats.data_ptr(), keys.data_ptr(),
+                           ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    bd, xd = b.astype(np.float64), x.astype(np.float64)
+    with np.errstate(all="ignore"):
+        r = (xd - bd) / bd
+    valid = np.isfinite(r) & np.isfinite(bd) & np.isfinite(xd)
+    both0 = (bd == 0) & (xd == 0)
+    r[both0] = 0.0
+    valid |= both0
+    st = stats.cpu().numpy()
+    assert st[2] == valid.sum()
+    assert np.float64(st[0:1].view(np.float64)[0]) == r[valid].min()
+    assert np.float64(st[1:2].view(np.float64)[0]) == r[valid].max()
+    k = keys[:n].cpu().numpy().astype(np.float64)
+    assert np.isnan(k[~valid]).all()
+    fin = valid & np.isfinite(k)
+    assert np.all(np.abs(k[fin] - r[fin]) <= np.abs(k[fin]) * 2.0 ** -23)
+    assert np.all(np.isposinf(k[valid & ~np.isfinite(k)]))
+    # most elements with |r| < 1/4 and moderate |b| take the f32 fast path and
+    # must carry a finite key
+    mid = valid & (np.abs(r) < 0.2) & (np.abs(bd) > 2.0 ** -50) & (np.abs(bd) < 2.0 ** 50)
+    assert np.isfinite(k[mid]).all()
+
+
+@pytest.mark.parametrize("bits", [8, 10])
+def test_f32_boundary_pairs_bit_exact(bits):
+    rng = np.random.default_rng(11 + bits)
+    b, x = _f32_boundary_pair(rng, (1 << 16) + 5)
+    _run_all(b, x, 1e-3, bits)
