@@ -24,7 +24,10 @@
 
 namespace nmk {
 
-constexpr int kSelThreads = 1024;
+#ifndef NMK_SEL_THREADS
+#define NMK_SEL_THREADS 512   // A/B: 512 beats 1024 (cfg2 23 -> 18 us; fewer warps per barrier) and 256 (10^4 bins)
+#endif
+constexpr int kSelThreads = NMK_SEL_THREADS;
 constexpr int kAutoLo = 2, kAutoHi = 16;           // binning.py:22
 constexpr int kNSel = kAutoHi - kAutoLo + 1;       // 15 simultaneous selects
 
@@ -134,15 +137,18 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     s_prefix[tid] = 0; s_mask[tid] = 0; s_left[tid] = s_kk[tid];
   }
   __syncthreads();
+  const int nslots = autob ? kNSel : 1;   // fixed B: slot 0 only
+  bool any_sel = false;                   // some slot must select (k < m); else every bin is taken
+  for (int s = 0; s < nslots; ++s) any_sel |= s_kk[s] < m;
   int top = 63 - __clzll(maxc | 1ULL);
-  for (int shift = (top / 8) * 8; shift >= 0; shift -= 8) {
-    for (int i = tid; i < kNSel * 256; i += kSelThreads) (&hist[0][0])[i] = 0;
+  for (int shift = any_sel ? (top / 8) * 8 : -1; shift >= 0; shift -= 8) {
+    for (int i = tid; i < nslots * 256; i += kSelThreads) (&hist[0][0])[i] = 0;
     __syncthreads();
     for (uint64_t i0 = 0; i0 < M; i0 += kSelThreads) {   // warp-uniform trip count
       const uint64_t i = i0 + tid;
       const unsigned long long c = i < M ? bv.sel_count(i) : 0ULL;
       const unsigned d = (unsigned)(c >> shift) & 255u;
-      for (int s = 0; s < kNSel; ++s) {
+      for (int s = 0; s < nslots; ++s) {
         if (!(s_kk[s] < m)) continue;                      // uniform
         const bool want = c && (c & s_mask[s]) == s_prefix[s];
         const unsigned act = __ballot_sync(0xffffffffu, want);
@@ -158,8 +164,9 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     {
       // one warp per active slot: lane l owns digits 255-8l .. 248-8l; a warp
       // scan from the top digit finds where the running count reaches `left`
-      const int w = tid >> 5, lane = tid & 31;
-      if (w < kNSel && s_kk[w] < m) {
+      const int lane = tid & 31;
+      for (int w = tid >> 5; w < kNSel; w += kSelThreads / 32) {
+        if (!(s_kk[w] < m)) continue;
         unsigned long long h[8], sum = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
