@@ -767,8 +767,7 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     return k.left != 0;
   };
   // the rare keys: NaN (invalid -> sentinel), the f64 key test, the exact path
-  auto redo = [&](uint32_t& code, int64_t j) {
-    const float key = __ldg(keys + j);
+  auto redo = [&](uint32_t& code, int64_t j, float key) {   // key = keys[j] (already in registers)
     uint32_t v = key != key ? (sentinel | kInc) : classify_key64<kT16>(key, kg);
     if (v == kKeySlow) {
       v = slow(__ldg(base + j), __ldg(cur + j));
@@ -819,10 +818,12 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     if (flags) {
       if (flags & kKeySlow) {
         if (any & kKeySlow) {
+          const float kva[kGroup] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+          const float kvb[kGroup] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
           for (int e = 0; e < kGroup; ++e) {
-            if (ca[e] & kKeySlow) redo(ca[e], li + e);
-            if (cb[e] & kKeySlow) redo(cb[e], li + kChunk + e);
+            if (ca[e] & kKeySlow) redo(ca[e], li + e, kva[e]);
+            if (cb[e] & kKeySlow) redo(cb[e], li + kChunk + e, kvb[e]);
           }
         }
       }
@@ -880,9 +881,10 @@ __device__ __forceinline__ void encode_chunks_keyed(const float* __restrict__ ke
     unsigned total = 0;
     if (flags) {
       if (any & kKeySlow) {
+        const float kv[kGroup] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
         for (int e = 0; e < kGroup; ++e)
-          if (code[e] & kKeySlow) redo(code[e], li + e);
+          if (code[e] & kKeySlow) redo(code[e], li + e, fast ? kv[e] : __ldg(keys + li + e));
       }
       // incompressible elements: the chunk's count and its 256-bit position
       // mask (one byte per lane); k_enc_finalize gathers the values from cur
