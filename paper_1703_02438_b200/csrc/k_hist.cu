@@ -519,6 +519,9 @@ constexpr uint32_t kNoBin = 0xffffffffu;
 #ifndef NMK_PRIV_ATOM
 #define NMK_PRIV_ATOM 1   // A/B: atomicAdd beats the plain read-modify-write by 8 % (cfg4)
 #endif
+#ifndef NMK_HIST_DIRECT
+#define NMK_HIST_DIRECT 1   // out-of-line direct tiles for spread fields (hist_tile_direct)
+#endif
 #ifndef NMK_HIST_PRIV
 #define NMK_HIST_PRIV 1     // lane-private counters for spans <= 63 bins
 #endif
@@ -594,6 +597,60 @@ __device__ __forceinline__ void hot_params(uint32_t h, uint32_t nbins, const Hot
   hi = __double2float_rz(t);
 }
 
+// One tile of a spread field, out of line (hist_keys_hot calls it for tiles
+// that follow a tile which missed its hot pair on > 1/4 of the keys):
+// every key takes its f32 ordinal (undecided ones the full ordinal); hits on
+// the warp's hot pair are counted and returned, other bins go straight to the
+// warp's replica.  The deferral loop of the hot path would instead run at the
+// pace of the lane with the most misses (cfg5: ~70 % of keys).
+struct DirectTile {
+  uint32_t c1, c2, miss, last;
+};
+
+template <typename T>
+__device__ __noinline__ DirectTile hist_tile_direct(const float* sk, const T* __restrict__ base,
+                                                    const T* __restrict__ cur, uint64_t j0, double gmin,
+                                                    double gmax, double width, double inv_w, uint32_t nbins,
+                                                    uint32_t* my, uint32_t hot1, uint32_t hot2) {
+  const int lane = threadIdx.x & 31;
+  const KeyGrid32 g32 = key_grid32(gmin, gmax, inv_w, nbins);
+  DirectTile r{0u, 0u, 0u, kNoBin};
+  auto count = [&](uint32_t qi) {
+    if (qi == hot1) {
+      ++r.c1;
+    } else if (qi == hot2) {
+      ++r.c2;
+    } else {
+      atomicAdd(&my[qi], 1u);   // qi <= nbins
+      ++r.miss;
+      r.last = qi;
+    }
+  };
+  uint32_t defer = 0;
+#pragma unroll
+  for (int u = 0; u < kKeyPerLane / 4; ++u) {
+    const float4 w = reinterpret_cast<const float4*>(sk)[u * 32 + lane];
+    const float kv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t qi;
+      if (key_ordinal32(kv[e], g32, qi)) count(qi);
+      else defer |= 1u << (4 * u + e);
+    }
+  }
+  if (defer) {
+    const double et_c = key_bound(gmin, gmax, inv_w);
+    while (defer) {
+      const int e = __ffs(defer) - 1;
+      defer &= defer - 1;
+      const int idx = ((e >> 2) * 32 + lane) * 4 + (e & 3);
+      const uint32_t qi = key_ordinal_slow<T>(sk[idx], base, cur, j0 + idx, gmin, width, inv_w, et_c, nbins);
+      if (qi != kNoBin) count(qi);
+    }
+  }
+  return r;
+}
+
 template <typename T>
 __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, const T* __restrict__ base,
                                               const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
@@ -616,6 +673,7 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     n2c2 = ((unsigned long long)__float_as_uint(-h2c) << 32) | __float_as_uint(-h2c);
   };
   uint32_t c2 = 0, miss = 0, last_miss = kNoBin;
+  bool spread = false;   // warp-uniform: the last tile missed the hot pair on > 1/4 of its keys
   // hot-pair counts: c2 = hot2 hits of the f32 test; hot1 hits are derived,
   // c1 = tested - ndef - c2 + c1x; c1x / c2x: deferred keys resolving to hot1 / hot2
   uint32_t tested = 0, ndef = 0, c1x = 0, c2x = 0;
@@ -691,14 +749,27 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     mbar_wait(&bars[st], (unsigned)((kk / kKeyStages) & 1));
     const float* sk = stage + st * kKeyTile;
     uint32_t defer = 0;
+    // the previous tile missed the hot pair on > 1/4 of its keys: this one
+    // runs the direct loop (A/B: also sampling the tile's own concentration
+    // with __match_any_sync before choosing cost cfg2 more than it saved)
+    const bool direct = NMK_HIST_DIRECT && spread;
+    if (direct) {
+      const DirectTile r = hist_tile_direct<T>(sk, base, cur, t * kKeyTile, gmin, gmax, width, inv_w, nbins, my,
+                                               hot1, hot2);
+      c1x += r.c1;
+      c2x += r.c2;
+      miss += r.miss;
+      if (r.miss) last_miss = r.last;
+    } else {
 #pragma unroll
-    for (int u = 0; u < kKeyPerLane / 4; ++u) {
-      const float4 w = reinterpret_cast<const float4*>(sk)[u * 32 + lane];
-      hot2keys(w.x, w.y, 4 * u, defer);
-      hot2keys(w.z, w.w, 4 * u + 2, defer);
+      for (int u = 0; u < kKeyPerLane / 4; ++u) {
+        const float4 w = reinterpret_cast<const float4*>(sk)[u * 32 + lane];
+        hot2keys(w.x, w.y, 4 * u, defer);
+        hot2keys(w.z, w.w, 4 * u + 2, defer);
+      }
+      tested += kKeyPerLane;
+      ndef += __popc(defer);
     }
-    tested += kKeyPerLane;
-    ndef += __popc(defer);
     while (defer) {   // this lane's non-hit keys, re-read from the stage
       const int e = __ffs(defer) - 1;
       defer &= defer - 1;
@@ -706,7 +777,9 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
       visit(ord(sk[idx], t * kKeyTile + idx));
     }
     // adapt: promote the most recent miss when the hot pair covers too little
-    if (__reduce_add_sync(FULL, miss) > (unsigned)(kKeyTile / 8)) {
+    const unsigned tile_miss = __reduce_add_sync(FULL, miss);
+    spread = tile_miss > (unsigned)(kKeyTile / 4);
+    if (tile_miss > (unsigned)(kKeyTile / 8)) {
       const unsigned have = __ballot_sync(FULL, last_miss < nbins);
       if (have) {
         const uint32_t cand = __shfl_sync(FULL, last_miss, __ffs(have) - 1);
