@@ -254,3 +254,41 @@ def test_f32_boundary_pairs_bit_exact(bits):
     rng = np.random.default_rng(11 + bits)
     b, x = _f32_boundary_pair(rng, (1 << 16) + 5)
     _run_all(b, x, 1e-3, bits)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("E,kind", [(1e-3, "bimodal"), (1e-2, "bimodal"), (2e-3, "uniform"), (1e-3, "narrow")])
+def test_histogram_forms_exact(dtype, E, kind):
+    """All three forms of K2's key histogram against np.unique at sizes where
+    every warp runs several tiles: lane-private counters (span <= 63 bins:
+    "narrow"), the hot pair, and the out-of-line direct tiles a spread field
+    switches to (cfg5's bimodal mixture, uniform ratios over ~10^3 bins)."""
+    rng = np.random.default_rng(7)
+    n = (1 << 23) + 1234
+    b = rng.lognormal(0.0, 1.0, n)
+    if kind == "bimodal":
+        m = rng.uniform(size=n)
+        r = np.where(m < 0.4, rng.normal(-0.02, 0.004, n), rng.normal(0.03, 0.006, n))
+        out = m > 0.8
+        r[out] = rng.uniform(-1.0, 1.0, out.sum())
+    elif kind == "uniform":
+        r = rng.uniform(-1.0, 1.0, n)
+    else:
+        r = rng.normal(0.0, 0.008, n)
+    c = b * (1.0 + r)
+    b[rng.uniform(size=n) < 0.003] = 0.0
+    b, c = b.astype(dtype), c.astype(dtype)
+    bt, ct = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(bt.numel(), bt.dtype, E, 8)
+    out_t = torch.empty_like(bt)
+    pipe.step(bt, ct, out_t)
+    chk = pipe.check()
+    assert chk["status"] == 0 and chk["tripwire"] == 0
+    rr, v = O.ratios_of(b, c)
+    keys, counts = O.histogram(rr[v], chk["gmin"], 2 * E)
+    dense = np.zeros(chk["nbins"], dtype=np.int64)
+    dense[keys.astype(np.int64)] = counts
+    got = _dense_counts(pipe, chk["nbins"])
+    np.testing.assert_array_equal(got[: chk["nbins"]], dense)
+    if kind == "narrow":
+        assert chk["nbins"] <= 63
