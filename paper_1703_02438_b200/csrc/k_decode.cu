@@ -147,6 +147,59 @@ __device__ __forceinline__ unsigned lane_sentinels(const uint8_t (&raw)[B], uint
   }
 }
 
+// SWAR sentinel count for B in {10, 12, 14} (cfg3's and cfg5's widths):
+// the lane's B bytes as a big-endian 128-bit string (hi:lo), its 8 codes as
+// fields from the top.  A code is the sentinel iff its field in ~X is zero;
+// per 64-bit word of whole fields, ((Z & LO) + LO) | Z) & MSB sets a field's
+// top bit iff the field is nonzero (the add never carries out of a field).
+// Padding never forms a sentinel: bits past the block's last code are zero
+// and fewer than 8 (B > 8), bytes past nbytes read as zero.
+template <int B>
+struct SwarCount {
+  static constexpr bool kOn = B == 10 || B == 12 || B == 14;
+  static constexpr int kFa = 64 / B;        // whole fields in the top word
+  static constexpr int kFb = 8 - kFa;       // the rest, top-aligned in the second word
+  static constexpr unsigned long long fields(int nf, bool msb) {
+    unsigned long long m = 0;
+    for (int e = 0; e < nf; ++e) {
+      const int lo = 64 - (e + 1) * B;
+      m |= msb ? (1ULL << (lo + B - 1)) : (((1ULL << (B - 1)) - 1ULL) << lo);
+    }
+    return m;
+  }
+};
+
+template <int B>
+__device__ __forceinline__ unsigned lane_sentinels_swar(const uint8_t* src, uint32_t nbytes, int lane) {
+  using S = SwarCount<B>;
+  const uint32_t s0 = (uint32_t)lane * B;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};   // little-endian words of bytes s0 .. s0 + 15
+  if (s0 + B <= nbytes) {
+    if constexpr (B == 12) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) w[j] = __ldg(reinterpret_cast<const unsigned int*>(src + s0) + j);
+    } else {
+      const unsigned short* h = reinterpret_cast<const unsigned short*>(src + s0);
+#pragma unroll
+      for (int j = 0; j < B / 2; ++j) w[j >> 1] |= (uint32_t)__ldg(h + j) << (16 * (j & 1));
+    }
+  } else {
+    for (int i = 0; i < B; ++i)
+      if (s0 + i < nbytes) w[i >> 2] |= (uint32_t)__ldg(src + s0 + i) << (8 * (i & 3));
+  }
+  const unsigned long long hi = ((unsigned long long)__byte_perm(w[0], 0, 0x0123) << 32) | __byte_perm(w[1], 0, 0x0123);
+  const unsigned long long lo = ((unsigned long long)__byte_perm(w[2], 0, 0x0123) << 32) | __byte_perm(w[3], 0, 0x0123);
+  constexpr int sh = S::kFa * B;   // < 64
+  const unsigned long long wb = (hi << sh) | (lo >> (64 - sh));
+  auto zero_fields = [](unsigned long long x, unsigned long long lom, unsigned long long msb, int nf) {
+    const unsigned long long z = ~x;
+    const unsigned long long t = (((z & lom) + lom) | z) & msb;
+    return (unsigned)(nf - __popcll(t));
+  };
+  return zero_fields(hi, S::fields(S::kFa, false), S::fields(S::kFa, true), S::kFa) +
+         zero_fields(wb, S::fields(S::kFb, false), S::fields(S::kFb, true), S::kFb);
+}
+
 template <int B>
 __global__ void __launch_bounds__(kDecThreads)
 k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
@@ -155,9 +208,15 @@ k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __rest
   const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
   for (uint32_t c = blockIdx.x * (kDecThreads / 32) + wid; c < (uint32_t)geo.nchunks; c += nwarps) {
     const DChunk d = dchunk<B>(geo, g0 + c);
-    uint8_t raw[B];
-    lane_bytes<B>(chunk_src<B>(packed, geo, d), d.nbytes, lane, raw);
-    const unsigned n = __reduce_add_sync(0xffffffffu, lane_sentinels<B>(raw, d.valid, lane));
+    unsigned mine;
+    if constexpr (SwarCount<B>::kOn) {
+      mine = lane_sentinels_swar<B>(chunk_src<B>(packed, geo, d), d.nbytes, lane);
+    } else {
+      uint8_t raw[B];
+      lane_bytes<B>(chunk_src<B>(packed, geo, d), d.nbytes, lane, raw);
+      mine = lane_sentinels<B>(raw, d.valid, lane);
+    }
+    const unsigned n = __reduce_add_sync(0xffffffffu, mine);
     if (lane == 0) counts[c] = n;
   }
 }

@@ -411,3 +411,23 @@ def test_device_partial_segments_batch():
                         base_cat, segs)
     assert not res.bad_index and not res.exhausted
     assert torch.equal(res.out.view(torch.int64), full[idx].view(torch.int64))
+
+
+@pytest.mark.parametrize("bits", [9, 10, 11, 12, 14, 15])
+@pytest.mark.parametrize("n", [256 * 37, 256 * 37 + 101, 7])
+@pytest.mark.parametrize("frac", [0.0, 0.3, 1.0])
+def test_decode_sentinel_counts_vs_oracle(bits, n, frac):
+    """K5's per-chunk sentinel counts (the SWAR count for B = 10/12/14, the
+    code-extraction count otherwise) through reconstruct: random ids with a
+    given sentinel fraction, ragged element counts, all-sentinel streams."""
+    rng = np.random.default_rng(bits * 1000 + n)
+    k = 37
+    sentinel = (1 << bits) - 1
+    idx = rng.integers(0, k, n)
+    idx[rng.uniform(size=n) < frac] = sentinel
+    centers = np.sort(rng.uniform(-0.05, 0.05, k))
+    base = rng.lognormal(0.0, 1.0, n)
+    exact = rng.normal(size=int((idx == sentinel).sum()))
+    got = nmk.reconstruct(base, centers, idx, exact, bits=bits)
+    want = O.reconstruct(base, centers, idx, exact, bits)
+    assert got.tobytes() == want.tobytes()
