@@ -6,6 +6,7 @@
 // Streaming kernel: 16-byte vector loads of both snapshots, 4 vectors in
 // flight per thread, warp-shuffle + smem CTA reduction, last-CTA grid
 // reduction (no second launch).
+#include <algorithm>
 #include <cfloat>
 
 #include "nmk_common.cuh"
@@ -23,6 +24,9 @@ constexpr int kMinmaxThreads = 256;
 #define NMK_MM_CTAS 8
 #endif
 constexpr int kMinmaxUnroll = NMK_MM_UNROLL;
+#ifndef NMK_MM_CTAS32
+#define NMK_MM_CTAS32 4   // A/B on cfg3: 4 beats 8 (K1 86 -> 82 us) and 2
+#endif
 #ifndef NMK_MM_UNROLL32
 #define NMK_MM_UNROLL32 2   // f32: 2 x 16-byte vectors of each snapshot per thread in flight
 #endif
@@ -280,9 +284,11 @@ static int sm_count() {
   return sms;
 }
 
-static unsigned minmax_grid(uint64_t n) {
+static unsigned minmax_grid(uint64_t n, int dtype = NMK_F64) {
   uint64_t want = (n + 4095) / 4096;  // >= 4096 elements per CTA
-  uint64_t cap = (uint64_t)sm_count() * NMK_MM_CTAS;
+  // f32: fewer, longer-lived threads -- each thread's first elements are all
+  // extreme candidates (exact f64 division), so more elements per thread pay
+  uint64_t cap = (uint64_t)sm_count() * (dtype == NMK_F32 ? NMK_MM_CTAS32 : NMK_MM_CTAS);
   if (want < 1) want = 1;
   return (unsigned)(want < cap ? want : cap);
 }
@@ -292,7 +298,8 @@ static unsigned minmax_grid(uint64_t n) {
 using namespace nmk;
 
 extern "C" size_t nmk_minmax_ws_bytes(uint64_t n) {
-  return 256 + (size_t)minmax_grid(n) * sizeof(MinMax);
+  const unsigned g = std::max(minmax_grid(n, NMK_F64), minmax_grid(n, NMK_F32));
+  return 256 + (size_t)g * sizeof(MinMax);
 }
 
 extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
@@ -300,7 +307,7 @@ extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dty
   if (n == 0 || !base || !cur || !stats || !ws) return set_error(NMK_ERR_ARG, "nmk_minmax: bad argument");
   if (ws_bytes < nmk_minmax_ws_bytes(n)) return set_error(NMK_ERR_ARG, "nmk_minmax: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned grid = minmax_grid(n);
+  unsigned grid = minmax_grid(n, dtype);
   unsigned* ticket = (unsigned*)ws;
   MinMax* partials = (MinMax*)((char*)ws + 256);
   // The ticket word must be zero on entry: callers zero a fresh workspace
