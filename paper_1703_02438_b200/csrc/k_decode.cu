@@ -237,7 +237,13 @@ __device__ __forceinline__ unsigned sentinels_in_vec(const uint4& v) {
          sentinels_in_word<B>(v.w);
 }
 
-constexpr int kDecPairs = 4;   // chunk pairs per warp iteration
+#ifndef NMK_DEC_PAIRS
+#define NMK_DEC_PAIRS 4   // A/B: 2 and 8 pairs, 4 or 8 CTAs/SM all within 1 %
+#endif
+#ifndef NMK_CNT_CTAS
+#define NMK_CNT_CTAS 4
+#endif
+constexpr int kDecPairs = NMK_DEC_PAIRS;   // chunk pairs per warp iteration
 
 // Each warp counts a contiguous run of chunks; half-warp h takes chunks
 // cA + h, cA + h + 2, ... through a cursor advanced without division.
@@ -787,7 +793,7 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   if constexpr (B == 8 || B == 16) {
     const uint64_t per_cta = (uint64_t)(kDecThreads / 32) * 2 * kDecPairs;
     const uint64_t g1 = (geo.nchunks + per_cta - 1) / per_cta;
-    const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 4 ? g1 : (uint64_t)sms * 4);
+    const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * NMK_CNT_CTAS ? g1 : (uint64_t)sms * NMK_CNT_CTAS);
     k_dec_count_wide<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   } else {
     const uint64_t g1 = (geo.nchunks + 7) / 8;
