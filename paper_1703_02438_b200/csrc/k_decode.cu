@@ -237,6 +237,9 @@ __device__ __forceinline__ unsigned sentinels_in_vec(const uint4& v) {
          sentinels_in_word<B>(v.w);
 }
 
+#ifndef NMK_DEC_WIN96
+#define NMK_DEC_WIN96 1   // codes_at: one 96-bit window for VN * B <= 64
+#endif
 #ifndef NMK_DEC_PAIRS
 #define NMK_DEC_PAIRS 4   // A/B: 2 and 8 pairs, 4 or 8 CTAs/SM all within 1 %
 #endif
@@ -375,6 +378,19 @@ __device__ __forceinline__ void codes_at(const uint8_t* pk, int e0, uint32_t (&c
     const int off = bit & 31;
 #pragma unroll
     for (int v = 0; v < VN; ++v) cd[v] = (uint32_t)(x >> (64 - off - (v + 1) * B)) & ((1u << B) - 1u);
+  } else if constexpr (VN * B <= 64 && NMK_DEC_WIN96) {
+    // a 96-bit window (three aligned words) holds the VN codes at any offset
+    // (off + VN*B <= 31 + 64); the stage's +16 pad keeps the third word in bounds
+    const int bit = e0 * B;
+    const int w = (bit >> 5) << 2;
+    const uint32_t a = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w), 0, 0x0123);
+    const uint32_t m = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w + 4), 0, 0x0123);
+    const uint32_t z = __byte_perm(*reinterpret_cast<const uint32_t*>(pk + w + 8), 0, 0x0123);
+    const int off = bit & 31;
+    const unsigned long long top = ((((unsigned long long)a << 32) | m) << off) |
+                                   ((((unsigned long long)z) << off) >> 32);
+#pragma unroll
+    for (int v = 0; v < VN; ++v) cd[v] = (uint32_t)(top >> (64 - (v + 1) * B)) & ((1u << B) - 1u);
   } else {
 #pragma unroll
     for (int v = 0; v < VN; ++v) cd[v] = code_at<B>(pk, e0 + v);
