@@ -575,20 +575,17 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         }
       }
       // ids in [k, sentinel) are errors; impossible with a full code book
+      // ((code + 1) mod 2^B) maps the sentinel to 0 and id c to c + 1, so one
+      // max per element finds the largest non-sentinel id
       if (k < sentinel) {
-        unsigned maxbad = 0;
-        bool anybad = false;
+        uint32_t mx = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q)
 #pragma unroll
-          for (int v = 0; v < VN; ++v)
-            if (code[q][v] - k < sentinel - k) {
-              anybad = true;
-              maxbad = max(maxbad, code[q][v]);
-            }
-        if (anybad) {
+          for (int v = 0; v < VN; ++v) mx = max(mx, (code[q][v] + 1u) & sentinel);
+        if (mx > k) {
           atomicOr(&err->bad_index, 1u);
-          atomicMax(&err->max_bad_index, maxbad);
+          atomicMax(&err->max_bad_index, mx - 1u);
         }
       }
       if (nsent) {   // warp-uniform (from the count pass)

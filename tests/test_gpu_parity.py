@@ -431,3 +431,24 @@ def test_decode_sentinel_counts_vs_oracle(bits, n, frac):
     got = nmk.reconstruct(base, centers, idx, exact, bits=bits)
     want = O.reconstruct(base, centers, idx, exact, bits)
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("bits", [8, 10, 17])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_bad_index_reports_largest_id(bits, dtype):
+    """Ids in [k, 2^B - 1) inside whole chunks (K5's fast path) are reported
+    with the largest such id, as the reference's reconstruct does
+    (core.py:181-187); the sentinel itself is never a bad id."""
+    rng = np.random.default_rng(bits)
+    n = 256 * 64
+    k = 5
+    sentinel = (1 << bits) - 1
+    idx = rng.integers(0, k, n)
+    idx[rng.uniform(size=n) < 0.2] = sentinel
+    bad_pos = rng.choice(n, 7, replace=False)
+    bad_ids = rng.integers(k, sentinel, 7)
+    idx[bad_pos] = bad_ids
+    base = rng.lognormal(0.0, 1.0, n).astype(dtype)
+    exact = rng.normal(size=int((idx == sentinel).sum())).astype(dtype)
+    with pytest.raises(ValueError, match=f"index {int(bad_ids.max())} out of range for {k} centers"):
+        nmk.reconstruct(base, np.linspace(-0.01, 0.01, k), idx, exact, bits=bits)
