@@ -16,7 +16,10 @@
 namespace nmk {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanRounds = 8;                                    // uint4 per lane
+#ifndef NMK_SCAN_ROUNDS
+#define NMK_SCAN_ROUNDS 8   // A/B: 2 and 4 (more, smaller tiles) no faster on cfg2
+#endif
+constexpr int kScanRounds = NMK_SCAN_ROUNDS;                      // uint4 per lane
 constexpr int kScanWarpItems = 32 * 4 * kScanRounds;              // 1024 contiguous counts per warp
 constexpr int kScanTile = (kScanThreads / 32) * kScanWarpItems;   // 8192 per CTA (few tiles: short look-back)
 constexpr unsigned long long kFlagAgg = 1ULL << 62;    // tile aggregate published
