@@ -141,3 +141,52 @@ def test_product_path_does_not_import_oracle():
     for fn in os.listdir(pkg):
         if fn.endswith(".py"):
             assert "oracle" not in open(os.path.join(pkg, fn)).read().replace("no CPU fallback", ""), fn
+
+
+def _swar_model(raw: bytes, bits: int) -> int:
+    """Python model of k_decode.cu lane_sentinels_swar: the lane's bytes as a
+    big-endian 128-bit string, 8 codes as fields from the top; a field of ~X
+    is zero iff the code is the sentinel; ((Z & LO) + LO) | Z) & MSB marks the
+    nonzero fields of a 64-bit word of whole fields."""
+    m64 = (1 << 64) - 1
+    x = int.from_bytes(raw.ljust(16, b"\0"), "big")
+    hi, lo = x >> 64, x & m64
+    fa = 64 // bits
+    sh = fa * bits
+    wb = ((hi << sh) | (lo >> (64 - sh))) & m64
+
+    def fields(nf, msb):
+        m = 0
+        for e in range(nf):
+            low = 64 - (e + 1) * bits
+            m |= (1 << (low + bits - 1)) if msb else (((1 << (bits - 1)) - 1) << low)
+        return m
+
+    def zero_fields(w, nf):
+        z = ~w & m64
+        lom, msb = fields(nf, False), fields(nf, True)
+        t = ((((z & lom) + lom) & m64) | z) & msb
+        return nf - bin(t).count("1")
+
+    return zero_fields(hi, fa) + zero_fields(wb, 8 - fa)
+
+
+@pytest.mark.parametrize("bits", [10, 12, 14])
+def test_swar_sentinel_count_model(bits):
+    """The SWAR sentinel count equals a plain count of all-ones codes for
+    random lanes, all-sentinel lanes and lanes cut short by the block end."""
+    rng = np.random.default_rng(bits)
+    sentinel = (1 << bits) - 1
+    for trial in range(3000):
+        codes = rng.integers(0, 1 << bits, 8)
+        codes[rng.uniform(size=8) < (0.5 if trial % 3 else 1.0)] = sentinel
+        acc = 0
+        for c in codes:
+            acc = (acc << bits) | int(c)
+        raw = acc.to_bytes(bits, "big")
+        keep = bits if trial % 5 else int(rng.integers(0, bits + 1))   # bytes past nbytes read as 0
+        raw = raw[:keep] + b"\0" * (bits - keep)
+        got = _swar_model(raw, bits)
+        full = int.from_bytes(raw, "big")
+        want = sum(((full >> (8 * bits - (e + 1) * bits)) & sentinel) == sentinel for e in range(8))
+        assert got == want
