@@ -38,8 +38,9 @@ METRIC = "compress+decompress GB/s of input (n*L per timestep / (t_compress + t_
 CONFIG_NAME = "cfg2: 512^3 fp64 8^3-block field, E=1e-3, B=8, top-k, 1 MiB index blocks"
 # k_minmax, k_hist_prep, k_hist_dev, k_select, k_encode_keyed, k_encode (exits when the
 # keyed kernel did the work), k_chunk_scan, k_enc_finalize, k_dec_count_wide, k_chunk_scan,
-# k_dec_chunks
-GPU_LAUNCHES_PER_STEP = 11   # K1, prep, K2, K3, K4 keyed + fallback, scan, finalize | count, scan, K5 (ncu launch list)
+# k_dec_chunks x 2 (six- and five-stage rings; the one whose exact-value regime does not match
+# exits at entry)
+GPU_LAUNCHES_PER_STEP = 12   # K1, prep, K2, K3, K4 keyed + fallback, scan, finalize | count, scan, K5 x 2
 
 
 def parse():

@@ -35,6 +35,18 @@ constexpr int kTmaThreads = 32 * kTmaWarps;
 #define NMK_TMA_MINB 4
 #endif
 constexpr int kStages = NMK_STAGES;    // chunks in flight per warp
+#ifndef NMK_STAGES_DENSE
+#define NMK_STAGES_DENSE 5   // A/B: 5 beats 6 by 8-15 % of K5 when sentinels fill most chunks (profiles/README)
+#endif
+constexpr int kStagesDense = NMK_STAGES_DENSE;
+#ifndef NMK_DENSE_DIV
+#define NMK_DENSE_DIV 400    // "dense": more than 1 exact value per 400 elements (cfg2 0.16 % sparse, cfg4 0.5 % dense)
+#endif
+// Which ring depth decodes the stream.  A shallower ring leaves more of the
+// unified shared/L1 array to L1, which serves the exact-value loads.
+__host__ __device__ inline bool dec_dense(uint64_t n_exact, uint64_t n_total) {
+  return n_exact * (uint64_t)NMK_DENSE_DIV > n_total;
+}
 
 struct Seg {
   uint64_t start, count, out;   // global element range, output offset
@@ -332,13 +344,13 @@ template <typename T> struct DVec;
 template <> struct DVec<double> { using V = double2; static constexpr int N = 2; };
 template <> struct DVec<float>  { using V = float4;  static constexpr int N = 4; };
 
-template <typename T, int B>
+template <typename T, int B, int S = kStages>
 struct DecStage {
   static constexpr int kBase = kDChunk * (int)sizeof(T);   // 2048 (f64) / 1024 (f32)
   static constexpr int kPk = 32 * B;                        // a multiple of 16
   static constexpr int kAux = kBase + kPk + 16;             // +16: 8-byte code windows
   static constexpr int kBytes = kAux + 32;                  // rank anchors (4 x u64)
-  static constexpr size_t kSmem = (size_t)kTmaWarps * kStages * kBytes;
+  static constexpr size_t kSmem = (size_t)kTmaWarps * S * kBytes;
 };
 
 // B-bit code of chunk element e from the staged packed bytes (MSB-first).
@@ -455,37 +467,39 @@ __device__ __forceinline__ void cp_async_arrive(unsigned long long* bar) {
 // when all of them landed, so no global load sits on a warp's critical path
 // except the exact values, which are fetched right after the wait (one per
 // lane, coalesced) and handed to the sentinels by shuffle.
-template <typename T, int B>
+template <typename T, int B, int S>
 __global__ void __launch_bounds__(kTmaThreads, NMK_TMA_MINB)
 k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __restrict__ segs, SegParams sp,
              const unsigned long long* __restrict__ offsets, const unsigned long long* __restrict__ prefix_rel,
              const double* __restrict__ centers_g, const T* __restrict__ exact, const T* __restrict__ base,
              T* __restrict__ out, nmk_segment_info* __restrict__ info, nmk_decode_err* __restrict__ err,
-             const nmk_model* __restrict__ model, const unsigned long long* __restrict__ n_exact_dev) {
-  using ST = DecStage<T, B>;
+             const nmk_model* __restrict__ model, const unsigned long long* __restrict__ n_exact_dev,
+             int regime) {
+  using ST = DecStage<T, B, S>;
   constexpr int VN = DVec<T>::N;          // elements per 16-byte vector
   constexpr int Q = kGroup / VN;          // vectors per lane per chunk
   using V = typename DVec<T>::V;
   const unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ __align__(8) unsigned long long bars[kTmaWarps][kStages];
+  __shared__ __align__(8) unsigned long long bars[kTmaWarps][S];
   __shared__ Seg s_segs[kSmemSegs];
-  __shared__ DItem s_items[kTmaWarps][kStages];   // geometry of each staged chunk (written at issue)
+  __shared__ DItem s_items[kTmaWarps][S];   // geometry of each staged chunk (written at issue)
   constexpr bool kOpcSmem = ((1 << B) - 1) <= kOpcMax;
-  double* s_opc = reinterpret_cast<double*>(dsm + DecStage<T, B>::kSmem);   // [2^B - 1] when kOpcSmem
+  double* s_opc = reinterpret_cast<double*>(dsm + DecStage<T, B, S>::kSmem);   // [2^B - 1] when kOpcSmem
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (model) {                       // sync-free path: scalars from the device
     if (model->status != 0) return;
     geo.k = model->k;
   }
   if (n_exact_dev) geo.n_exact = *n_exact_dev;
+  if (regime != 0 && (regime == 2) != dec_dense(geo.n_exact, geo.n_total)) return;   // the other ring runs
   const bool seg_smem = geo.nseg <= kSmemSegs;
   if (!segs)
     for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = sp.s[i];
   else if (seg_smem)
     for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = segs[i];
   if (lane == 0) {
-    for (int st = 0; st < kStages; ++st) mbar_init(&bars[wid][st], 2);
+    for (int st = 0; st < S; ++st) mbar_init(&bars[wid][st], 2);
     mbar_fence_init();
   }
   if constexpr (kOpcSmem) {   // decoder arithmetic (1 + c) (core.py:202-205); codes >= k are errors
@@ -494,7 +508,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   }
   __syncthreads();
   const Seg* SG = (seg_smem || !segs) ? s_segs : segs;
-  uint8_t* wst = dsm + (size_t)wid * kStages * ST::kBytes;
+  uint8_t* wst = dsm + (size_t)wid * S * ST::kBytes;
   const uint32_t sentinel = (1u << B) - 1u;
   const uint32_t k = (uint32_t)geo.k;
   const bool out_al = ((uintptr_t)out & 15) == 0;
@@ -515,14 +529,14 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     cp_async_arrive(&bars[wid][st]);
   };
   if (lane == 0)
-    for (int st = 0; st < kStages; ++st)
+    for (int st = 0; st < S; ++st)
       if (gw + st * nw < geo.nitems) issue(st, gw + st * nw);
   __syncwarp();
 
   for (uint64_t kk = 0;; ++kk) {
     const uint64_t it = gw + kk * nw;
     if (it >= geo.nitems) break;
-    const int st = (int)(kk % kStages);
+    const int st = (int)(kk % S);
     uint8_t* sb = wst + st * ST::kBytes;
     const DItem t = s_items[wid][st];
     T bv[Q][VN];
@@ -535,7 +549,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
           bv[q][v] = (e >= t.lo_rel && e < t.hi_rel) ? __ldg(base + (t.oi0 + e)) : T(0);
         }
     }
-    mbar_wait(&bars[wid][st], (unsigned)((kk / kStages) & 1));
+    mbar_wait(&bars[wid][st], (unsigned)((kk / S) & 1));
     // the chunk's rank anchor (codec.py:231-236: prefix of the segment's first
     // block + sentinels counted since) and its sentinel count
     const unsigned long long* ax = reinterpret_cast<const unsigned long long*>(sb + ST::kAux);
@@ -647,7 +661,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
       __syncwarp();
       if (lane == 0) {
         fence_proxy_async_smem();
-        const uint64_t nx = it + (uint64_t)kStages * nw;
+        const uint64_t nx = it + (uint64_t)S * nw;
         if (nx < geo.nitems) issue(st, nx);
       }
       continue;
@@ -745,11 +759,11 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
         if (t.last) atomicAdd(&info[t.seg].n_sentinel, chunk_off + up);
       }
     }
-    // stage consumed: refill it kStages chunks ahead
+    // stage consumed: refill it S chunks ahead
     __syncwarp();
     if (lane == 0) {
       fence_proxy_async_smem();
-      const uint64_t nx = it + (uint64_t)kStages * nw;
+      const uint64_t nx = it + (uint64_t)S * nw;
       if (nx < geo.nitems) issue(st, nx);
     }
   }
@@ -796,6 +810,30 @@ static DecodePlan decode_plan(const uint64_t* st, const uint64_t* ct, int nseg, 
   return p;
 }
 
+template <typename T, int B, int S>
+static void launch_dec_chunks(const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, const SegParams& sp,
+                              const unsigned long long* offsets, const unsigned long long* prefix_rel,
+                              const double* centers, const void* exact, const void* base, void* out,
+                              nmk_segment_info* info, nmk_decode_err* err, const nmk_model* model,
+                              const unsigned long long* n_exact_dev, int regime, cudaStream_t s) {
+  const int sms = sm_count_d();
+  const size_t smem = DecStage<T, B, S>::kSmem + (((1 << B) - 1) <= kOpcMax ? (size_t)((1 << B) - 1) * 8 : 0);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dec_chunks<T, B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B, S>, kTmaThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)sms * per_sm;
+  const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;
+  if (grid > need) grid = need;
+  k_dec_chunks<T, B, S><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, sp, offsets, prefix_rel, centers,
+                                                                   (const T*)exact, (const T*)base, (T*)out, info,
+                                                                   err, model, n_exact_dev, regime);
+}
+
 template <typename T, int B>
 static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Seg* segs, const SegParams& sp,
                           uint32_t* counts, unsigned long long* offsets, void* scan_ws,
@@ -814,21 +852,22 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
     k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
   }
   chunk_scan(counts, geo.nchunks, offsets, scan_ws, s);
-  const size_t smem = DecStage<T, B>::kSmem + (((1 << B) - 1) <= kOpcMax ? (size_t)((1 << B) - 1) * 8 : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dec_chunks<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  // The host knows the exact count on the host-scalar path and picks one ring.
+  // The sync-free path only knows it on the device: both rings launch and
+  // the one whose regime does not match exits at entry.
+  if (!n_exact_dev) {
+    if (dec_dense(geo.n_exact, geo.n_total))
+      launch_dec_chunks<T, B, kStagesDense>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
+                                            info, err, model, n_exact_dev, 0, s);
+    else
+      launch_dec_chunks<T, B, kStages>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out, info,
+                                       err, model, n_exact_dev, 0, s);
+  } else {
+    launch_dec_chunks<T, B, kStages>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out, info,
+                                     err, model, n_exact_dev, 1, s);
+    launch_dec_chunks<T, B, kStagesDense>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
+                                          info, err, model, n_exact_dev, 2, s);
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B>, kTmaThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (uint64_t)sms * per_sm;
-  const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;
-  if (grid > need) grid = need;
-  k_dec_chunks<T, B><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, sp, offsets, prefix_rel, centers,
-                                                                (const T*)exact, (const T*)base, (T*)out, info,
-                                                                err, model, n_exact_dev);
 }
 
 template <typename T>
