@@ -452,3 +452,18 @@ def test_bad_index_reports_largest_id(bits, dtype):
     exact = rng.normal(size=int((idx == sentinel).sum())).astype(dtype)
     with pytest.raises(ValueError, match=f"index {int(bad_ids.max())} out of range for {k} centers"):
         nmk.reconstruct(base, np.linspace(-0.01, 0.01, k), idx, exact, bits=bits)
+
+
+@pytest.mark.parametrize("zero_frac", [0.0, 0.0020, 0.0030, 0.05])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_decode_ring_regimes(zero_frac, dtype):
+    """K5 picks its TMA ring by exact-value density (1 per 400 elements,
+    `dec_dense` in k_decode.cu): streams on both sides of the threshold decode
+    bit-exactly like the oracle, in full and in partial ranges."""
+    rng = np.random.default_rng(1703)
+    n = (1 << 20) + 4093
+    base = rng.lognormal(0.0, 1.0, n).astype(dtype)
+    base[rng.random(n) < zero_frac] = 0
+    r = 0.9 * rng.normal(0, 0.002, n) + 0.1 * rng.uniform(-0.05, 0.05, n)
+    cur = (base * (1 + r)).astype(dtype)
+    _check_against_oracle(base, cur, 1e-3, 8, ranges=[(0, 1000), (12345, 65536), (n - 777, 777)])
