@@ -119,7 +119,9 @@ int nmk_hist_merge(unsigned long long* keys, unsigned long long* counts, uint64_
 
 /* -- K3: single-CTA top-k + auto-B + quantisation + cuts
  *        (binning.py:135-152,155-206; pipeline.py:112-124,163-167,229).
- * keys == NULL selects the dense form (ordinal = array index, nbins = m_max).
+ * keys == NULL selects the dense form (ordinal = array index, nbins = m_max);
+ * counts then holds nbins + 1 entries, the last being K2's out-of-span
+ * tripwire, which must be 0 (model->status = NMK_ERR_ARG otherwise).
  * nruns: device count for the sparse form (NULL for dense).
  * bits < 0 selects B automatically over [2, 16].
  * centers/cuts: capacity cap_k doubles; centers_t: cap_k elements of dtype. */

@@ -195,7 +195,7 @@ def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_off
     base_inc = int(pre[0])
     d_prefix_rel = torch.from_numpy(pre - base_inc).to(dev)
     d_centers = torch.tensor(np.asarray(centers64, dtype=np.float64), device=dev)   # copies (read-only ok)
-    ex = np.array(exact[max(base_inc - exact_offset, 0):], copy=True)
+    ex = np.array(exact[max(base_inc - exact_offset, 0):], copy=True)   # covering blocks only
     if base_inc < exact_offset:
         raise ValueError("exact values start after the covering block")
     d_exact = torch.from_numpy(ex).to(dev) if ex.size else torch.empty(0, dtype=_tdt(base.dtype), device=dev)
@@ -252,9 +252,17 @@ def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> n
 def partial_decode(variable, start: int, count: int, base_reconstructed) -> np.ndarray:
     """Reconstruct ``[start, start + count)`` touching only the covering
     blocks (codec.py:242-258); bit-identical to a full-decode slice."""
+    epb = variable.elements_per_block
+
+    def inc_slice(lo: int):
+        # only the exact values of the covering blocks travel to the device
+        last = (start + count - 1) // epb if count else start // epb
+        hi = int(variable.incompressible_prefix[last + 1]) if last + 1 < variable.nblocks \
+            else variable.n_incompressible
+        return variable.incompressible_table[lo:max(hi, lo)], lo
+
     return _decode_range(variable, start, count, base_reconstructed,
-                         lambda b: _block_bytes_of(variable, b),
-                         lambda lo: (variable.incompressible_table[lo:], lo))
+                         lambda b: _block_bytes_of(variable, b), inc_slice)
 
 
 def partial_decode_file(handle, start: int, count: int, base_reconstructed) -> np.ndarray:

@@ -43,9 +43,11 @@ constexpr int kStagesDense = NMK_STAGES_DENSE;
 #define NMK_DENSE_DIV 400    // "dense": more than 1 exact value per 400 elements (cfg2 0.16 % sparse, cfg4 0.5 % dense)
 #endif
 // Which ring depth decodes the stream.  A shallower ring leaves more of the
-// unified shared/L1 array to L1, which serves the exact-value loads.
-__host__ __device__ inline bool dec_dense(uint64_t n_exact, uint64_t n_total) {
-  return n_exact * (uint64_t)NMK_DENSE_DIV > n_total;
+// unified shared/L1 array to L1, which serves the exact-value loads.  The
+// density is the exact values available over the elements of the decoded
+// chunk span (not the variable's n: a rank or a partial range decodes less).
+__host__ __device__ inline bool dec_dense(uint64_t n_exact, uint64_t span_chunks) {
+  return n_exact * (uint64_t)NMK_DENSE_DIV > span_chunks * 256ULL;
 }
 
 struct Seg {
@@ -492,7 +494,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     geo.k = model->k;
   }
   if (n_exact_dev) geo.n_exact = *n_exact_dev;
-  if (regime != 0 && (regime == 2) != dec_dense(geo.n_exact, geo.n_total)) return;   // the other ring runs
+  if (regime != 0 && (regime == 2) != dec_dense(geo.n_exact, geo.nchunks)) return;   // the other ring runs
   const bool seg_smem = geo.nseg <= kSmemSegs;
   if (!segs)
     for (int i = threadIdx.x; i < geo.nseg; i += kTmaThreads) s_segs[i] = sp.s[i];
@@ -769,16 +771,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   }
 }
 
-static int sm_count_d() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+static int sm_count_d() { return sm_count(); }
 
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -818,11 +811,7 @@ static void launch_dec_chunks(const uint8_t* packed, const DecodeGeom& geo, cons
                               const unsigned long long* n_exact_dev, int regime, cudaStream_t s) {
   const int sms = sm_count_d();
   const size_t smem = DecStage<T, B, S>::kSmem + (((1 << B) - 1) <= kOpcMax ? (size_t)((1 << B) - 1) * 8 : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dec_chunks<T, B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_dyn_smem(k_dec_chunks<T, B, S>, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B, S>, kTmaThreads, smem);
   if (per_sm < 1) per_sm = 1;
@@ -856,7 +845,7 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   // The sync-free path only knows it on the device: both rings launch and
   // the one whose regime does not match exits at entry.
   if (!n_exact_dev) {
-    if (dec_dense(geo.n_exact, geo.n_total))
+    if (dec_dense(geo.n_exact, geo.nchunks))
       launch_dec_chunks<T, B, kStagesDense>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
                                             info, err, model, n_exact_dev, 0, s);
     else

@@ -467,11 +467,7 @@ extern "C" int nmk_deflate(const uint8_t* packed, uint64_t block_stride, uint64_
   uint32_t* seg_len = (uint32_t*)(wb + p.off_len);
   unsigned long long* offsets = (unsigned long long*)(wb + p.off_offsets);
   const size_t smem = (size_t)kDefThreads * kDefHash * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_deflate_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_dyn_smem(k_deflate_segments, smem);
   const uint64_t g1 = (p.nseg + kDefThreads - 1) / kDefThreads;
   k_deflate_segments<<<(unsigned)g1, kDefThreads, smem, s>>>(packed, block_stride, nblocks, block_len, last_len,
                                                              seg_bytes, (uint32_t)p.segs_per_block, scratch,

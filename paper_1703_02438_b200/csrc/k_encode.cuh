@@ -1132,16 +1132,7 @@ k_encode_keyed(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom
                                              counts, wbytes[threadIdx.x >> 5], recon, kg, kring, kbars, slow, rec);
 }
 
-static int sm_count_e() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+static int sm_count_e() { return sm_count(); }
 
 template <typename T, int B, bool kRecon>
 static void launch_encode_k(const void* base, const void* cur, const EncodeGeom& geo, const double* centers,
@@ -1150,11 +1141,7 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
                             cudaStream_t s) {
   const bool smem_ok = k_cap <= kSmemCuts + 1;
   const size_t smem = smem_ok ? (size_t)(k_cap + 2) * 8 : 0;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_encode<T, B, kRecon>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  ensure_dyn_smem(k_encode<T, B, kRecon>, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode<T, B, kRecon>, kEncThreads, smem);
   if (per_sm < 1) per_sm = 1;
@@ -1163,11 +1150,7 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
   if (grid > need) grid = need;
   if (kx.keys && model && smem_ok) {
     const size_t smem_k = keyed_smem_bytes(k_cap);
-    static size_t attr_k = 0;
-    if (smem_k > attr_k) {
-      cudaFuncSetAttribute(k_encode_keyed<T, B, kRecon>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
-      attr_k = smem_k;
-    }
+    ensure_dyn_smem(k_encode_keyed<T, B, kRecon>, smem_k);
     int per_sm_k = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_k, k_encode_keyed<T, B, kRecon>, kEncThreads, smem_k);
     if (per_sm_k < 1) per_sm_k = 1;

@@ -265,16 +265,7 @@ __global__ void k_valid_end(const unsigned long long* __restrict__ keys, uint64_
   }
 }
 
-static int sm_count_h() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+static int sm_count_h() { return sm_count(); }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -1056,12 +1047,8 @@ extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, const float
   // 48 KB of counters for the pair paths; the key path uses 32 KB of
   // counters + the per-warp TMA key stages in the same allocation
   const size_t smem = std::max<size_t>(kDevSmemBins * 4, kKeySmemBins * 4 + (kHistThreads / 32) * kKeyStages * kKeyTile * 4);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_hist_dev<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_hist_dev<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_dyn_smem(k_hist_dev<double>, smem);
+  ensure_dyn_smem(k_hist_dev<float>, smem);
   // one resident wave: the grid-stride loops split the work evenly over it
   static int per_sm = 0;
   if (!per_sm) {

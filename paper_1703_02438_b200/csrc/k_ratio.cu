@@ -273,17 +273,6 @@ __global__ void k_ratio(const T* __restrict__ base, const T* __restrict__ cur, u
   }
 }
 
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
 static unsigned minmax_grid(uint64_t n, int dtype = NMK_F64) {
   uint64_t want = (n + 4095) / 4096;  // >= 4096 elements per CTA
   // f32: fewer, longer-lived threads -- each thread's first elements are all

@@ -99,6 +99,10 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
       return;
     }
   }
+  if (!keys && counts[Mv] != 0) {   // dense form: K2's out-of-span tripwire slot must be empty
+    if (tid == 0) { model->status = NMK_ERR_ARG; model->k = 0; model->m_selectable = 0; }
+    return;
+  }
   BinView bv{keys, counts, Mv, st->gmin, width, nullptr};
   const uint64_t M = bv.m;
   if ((m_max == 0 && !keys) ? M <= kSelCache : m_max <= kSelCache) {   // passes then read shared memory
@@ -324,12 +328,8 @@ extern "C" int nmk_select(const unsigned long long* keys, const unsigned long lo
   if (keys && !nruns) return set_error(NMK_ERR_ARG, "nmk_select: sparse form needs nruns");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = (m_max == 0 && !keys) ? kSelCache * 8 : (m_max <= kSelCache ? (size_t)m_max * 8 : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelCache * 8));
-    cudaFuncSetAttribute(k_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelCache * 8));
-    attr = true;
-  }
+  ensure_dyn_smem(k_select<double>, kSelCache * 8);
+  ensure_dyn_smem(k_select<float>, kSelCache * 8);
   if (dtype == NMK_F64)
     k_select<double><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
                                                centers, cuts, (double*)centers_t, cap_k, model);

@@ -316,4 +316,12 @@ struct FastDiv {
 namespace nmk {
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the current device if
+// `bytes` exceeds what was set there before (the attribute is per device, so
+// one process driving several GPUs sets it once per device); defined in abi.cu.
+void ensure_dyn_smem(const void* func, size_t bytes);
+template <typename F>
+inline void ensure_dyn_smem(F* func, size_t bytes) { ensure_dyn_smem(reinterpret_cast<const void*>(func), bytes); }
+// multiprocessor count of the current device (cached per device)
+int sm_count();
 }  // namespace nmk

@@ -286,6 +286,8 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
     model = _read_struct(model_t, N.NmkModel)
     if model.status == N.NMK_ERR_EMPTY_HIST:
         raise N.NativeError(N.NMK_ERR_EMPTY_HIST, "empty histogram")
+    if model.status == N.NMK_ERR_ARG and form == "dense":
+        raise N.NativeError(N.NMK_ERR_ARG, "histogram ordinal beyond the dense span (K2 tripwire)")
     if model.status != 0:
         raise N.NativeError(model.status, "nmk_select failed")
     if form == "dense" and n_local > 0:

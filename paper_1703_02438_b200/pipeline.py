@@ -392,7 +392,8 @@ class StreamCompressor:
                 "h_packed": torch.empty(pipe.packed.numel(), dtype=torch.uint8, pin_memory=True),
                 "h_exact": torch.empty(max(self.n // 64, 1), dtype=self.torch_dtype, pin_memory=True),
                 "h_prefix": torch.empty(pipe.prefix.numel(), dtype=torch.int64, pin_memory=True),
-                "h_scal": torch.empty(4 + pipe.model.numel() + 1, dtype=torch.int64, pin_memory=True),
+                # stats | model | n_inc | decode err word | segment info (inc_before, n_sentinel)
+                "h_scal": torch.empty(4 + pipe.model.numel() + 1 + 2 + 2, dtype=torch.int64, pin_memory=True),
                 "h_centers": torch.empty(pipe.k_cap, dtype=self.torch_dtype, pin_memory=True),
                 "h_out": torch.empty(self.n, dtype=self.torch_dtype, pin_memory=True),
                 "ev_in": torch.cuda.Event(), "ev_cmp": torch.cuda.Event(), "ev_out": torch.cuda.Event(),
@@ -425,7 +426,10 @@ class StreamCompressor:
             sl["h_prefix"].copy_(p.prefix, non_blocking=True)
             sl["h_scal"][:4].copy_(p.stats, non_blocking=True)
             sl["h_scal"][4:4 + p.model.numel()].copy_(p.model, non_blocking=True)
-            sl["h_scal"][-1:].copy_(p.n_inc, non_blocking=True)
+            m = 4 + p.model.numel()
+            sl["h_scal"][m:m + 1].copy_(p.n_inc, non_blocking=True)
+            sl["h_scal"][m + 1:m + 3].copy_(p.err, non_blocking=True)
+            sl["h_scal"][m + 3:m + 5].copy_(p.seg_info, non_blocking=True)
             sl["h_centers"].copy_(p.centers_t, non_blocking=True)
             sl["h_out"].copy_(sl["out"], non_blocking=True)
             sl["ev_out"].record(self.s_d2h)
@@ -438,7 +442,8 @@ class StreamCompressor:
         sl["ev_out"].synchronize()
         p = sl["pipe"]
         scal = sl["h_scal"].numpy()
-        n_inc = int(scal[-1])
+        m = 4 + p.model.numel()
+        n_inc = int(scal[m])
         if n_inc > sl["h_exact"].numel():
             sl["h_exact"] = torch.empty(n_inc, dtype=self.torch_dtype, pin_memory=True)
         if n_inc:
@@ -446,13 +451,20 @@ class StreamCompressor:
                 sl["h_exact"][:n_inc].copy_(p.exact[:n_inc], non_blocking=True)
             self.s_x.synchronize()
         self.last_d2h_bytes = (p.packed.numel() + n_inc * self.np_dtype.itemsize + p.prefix.numel() * 8
-                               + (4 + p.model.numel() + 1) * 8 + p.k_cap * self.np_dtype.itemsize
+                               + sl["h_scal"].numel() * 8 + p.k_cap * self.np_dtype.itemsize
                                + self.n * self.np_dtype.itemsize)
-        model = N.NmkModel.from_buffer_copy(scal[4:4 + p.model.numel()].tobytes()[: ctypes.sizeof(N.NmkModel)])
+        model = N.NmkModel.from_buffer_copy(scal[4:m].tobytes()[: ctypes.sizeof(N.NmkModel)])
         if model.status == N.NMK_ERR_NEEDS_SPARSE:
             return self._general_path(sl)
+        if model.status == N.NMK_ERR_ARG:
+            raise PipelineError("binning", "histogram ordinal beyond the dense span (K2 tripwire)")
         if model.status != 0:
             raise PipelineError("binning", f"sync-free pipeline status {model.status}")
+        err = N.NmkDecodeErr.from_buffer_copy(scal[m + 1:m + 3].tobytes())
+        n_sent = int(scal[m + 4])
+        if err.bad_index or err.exhausted or n_sent != n_inc:
+            raise PipelineError("assign_index", f"decode of the fresh encoding disagrees with it: bad_index="
+                                f"{err.bad_index} exhausted={err.exhausted} sentinels={n_sent} n_inc={n_inc}")
         k = int(model.k)
         enc = HostEncoding(self.n, self.np_dtype, p.bits, k, p.epb, p.nblocks, p.stride, p.b0,
                            sl["h_packed"].numpy(), sl["h_exact"].numpy()[:n_inc],
