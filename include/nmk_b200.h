@@ -117,6 +117,21 @@ size_t nmk_hist_merge_ws_bytes(uint64_t n_in);
 int nmk_hist_merge(unsigned long long* keys, unsigned long long* counts, uint64_t n_in,
                    unsigned long long* nruns, void* ws, size_t ws_bytes, void* stream);
 
+/* Histograms of a ratio ARRAY (binning.histogram_of / build_histogram,
+ * binning.py:102-116; merge_histograms, binning.py:119-132) for callers that
+ * already hold ratios.  ordinals/counts receive the sorted distinct ordinals
+ * floor(RN(RN(r - origin) / width)) as f64 (np.unique order: -0 merged into
+ * +0, NaN last, one NaN bin) and their counts; *nruns their number.
+ * valid (nullable, u8[n]): elements with 0 are excluded.
+ * nmk_hist_merge_values sorts and sums gathered (ordinal, count) pairs in
+ * place (n_in entries) -- the device form of merge_histograms. */
+size_t nmk_hist_values_ws_bytes(uint64_t n);
+int nmk_hist_values(const double* ratios, const uint8_t* valid, uint64_t n, double origin, double width,
+                    double* ordinals, unsigned long long* counts, unsigned long long* nruns,
+                    void* ws, size_t ws_bytes, void* stream);
+int nmk_hist_merge_values(double* ordinals, unsigned long long* counts, uint64_t n_in,
+                          unsigned long long* nruns, void* ws, size_t ws_bytes, void* stream);
+
 /* -- K3: single-CTA top-k + auto-B + quantisation + cuts
  *        (binning.py:135-152,155-206; pipeline.py:112-124,163-167,229).
  * keys == NULL selects the dense form (ordinal = array index, nbins = m_max);
@@ -131,6 +146,27 @@ int nmk_select(const unsigned long long* keys, const unsigned long long* counts,
                int bits, uint64_t n_total, int dtype,
                double* centers, double* cuts, void* centers_t, uint64_t cap_k,
                nmk_model* model, void* stream);
+
+/* Coverage table of select_index_length (binning._coverage_by_bits,
+ * binning.py:165-174): coverage[B - bits_lo] = total count of the
+ * min(2^B - 1, m) most populous selectable bins, B in [bits_lo, bits_hi]
+ * (2 <= lo <= hi <= 30).  Same histogram forms and stats as nmk_select
+ * (stats->gmin = origin, stats->nvalid > 0); model is scratch (status
+ * NMK_ERR_EMPTY_HIST and zero coverage when no bin is selectable). */
+int nmk_coverage(const unsigned long long* keys, const unsigned long long* counts, uint64_t m_max,
+                 const unsigned long long* nruns, const nmk_stats* stats, double width,
+                 int bits_lo, int bits_hi, unsigned long long* coverage, nmk_model* model, void* stream);
+
+/* Nearest center and compressibility on a ratio array (binning.nearest_center
+ * / compressible_mask, binning.py:287-301,350-359): idx = searchsorted(cuts,
+ * v, 'left') with cuts = RN(0.5*RN(c[i]+c[i+1])) (NaN -> k-1; k == 1 -> 0),
+ * dist = |v - c[idx]|, flag = valid && dist <= tolerance.  centers: k
+ * strictly increasing f64.  dist is nullable. */
+int nmk_nearest_center(const double* values, uint64_t n, const double* centers, int k,
+                       long long* idx, double* dist, void* stream);
+int nmk_compressible_mask(const double* ratios, const uint8_t* valid, uint64_t n,
+                          const double* centers, int k, double tolerance,
+                          uint8_t* flags, long long* idx, void* stream);
 
 /* -- K4: fused classify + round-trip filter + B-bit pack + stable compaction
  *        (binning.py:287-301,350-359; pipeline.py:143-160,238-288; codec.py:83-92)

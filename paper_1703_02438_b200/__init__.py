@@ -9,6 +9,8 @@ fallback: without the library or a CUDA device the entry points raise
 """
 
 from ._native import NativeError, NativeUnavailable
+from .binning import (BinModel, Histogram, build_histogram, compressible_mask, merge_histograms, nearest_center,
+                      select_index_length, top_k_bins)
 from .codec import (BlockLayout, CodecError, decode_all_indices, pack_block, partial_decode, partial_decode_file,
                     unpack_block)
 from .container import CompressedVariable, ContainerError, VariableHandle, read_file, scan_file, write_file
@@ -20,6 +22,8 @@ from .pipeline import (PhaseTimings, PipelineConfig, PipelineError, compress_pai
 __version__ = "0.1.0"
 
 __all__ = [
+    "BinModel", "Histogram", "build_histogram", "compressible_mask", "merge_histograms", "nearest_center",
+    "select_index_length", "top_k_bins",
     "BlockLayout", "ChangeRatioField", "CodecError", "CompressedVariable", "ContainerError",
     "NativeError", "NativeUnavailable", "PhaseTimings", "PipelineConfig", "PipelineError",
     "TemporalPair", "Tolerance", "compress_pair", "compress_series", "compute_change_ratios",

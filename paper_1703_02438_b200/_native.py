@@ -66,6 +66,12 @@ SIGNATURES = {
     "nmk_hist_sparse": (i32, [vp, vp, u64, i32, vp, dbl, vp, vp, vp, vp, sz, vp]),
     "nmk_hist_merge_ws_bytes": (sz, [u64]),
     "nmk_hist_merge": (i32, [vp, vp, u64, vp, vp, sz, vp]),
+    "nmk_hist_values_ws_bytes": (sz, [u64]),
+    "nmk_hist_values": (i32, [vp, vp, u64, dbl, dbl, vp, vp, vp, vp, sz, vp]),
+    "nmk_hist_merge_values": (i32, [vp, vp, u64, vp, vp, sz, vp]),
+    "nmk_coverage": (i32, [vp, vp, u64, vp, vp, dbl, i32, i32, vp, vp, vp]),
+    "nmk_nearest_center": (i32, [vp, u64, vp, i32, vp, vp, vp]),
+    "nmk_compressible_mask": (i32, [vp, vp, u64, vp, i32, dbl, vp, vp, vp]),
     "nmk_select": (i32, [vp, vp, u64, vp, vp, dbl, dbl, i32, u64, i32, vp, vp, vp, u64, vp, vp]),
     "nmk_encode_ws_bytes": (sz, [u64, u64, u64, i32]),
     "nmk_encode": (i32, [vp, vp, u64, u64, u64, i32, vp, vp, i32, i32, dbl, dbl, u64, vp, u64, vp,

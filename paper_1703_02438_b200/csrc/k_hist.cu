@@ -265,6 +265,45 @@ __global__ void k_valid_end(const unsigned long long* __restrict__ keys, uint64_
   }
 }
 
+// ---- ratio-array histograms (binning.histogram_of / merge_histograms) -----
+// Keys are an order-preserving u64 image of the f64 ordinal, so negative,
+// infinite and NaN ordinals (a Histogram built against any origin) sort like
+// np.unique: -inf < ... < -0 == +0 < ... < +inf < NaN (one NaN bin).
+// ~0ULL stays the "excluded" marker (no canonical value maps to it).
+__device__ __forceinline__ unsigned long long ord_key(double q) {
+  q = __dadd_rn(q, 0.0);                                   // -0 -> +0
+  unsigned long long b = (unsigned long long)__double_as_longlong(q);
+  if (q != q) b = 0x7ff8000000000000ULL;                   // one canonical NaN
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double key_ord(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// floor(RN(RN(r - origin) / width)) per element (binning.py:113); elements
+// with valid[j] == 0 are excluded (build_histogram's valid_ratios, core.py:99)
+__global__ void __launch_bounds__(256)
+k_ratio_keys(const double* __restrict__ ratios, const uint8_t* __restrict__ valid, uint64_t n, double origin,
+             double width, unsigned long long* __restrict__ keys) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    if (valid && !valid[j]) { keys[j] = ~0ULL; continue; }
+    keys[j] = ord_key(floor(__ddiv_rn(__dsub_rn(ratios[j], origin), width)));
+  }
+}
+
+// in place: each element's f64 ordinal is replaced by its key
+__global__ void k_ords_to_keys(unsigned long long* keys, uint64_t n) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+    keys[j] = ord_key(__longlong_as_double((long long)keys[j]));
+}
+
+__global__ void k_keys_to_ords(unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ nruns) {
+  const uint64_t nr = *nruns;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nr; j += (uint64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<double*>(keys)[j] = key_ord(keys[j]);
+}
+
 static int sm_count_h() { return sm_count(); }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -458,6 +497,51 @@ extern "C" int nmk_hist_merge(unsigned long long* keys, unsigned long long* coun
   if (g2 > (unsigned)sm_count_h() * 8) g2 = sm_count_h() * 8;
   k_rle_lengths_dev<<<g2, 256, 0, s>>>(w.run_start, nruns, w.scal, w.incl, counts);
   return check_launch("nmk_hist_merge");
+}
+
+extern "C" size_t nmk_hist_values_ws_bytes(uint64_t n) { return rle_layout(n, false, nullptr).total; }
+
+extern "C" int nmk_hist_values(const double* ratios, const uint8_t* valid, uint64_t n, double origin, double width,
+                               double* ordinals, unsigned long long* counts, unsigned long long* nruns, void* ws,
+                               size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!ordinals || !counts || !nruns) return set_error(NMK_ERR_ARG, "nmk_hist_values: bad argument");
+  if (n == 0) {
+    cudaMemsetAsync(nruns, 0, 8, s);
+    return check_launch("nmk_hist_values");
+  }
+  if (!ratios || !ws) return set_error(NMK_ERR_ARG, "nmk_hist_values: bad argument");
+  RleWs w = rle_layout(n, false, ws);
+  if (ws_bytes < w.total) return set_error(NMK_ERR_ARG, "nmk_hist_values: workspace too small");
+  unsigned grid = (unsigned)((n + 255) / 256);
+  if (grid > (unsigned)sm_count_h() * 8) grid = sm_count_h() * 8;
+  k_ratio_keys<<<grid, 256, 0, s>>>(ratios, valid, n, origin, width, w.keys_a);
+  size_t tb = w.cub_bytes;
+  cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keys_a, w.keys_b, n, 0, 64, s);
+  unsigned long long* out_keys = reinterpret_cast<unsigned long long*>(ordinals);
+  rle_tail(w, n, false, out_keys, counts, nruns, s);
+  k_rle_lengths_dev<<<grid, 256, 0, s>>>(w.run_start, nruns, w.scal, nullptr, counts);
+  k_keys_to_ords<<<grid, 256, 0, s>>>(out_keys, nruns);
+  return check_launch("nmk_hist_values");
+}
+
+extern "C" int nmk_hist_merge_values(double* ordinals, unsigned long long* counts, uint64_t n_in,
+                                     unsigned long long* nruns, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!nruns) return set_error(NMK_ERR_ARG, "nmk_hist_merge_values: bad argument");
+  if (n_in == 0) {
+    cudaMemsetAsync(nruns, 0, 8, s);
+    return check_launch("nmk_hist_merge_values");
+  }
+  if (!ordinals || !counts || !ws) return set_error(NMK_ERR_ARG, "nmk_hist_merge_values: bad argument");
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(ordinals);
+  unsigned grid = (unsigned)((n_in + 255) / 256);
+  if (grid > (unsigned)sm_count_h() * 8) grid = sm_count_h() * 8;
+  k_ords_to_keys<<<grid, 256, 0, s>>>(keys, n_in);
+  const int rc = nmk_hist_merge(keys, counts, n_in, nruns, ws, ws_bytes, stream);
+  if (rc) return rc;
+  k_keys_to_ords<<<grid, 256, 0, s>>>(keys, nruns);
+  return check_launch("nmk_hist_merge_values");
 }
 
 // ---- sync-free dense histogram: the span is decided on the device ---------

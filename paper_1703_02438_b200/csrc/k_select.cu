@@ -29,7 +29,8 @@ namespace nmk {
 #endif
 constexpr int kSelThreads = NMK_SEL_THREADS;
 constexpr int kAutoLo = 2, kAutoHi = 16;           // binning.py:22
-constexpr int kNSel = kAutoHi - kAutoLo + 1;       // 15 simultaneous selects
+constexpr int kNSel = kAutoHi - kAutoLo + 1;       // 15 simultaneous selects (auto B)
+constexpr int kNSelMax = 29;                       // B = 2..30: select_index_length's widest range
 
 constexpr uint64_t kSelCache = 8192;  // bins whose selectable counts live in smem
 
@@ -55,22 +56,26 @@ struct BinView {
 template <typename T>
 __device__ __forceinline__ double quantize(double c) { return to_f64(narrow<T>(c)); }
 
-template <typename T>
+// NS = radix-select slots compiled in; auto B (bits_cfg < 0) runs auto_n of
+// them for B = auto_lo .. auto_lo + auto_n - 1.  cov_out != null: coverage
+// only (binning._coverage_by_bits) -- write the covered counts and stop.
+template <typename T, int NS>
 __global__ void __launch_bounds__(kSelThreads)
 k_select(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ counts,
          uint64_t m_max, const unsigned long long* __restrict__ nruns,
          const nmk_stats* __restrict__ st, double width, double tolerance, int bits_cfg,
          uint64_t n_total, double* __restrict__ centers, double* __restrict__ cuts,
-         T* __restrict__ centers_t, uint64_t cap_k, nmk_model* __restrict__ model) {
+         T* __restrict__ centers_t, uint64_t cap_k, nmk_model* __restrict__ model,
+         int auto_lo, int auto_n, unsigned long long* __restrict__ cov_out) {
   typedef cub::BlockReduce<unsigned long long, kSelThreads> BRed;
   typedef cub::BlockScan<unsigned, kSelThreads> BScan;
   __shared__ union {
     typename BRed::TempStorage red;
     typename BScan::TempStorage scan;
   } tmp;
-  __shared__ unsigned hist[kNSel][256];
-  __shared__ unsigned long long s_prefix[kNSel], s_mask[kNSel], s_left[kNSel], s_kk[kNSel];
-  __shared__ unsigned long long s_cov[kNSel];
+  __shared__ unsigned hist[NS][256];
+  __shared__ unsigned long long s_prefix[NS], s_mask[NS], s_left[NS], s_kk[NS];
+  __shared__ unsigned long long s_cov[NS];
   __shared__ unsigned long long s_bcast[4];
   __shared__ int s_bits;
   __shared__ double s_prev;
@@ -78,6 +83,11 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
 
   const int tid = threadIdx.x;
   const uint64_t nvalid = st->nvalid;
+  if (nvalid == 0 && cov_out) {   // coverage of an empty histogram
+    if (tid < auto_n) cov_out[tid] = 0;
+    if (tid == 0) { model->status = NMK_ERR_EMPTY_HIST; model->k = 0; model->m_selectable = 0; }
+    return;
+  }
   if (nvalid == 0) {  // degenerate model (pipeline.py:163-167)
     if (tid == 0) {
       model->bits = bits_cfg >= 0 ? bits_cfg : 2;
@@ -127,21 +137,22 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
   m = s_bcast[0]; maxc = s_bcast[1]; tot = s_bcast[2];
   if (m == 0) {
     if (tid == 0) { model->status = NMK_ERR_EMPTY_HIST; model->k = 0; model->m_selectable = 0; }
+    if (cov_out && tid < auto_n) cov_out[tid] = 0;
     return;
   }
 
   // ---- multi radix select: one lane per requested k --------------------
   // slot s requests kk[s]; slot inactive when kk >= m (everything selected)
   const bool autob = bits_cfg < 0;
-  if (tid < kNSel) {
-    int b = autob ? kAutoLo + tid : bits_cfg;
+  if (tid < NS) {
+    int b = autob ? auto_lo + tid : bits_cfg;
     unsigned long long kk = (b >= 63) ? ~0ULL : ((1ULL << b) - 1);
     if (kk > m) kk = m;
-    s_kk[tid] = (autob || tid == 0) ? kk : m;  // fixed B uses slot 0 only
+    s_kk[tid] = ((autob && tid < auto_n) || tid == 0) ? kk : m;  // fixed B uses slot 0 only
     s_prefix[tid] = 0; s_mask[tid] = 0; s_left[tid] = s_kk[tid];
   }
   __syncthreads();
-  const int nslots = autob ? kNSel : 1;   // fixed B: slot 0 only
+  const int nslots = autob ? auto_n : 1;   // fixed B: slot 0 only
   bool any_sel = false;                   // some slot must select (k < m); else every bin is taken
   for (int s = 0; s < nslots; ++s) any_sel |= s_kk[s] < m;
   int top = 63 - __clzll(maxc | 1ULL);
@@ -169,7 +180,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
       // one warp per active slot: lane l owns digits 255-8l .. 248-8l; a warp
       // scan from the top digit finds where the running count reaches `left`
       const int lane = tid & 31;
-      for (int w = tid >> 5; w < kNSel; w += kSelThreads / 32) {
+      for (int w = tid >> 5; w < nslots; w += kSelThreads / 32) {
         if (!(s_kk[w] < m)) continue;
         unsigned long long h[8], sum = 0;
 #pragma unroll
@@ -206,31 +217,36 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
 
   // ---- auto B: coverage per B, then the Eq. 6 argmin ---------------------
   if (autob) {
-    unsigned long long acc[kNSel];
+    unsigned long long acc[NS];
 #pragma unroll
-    for (int s = 0; s < kNSel; ++s) acc[s] = 0;
+    for (int s = 0; s < NS; ++s) acc[s] = 0;
     for (uint64_t i = tid; i < M; i += kSelThreads) {
       unsigned long long c = bv.sel_count(i);
       if (!c) continue;
 #pragma unroll
-      for (int s = 0; s < kNSel; ++s)
+      for (int s = 0; s < NS; ++s)
         if (s_kk[s] < m && c > s_prefix[s]) acc[s] += c;
     }
 #pragma unroll
-    for (int s = 0; s < kNSel; ++s) {
+    for (int s = 0; s < NS; ++s) {
       unsigned long long v = BRed(tmp.red).Sum(acc[s]);
       if (tid == 0) s_cov[s] = (s_kk[s] < m) ? v + s_left[s] * s_prefix[s] : tot;
       __syncthreads();
+    }
+    if (cov_out) {   // select_index_length's coverage table only
+      if (tid < auto_n) cov_out[tid] = s_cov[tid];
+      if (tid == 0) { model->status = 0; model->k = 0; model->m_selectable = (int)(m > 0x7fffffffULL ? 0x7fffffff : m); }
+      return;
     }
     if (tid == 0) {
       // size(B) = 2^B*L + n*B/8 + (n - cov)*L, evaluated exactly as 8*size in
       // integers (every term is an exact integer or a multiple of 1/8 far below
       // 2^50, so the reference's float arithmetic is exact too).
       const unsigned long long L = sizeof(T);
-      int best = kAutoLo;
+      int best = auto_lo;
       unsigned long long best8 = 0;
-      for (int s = 0; s < kNSel; ++s) {
-        int b = kAutoLo + s;
+      for (int s = 0; s < auto_n; ++s) {
+        int b = auto_lo + s;
         unsigned long long s8 = 8ULL * (1ULL << b) * L + (unsigned long long)n_total * b +
                                 8ULL * (n_total - s_cov[s]) * L;
         if (s == 0 || s8 < best8) { best8 = s8; best = b; }
@@ -243,7 +259,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
   }
   __syncthreads();
   const int bits = s_bits;
-  const int slot = autob ? bits - kAutoLo : 0;
+  const int slot = autob ? bits - auto_lo : 0;
   const unsigned long long K = s_kk[slot];
   const bool take_all = (K >= m);
   const unsigned long long t = s_prefix[slot];
@@ -310,7 +326,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     model->tol_bin = width / 2.0;
     for (int b = 0; b < 17; ++b) model->coverage[b] = 0;
     if (autob)
-      for (int s = 0; s < kNSel; ++s) model->coverage[kAutoLo + s] = s_cov[s];
+      for (int s = 0; s < auto_n && auto_lo + s <= kAutoHi; ++s) model->coverage[auto_lo + s] = s_cov[s];
   }
 }
 
@@ -328,15 +344,34 @@ extern "C" int nmk_select(const unsigned long long* keys, const unsigned long lo
   if (keys && !nruns) return set_error(NMK_ERR_ARG, "nmk_select: sparse form needs nruns");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = (m_max == 0 && !keys) ? kSelCache * 8 : (m_max <= kSelCache ? (size_t)m_max * 8 : 0);
-  ensure_dyn_smem(k_select<double>, kSelCache * 8);
-  ensure_dyn_smem(k_select<float>, kSelCache * 8);
+  ensure_dyn_smem(k_select<double, kNSel>, kSelCache * 8);
+  ensure_dyn_smem(k_select<float, kNSel>, kSelCache * 8);
   if (dtype == NMK_F64)
-    k_select<double><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
-                                               centers, cuts, (double*)centers_t, cap_k, model);
+    k_select<double, kNSel><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits,
+                                                         n_total, centers, cuts, (double*)centers_t, cap_k, model,
+                                                         kAutoLo, kNSel, nullptr);
   else if (dtype == NMK_F32)
-    k_select<float><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits, n_total,
-                                              centers, cuts, (float*)centers_t, cap_k, model);
+    k_select<float, kNSel><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits,
+                                                        n_total, centers, cuts, (float*)centers_t, cap_k, model,
+                                                        kAutoLo, kNSel, nullptr);
   else
     return set_error(NMK_ERR_ARG, "nmk_select: bad dtype");
   return check_launch("k_select");
+}
+
+extern "C" int nmk_coverage(const unsigned long long* keys, const unsigned long long* counts, uint64_t m_max,
+                            const unsigned long long* nruns, const nmk_stats* stats, double width, int bits_lo,
+                            int bits_hi, unsigned long long* coverage, nmk_model* model, void* stream) {
+  if (!counts || !stats || !coverage || !model) return set_error(NMK_ERR_ARG, "nmk_coverage: bad argument");
+  if (bits_lo < 2 || bits_hi > 30 || bits_lo > bits_hi)
+    return set_error(NMK_ERR_ARG, "nmk_coverage: bits range [%d, %d] outside [2, 30]", bits_lo, bits_hi);
+  if (keys && !nruns) return set_error(NMK_ERR_ARG, "nmk_coverage: sparse form needs nruns");
+  if (!keys && m_max == 0) return set_error(NMK_ERR_ARG, "nmk_coverage: dense form needs m_max");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = m_max <= kSelCache ? (size_t)m_max * 8 : 0;
+  ensure_dyn_smem(k_select<double, kNSelMax>, kSelCache * 8);
+  k_select<double, kNSelMax><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, width / 2.0, -1,
+                                                          0, nullptr, nullptr, nullptr, 1, model, bits_lo,
+                                                          bits_hi - bits_lo + 1, coverage);
+  return check_launch("k_select(coverage)");
 }

@@ -163,7 +163,7 @@ def assemble_variable(enc: engine.DeviceEncoding, config: PipelineConfig, name: 
                       timings: PhaseTimings | None = None) -> container.CompressedVariable:
     """Device encoding -> CompressedVariable (pipeline.py:290-324)."""
     t0 = time.perf_counter()
-    if config.deflate == "gpu":
+    if getattr(config, "deflate", "host") == "gpu":   # the reference's PipelineConfig has no such field
         # the packed stream never comes to the host: only the DEFLATE output
         try:
             deflated = codec.gpu_deflate_blocks(enc.packed, enc.stride, enc.block_lengths())

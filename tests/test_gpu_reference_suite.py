@@ -1,0 +1,63 @@
+"""Parity level 4: the reference's OWN test files, run with
+every hot-path entry point of the reference package bound to the B200
+drop-in (tests/ref_dropin.py).  The reference tree is vendored into
+oracle/_ref by oracle/make_ref.py (test infrastructure, git-ignored).
+
+Deselected: the seven tests that compress with the equal-width, log-scale or
+k-means dictionary through ``compress_pair``.  Those strategies are outside
+the accelerated path (the drop-in raises NotImplementedError for
+them); every other test of test_core / test_binning / test_codec /
+test_pipeline / test_acceptance / test_container / test_cli /
+test_generators runs against the GPU implementation.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "oracle", "_ref")
+
+OUT_OF_SCOPE = [
+    "test_pipeline.py::TestDeterminism::test_identical_across_worker_counts[equal_width]",
+    "test_pipeline.py::TestDeterminism::test_identical_across_worker_counts[log_scale]",
+    "test_pipeline.py::TestDeterminism::test_identical_across_worker_counts[kmeans]",
+    "test_pipeline.py::TestCompressPair::test_constant_pair_all_zero_deltas",
+    "test_pipeline.py::TestCompressPair::test_strategy_affects_dictionary",
+    "test_pipeline.py::TestCompressSeries::test_small_noise_chain_fully_compressible",
+    "test_pipeline.py::TestCompressSeries::test_identical_snapshots_zero_deltas",
+]
+
+
+def _have_ref() -> bool:
+    return os.path.exists(os.path.join(REF, "nmk", "pipeline.py")) and os.path.isdir(os.path.join(REF, "tests"))
+
+
+@pytest.mark.gpu
+def test_reference_suite_against_dropin(tmp_path):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if not _have_ref():
+        pytest.skip("oracle/_ref not vendored (run oracle/make_ref.py where /root/reference exists)")
+    tests_dir = os.path.join(REF, "tests")
+    xml = tmp_path / "ref.xml"
+    cmd = [sys.executable, "-m", "pytest", "-p", "ref_dropin", "-q", "-p", "no:cacheprovider",
+           f"--rootdir={REF}", f"--junitxml={xml}", tests_dir]
+    for node in OUT_OF_SCOPE:
+        cmd += ["--deselect", os.path.join(tests_dir, node)]
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "tests"), REF, ROOT]))
+    r = subprocess.run(cmd, cwd=str(tmp_path), env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    suite = ET.parse(xml).getroot()
+    suite = suite if suite.tag == "testsuite" else suite.find("testsuite")
+    total, fails, errs, skips = (int(suite.get(k)) for k in ("tests", "failures", "errors", "skipped"))
+    assert fails == 0 and errs == 0
+    # 215 reference tests - 7 out-of-scope strategy tests
+    assert total - skips >= 208, (total, skips)
+    assert "reference entry points bound to the B200 drop-in" in r.stdout

@@ -190,3 +190,21 @@ def test_swar_sentinel_count_model(bits):
         full = int.from_bytes(raw, "big")
         want = sum(((full >> (8 * bits - (e + 1) * bits)) & sentinel) == sentinel for e in range(8))
         assert got == want
+
+
+def test_ref_dropin_plugin_binds_every_entry_point():
+    """The parity-level-4 plugin finds every reference entry point it rebinds
+    (CPU, in a subprocess: binding only, no kernel launches)."""
+    import subprocess
+    import sys
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "nmk", "pipeline.py")):
+        pytest.skip("oracle/_ref not vendored")
+    code = ("import ref_dropin, nmk, paper_1703_02438_b200 as o; p = ref_dropin.install(); "
+            "assert nmk.pipeline.compress_pair is o.pipeline.compress_pair; "
+            "assert nmk.binning.top_k_bins is o.binning.top_k_bins; "
+            "assert nmk.codec.partial_decode is o.codec.partial_decode; "
+            "print(sum(len(v) for v in p.values()))")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "tests"), ROOT]))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip() == "19"
