@@ -126,21 +126,8 @@ class ProcessGroupComm:
     def merge_sparse(self, keys, counts, nruns, ws):
         """Gathered runs merged on the device (nmk_hist_merge: sort by key and
         sum equal keys) -> (keys, counts, nruns) as nmk_select expects."""
-        import torch
-        from . import _native as N
-        from .engine import _stream
         ks, cs = self.gather_runs(keys, counts, nruns)
-        ks, cs = ks.contiguous(), cs.contiguous()
-        out_n = torch.zeros(1, dtype=torch.int64, device=ks.device)
-        lib = N.lib()
-        nb = lib.nmk_hist_merge_ws_bytes(ks.numel())
-        buf = ws.get("hist_merge_ws", nb)
-        N.check(lib.nmk_hist_merge(ks.data_ptr(), cs.data_ptr(), ks.numel(), out_n.data_ptr(), buf.data_ptr(), nb,
-                                   _stream()))
-        if ks.numel() == 0:
-            ks = torch.zeros(1, dtype=torch.int64, device=keys.device)
-            cs = torch.zeros(1, dtype=torch.int64, device=keys.device)
-        return ks, cs, out_n
+        return merge_gathered_runs(ks, cs, ws)
 
     # -- 3. incompressible-count scan --------------------------------------------
     def exscan(self, value: int) -> tuple[int, int]:
@@ -152,6 +139,27 @@ class ProcessGroupComm:
         self.dist.all_gather_into_tensor(allv, v, group=self.group)
         a = allv.cpu().tolist()
         return int(sum(a[: self.rank])), int(sum(a))
+
+
+def merge_gathered_runs(ks, cs, ws):
+    """Every rank's sparse (key, count) runs, concatenated -> one sorted
+    histogram on the device (binning.merge_histograms, binning.py:119-132):
+    nmk_hist_merge sorts by key and sums the counts of equal keys.  Returns
+    (keys, counts, nruns) as nmk_select's sparse form expects."""
+    import torch
+    from . import _native as N
+    from .engine import _stream
+    ks, cs = ks.contiguous(), cs.contiguous()
+    out_n = torch.zeros(1, dtype=torch.int64, device=ks.device)
+    lib = N.lib()
+    nb = lib.nmk_hist_merge_ws_bytes(ks.numel())
+    buf = ws.get("hist_merge_ws", nb)
+    N.check(lib.nmk_hist_merge(ks.data_ptr(), cs.data_ptr(), ks.numel(), out_n.data_ptr(), buf.data_ptr(), nb,
+                               _stream()))
+    if ks.numel() == 0:
+        ks = torch.zeros(1, dtype=torch.int64, device=ks.device)
+        cs = torch.zeros(1, dtype=torch.int64, device=ks.device)
+    return ks, cs, out_n
 
 
 @dataclass

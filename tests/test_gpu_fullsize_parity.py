@@ -1,0 +1,137 @@
+"""Bit-exact parity against the oracle at the BASELINE configs' FULL sizes,
+on the exact path bench.py times (engine.DevicePipeline: sync-free, keyed
+K2/K4, captured as a CUDA graph and replayed).
+
+The oracle (oracle/nmk_oracle.py, pinned to the reference's golden vectors)
+runs on host copies of the same device-generated fields with one worker
+thread per host core, as the reference's ThreadPoolExecutor would
+(pipeline.py:84-109).  Compared per config: bits, stored centers, every
+packed index block, the exact-value list, the prefix table, the
+incompressible count, and the reconstruction (oracle core.reconstruct of
+the oracle's own codes -- the codes are pinned by the packed blocks).
+
+  cfg2  512^3 fp64 (1 GiB / timestep), E=1e-3, B=8, graph-replayed
+  cfg3  1440x720x30 fp32, all 15 transitions of the chain, E=5e-3, B=10
+  cfg5  2^28 fp64: (B8, E1e-4), (B10, E1e-3), (B12, E1e-4)
+  cfg4  a 2^28 slice of config 1's distribution (weak share = 2^29)
+"""
+
+import gc
+
+import numpy as np
+import pytest
+
+import nmk_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1703_02438_b200 import engine, workloads  # noqa: E402
+
+WORKERS = O.default_workers()
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def _assert_matches_oracle(ref, pipe, out, base_h, what):
+    """DevicePipeline result (after check()) == oracle encode + reconstruct."""
+    chk = pipe.check()
+    assert chk["status"] == 0 and chk["tripwire"] == 0, (what, chk)
+    assert not chk["bad_index"] and not chk["exhausted"], (what, chk)
+    enc = pipe.encoding()
+    assert enc.bits == ref["bits"], what
+    assert enc.nblocks == ref["nblocks"] and enc.epb == ref["epb"], what
+    dt = base_h.dtype
+    assert _host(enc.centers_t).tobytes() == ref["centers"].astype(dt).tobytes(), what
+    assert enc.n_inc == ref["n_inc"], (what, enc.n_inc, ref["n_inc"])
+    assert _host(enc.exact).tobytes() == ref["exact"].tobytes(), what
+    assert _host(enc.prefix).view(np.uint64).tobytes() == ref["prefix"].tobytes(), what
+    packed = _host(enc.packed)
+    lens = enc.block_lengths()
+    for b in range(enc.nblocks):
+        got = packed[b * enc.stride: b * enc.stride + int(lens[b])].tobytes()
+        assert got == ref["blocks"][b], (what, "block", b)
+    assert chk["n_sentinel"] == ref["n_inc"], what
+    want = O.reconstruct(base_h, ref["centers"].astype(dt).astype(np.float64), ref["codes"], ref["exact"],
+                         ref["bits"])
+    assert _host(out).tobytes() == want.tobytes(), (what, "reconstruction")
+
+
+def _pipeline_graph(base, cur, E, bits, replays=2):
+    """The bench path: DevicePipeline captured once, replayed."""
+    pipe = engine.DevicePipeline(base.numel(), base.dtype, E, bits)
+    out = torch.empty_like(base)
+    pipe.step(base, cur, out)
+    g = pipe.capture(base, cur, out)
+    out.fill_(0)
+    for _ in range(replays):
+        g.replay()
+    torch.cuda.synchronize()
+    return pipe, out
+
+
+def test_cfg2_full_size_bench_path():
+    base, cur = workloads.cfg2_device(512, seed=0)
+    pipe, out = _pipeline_graph(base, cur, 1e-3, 8)
+    base_h, cur_h = _host(base), _host(cur)
+    ref = O.encode(base_h, cur_h, 1e-3, 8, 1 << 20, workers=WORKERS)
+    assert ref["bits"] == 8 and len(ref["centers"]) == 255
+    _assert_matches_oracle(ref, pipe, out, base_h, "cfg2 512^3")
+
+
+@pytest.mark.parametrize("bits,E", [(8, 1e-4), (10, 1e-3), (12, 1e-4)])
+def test_cfg5_full_size(bits, E):
+    base, cur = workloads.cfg5_device(1 << 28, seed=5)
+    pipe, out = _pipeline_graph(base, cur, E, bits, replays=1)
+    base_h, cur_h = _host(base), _host(cur)
+    del base, cur
+    ref = O.encode(base_h, cur_h, E, bits, 1 << 20, workers=WORKERS)
+    assert ref["n_inc"] > 0
+    _assert_matches_oracle(ref, pipe, out, base_h, f"cfg5 B{bits} E{E}")
+    del ref, pipe, out
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_slice_2e28():
+    base, cur = workloads.cfg1_device(1 << 28, seed=4)
+    pipe, out = _pipeline_graph(base, cur, 1e-3, 8, replays=1)
+    base_h, cur_h = _host(base), _host(cur)
+    del base, cur
+    ref = O.encode(base_h, cur_h, 1e-3, 8, 1 << 20, workers=WORKERS)
+    assert 0.004 < ref["n_inc"] / base_h.size < 0.006
+    _assert_matches_oracle(ref, pipe, out, base_h, "cfg4 2^28 slice")
+    del ref, pipe, out
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_cfg3_full_chain():
+    """All 15 transitions: step t is encoded against the reconstruction of
+    step t-1, on the device (K4's fused reconstruction) and in the oracle."""
+    E, bits = 5e-3, 10
+    x = workloads.cfg3_device_first(seed=0)
+    n = x.numel()
+    assert n == 31_104_000
+    pipe = engine.DevicePipeline(n, torch.float32, E, bits)
+    recon_d = x.clone()
+    nxt_d = torch.empty_like(x)
+    recon_h = _host(x).copy()
+    for t in range(1, 16):
+        x = workloads.cfg3_device_step(x, t, seed=0)
+        pipe.encode(recon_d, x, recon=nxt_d)
+        x_h = _host(x)
+        ref = O.encode(recon_h, x_h, E, bits, 1 << 20, workers=WORKERS)
+        # nmk_decode of the same encoding equals K4's fused reconstruction
+        dec = torch.empty_like(x)
+        pipe.decode(recon_d, dec)
+        assert torch.equal(dec.view(torch.int32), nxt_d.view(torch.int32)), t
+        _assert_matches_oracle(ref, pipe, nxt_d, recon_h, f"cfg3 transition {t}")
+        recon_h = O.reconstruct(recon_h, ref["centers"].astype(np.float32).astype(np.float64), ref["codes"],
+                                ref["exact"], bits)
+        recon_d, nxt_d = nxt_d, recon_d
+    assert _host(recon_d).tobytes() == recon_h.tobytes()
