@@ -12,6 +12,7 @@ from ._native import NativeError, NativeUnavailable
 from .binning import (BinModel, Histogram, build_histogram, compressible_mask, merge_histograms, nearest_center,
                       select_index_length, top_k_bins)
 from .codec import (BlockLayout, CodecError, decode_all_indices, pack_block, partial_decode, partial_decode_file,
+                    partial_decode_many,
                     unpack_block)
 from .container import CompressedVariable, ContainerError, VariableHandle, read_file, scan_file, write_file
 from .core import (ChangeRatioField, TemporalPair, Tolerance, compute_change_ratios, ratio_arrays,
@@ -27,6 +28,6 @@ __all__ = [
     "BlockLayout", "ChangeRatioField", "CodecError", "CompressedVariable", "ContainerError",
     "NativeError", "NativeUnavailable", "PhaseTimings", "PipelineConfig", "PipelineError",
     "TemporalPair", "Tolerance", "compress_pair", "compress_series", "compute_change_ratios",
-    "decode_all_indices", "decompress", "pack_block", "partial_decode", "partial_decode_file", "ratio_arrays",
+    "decode_all_indices", "decompress", "pack_block", "partial_decode", "partial_decode_file", "partial_decode_many", "ratio_arrays",
     "read_file", "reconstruct", "scan_file", "unpack_block", "VariableHandle", "write_file",
 ]

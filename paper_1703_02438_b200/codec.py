@@ -265,6 +265,75 @@ def partial_decode(variable, start: int, count: int, base_reconstructed) -> np.n
                          lambda b: _block_bytes_of(variable, b), inc_slice)
 
 
+def partial_decode_many(variable, ranges, bases, *, inflated: dict | None = None) -> list:
+    """Batched :func:`partial_decode`: ``ranges`` = [(start, count), ...],
+    ``bases[i]`` the base slice of range i.  Every covering block is inflated
+    once (host zlib, as ``decompress_block``; pass ``inflated`` = {block:
+    packed bytes} to reuse earlier inflates) and ALL ranges decode in one K5
+    launch.  Results equal ``partial_decode`` range by range (codec.py:242-258),
+    including its errors."""
+    import torch
+    from . import engine
+    ranges = [(int(a), int(c)) for a, c in ranges]
+    if len(bases) != len(ranges):
+        raise ValueError("one base slice per range")
+    out = [None] * len(ranges)
+    live = []
+    for i, (a, c) in enumerate(ranges):
+        if a < 0 or c < 0 or a + c > variable.n:
+            raise ValueError(f"range [{a}, {a + c}) outside 0..{variable.n}")
+        if np.asarray(bases[i]).shape[0] != c:
+            raise ValueError(f"base slice holds {np.asarray(bases[i]).shape[0]} elements, need {c}")
+        if c == 0:
+            out[i] = np.zeros(0, dtype=variable.numpy_dtype)
+        else:
+            live.append(i)
+    if not live:
+        return out
+    epb, bits, n = variable.elements_per_block, variable.bits, variable.n
+    need = sorted({b for i in live for b in range(ranges[i][0] // epb, (ranges[i][0] + ranges[i][1] - 1) // epb + 1)})
+    first, last = need[0], need[-1]
+    stride = engine.block_stride(epb, bits)
+    host = np.zeros((last - first + 1) * stride, dtype=np.uint8)
+    inflated = {} if inflated is None else inflated
+    for b in need:
+        blk = inflated.get(b)
+        if blk is None:
+            blk = inflated[b] = decompress_block(_block_bytes_of(variable, b))
+        s_, e_ = b * epb, min((b + 1) * epb, n)
+        nb = packed_size(e_ - s_, bits)
+        if len(blk) < nb:
+            raise CodecError(f"short buffer: {len(blk)} bytes, need {nb}")
+        o = (b - first) * stride
+        host[o:o + nb] = np.frombuffer(blk, dtype=np.uint8, count=nb)
+    prefix = np.asarray(variable.incompressible_prefix, dtype=np.uint64)
+    lo = int(prefix[first])
+    hi = int(prefix[last + 1]) if last + 1 < variable.nblocks else int(variable.n_incompressible)
+    dt = variable.numpy_dtype
+    exact = np.array(variable.incompressible_table[lo:max(hi, lo)], dtype=dt, copy=True)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_packed = torch.from_numpy(host).to(dev)
+    d_prefix = torch.from_numpy(prefix[first:last + 1].astype(np.int64) - lo).to(dev)
+    d_centers = torch.tensor(np.asarray(variable.centers, dtype=np.float64), device=dev)
+    d_exact = torch.from_numpy(exact).to(dev) if exact.size else torch.empty(0, dtype=_tdt(dt), device=dev)
+    offs = np.zeros(len(live) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([ranges[i][1] for i in live])
+    base_all = np.concatenate([np.asarray(bases[i], dtype=dt) for i in live])
+    d_base = torch.from_numpy(base_all).to(dev)
+    segs = [(ranges[i][0], ranges[i][1], int(offs[j])) for j, i in enumerate(live)]
+    res = engine.decode(d_packed, stride, first, bits, epb, n, d_prefix, d_centers, d_exact, d_base, segs)
+    if res.bad_index:
+        raise ValueError(f"index {res.max_bad_index} out of range for {len(variable.centers)} centers")
+    avail = exact.shape[0] - res.inc_before
+    if (res.n_sentinel > np.maximum(avail, 0)).any():
+        j = int(np.flatnonzero(res.n_sentinel > np.maximum(avail, 0))[0])
+        raise ValueError(f"incompressible values exhausted: need {int(res.n_sentinel[j])}, have {max(int(avail[j]), 0)}")
+    flat = res.out.cpu().numpy()
+    for j, i in enumerate(live):
+        out[i] = flat[offs[j]:offs[j + 1]].copy()
+    return out
+
+
 def partial_decode_file(handle, start: int, count: int, base_reconstructed) -> np.ndarray:
     """Like ``partial_decode`` straight from an on-disk variable
     (codec.py:261-278): only the covering blocks' DEFLATE bytes and the exact

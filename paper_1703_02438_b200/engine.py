@@ -414,7 +414,8 @@ class DevicePipeline:
     too wide for a dense histogram, empty histogram)."""
 
     def __init__(self, n_local: int, dtype, tolerance: float, bits: int, block_bytes: int = 1 << 20,
-                 *, elem0: int = 0, n_total: int | None = None, comm=None, ws: Workspace | None = None):
+                 *, elem0: int = 0, n_total: int | None = None, comm=None, ws: Workspace | None = None,
+                 comm_bins: int | None = None):
         torch = _torch()
         if bits is None or not MIN_BITS <= bits <= MAX_BITS:
             raise ValueError("the sync-free pipeline needs an explicit B in [2, 30]")
@@ -431,7 +432,9 @@ class DevicePipeline:
         self.b0 = self.elem0 // self.epb
         self.nlb = (self.elem0 + self.n_local - 1) // self.epb - self.b0 + 1
         self.k_cap = (1 << bits) - 1
-        self.cap_bins = ASYNC_COMM_BINS if comm is not None else DENSE_MAX_BINS
+        # dense span capacity; with a comm it is also the all-reduced histogram
+        # length (fit_comm_bins sizes it to the observed span)
+        self.cap_bins = (comm_bins or ASYNC_COMM_BINS) if comm is not None else DENSE_MAX_BINS
         ws = ws or Workspace()
         self.ws = ws
         lib = N.lib()
@@ -462,6 +465,20 @@ class DevicePipeline:
         self.err = torch.zeros(2, dtype=torch.int64, device=dev)
         if comm is not None:
             self.gathered_inc = torch.zeros(comm.world, dtype=torch.int64, device=dev)
+
+    def fit_comm_bins(self, nbins: int, headroom: float = 1.5, floor: int = 1024) -> int:
+        """Size the all-reduced histogram to an observed dense span (e.g. the
+        warm-up step's ``check()["nbins"]``) instead of ASYNC_COMM_BINS: the
+        exchange then moves (cap + 1) * 8 bytes.  A later span above the cap
+        is flagged on the device (NMK_ERR_NEEDS_SPARSE) and rerun through the
+        general path, so the cap never changes a result.  Call before capture."""
+        torch = _torch()
+        cap = max(floor, 1 << max(0, math.ceil(math.log2(max(1, nbins) * headroom))))
+        cap = min(cap, DENSE_MAX_BINS)
+        if cap != self.cap_bins:
+            self.cap_bins = cap
+            self.counts = torch.zeros(cap + 1, dtype=torch.int64, device=self.counts.device)
+        return cap
 
     # -- enqueue --------------------------------------------------------------
     def encode(self, base, cur, mark=None, recon=None):

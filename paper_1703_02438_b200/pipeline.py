@@ -508,6 +508,114 @@ class StreamCompressor:
         return 2 * self.n * self.np_dtype.itemsize
 
 
+class SeriesStreamCompressor:
+    """compress_series for a stream of HOST snapshots where only x_t crosses
+    PCIe: the base of step t is K4's fused reconstruction of step t-1, which
+    never leaves HBM (pipeline.py:364-372 without the decode pass).
+
+    ``start(x0)`` uploads the first snapshot; ``submit(x_t)`` (pinned host
+    tensor) enqueues H2D of x_t, K1..K4 against the resident reconstruction,
+    and D2H of the packed stream, prefix, centers and scalars, returning a
+    ticket; ``result(ticket)`` returns the step's HostEncoding (views of
+    pinned buffers owned by the ticket's slot, valid until ``depth`` later
+    submissions).  The H2D of step t+1 overlaps the kernels of step t."""
+
+    def __init__(self, n: int, dtype, config: PipelineConfig, depth: int = 2):
+        import torch
+        _check_strategy(config)
+        if config.bits is None:
+            raise ValueError("SeriesStreamCompressor needs an explicit B (PipelineConfig.bits)")
+        N.require_cuda()
+        self.n, self.config, self.depth = int(n), config, int(depth)
+        self.torch_dtype = torch.float64 if np.dtype(dtype).itemsize == 8 else torch.float32
+        self.np_dtype = np.dtype("<f8") if self.torch_dtype == torch.float64 else np.dtype("<f4")
+        self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self.recon = [torch.empty(self.n, dtype=self.torch_dtype, device="cuda") for _ in range(2)]
+        self.ev_recon = torch.cuda.Event()
+        self.slots = []
+        for _ in range(self.depth):
+            pipe = engine.DevicePipeline(self.n, self.torch_dtype, config.tolerance, config.bits,
+                                         config.block_bytes, ws=engine.Workspace())
+            self.slots.append({
+                "pipe": pipe, "cur": torch.empty(self.n, dtype=self.torch_dtype, device="cuda"),
+                "h_packed": torch.empty(pipe.packed.numel(), dtype=torch.uint8, pin_memory=True),
+                "h_exact": torch.empty(max(self.n // 64, 1), dtype=self.torch_dtype, pin_memory=True),
+                "h_prefix": torch.empty(pipe.prefix.numel(), dtype=torch.int64, pin_memory=True),
+                "h_scal": torch.empty(4 + pipe.model.numel() + 1, dtype=torch.int64, pin_memory=True),
+                "h_centers": torch.empty(pipe.k_cap, dtype=self.torch_dtype, pin_memory=True),
+                "ev_in": torch.cuda.Event(), "ev_cmp": torch.cuda.Event(), "ev_out": torch.cuda.Event(),
+                "busy": False,
+            })
+        self.count = 0
+
+    def start(self, first) -> None:
+        import torch
+        with torch.cuda.stream(self.s_cmp):
+            self.recon[0].copy_(torch.as_tensor(first), non_blocking=True)
+        self.s_cmp.synchronize()
+        self.count = 0
+
+    def submit(self, cur) -> int:
+        import torch
+        t = self.count
+        sl = self.slots[t % self.depth]
+        if sl["busy"]:
+            sl["ev_out"].synchronize()
+        sl["busy"] = True
+        with torch.cuda.stream(self.s_h2d):
+            self.s_h2d.wait_event(sl["ev_cmp"])
+            sl["cur"].copy_(cur, non_blocking=True)
+            sl["ev_in"].record(self.s_h2d)
+        base, nxt = self.recon[t % 2], self.recon[(t + 1) % 2]
+        with torch.cuda.stream(self.s_cmp):
+            self.s_cmp.wait_event(sl["ev_in"])
+            self.s_cmp.wait_event(sl["ev_out"])
+            sl["pipe"].encode(base, sl["cur"], recon=nxt)
+            sl["ev_cmp"].record(self.s_cmp)
+        with torch.cuda.stream(self.s_d2h):
+            self.s_d2h.wait_event(sl["ev_cmp"])
+            p = sl["pipe"]
+            m = 4 + p.model.numel()
+            sl["h_packed"].copy_(p.packed, non_blocking=True)
+            sl["h_prefix"].copy_(p.prefix, non_blocking=True)
+            sl["h_scal"][:4].copy_(p.stats, non_blocking=True)
+            sl["h_scal"][4:m].copy_(p.model, non_blocking=True)
+            sl["h_scal"][m:m + 1].copy_(p.n_inc, non_blocking=True)
+            sl["h_centers"].copy_(p.centers_t, non_blocking=True)
+            sl["ev_out"].record(self.s_d2h)
+        self.count += 1
+        return t
+
+    def result(self, ticket: int) -> HostEncoding:
+        import torch
+        sl = self.slots[ticket % self.depth]
+        sl["ev_out"].synchronize()
+        p = sl["pipe"]
+        scal = sl["h_scal"].numpy()
+        m = 4 + p.model.numel()
+        n_inc = int(scal[m])
+        model = N.NmkModel.from_buffer_copy(scal[4:m].tobytes()[: ctypes.sizeof(N.NmkModel)])
+        if model.status != 0:
+            raise PipelineError("binning", f"series step {ticket}: sync-free pipeline status {model.status} "
+                                "(use compress_series for spans beyond the dense histogram)")
+        if n_inc > sl["h_exact"].numel():
+            sl["h_exact"] = torch.empty(n_inc, dtype=self.torch_dtype, pin_memory=True)
+        if n_inc:
+            with torch.cuda.stream(self.s_d2h):
+                sl["h_exact"][:n_inc].copy_(p.exact[:n_inc], non_blocking=True)
+            self.s_d2h.synchronize()
+        self.last_d2h_bytes = (p.packed.numel() + n_inc * self.np_dtype.itemsize + p.prefix.numel() * 8
+                               + sl["h_scal"].numel() * 8 + p.k_cap * self.np_dtype.itemsize)
+        k = int(model.k)
+        return HostEncoding(self.n, self.np_dtype, p.bits, k, p.epb, p.nblocks, p.stride, p.b0,
+                            sl["h_packed"].numpy(), sl["h_exact"].numpy()[:n_inc],
+                            sl["h_prefix"].numpy().view(np.uint64), sl["h_centers"].numpy()[:k], n_inc)
+
+    def h2d_bytes(self) -> int:
+        """Host->device bytes per step: the new snapshot only."""
+        return self.n * self.np_dtype.itemsize
+
+
 def compress_series(snapshots, config: PipelineConfig, name: str = "var0"):
     """Compress a snapshot chain (pipeline.py:343-372).
 

@@ -50,6 +50,24 @@ def cfg1_device(n: int, seed: int = 0, device="cuda", dtype=None):
     return base.to(dtype), cur.to(dtype)
 
 
+def cfg1_device_range(lo: int, hi: int, seed: int = 0, chunk: int = 1 << 26, device="cuda"):
+    """Elements [lo, hi) of ONE global config-1 field of any length (config 4
+    strong scaling: 4e9 elements), generated chunk by chunk with per-chunk
+    seeds, so every rank of every world size sees the same global field."""
+    import torch
+    n = hi - lo
+    base = torch.empty(n, dtype=torch.float64, device=device)
+    cur = torch.empty(n, dtype=torch.float64, device=device)
+    c0, c1 = lo // chunk, (hi - 1) // chunk if n else lo // chunk - 1
+    for c in range(c0, c1 + 1):
+        a, b_ = max(lo, c * chunk), min(hi, (c + 1) * chunk)
+        cb, cc = cfg1_device(chunk, seed=seed * 1_000_003 + c, device=device)
+        base[a - lo:b_ - lo] = cb[a - c * chunk:b_ - c * chunk]
+        cur[a - lo:b_ - lo] = cc[a - c * chunk:b_ - c * chunk]
+        del cb, cc
+    return base, cur
+
+
 # ---------------------------------------------------------------------------
 # cfg2: 3-D smooth field on an N^3 grid in 8^3-cell blocks (row-major block
 # order), box-filtered N(0, 0.003) ratio + 2 % Laplace(0, 0.1) outliers.
