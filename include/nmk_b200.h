@@ -64,7 +64,9 @@ typedef struct nmk_model {
     int32_t status;        /* 0 ok, NMK_ERR_EMPTY_HIST                          */
     int32_t m_selectable;  /* nonempty bins with a finite center                */
     double  tol_bin;       /* BinModel.tolerance: (2E)/2, or E when degenerate  */
-    unsigned long long coverage[17]; /* auto-B: covered elements for B=2..16    */
+    unsigned long long coverage[17]; /* auto-B: covered elements for B=2..16;
+                                        [0], [1] = the two largest selectable
+                                        bin counts                              */
 } nmk_model;
 
 /* Decode error word (device), checked by the caller after nmk_decode. */
@@ -243,6 +245,15 @@ int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins,
 int nmk_hist_dense_dev(const void* base, const void* cur, const float* keys, uint64_t n,
                        int dtype, const nmk_stats* stats, double width,
                        unsigned long long* counts, void* stream);
+/* nmk_hist_dense_dev with hints from the previous step (span_hint: its dense
+ * span, 0 = none; spread_hint: its two largest bins held under 3/4 of the
+ * valid ratios, nmk_model.coverage[0..1] vs stats.nvalid): picks the launch shape and
+ * counting policy -- a 512-thread CTA per SM with 96 KB of counters for
+ * spans of 8K..24K bins, a no-hot-bin direct loop for spread fields.  The
+ * counts never depend on the hints. */
+int nmk_hist_dense_dev2(const void* base, const void* cur, const float* keys, uint64_t n,
+                        int dtype, const nmk_stats* stats, double width,
+                        unsigned long long* counts, uint64_t span_hint, int spread_hint, void* stream);
 int nmk_encode_dev(const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
                    uint64_t n_total, int dtype, const double* centers, const double* cuts,
                    const nmk_model* model, int k_cap, int bits, double tolerance, uint64_t epb,

@@ -81,6 +81,7 @@ SIGNATURES = {
                          u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
     "nmk_hist_prep": (i32, [vp, dbl, u64, vp, vp]),
     "nmk_hist_dense_dev": (i32, [vp, vp, vp, u64, i32, vp, dbl, vp, vp]),
+    "nmk_hist_dense_dev2": (i32, [vp, vp, vp, u64, i32, vp, dbl, vp, u64, i32, vp]),
     "nmk_encode_dev": (i32, [vp, vp, u64, u64, u64, i32, vp, vp, vp, i32, i32, dbl, u64, vp, u64, vp,
                              vp, vp, vp, vp, sz, vp]),
     "nmk_encode_keyed_dev": (i32, [vp, vp, dbl, vp, vp, u64, u64, u64, i32, vp, vp, vp, i32, i32, dbl, u64, vp,

@@ -39,6 +39,15 @@ constexpr int kStages = NMK_STAGES;    // chunks in flight per warp
 #define NMK_STAGES_DENSE 5   // A/B: 5 beats 6 by 8-15 % of K5 when sentinels fill most chunks (profiles/README)
 #endif
 constexpr int kStagesDense = NMK_STAGES_DENSE;
+// f32 chunks carry half the bytes of f64 ones: more of them in flight
+#ifndef NMK_STAGES_F32
+#define NMK_STAGES_F32 6
+#endif
+#ifndef NMK_STAGES_DENSE_F32
+#define NMK_STAGES_DENSE_F32 5
+#endif
+template <typename T> struct Rings { static constexpr int kS = kStages, kD = kStagesDense; };
+template <> struct Rings<float> { static constexpr int kS = NMK_STAGES_F32, kD = NMK_STAGES_DENSE_F32; };
 #ifndef NMK_DENSE_DIV
 #define NMK_DENSE_DIV 400    // "dense": more than 1 exact value per 400 elements (cfg2 0.16 % sparse, cfg4 0.5 % dense)
 #endif
@@ -846,15 +855,15 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   // the one whose regime does not match exits at entry.
   if (!n_exact_dev) {
     if (dec_dense(geo.n_exact, geo.nchunks))
-      launch_dec_chunks<T, B, kStagesDense>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
+      launch_dec_chunks<T, B, Rings<T>::kD>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
                                             info, err, model, n_exact_dev, 0, s);
     else
-      launch_dec_chunks<T, B, kStages>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out, info,
+      launch_dec_chunks<T, B, Rings<T>::kS>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out, info,
                                        err, model, n_exact_dev, 0, s);
   } else {
-    launch_dec_chunks<T, B, kStages>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out, info,
+    launch_dec_chunks<T, B, Rings<T>::kS>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out, info,
                                      err, model, n_exact_dev, 1, s);
-    launch_dec_chunks<T, B, kStagesDense>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
+    launch_dec_chunks<T, B, Rings<T>::kD>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
                                           info, err, model, n_exact_dev, 2, s);
   }
 }

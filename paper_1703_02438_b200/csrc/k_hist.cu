@@ -685,10 +685,9 @@ struct DirectTile {
 template <typename T>
 __device__ __noinline__ DirectTile hist_tile_direct(const float* sk, const T* __restrict__ base,
                                                     const T* __restrict__ cur, uint64_t j0, double gmin,
-                                                    double gmax, double width, double inv_w, uint32_t nbins,
-                                                    uint32_t* my, uint32_t hot1, uint32_t hot2) {
+                                                    double et_c, double width, double inv_w, uint32_t nbins,
+                                                    uint32_t* my, uint32_t hot1, uint32_t hot2, KeyGrid32 g32) {
   const int lane = threadIdx.x & 31;
-  const KeyGrid32 g32 = key_grid32(gmin, gmax, inv_w, nbins);
   DirectTile r{0u, 0u, 0u, kNoBin};
   auto count = [&](uint32_t qi) {
     if (qi == hot1) {
@@ -714,7 +713,6 @@ __device__ __noinline__ DirectTile hist_tile_direct(const float* sk, const T* __
     }
   }
   if (defer) {
-    const double et_c = key_bound(gmin, gmax, inv_w);
     while (defer) {
       const int e = __ffs(defer) - 1;
       defer &= defer - 1;
@@ -726,7 +724,10 @@ __device__ __noinline__ DirectTile hist_tile_direct(const float* sk, const T* __
   return r;
 }
 
-template <typename T>
+// kSpread: the spread policy -- every tile takes the direct loop and the hot
+// pair is never promoted (fields whose keys are spread over hundreds of bins,
+// e.g. cfg5's bimodal mixture, where a promotion would be paid per tile)
+template <typename T, bool kSpread>
 __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, const T* __restrict__ base,
                                               const T* __restrict__ cur, uint64_t n, double gmin, double gmax,
                                               double width, double inv_w, uint32_t nbins, uint32_t* my,
@@ -817,6 +818,47 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
   if (lane == 0)
     for (int st = 0; st < kKeyStages; ++st)
       if (wg + st * nw < ntiles) issue(st, wg + st * nw);
+  if constexpr (kSpread) {
+    // spread policy: every decided key is one shared-memory add into the
+    // warp's replica (no hot pair, no per-tile bookkeeping)
+    for (uint64_t kk = 0;; ++kk) {   // warp-uniform
+      const uint64_t t = wg + kk * nw;
+      if (t >= ntiles) break;
+      const int st = (int)(kk % kKeyStages);
+      mbar_wait(&bars[st], (unsigned)((kk / kKeyStages) & 1));
+      const float* sk = stage + st * kKeyTile;
+      uint32_t defer = 0;
+#pragma unroll
+      for (int u = 0; u < kKeyPerLane / 4; ++u) {
+        const float4 w = reinterpret_cast<const float4*>(sk)[u * 32 + lane];
+        const float kv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t qi;
+          const bool ok = key_ordinal32(kv[e], g32, qi);
+          if (ok) atomicAdd(&my[qi], 1u);
+          defer |= ok ? 0u : 1u << (4 * u + e);
+        }
+      }
+      while (defer) {
+        const int e = __ffs(defer) - 1;
+        defer &= defer - 1;
+        const int idx = ((e >> 2) * 32 + lane) * 4 + (e & 3);
+        const uint32_t qi = ord(sk[idx], t * kKeyTile + idx);
+        if (qi != kNoBin) atomicAdd(&my[qi], 1u);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        const uint64_t nx = t + (uint64_t)kKeyStages * nw;
+        if (nx < ntiles) issue(st, nx);
+      }
+    }
+    for (uint64_t j = ntiles * kKeyTile + wg * 32 + lane; j < n; j += nw * 32) {
+      const uint32_t qi = ord(keys[j], j);
+      if (qi != kNoBin) atomicAdd(&my[qi], 1u);
+    }
+  } else {
   for (uint64_t kk = 0;; ++kk) {   // warp-uniform
     const uint64_t t = wg + kk * nw;
     if (t >= ntiles) break;
@@ -827,10 +869,10 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
     // the previous tile missed the hot pair on > 1/4 of its keys: this one
     // runs the direct loop (A/B: also sampling the tile's own concentration
     // with __match_any_sync before choosing cost cfg2 more than it saved)
-    const bool direct = NMK_HIST_DIRECT && spread;
+    const bool direct = NMK_HIST_DIRECT && (kSpread || spread);
     if (direct) {
-      const DirectTile r = hist_tile_direct<T>(sk, base, cur, t * kKeyTile, gmin, gmax, width, inv_w, nbins, my,
-                                               hot1, hot2);
+      const DirectTile r = hist_tile_direct<T>(sk, base, cur, t * kKeyTile, gmin, et_c, width, inv_w, nbins, my,
+                                               hot1, hot2, g32);
       c1x += r.c1;
       c2x += r.c2;
       miss += r.miss;
@@ -852,9 +894,10 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
       visit(ord(sk[idx], t * kKeyTile + idx));
     }
     // adapt: promote the most recent miss when the hot pair covers too little
+    // (the spread policy never promotes: every tile is direct)
     const unsigned tile_miss = __reduce_add_sync(FULL, miss);
     spread = tile_miss > (unsigned)(kKeyTile / 4);
-    if (tile_miss > (unsigned)(kKeyTile / 8)) {
+    if (!kSpread && tile_miss > (unsigned)(kKeyTile / 8)) {
       const unsigned have = __ballot_sync(FULL, last_miss < nbins);
       if (have) {
         const uint32_t cand = __shfl_sync(FULL, last_miss, __ffs(have) - 1);
@@ -880,6 +923,7 @@ __device__ __forceinline__ void hist_keys_hot(const float* __restrict__ keys, co
   for (uint64_t j = ntiles * kKeyTile + wg * 32 + lane; j < n; j += nw * 32) visit(ord(keys[j], j));
   flush(hot1, tested - ndef - c2 + c1x);
   flush(hot2, c2 + c2x);
+  }
 }
 
 // ---- key histogram with lane-private counters (spans of <= 63 bins) ---------
@@ -1007,25 +1051,88 @@ __device__ __forceinline__ void hist_keys_priv(const float* __restrict__ keys, c
   (void)FULL;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kHistThreads, 3)
+// Two launch shapes of the same kernel.  kW = 0: 256 threads, 3 CTAs/SM,
+// key replicas of up to 8192 counters (spans of the concentrated fields).
+// kW = 1 ("wide"): one 512-thread CTA per SM with 96 KB of replica counters,
+// so spans of 8K..24K bins (cfg5 at E = 1e-4: 10^4 bins) still count into
+// shared memory -- 2 replicas of 10^4 bins, 8 warps each -- instead of one
+// 48 KB replica per CTA with run-length atomics.  The host picks the shape
+// from a span hint (the previous step's span); the kernel decides its path
+// from the actual span, so a wrong hint costs speed, never correctness.
+#ifndef NMK_K2_MINB
+#define NMK_K2_MINB 3
+#endif
+template <int kW> struct HistShape;
+template <> struct HistShape<0> {   // concentrated fields: hot-pair policy
+  static constexpr int kThreads = kHistThreads, kMinBlocks = NMK_K2_MINB;
+  static constexpr uint32_t kRepWords = kKeySmemBins;
+  static constexpr bool kSpread = false;
+};
+#ifndef NMK_WIDE_WORDS
+#define NMK_WIDE_WORDS 20480    // 80 KB of counters + 32 warps x 4 KB of key stages
+#endif
+#ifndef NMK_WIDE_THREADS
+#define NMK_WIDE_THREADS 1024   // A/B (cfg5 E=1e-4 K2): 512 0.39 ms, 768 0.29, 1024 0.26
+#endif
+template <> struct HistShape<1> {   // spread fields over 8K..24K bins
+  static constexpr int kThreads = NMK_WIDE_THREADS, kMinBlocks = 1;
+  static constexpr uint32_t kRepWords = NMK_WIDE_WORDS;
+  static constexpr bool kSpread = true;
+};
+template <> struct HistShape<2> {   // spread fields over < 8K bins
+  static constexpr int kThreads = kHistThreads, kMinBlocks = NMK_K2_MINB;
+  static constexpr uint32_t kRepWords = kKeySmemBins;
+  static constexpr bool kSpread = true;
+};
+template <int kW>
+constexpr size_t hist_dev_smem() {
+  return std::max<size_t>(kDevSmemBins * 4, HistShape<kW>::kRepWords * 4 +
+                                                (HistShape<kW>::kThreads / 32) * kKeyStages * kKeyTile * 4);
+}
+
+template <typename T, int kW>
+__global__ void __launch_bounds__(HistShape<kW>::kThreads, HistShape<kW>::kMinBlocks)
 k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* __restrict__ keys, uint64_t n,
            const nmk_stats* __restrict__ st, double width, unsigned long long* __restrict__ counts, bool vec_ok) {
+  constexpr int kT = HistShape<kW>::kThreads;
+  constexpr uint32_t kRW = HistShape<kW>::kRepWords;
   extern __shared__ uint32_t h[];
   const unsigned long long nb64 = st->reserved;
   if (nb64 == 0 || nb64 == NMK_SPAN_SPARSE) return;
   const uint32_t nbins = (uint32_t)nb64;
   const double gmin = st->gmin;
   const double inv_w = 1.0 / width;
-  if (nbins <= kDevSmemBins) {
-    __shared__ unsigned long long s_bars[kHistThreads / 32][kKeyStages];
-    static_assert(kPrivWords * (kHistThreads / 32) <= kKeySmemBins, "private tables alias the replicas");
+  if constexpr (HistShape<kW>::kSpread) {
+    // spread shapes carry only their replica path (fewer registers); a span
+    // they do not fit -- a stale hint -- takes the global-atomic path below
+    if (keys && nbins + 1 <= kRW) {
+      __shared__ unsigned long long s_bars_sp[kT / 32][kKeyStages];
+      const uint32_t nb1 = nbins + 1;
+      int reps = (int)(kRW / nb1);
+      if (reps > kT / 32) reps = kT / 32;
+      for (uint32_t i = threadIdx.x; i < nb1 * (uint32_t)reps; i += blockDim.x) h[i] = 0;
+      __syncthreads();
+      const int wid = threadIdx.x >> 5;
+      float* stage = reinterpret_cast<float*>(h + kRW) + wid * kKeyStages * kKeyTile;
+      hist_keys_hot<T, true>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins,
+                             h + (uint32_t)(wid % reps) * nb1, stage, s_bars_sp[wid]);
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < nb1; i += blockDim.x) {
+        uint32_t s = 0;
+        for (int r = 0; r < reps; ++r) s += h[r * nb1 + i];
+        if (s) atomicAdd(&counts[i], (unsigned long long)s);
+      }
+      return;
+    }
+  } else if (nbins <= kDevSmemBins || (keys && nbins + 1 <= kRW)) {
+    __shared__ unsigned long long s_bars[kT / 32][kKeyStages];
+    static_assert(kPrivWords * (kT / 32) <= kRW, "private tables alias the replicas");
     if (NMK_HIST_PRIV && keys && nbins + 1 <= kPrivBins) {   // lane-private counters (tripwire = slot nbins)
       __shared__ uint32_t s_tot[kPrivBins];
       if (threadIdx.x < kPrivBins) s_tot[threadIdx.x] = 0;
       __syncthreads();
       const int wid = threadIdx.x >> 5;
-      float* stage = reinterpret_cast<float*>(h + kKeySmemBins) + wid * kKeyStages * kKeyTile;
+      float* stage = reinterpret_cast<float*>(h + kRW) + wid * kKeyStages * kKeyTile;
       hist_keys_priv<T>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins, h + wid * kPrivWords, s_tot, stage,
                         s_bars[wid]);
       __syncthreads();
@@ -1033,16 +1140,16 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
         atomicAdd(&counts[threadIdx.x], (unsigned long long)s_tot[threadIdx.x]);
       return;
     }
-    if (keys && nbins < kKeySmemBins) {   // replicas of nbins + 1 slots (tripwire last)
+    if (keys && nbins + 1 <= kRW) {   // replicas of nbins + 1 slots (tripwire last)
       const uint32_t nb1 = nbins + 1;
-      int reps = (int)(kKeySmemBins / nb1);
-      if (reps > kHistThreads / 32) reps = kHistThreads / 32;
+      int reps = (int)(kRW / nb1);
+      if (reps > kT / 32) reps = kT / 32;
       for (uint32_t i = threadIdx.x; i < nb1 * (uint32_t)reps; i += blockDim.x) h[i] = 0;
       __syncthreads();
       const int wid = threadIdx.x >> 5;
-      float* stage = reinterpret_cast<float*>(h + kKeySmemBins) + wid * kKeyStages * kKeyTile;
-      hist_keys_hot<T>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins, h + (uint32_t)(wid % reps) * nb1,
-                       stage, s_bars[wid]);
+      float* stage = reinterpret_cast<float*>(h + kRW) + wid * kKeyStages * kKeyTile;
+      hist_keys_hot<T, false>(keys, base, cur, n, gmin, st->gmax, width, inv_w, nbins,
+                              h + (uint32_t)(wid % reps) * nb1, stage, s_bars[wid]);
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < nb1; i += blockDim.x) {
         uint32_t s = 0;
@@ -1052,7 +1159,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
       return;
     }
     int reps = (int)(kDevSmemBins / nbins);
-    if (reps > kHistThreads / 32) reps = kHistThreads / 32;
+    if (reps > kT / 32) reps = kT / 32;
     for (uint32_t i = threadIdx.x; i < nbins * (uint32_t)reps; i += blockDim.x) h[i] = 0;
     __syncthreads();
     uint32_t* my = h + (uint32_t)((threadIdx.x >> 5) % reps) * nbins;
@@ -1088,7 +1195,9 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
       for (int r = 0; r < reps; ++r) s += h[r * nbins + i];
       if (s) atomicAdd(&counts[i], (unsigned long long)s);
     }
-  } else {
+    return;
+  }
+  {
     uint64_t last = ~0ULL;
     unsigned long long run = 0;
     auto add_q = [&](auto q) {
@@ -1122,33 +1231,46 @@ extern "C" int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins, 
   return check_launch("k_hist_prep");
 }
 
-extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, const float* keys, uint64_t n, int dtype,
-                                  const nmk_stats* stats, double width, unsigned long long* counts, void* stream) {
-  if (keys && ((uintptr_t)keys & 15)) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: keys must be 16-byte aligned");
-  if (!base || !cur || !stats || !counts || n == 0) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad argument");
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
-  // 48 KB of counters for the pair paths; the key path uses 32 KB of
-  // counters + the per-warp TMA key stages in the same allocation
-  const size_t smem = std::max<size_t>(kDevSmemBins * 4, kKeySmemBins * 4 + (kHistThreads / 32) * kKeyStages * kKeyTile * 4);
-  ensure_dyn_smem(k_hist_dev<double>, smem);
-  ensure_dyn_smem(k_hist_dev<float>, smem);
+template <int kW>
+static void launch_hist_dev(const void* base, const void* cur, const float* keys, uint64_t n, int dtype,
+                            const nmk_stats* stats, double width, unsigned long long* counts, bool aligned,
+                            cudaStream_t s) {
+  constexpr size_t smem = hist_dev_smem<kW>();
+  constexpr int kT = HistShape<kW>::kThreads;
+  ensure_dyn_smem(k_hist_dev<double, kW>, smem);
+  ensure_dyn_smem(k_hist_dev<float, kW>, smem);
   // one resident wave: the grid-stride loops split the work evenly over it
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist_dev<double>, kHistThreads, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hist_dev<double, kW>, kT, smem);
+  if (per_sm < 1) per_sm = 1;
   uint64_t want = (n + 8191) / 8192;
   uint64_t grid = (uint64_t)sm_count_h() * per_sm;
   if (want < grid) grid = want ? want : 1;
   if (dtype == NMK_F64)
-    k_hist_dev<double><<<(unsigned)grid, kHistThreads, smem, s>>>((const double*)base, (const double*)cur, keys, n,
-                                                                  stats, width, counts, aligned);
-  else if (dtype == NMK_F32)
-    k_hist_dev<float><<<(unsigned)grid, kHistThreads, smem, s>>>((const float*)base, (const float*)cur, keys, n,
-                                                                 stats, width, counts, aligned);
+    k_hist_dev<double, kW><<<(unsigned)grid, kT, smem, s>>>((const double*)base, (const double*)cur, keys, n, stats,
+                                                            width, counts, aligned);
   else
-    return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad dtype");
+    k_hist_dev<float, kW><<<(unsigned)grid, kT, smem, s>>>((const float*)base, (const float*)cur, keys, n, stats,
+                                                           width, counts, aligned);
+}
+
+extern "C" int nmk_hist_dense_dev2(const void* base, const void* cur, const float* keys, uint64_t n, int dtype,
+                                   const nmk_stats* stats, double width, unsigned long long* counts,
+                                   uint64_t span_hint, int spread_hint, void* stream) {
+  if (keys && ((uintptr_t)keys & 15)) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: keys must be 16-byte aligned");
+  if (!base || !cur || !stats || !counts || n == 0) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad argument");
+  if (dtype != NMK_F32 && dtype != NMK_F64) return set_error(NMK_ERR_ARG, "nmk_hist_dense_dev: bad dtype");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool aligned = (((uintptr_t)base | (uintptr_t)cur) & 15) == 0;
+  // wide shape only where its replicas are the ones that fit
+  const bool wide = keys && span_hint + 1 > kKeySmemBins && span_hint + 1 <= HistShape<1>::kRepWords;
+  if (wide) launch_hist_dev<1>(base, cur, keys, n, dtype, stats, width, counts, aligned, s);
+  else if (keys && spread_hint && span_hint + 1 > kPrivBins) launch_hist_dev<2>(base, cur, keys, n, dtype, stats, width, counts, aligned, s);
+  else launch_hist_dev<0>(base, cur, keys, n, dtype, stats, width, counts, aligned, s);
   return check_launch("k_hist_dev");
+}
+
+extern "C" int nmk_hist_dense_dev(const void* base, const void* cur, const float* keys, uint64_t n, int dtype,
+                                  const nmk_stats* stats, double width, unsigned long long* counts, void* stream) {
+  return nmk_hist_dense_dev2(base, cur, keys, n, dtype, stats, width, counts, 0, 0, stream);
 }

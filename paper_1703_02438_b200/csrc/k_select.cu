@@ -32,7 +32,7 @@ constexpr int kAutoLo = 2, kAutoHi = 16;           // binning.py:22
 constexpr int kNSel = kAutoHi - kAutoLo + 1;       // 15 simultaneous selects (auto B)
 constexpr int kNSelMax = 29;                       // B = 2..30: select_index_length's widest range
 
-constexpr uint64_t kSelCache = 8192;  // bins whose selectable counts live in smem
+constexpr uint64_t kSelCache = 20480;  // bins whose selectable counts live in smem (160 KB)
 
 struct BinView {
   const unsigned long long* keys;    // null -> dense (ordinal = index)
@@ -56,6 +56,23 @@ struct BinView {
 template <typename T>
 __device__ __forceinline__ double quantize(double c) { return to_f64(narrow<T>(c)); }
 
+// pass A's per-thread record: selectable bins, their total, the two largest counts
+struct PassA {
+  unsigned long long m, tot, a, b;
+};
+struct PassAOp {
+  __device__ __forceinline__ PassA operator()(const PassA& x, const PassA& y) const {
+    PassA r;
+    r.m = x.m + y.m;
+    r.tot = x.tot + y.tot;
+    r.a = x.a > y.a ? x.a : y.a;
+    const unsigned long long lo = x.a > y.a ? y.a : x.a;   // the smaller top
+    const unsigned long long sb = x.b > y.b ? x.b : y.b;
+    r.b = lo > sb ? lo : sb;
+    return r;
+  }
+};
+
 // NS = radix-select slots compiled in; auto B (bits_cfg < 0) runs auto_n of
 // them for B = auto_lo .. auto_lo + auto_n - 1.  cov_out != null: coverage
 // only (binning._coverage_by_bits) -- write the covered counts and stop.
@@ -68,9 +85,11 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
          T* __restrict__ centers_t, uint64_t cap_k, nmk_model* __restrict__ model,
          int auto_lo, int auto_n, unsigned long long* __restrict__ cov_out) {
   typedef cub::BlockReduce<unsigned long long, kSelThreads> BRed;
+  typedef cub::BlockReduce<PassA, kSelThreads> BRedA;
   typedef cub::BlockScan<unsigned, kSelThreads> BScan;
   __shared__ union {
     typename BRed::TempStorage red;
+    typename BRedA::TempStorage reda;
     typename BScan::TempStorage scan;
   } tmp;
   __shared__ unsigned hist[NS][256];
@@ -121,20 +140,24 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     bv.cache = s_cache;
   }
 
-  // ---- pass A: m (selectable bins), max count, total selectable count ----
-  unsigned long long my_m = 0, my_max = 0, my_tot = 0;
+  // ---- pass A: m (selectable bins), total selectable count, and the two
+  // largest counts (the second tells the next step's K2 how much of the
+  // field a hot pair of bins can hold) -- one block reduction
+  PassA pa{0, 0, 0, 0};
   for (uint64_t i = tid; i < M; i += kSelThreads) {
     unsigned long long c = bv.sel_count(i);
-    if (c) { ++my_m; my_tot += c; if (c > my_max) my_max = c; }
+    if (c) {
+      ++pa.m;
+      pa.tot += c;
+      if (c > pa.a) { pa.b = pa.a; pa.a = c; }
+      else if (c > pa.b) pa.b = c;
+    }
   }
-  unsigned long long m = BRed(tmp.red).Sum(my_m);
+  pa = BRedA(tmp.reda).Reduce(pa, PassAOp());
+  if (tid == 0) { s_bcast[0] = pa.m; s_bcast[1] = pa.a; s_bcast[2] = pa.tot; s_bcast[3] = pa.b; }
   __syncthreads();
-  unsigned long long maxc = BRed(tmp.red).Reduce(my_max, cub::Max());
-  __syncthreads();
-  unsigned long long tot = BRed(tmp.red).Sum(my_tot);
-  if (tid == 0) { s_bcast[0] = m; s_bcast[1] = maxc; s_bcast[2] = tot; }
-  __syncthreads();
-  m = s_bcast[0]; maxc = s_bcast[1]; tot = s_bcast[2];
+  unsigned long long m = s_bcast[0], maxc = s_bcast[1], tot = s_bcast[2];
+  const unsigned long long second = s_bcast[3];
   if (m == 0) {
     if (tid == 0) { model->status = NMK_ERR_EMPTY_HIST; model->k = 0; model->m_selectable = 0; }
     if (cov_out && tid < auto_n) cov_out[tid] = 0;
@@ -325,6 +348,8 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     model->m_selectable = (int)(m > 0x7fffffffULL ? 0x7fffffff : m);
     model->tol_bin = width / 2.0;
     for (int b = 0; b < 17; ++b) model->coverage[b] = 0;
+    model->coverage[0] = maxc;   // K2's spread hint for the next step (nmk_hist_dense_dev2)
+    model->coverage[1] = second;
     if (autob)
       for (int s = 0; s < auto_n && auto_lo + s <= kAutoHi; ++s) model->coverage[auto_lo + s] = s_cov[s];
   }

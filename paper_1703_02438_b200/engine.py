@@ -241,8 +241,8 @@ def encode(base, cur, tolerance: float, bits: int | None = None, block_bytes: in
             if n_local > 0 and keyed:
                 # device span (same arithmetic as above) + K2 from the keys
                 N.check(lib.nmk_hist_prep(_p(stats), width, DENSE_MAX_BINS, _p(counts_t), st))
-                N.check(lib.nmk_hist_dense_dev(_p(base), _p(cur), _p(keys), n_local, dt, _p(stats), width,
-                                               _p(counts_t), st))
+                N.check(lib.nmk_hist_dense_dev2(_p(base), _p(cur), _p(keys), n_local, dt, _p(stats), width,
+                                                _p(counts_t), nbins, 0, st))
             elif n_local > 0:
                 N.check(lib.nmk_hist_dense(_p(base), _p(cur), n_local, dt, _p(stats), width, nbins,
                                            _p(counts_t), st))
@@ -432,6 +432,10 @@ class DevicePipeline:
         self.b0 = self.elem0 // self.epb
         self.nlb = (self.elem0 + self.n_local - 1) // self.epb - self.b0 + 1
         self.k_cap = (1 << bits) - 1
+        # K2 launch shape follows the last observed dense span (check()); the
+        # counts never depend on it
+        self.span_hint = 0
+        self.spread_hint = 0
         # dense span capacity; with a comm it is also the all-reduced histogram
         # length (fit_comm_bins sizes it to the observed span)
         self.cap_bins = (comm_bins or ASYNC_COMM_BINS) if comm is not None else DENSE_MAX_BINS
@@ -494,8 +498,8 @@ class DevicePipeline:
             self.comm.allreduce_stats_device(self.stats)
         mark("K1_minmax")
         N.check(lib.nmk_hist_prep(P(self.stats), self.width, self.cap_bins, P(self.counts), st))
-        N.check(lib.nmk_hist_dense_dev(P(base), P(cur), P(self.keys), self.n_local, self.dt, P(self.stats),
-                                       self.width, P(self.counts), st))
+        N.check(lib.nmk_hist_dense_dev2(P(base), P(cur), P(self.keys), self.n_local, self.dt, P(self.stats),
+                                        self.width, P(self.counts), self.span_hint, self.spread_hint, st))
         if self.comm is not None:
             self.comm.allreduce_counts(self.counts)
         mark("K2_histogram")
@@ -551,6 +555,12 @@ class DevicePipeline:
         n_inc = int(self.n_inc.item())
         trip = int(self.counts[min(int(sv.reserved), self.cap_bins)].item()) \
             if 0 < sv.reserved <= self.cap_bins else 0
+        if 0 < sv.reserved <= self.cap_bins and model.status == 0:
+            self.span_hint = int(sv.reserved)
+            # spread field: a hot pair of bins would hold under 3/4 of the valid
+            # ratios (K3 leaves the two largest selectable counts in coverage[0..1])
+            top2 = int(model.coverage[0]) + int(model.coverage[1])
+            self.spread_hint = int(4 * top2 < 3 * int(sv.nvalid))
         return {"status": int(model.status), "bits": int(model.bits), "k": int(model.k), "n_inc": n_inc,
                 "gmin": float(sv.gmin), "gmax": float(sv.gmax), "nvalid": int(sv.nvalid), "nbins": int(sv.reserved),
                 "tripwire": trip, "bad_index": bool(e.bad_index), "exhausted": bool(e.exhausted),

@@ -66,6 +66,7 @@ def _pipeline_graph(base, cur, E, bits, replays=2):
     pipe = engine.DevicePipeline(base.numel(), base.dtype, E, bits)
     out = torch.empty_like(base)
     pipe.step(base, cur, out)
+    pipe.check()   # as bench.py: the warm-up step's span / spread hints pick K2's launch shape
     g = pipe.capture(base, cur, out)
     out.fill_(0)
     for _ in range(replays):

@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
-from paper_1703_02438_b200 import engine  # noqa: E402
+from paper_1703_02438_b200 import _native as N, engine  # noqa: E402
 
 
 def _blocks(enc):
@@ -292,3 +292,51 @@ def test_histogram_forms_exact(dtype, E, kind):
     np.testing.assert_array_equal(got[: chk["nbins"]], dense)
     if kind == "narrow":
         assert chk["nbins"] <= 63
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("E,kind", [(1e-4, "bimodal"), (1e-3, "bimodal"), (1e-2, "bimodal"), (1e-3, "narrow"),
+                                    (2e-5, "uniform"), (1e-3, "concentrated")])
+@pytest.mark.parametrize("span_hint,spread_hint", [(0, 0), (1116, 1), (10000, 1), (20000, 0), (3, 1)])
+def test_histogram_launch_shapes_exact(dtype, E, kind, span_hint, spread_hint):
+    """K2's launch shapes (hot-pair / spread replicas / wide 1024-thread
+    replicas) and counting policies, chosen by the previous step's span and
+    spread hints, give the same exact counts whatever the hint -- including
+    hints that do not match the data (a stale hint costs speed only).
+    Spans: bimodal at E = 1e-4 -> 10^4 bins (the wide shape), uniform at
+    E = 2e-5 -> 5*10^4 bins (beyond every replica: the global fallback)."""
+    rng = np.random.default_rng(11)
+    n = (1 << 22) + 4321
+    b = rng.lognormal(0.0, 1.0, n)
+    if kind == "bimodal":
+        m = rng.uniform(size=n)
+        r = np.where(m < 0.4, rng.normal(-0.02, 0.004, n), rng.normal(0.03, 0.006, n))
+        out = m > 0.8
+        r[out] = rng.uniform(-1.0, 1.0, out.sum())
+    elif kind == "uniform":
+        r = rng.uniform(-1.0, 1.0, n)
+    elif kind == "concentrated":
+        r = np.where(rng.uniform(size=n) < 0.95, rng.normal(0.0, 1e-4, n), rng.normal(0.0, 0.05, n))
+    else:
+        r = rng.normal(0.0, 0.008, n)
+    c = b * (1.0 + r)
+    b, c = b.astype(dtype), c.astype(dtype)
+    bt, ct = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(bt.numel(), bt.dtype, E, 8)
+    pipe.span_hint, pipe.spread_hint = span_hint, spread_hint
+    out_t = torch.empty_like(bt)
+    pipe.encode(bt, ct)
+    torch.cuda.synchronize()
+    sv = engine._read_struct(pipe.stats, N.NmkStats)
+    nbins = int(sv.reserved)
+    rr, v = O.ratios_of(b, c)
+    keys, counts = O.histogram(rr[v], float(sv.gmin), 2 * E)
+    dense = np.zeros(nbins, dtype=np.int64)
+    dense[keys.astype(np.int64)] = counts
+    got = _dense_counts(pipe, nbins)
+    np.testing.assert_array_equal(got[:nbins], dense)
+    assert int(pipe.counts[nbins].item()) == 0   # tripwire
+    if kind == "bimodal" and E == 1e-4:
+        assert 8192 < nbins + 1 <= 20480       # the wide shape's range
+    if kind == "uniform":
+        assert nbins + 1 > 20480

@@ -45,14 +45,14 @@ def test_reference_suite_against_dropin(tmp_path):
         pytest.skip("no CUDA device")
     if not _have_ref():
         pytest.skip("oracle/_ref not vendored (run oracle/make_ref.py where /root/reference exists)")
-    tests_dir = os.path.join(REF, "tests")
     xml = tmp_path / "ref.xml"
+    # run from oracle/_ref so node ids are "tests/<file>::<test>" (what --deselect matches)
     cmd = [sys.executable, "-m", "pytest", "-p", "ref_dropin", "-q", "-p", "no:cacheprovider",
-           f"--rootdir={REF}", f"--junitxml={xml}", tests_dir]
+           f"--rootdir={REF}", f"--junitxml={xml}", "tests"]
     for node in OUT_OF_SCOPE:
-        cmd += ["--deselect", os.path.join(tests_dir, node)]
+        cmd += ["--deselect", f"tests/{node}"]
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "tests"), REF, ROOT]))
-    r = subprocess.run(cmd, cwd=str(tmp_path), env=env, capture_output=True, text=True, timeout=900)
+    r = subprocess.run(cmd, cwd=REF, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     suite = ET.parse(xml).getroot()
     suite = suite if suite.tag == "testsuite" else suite.find("testsuite")

@@ -23,6 +23,7 @@ cases = [("cfg3", cfg3_pair, 5e-3, 10),
          ("cfg2", lambda: workloads.cfg2_device(512, seed=0), 1e-3, 8),
          ("cfg4w", lambda: workloads.cfg1_device(1 << 29, seed=4), 1e-3, 8),
          ("cfg5 B8 E1e-3", lambda: workloads.cfg5_device(1 << 28, seed=5), 1e-3, 8),
+         ("cfg5 B8 E1e-4", lambda: workloads.cfg5_device(1 << 28, seed=5), 1e-4, 8),
          ("cfg5 B8 E1e-2", lambda: workloads.cfg5_device(1 << 28, seed=5), 1e-2, 8),
          ("cfg5 B12 E1e-4", lambda: workloads.cfg5_device(1 << 28, seed=5), 1e-4, 12)]
 only = os.environ.get("AB_CASES")   # comma-separated case names to run (default: all)

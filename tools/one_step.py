@@ -21,5 +21,5 @@ out = torch.empty_like(base)
 pipe = engine.DevicePipeline(base.numel(), base.dtype, E, B)
 for _ in range(2):
     pipe.step(base, cur, out)
-torch.cuda.synchronize()
-print(pipe.check())
+    torch.cuda.synchronize()
+    print(pipe.check())   # also sets the span hint the next step's K2 launch uses
