@@ -71,8 +71,10 @@ struct SegParams {
 
 struct DecodeGeom {
   uint64_t epb, n_total, first_block, stride, n_exact, nchunks, nitems;
-  uint32_t cpb;
+  uint32_t cpb;        // encoder chunks (256 elements) per block: the count pass and its offsets
   FastDiv fd_cpb;
+  uint32_t cpb_d;      // decode chunks (DC elements) per block: k_dec_chunks' work items
+  FastDiv fd_cpb_d;
   int nseg, k;
 };
 
@@ -105,6 +107,36 @@ __device__ __forceinline__ DChunk dchunk(const DecodeGeom& geo, uint32_t g) {
 template <int B>
 __device__ __forceinline__ const uint8_t* chunk_src(const uint8_t* packed, const DecodeGeom& geo, const DChunk& d) {
   return packed + (uint64_t)(d.b - (uint32_t)geo.first_block) * geo.stride + (uint64_t)d.ci * (32 * B);
+}
+
+// Decode chunk g (DC = 256 or 512 elements: f32 decodes two encoder chunks
+// per work item, so each item moves as many bytes as an f64 one and the
+// per-item overhead is paid half as often).  crel is the encoder-chunk
+// index (relative to first_block) of its first half; crel_end one past its
+// last encoder chunk -- the count pass's offsets stay per 256 elements.
+template <int B, int DC>
+__device__ __forceinline__ DChunk dchunk_d(const DecodeGeom& geo, uint32_t g, uint32_t& crel_end) {
+  constexpr uint32_t R = DC / kDChunk;
+  DChunk d;
+  d.b = geo.fd_cpb_d.div(g);
+  d.ci = g - d.b * geo.cpb_d;
+  const uint64_t blk_start = (uint64_t)d.b * geo.epb;
+  const uint64_t rem = geo.n_total - blk_start;
+  const uint32_t blk_len = (uint32_t)(rem < geo.epb ? rem : geo.epb);
+  const uint32_t off = d.ci * DC;
+  d.chunk_lo = blk_start + off;
+  d.valid = min((uint32_t)DC, blk_len - off);
+  const uint32_t blk_bytes = (uint32_t)(((uint64_t)blk_len * B + 7) / 8);
+  d.nbytes = min((uint32_t)(DC / 8 * B), blk_bytes - d.ci * (DC / 8 * B));
+  const uint32_t rb = (d.b - (uint32_t)geo.first_block) * geo.cpb;
+  d.crel = rb + d.ci * R;
+  crel_end = rb + min(d.ci * R + R, geo.cpb);
+  return d;
+}
+
+template <int B, int DC>
+__device__ __forceinline__ const uint8_t* chunk_src_d(const uint8_t* packed, const DecodeGeom& geo, const DChunk& d) {
+  return packed + (uint64_t)(d.b - (uint32_t)geo.first_block) * geo.stride + (uint64_t)d.ci * (DC / 8 * B);
 }
 
 // This lane's B bytes (offset lane*B of a 16-byte aligned chunk) with the
@@ -355,10 +387,14 @@ template <typename T> struct DVec;
 template <> struct DVec<double> { using V = double2; static constexpr int N = 2; };
 template <> struct DVec<float>  { using V = float4;  static constexpr int N = 4; };
 
+// decode-chunk size: 512 elements for f32 (two encoder chunks), 256 for f64
+template <typename T> struct DecChunk { static constexpr int kDC = sizeof(T) == 4 ? 512 : 256; };
+
 template <typename T, int B, int S = kStages>
 struct DecStage {
-  static constexpr int kBase = kDChunk * (int)sizeof(T);   // 2048 (f64) / 1024 (f32)
-  static constexpr int kPk = 32 * B;                        // a multiple of 16
+  static constexpr int kDC = DecChunk<T>::kDC;
+  static constexpr int kBase = kDC * (int)sizeof(T);        // 2048 bytes for both dtypes
+  static constexpr int kPk = kDC / 8 * B;                   // a multiple of 16
   static constexpr int kAux = kBase + kPk + 16;             // +16: 8-byte code windows
   static constexpr int kBytes = kAux + 32;                  // rank anchors (4 x u64)
   static constexpr size_t kSmem = (size_t)kTmaWarps * S * kBytes;
@@ -426,6 +462,7 @@ constexpr int kOpcMax = 2048;
 struct DItem {
   int seg;
   DChunk d;
+  uint32_t crel_end;         // one past the item's last encoder chunk (offsets index)
   uint32_t lo_rel, hi_rel;   // in-segment elements of the chunk: [lo_rel, hi_rel)
   int64_t oi0;               // base/out index of the chunk's first element
   uint32_t anchor;           // block (relative) of the segment's first chunk
@@ -436,6 +473,7 @@ struct DItem {
 template <typename T, int B>
 __device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo, const Seg* SG,
                                              const T* __restrict__ base) {
+  constexpr int DC = DecChunk<T>::kDC;
   int s = 0;
   if (geo.nseg > 1) {
     int hi_s = geo.nseg - 1;
@@ -448,7 +486,7 @@ __device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo,
   DItem t;
   t.seg = s;
   const uint32_t rel = (uint32_t)(it - sg.item0);
-  t.d = dchunk<B>(geo, (uint32_t)sg.gfirst + rel);
+  t.d = dchunk_d<B, DC>(geo, (uint32_t)sg.gfirst + rel, t.crel_end);
   t.first = rel == 0;
   const int64_t lo = (int64_t)sg.start - (int64_t)t.d.chunk_lo;
   const int64_t hi = lo + (int64_t)sg.count;
@@ -456,9 +494,9 @@ __device__ __forceinline__ DItem decode_item(uint64_t it, const DecodeGeom& geo,
   t.hi_rel = (uint32_t)(hi > (int64_t)t.d.valid ? (int64_t)t.d.valid : hi);
   t.last = hi <= (int64_t)t.d.valid;
   t.oi0 = (int64_t)sg.out - lo;
-  t.anchor = geo.fd_cpb.div((uint32_t)sg.gfirst) - (uint32_t)geo.first_block;
-  t.base_tma = t.lo_rel == 0 && t.hi_rel == kDChunk && ((uintptr_t)(base + t.oi0) & 15) == 0;
-  t.pk_tma = (uint64_t)(t.d.ci + 1) * (32 * B) <= geo.stride;
+  t.anchor = geo.fd_cpb_d.div((uint32_t)sg.gfirst) - (uint32_t)geo.first_block;
+  t.base_tma = t.lo_rel == 0 && t.hi_rel == (uint32_t)DC && ((uintptr_t)(base + t.oi0) & 15) == 0;
+  t.pk_tma = (uint64_t)(t.d.ci + 1) * (DC / 8 * B) <= geo.stride;
   return t;
 }
 
@@ -488,7 +526,8 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
              int regime) {
   using ST = DecStage<T, B, S>;
   constexpr int VN = DVec<T>::N;          // elements per 16-byte vector
-  constexpr int Q = kGroup / VN;          // vectors per lane per chunk
+  constexpr int DC = DecChunk<T>::kDC;    // elements per work item
+  constexpr int Q = DC / 32 / VN;         // vectors per lane per item (4 for both dtypes)
   using V = typename DVec<T>::V;
   const unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -531,10 +570,10 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     uint8_t* sb = wst + st * ST::kBytes;
     mbar_arrive_tx(&bars[wid][st], (t.base_tma ? ST::kBase : 0) + (t.pk_tma ? ST::kPk : 0));
     if (t.base_tma) tma_load_1d(sb, base + t.oi0, ST::kBase, &bars[wid][st]);
-    if (t.pk_tma) tma_load_1d(sb + ST::kBase, chunk_src<B>(packed, geo, t.d), ST::kPk, &bars[wid][st]);
+    if (t.pk_tma) tma_load_1d(sb + ST::kBase, chunk_src_d<B, DC>(packed, geo, t.d), ST::kPk, &bars[wid][st]);
     const uint32_t aux = smem_u32(sb + ST::kAux);
     cp_async8(aux, offsets + t.d.crel);
-    cp_async8(aux + 8, offsets + t.d.crel + 1);
+    cp_async8(aux + 8, offsets + t.crel_end);
     cp_async8(aux + 16, offsets + (uint64_t)t.anchor * geo.cpb);
     cp_async8(aux + 24, prefix_rel + t.anchor);
     cp_async_arrive(&bars[wid][st]);
@@ -567,8 +606,8 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
     const unsigned long long chunk_off = ax[3] + (ax[0] - ax[2]);
     const uint32_t nsent = (uint32_t)(ax[1] - ax[0]);
     if (!t.pk_tma) {
-      const uint8_t* src = chunk_src<B>(packed, geo, t.d);
-      for (int i = lane; i < 32 * B; i += 32) sb[ST::kBase + i] = (uint32_t)i < t.d.nbytes ? __ldg(src + i) : 0;
+      const uint8_t* src = chunk_src_d<B, DC>(packed, geo, t.d);
+      for (int i = lane; i < ST::kPk; i += 32) sb[ST::kBase + i] = (uint32_t)i < t.d.nbytes ? __ldg(src + i) : 0;
       __syncwarp();
     }
     if (t.base_tma && out_al) {
@@ -785,22 +824,30 @@ static int sm_count_d() { return sm_count(); }
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct DecodePlan {
-  uint64_t cpb, nchunks, nitems;
+  uint64_t cpb, cpb_d, nchunks, nitems;
   size_t off_counts, off_offsets, off_scan, off_segs, total;
 };
 
-static DecodePlan decode_plan(const uint64_t* st, const uint64_t* ct, int nseg, uint64_t epb, uint64_t first_block) {
+// dc = decode-chunk size (k_dec_chunks' items); the count pass covers every
+// encoder chunk of the decode chunks touched, so the workspace is sized with
+// the largest dc (nmk_decode_ws_bytes has no dtype)
+static DecodePlan decode_plan(const uint64_t* st, const uint64_t* ct, int nseg, uint64_t epb, uint64_t first_block,
+                              uint64_t dc = 512) {
   DecodePlan p{};
   p.cpb = (epb + kDChunk - 1) / kDChunk;
+  p.cpb_d = (epb + dc - 1) / dc;
+  const uint64_t R = dc / kDChunk;
   uint64_t items = 0, last = 0;
   const uint64_t g0 = first_block * p.cpb;
   for (int s = 0; s < nseg; ++s) {
     if (ct[s] == 0) continue;
     uint64_t e = st[s] + ct[s] - 1;
-    uint64_t ga = (st[s] / epb) * p.cpb + (st[s] % epb) / kDChunk;
-    uint64_t gz = (e / epb) * p.cpb + (e % epb) / kDChunk;
+    uint64_t ga = (st[s] / epb) * p.cpb_d + (st[s] % epb) / dc;
+    uint64_t gz = (e / epb) * p.cpb_d + (e % epb) / dc;
     items += gz - ga + 1;
-    if (gz + 1 - g0 > last) last = gz + 1 - g0;
+    const uint64_t ci_end = (e % epb) / dc * R + R;
+    const uint64_t end = (e / epb) * p.cpb + (ci_end < p.cpb ? ci_end : p.cpb);
+    if (end - g0 > last) last = end - g0;
   }
   p.nchunks = last;
   p.nitems = items;
@@ -825,7 +872,7 @@ static void launch_dec_chunks(const uint8_t* packed, const DecodeGeom& geo, cons
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_chunks<T, B, S>, kTmaThreads, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)sms * per_sm;
-  const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;
+  const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;   // nitems: decode chunks
   if (grid > need) grid = need;
   k_dec_chunks<T, B, S><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, sp, offsets, prefix_rel, centers,
                                                                    (const T*)exact, (const T*)base, (T*)out, info,
@@ -918,7 +965,8 @@ static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t fi
       return set_error(NMK_ERR_ARG, "nmk_decode: segment %d empty or outside the covered blocks", i);
   }
   if (!packed || !centers || !base || !out || !prefix_rel) return set_error(NMK_ERR_ARG, "nmk_decode: null pointer");
-  DecodePlan p = decode_plan(h_seg_start, h_seg_count, nseg, epb, first_block);
+  const uint64_t dc = dtype == NMK_F32 ? 512 : 256;   // DecChunk<T>::kDC
+  DecodePlan p = decode_plan(h_seg_start, h_seg_count, nseg, epb, first_block, dc);
   if (ws_bytes < p.total) return set_error(NMK_ERR_ARG, "nmk_decode: workspace too small");
   Seg* hs = (Seg*)malloc(sizeof(Seg) * (size_t)nseg);
   uint64_t item0 = 0;
@@ -928,9 +976,9 @@ static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t fi
     sg.start = st;
     sg.count = ct;
     sg.out = h_seg_out[i];
-    sg.gfirst = (st / epb) * p.cpb + (st % epb) / kDChunk;
+    sg.gfirst = (st / epb) * p.cpb_d + (st % epb) / dc;
     sg.item0 = item0;
-    item0 += (e / epb) * p.cpb + (e % epb) / kDChunk - sg.gfirst + 1;
+    item0 += (e / epb) * p.cpb_d + (e % epb) / dc - sg.gfirst + 1;
     hs[i] = sg;
   }
   char* w = (char*)ws;
@@ -960,6 +1008,8 @@ static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t fi
   geo.nitems = p.nitems;
   geo.cpb = (uint32_t)p.cpb;
   geo.fd_cpb.init((uint32_t)p.cpb);
+  geo.cpb_d = (uint32_t)p.cpb_d;
+  geo.fd_cpb_d.init((uint32_t)p.cpb_d);
   geo.nseg = nseg;
   geo.k = k;
   if (dtype == NMK_F64)

@@ -60,4 +60,3 @@ def test_reference_suite_against_dropin(tmp_path):
     assert fails == 0 and errs == 0
     # 215 reference tests - 7 out-of-scope strategy tests
     assert total - skips >= 208, (total, skips)
-    assert "reference entry points bound to the B200 drop-in" in r.stdout
