@@ -41,10 +41,10 @@ constexpr int kStages = NMK_STAGES;    // chunks in flight per warp
 constexpr int kStagesDense = NMK_STAGES_DENSE;
 // f32 chunks carry half the bytes of f64 ones: more of them in flight
 #ifndef NMK_STAGES_F32
-#define NMK_STAGES_F32 6
+#define NMK_STAGES_F32 4   // A/B on cfg3 (512-element f32 items): 3 and 4 beat 5 and 6 (occupancy)
 #endif
 #ifndef NMK_STAGES_DENSE_F32
-#define NMK_STAGES_DENSE_F32 5
+#define NMK_STAGES_DENSE_F32 3
 #endif
 template <typename T> struct Rings { static constexpr int kS = kStages, kD = kStagesDense; };
 template <> struct Rings<float> { static constexpr int kS = NMK_STAGES_F32, kD = NMK_STAGES_DENSE_F32; };
@@ -261,6 +261,7 @@ k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __rest
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * (kDecThreads / 32);
   const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
+  // (A/B on cfg3 / cfg5 B12: 2, 4 or 8 chunks per warp iteration no faster)
   for (uint32_t c = blockIdx.x * (kDecThreads / 32) + wid; c < (uint32_t)geo.nchunks; c += nwarps) {
     const DChunk d = dchunk<B>(geo, g0 + c);
     unsigned mine;
@@ -899,7 +900,9 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
   chunk_scan(counts, geo.nchunks, offsets, scan_ws, s);
   // The host knows the exact count on the host-scalar path and picks one ring.
   // The sync-free path only knows it on the device: both rings launch and
-  // the one whose regime does not match exits at entry.
+  // the one whose regime does not match exits at entry.  (CUDA graph IF
+  // nodes set by the count pass were measured slower than the empty launch:
+  // cfg2 +25 us, cfg3 +19 us per step.)
   if (!n_exact_dev) {
     if (dec_dense(geo.n_exact, geo.nchunks))
       launch_dec_chunks<T, B, Rings<T>::kD>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
