@@ -223,6 +223,19 @@ int nmk_deflate(const uint8_t* packed, uint64_t block_stride, uint64_t nblocks, 
                 uint64_t last_len, uint32_t seg_bytes, uint8_t* out, unsigned long long* block_off,
                 void* ws, size_t ws_bytes, void* stream);
 
+/* -- lossless stage, decode half (codec.decompress_block, codec.py:119-128)
+ * Inflates nstreams raw RFC 1951 streams -- stream s is comp[comp_off[s] ..
+ * comp_off[s+1]) (comp_off: device, nstreams + 1 entries) -- into
+ * out + out_off[s] (out_off: device, nullable = s * out_stride), capacity
+ * out_stride bytes each, one warp per stream.  Any raw DEFLATE stream (zlib's or nmk_deflate's) is accepted.
+ * status[s]: 0 ok, 1 bad block type, 2 stored LEN/NLEN mismatch, 3 bad
+ * dynamic header, 4 bad Huffman code / symbol, 5 bad distance, 6 input ends
+ * before the final block, 7 bytes after the final block, 8 output past
+ * out_stride; produced[s]: bytes written. */
+int nmk_inflate(const uint8_t* comp, const unsigned long long* comp_off, uint64_t nstreams, uint8_t* out,
+                uint64_t out_stride, const unsigned long long* out_off, unsigned* status,
+                unsigned long long* produced, void* stream);
+
 /* -- sync-free (graph-capturable) variants ---------------------------------
  * Every decision scalar stays on the device, so a whole compress + decompress
  * step can be enqueued (or captured in a CUDA graph) without a host round

@@ -4,11 +4,14 @@
   reference (codec.py:28-59).
 * Bit packing / unpacking and range decoding run on the GPU (K4/K5 and the
   standalone nmk_pack / nmk_unpack kernels).
-* The lossless per-block DEFLATE stage (`compress_block` /
-  `decompress_block`) is OUTSIDE the accelerated path: it is the same raw
-  RFC 1951 stream at the same level, produced by the host's zlib exactly as
-  the reference does (codec.py:108-128), and is looked up through this
-  module's attributes so fault injection by monkeypatching still works.
+* The lossless per-block DEFLATE stage: `compress_block` / `decompress_block`
+  are the reference's host-zlib functions (the same raw RFC 1951 stream at
+  the same level, codec.py:108-128), looked up through this module's
+  attributes so fault injection by monkeypatching still works; compress_pair
+  deflates with them by default (byte-identical .nmk files).  The decode
+  path inflates on the GPU instead (k_inflate.cu, any raw DEFLATE stream:
+  zlib's or the optional GPU deflate's), so a decode ships only compressed
+  bytes to the device and never runs host zlib.
 """
 
 from __future__ import annotations
@@ -145,6 +148,64 @@ def gpu_deflate_blocks(packed_dev, stride: int, lengths, seg_bytes: int = 16384)
     return [data[int(o[b]): int(o[b + 1])] for b in range(nb)]
 
 
+_INFLATE_ERRORS = {
+    1: "inflate failed: invalid block type",
+    2: "inflate failed: invalid stored block lengths",
+    3: "inflate failed: invalid dynamic block header",
+    4: "inflate failed: invalid code",
+    5: "inflate failed: invalid distance",
+    6: "corrupt block: truncated or trailing bytes",
+    7: "corrupt block: truncated or trailing bytes",
+    8: "inflate failed: block inflates past its packed size",
+}
+
+
+def gpu_inflate_blocks(blobs, out_stride: int, device=None, slots=None, nslots: int | None = None):
+    """Inflate raw DEFLATE streams on the GPU (k_inflate.cu), the decode half
+    of the lossless stage (codec.py:119-128): stream i lands at
+    ``out[j*out_stride : j*out_stride + produced[i]]`` of the returned device
+    buffer, j = slots[i] (default i) of ``nslots`` slots -- the strided
+    packed-block layout K5 reads.  Returns ``(out, produced)``; a stream that
+    zlib would reject raises CodecError (truncated or trailing bytes with the
+    reference's message)."""
+    import torch
+    N.require_cuda()
+    blobs = [bytes(b) for b in blobs]
+    nb = len(blobs)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    total_slots = nslots if nslots is not None else nb
+    out = torch.zeros(max(total_slots * out_stride, 1), dtype=torch.uint8, device=dev)
+    if nb == 0:
+        return out, np.zeros(0, dtype=np.int64)
+    d_slot = None
+    if slots is not None:
+        d_slot = torch.from_numpy(np.asarray(slots, dtype=np.int64) * out_stride).to(dev)
+    off = np.zeros(nb + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(b) for b in blobs])
+    comp = np.frombuffer(b"".join(blobs) or b"\0", dtype=np.uint8)
+    d_comp = torch.from_numpy(comp.copy()).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    status = torch.empty(nb, dtype=torch.int32, device=dev)
+    produced = torch.empty(nb, dtype=torch.int64, device=dev)
+    N.check(N.lib().nmk_inflate(d_comp.data_ptr(), d_off.data_ptr(), nb, out.data_ptr(), out_stride,
+                                d_slot.data_ptr() if d_slot is not None else None, status.data_ptr(),
+                                produced.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    st = status.cpu().numpy()
+    bad = np.flatnonzero(st)
+    if bad.size:
+        raise CodecError(_INFLATE_ERRORS.get(int(st[bad[0]]), "inflate failed"))
+    return out, produced.cpu().numpy()
+
+
+def gpu_decompress_block(data: bytes, capacity: int | None = None) -> bytes:
+    """:func:`decompress_block` on the GPU (one stream).  ``capacity`` bounds
+    the inflated size (default: 1032x the input, DEFLATE's maximum ratio)."""
+    cap = capacity if capacity is not None else max(1032 * len(data) + 64, 64)
+    cap = (cap + 15) // 16 * 16
+    out, produced = gpu_inflate_blocks([data], cap)
+    return out[: int(produced[0])].cpu().numpy().tobytes()
+
+
 def decompress_block(data: bytes) -> bytes:
     """Inflate one raw deflate stream produced by :func:`compress_block`."""
     try:
@@ -168,9 +229,27 @@ def _block_bytes_of(variable, ordinal: int) -> bytes:
     return variable.index_table[lo:hi]
 
 
+def _inflate_covering(compressed, first, bits, epb, n):
+    """The covering blocks' DEFLATE streams inflated on the GPU straight into
+    the strided packed layout K5 reads (k_inflate.cu): only compressed bytes
+    cross PCIe.  A block that inflates to fewer bytes than its element count
+    needs fails as unpack_block would (codec.py:97-99)."""
+    from . import engine
+    stride = engine.block_stride(epb, bits)
+    d_packed, produced = gpu_inflate_blocks(compressed, stride)
+    for i in range(len(compressed)):
+        s, e = (first + i) * epb, min((first + i + 1) * epb, n)
+        need_b = packed_size(e - s, bits)
+        if int(produced[i]) < need_b:
+            raise CodecError(f"short buffer: {int(produced[i])} bytes, need {need_b}")
+    return d_packed
+
+
 def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_offset, start, count, base):
-    """Decode [start, start+count) from the inflated packed ``blocks`` of the
-    covering block ordinals first..last on the GPU.
+    """Decode [start, start+count) of the covering block ordinals first..last
+    on the GPU.  ``blocks``: the blocks' packed bytes (a list of host byte
+    strings) or a device buffer already in the strided layout
+    (_inflate_covering).
 
     ``prefix`` = incompressible_prefix (global), ``exact`` = the exact values
     from global index ``exact_offset`` on.  Returns
@@ -180,17 +259,21 @@ def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_off
     from . import engine
     N.require_cuda()
     first = start // epb
-    nb = len(blocks)
     stride = engine.block_stride(epb, bits)
-    host = np.zeros(nb * stride, dtype=np.uint8)
-    for i, blk in enumerate(blocks):
-        s, e = (first + i) * epb, min((first + i + 1) * epb, n)
-        need_b = packed_size(e - s, bits)
-        if len(blk) < need_b:
-            raise CodecError(f"short buffer: {len(blk)} bytes, need {need_b}")
-        host[i * stride: i * stride + need_b] = np.frombuffer(blk, dtype=np.uint8, count=need_b)
     dev = torch.device("cuda", torch.cuda.current_device())
-    d_packed = torch.from_numpy(host).to(dev)
+    if isinstance(blocks, (list, tuple)):
+        nb = len(blocks)
+        host = np.zeros(nb * stride, dtype=np.uint8)
+        for i, blk in enumerate(blocks):
+            s, e = (first + i) * epb, min((first + i + 1) * epb, n)
+            need_b = packed_size(e - s, bits)
+            if len(blk) < need_b:
+                raise CodecError(f"short buffer: {len(blk)} bytes, need {need_b}")
+            host[i * stride: i * stride + need_b] = np.frombuffer(blk, dtype=np.uint8, count=need_b)
+        d_packed = torch.from_numpy(host).to(dev)
+    else:
+        d_packed = blocks
+        nb = (start + count - 1) // epb - first + 1
     pre = np.asarray(prefix, dtype=np.uint64)[first:first + nb].astype(np.int64)
     base_inc = int(pre[0])
     d_prefix_rel = torch.from_numpy(pre - base_inc).to(dev)
@@ -216,8 +299,8 @@ def _tdt(np_dtype):
 
 
 def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> np.ndarray:
-    """Shared range decoder (codec.py:204-239): validation, inflate of the
-    covering blocks on the host, then one K5 launch."""
+    """Shared range decoder (codec.py:204-239): validation, GPU inflate of the
+    covering blocks, then one K5 launch (no host zlib on the decode path)."""
     if start < 0 or count < 0 or start + count > variable.n:
         raise ValueError(f"range [{start}, {start + count}) outside 0..{variable.n}")
     base = np.asarray(base)
@@ -228,11 +311,8 @@ def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> n
     epb = variable.elements_per_block
     first = start // epb
     last = (start + count - 1) // epb
-    blocks = [decompress_block(block_bytes(b)) for b in range(first, last + 1)]
-    for i, b in enumerate(range(first, last + 1)):
-        s, e = b * epb, min((b + 1) * epb, variable.n)
-        if len(blocks[i]) < packed_size(e - s, variable.bits):
-            raise CodecError(f"short buffer: {len(blocks[i])} bytes, need {packed_size(e - s, variable.bits)}")
+    blocks = _inflate_covering([block_bytes(b) for b in range(first, last + 1)], first, variable.bits, epb,
+                               variable.n)
     inc_lo = int(variable.incompressible_prefix[first])
     exact, exact_offset = inc_slice_all(inc_lo)
     exact = np.asarray(exact)
@@ -265,12 +345,11 @@ def partial_decode(variable, start: int, count: int, base_reconstructed) -> np.n
                          lambda b: _block_bytes_of(variable, b), inc_slice)
 
 
-def partial_decode_many(variable, ranges, bases, *, inflated: dict | None = None) -> list:
+def partial_decode_many(variable, ranges, bases) -> list:
     """Batched :func:`partial_decode`: ``ranges`` = [(start, count), ...],
     ``bases[i]`` the base slice of range i.  Every covering block is inflated
-    once (host zlib, as ``decompress_block``; pass ``inflated`` = {block:
-    packed bytes} to reuse earlier inflates) and ALL ranges decode in one K5
-    launch.  Results equal ``partial_decode`` range by range (codec.py:242-258),
+    once on the GPU (k_inflate.cu) and ALL ranges decode in one K5 launch.
+    Results equal ``partial_decode`` range by range (codec.py:242-258),
     including its errors."""
     import torch
     from . import engine
@@ -294,25 +373,19 @@ def partial_decode_many(variable, ranges, bases, *, inflated: dict | None = None
     need = sorted({b for i in live for b in range(ranges[i][0] // epb, (ranges[i][0] + ranges[i][1] - 1) // epb + 1)})
     first, last = need[0], need[-1]
     stride = engine.block_stride(epb, bits)
-    host = np.zeros((last - first + 1) * stride, dtype=np.uint8)
-    inflated = {} if inflated is None else inflated
-    for b in need:
-        blk = inflated.get(b)
-        if blk is None:
-            blk = inflated[b] = decompress_block(_block_bytes_of(variable, b))
+    d_packed, produced = gpu_inflate_blocks([_block_bytes_of(variable, b) for b in need], stride,
+                                            slots=[b - first for b in need], nslots=last - first + 1)
+    for i, b in enumerate(need):
         s_, e_ = b * epb, min((b + 1) * epb, n)
         nb = packed_size(e_ - s_, bits)
-        if len(blk) < nb:
-            raise CodecError(f"short buffer: {len(blk)} bytes, need {nb}")
-        o = (b - first) * stride
-        host[o:o + nb] = np.frombuffer(blk, dtype=np.uint8, count=nb)
+        if int(produced[i]) < nb:
+            raise CodecError(f"short buffer: {int(produced[i])} bytes, need {nb}")
     prefix = np.asarray(variable.incompressible_prefix, dtype=np.uint64)
     lo = int(prefix[first])
     hi = int(prefix[last + 1]) if last + 1 < variable.nblocks else int(variable.n_incompressible)
     dt = variable.numpy_dtype
     exact = np.array(variable.incompressible_table[lo:max(hi, lo)], dtype=dt, copy=True)
     dev = torch.device("cuda", torch.cuda.current_device())
-    d_packed = torch.from_numpy(host).to(dev)
     d_prefix = torch.from_numpy(prefix[first:last + 1].astype(np.int64) - lo).to(dev)
     d_centers = torch.tensor(np.asarray(variable.centers, dtype=np.float64), device=dev)
     d_exact = torch.from_numpy(exact).to(dev) if exact.size else torch.empty(0, dtype=_tdt(dt), device=dev)
@@ -359,7 +432,8 @@ def partial_decode_file(handle, start: int, count: int, base_reconstructed) -> n
 def decode_block_indices(variable, ordinal: int) -> np.ndarray:
     start = ordinal * variable.elements_per_block
     stop = min(start + variable.elements_per_block, variable.n)
-    packed = decompress_block(_block_bytes_of(variable, ordinal))
+    packed = gpu_decompress_block(_block_bytes_of(variable, ordinal),
+                                  capacity=packed_size(variable.elements_per_block, variable.bits) + 16)
     return unpack_block(packed, variable.bits, stop - start)
 
 

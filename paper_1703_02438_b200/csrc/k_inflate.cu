@@ -1,0 +1,300 @@
+// k_inflate.cu — GPU inflate of raw DEFLATE streams (RFC 1951): the decode
+// half of the lossless index-table stage (codec.decompress_block,
+// pkg/src/nmk/codec.py:119-128).
+//
+// Every 1 MiB index block of a variable is one raw DEFLATE stream, written
+// either by the host's zlib (the reference's bytes) or by k_deflate.cu, so
+// the blocks inflate independently: one warp per stream, into the strided
+// packed-block layout K5 reads, so a decode never ships inflated bytes over
+// PCIe.  Inside a stream DEFLATE is sequential; all 32 lanes run the same
+// bit-reader and Huffman decode (their state is identical, loads broadcast)
+// and split the bytes of every match (and stored block) between them --
+// out[pos + j] = out[pos - dist + (j mod dist)] holds for overlapping
+// matches too, since the source bytes precede pos.
+//
+// Huffman decode: a 2^10-entry table per code (canonical codes, bit-reversed
+// as they arrive LSB first) resolves every code of <= 10 bits in one lookup;
+// longer codes take the canonical count walk (zlib's puff).  Validation
+// follows zlib's inflate: over-subscribed codes, incomplete literal/length
+// or distance codes (unless a single one-bit code), incomplete code-length
+// codes, HLIT > 286, HDIST > 30, a missing end-of-block code, literal/length
+// symbols 286/287, distance symbols 30/31, distances before the start of
+// the stream, stored-block LEN/NLEN mismatch, input that ends before the
+// final block and bytes after it (codec.py:125-127) are errors.
+#include "nmk_common.cuh"
+
+namespace nmk {
+
+constexpr int kInfWarps = 4;          // streams per CTA
+constexpr int kLutBits = 10;
+constexpr int kLut = 1 << kLutBits;
+
+enum InflateStatus : unsigned {
+  kInfOk = 0,
+  kInfBadBlockType = 1,
+  kInfBadStored = 2,
+  kInfBadHeader = 3,      // HLIT/HDIST out of range, bad repeat, no end-of-block code
+  kInfBadCode = 4,        // over-subscribed / incomplete code, undecodable symbol
+  kInfBadDistance = 5,    // distance symbol >= 30 or too far back
+  kInfTruncated = 6,      // the input ended before the final block
+  kInfTrailing = 7,       // bytes after the final block
+  kInfOverflow = 8,       // the stream inflates past its output capacity
+};
+
+struct Huff {
+  uint16_t lut[kLut];   // (len << 9) | sym for codes of <= kLutBits bits, 0 = slow path
+  uint16_t count[16];
+  uint16_t sym[288];
+};
+
+struct InfState {
+  Huff lit, dist;
+  uint8_t lens[320];
+  uint16_t offs[16];
+  int status;
+};
+
+// bit reader (identical in every lane)
+struct Bits {
+  const uint8_t* p;
+  uint64_t len, pos;      // input bytes, next byte to load
+  uint64_t buf;
+  int cnt;
+  __device__ __forceinline__ void refill() {
+    while (cnt <= 56) {
+      const uint64_t b = pos < len ? (uint64_t)__ldg(p + pos) : 0ULL;
+      ++pos;
+      buf |= b << cnt;
+      cnt += 8;
+    }
+  }
+  __device__ __forceinline__ uint32_t get(int n) {   // n <= 32
+    if (cnt < n) refill();
+    const uint32_t v = (uint32_t)(buf & ((1ULL << n) - 1ULL));
+    buf >>= n;
+    cnt -= n;
+    return v;
+  }
+  // bits consumed so far > input size: the stream ran past its end
+  __device__ __forceinline__ bool overrun() const { return pos * 8 - (uint64_t)cnt > len * 8; }
+};
+
+__device__ __forceinline__ uint32_t bitrev(uint32_t c, int n) { return __brev(c) >> (32 - n); }
+
+// Build a canonical Huffman decoder from n code lengths in st.lens[first..].
+// kind: 0 = code-length code (must be complete), 1 = literal/length or
+// distance (complete, or a single one-bit code).  Returns false on a bad set.
+__device__ bool huff_build(Huff& h, const uint8_t* lens, int n, int kind, InfState& st) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kLut; i += 32) h.lut[i] = 0;
+  __shared__ int s_ok[kInfWarps];
+  const int w = threadIdx.x >> 5;
+  if (lane == 0) {
+    for (int l = 0; l < 16; ++l) h.count[l] = 0;
+    for (int s = 0; s < n; ++s) h.count[lens[s]]++;
+    int left = 1, maxl = 0;
+    bool ok = true;
+    for (int l = 1; l < 16; ++l) {
+      left <<= 1;
+      left -= h.count[l];
+      if (left < 0) ok = false;   // over-subscribed
+      if (h.count[l]) maxl = l;
+    }
+    if (ok && left > 0 && (kind == 0 || maxl != 1)) ok = false;   // incomplete (zlib inflate_table)
+    if (h.count[0] == n) ok = kind != 0;                          // no codes: only allowed for distances
+    st.offs[1] = 0;
+    for (int l = 1; l < 15; ++l) st.offs[l + 1] = st.offs[l] + h.count[l];
+    for (int s = 0; s < n; ++s)
+      if (lens[s]) h.sym[st.offs[lens[s]]++] = (uint16_t)s;
+    s_ok[w] = ok;
+  }
+  __syncwarp();
+  // LUT: symbols in canonical order; code of the i-th symbol of length l is
+  // first[l] + (i - index[l]).  Each lane fills the entries of a share of them.
+  if (s_ok[w]) {
+    int code = 0, index = 0;
+    for (int l = 1; l <= kLutBits; ++l) {
+      const int c = h.count[l];
+      for (int i = lane; i < c; i += 32) {
+        const uint32_t r = bitrev((uint32_t)(code + i), l);
+        const uint16_t e = (uint16_t)((l << 9) | h.sym[index + i]);
+        for (uint32_t j = r; j < (uint32_t)kLut; j += 1u << l) h.lut[j] = e;
+      }
+      code = (code + c) << 1;
+      index += c;
+    }
+  }
+  __syncwarp();
+  return s_ok[w] != 0;
+}
+
+// one symbol; -1 when no code matches
+__device__ __forceinline__ int huff_decode(const Huff& h, Bits& br) {
+  if (br.cnt < 15) br.refill();
+  const uint16_t e = h.lut[br.buf & (kLut - 1)];
+  if (e) {
+    const int l = e >> 9;
+    br.buf >>= l;
+    br.cnt -= l;
+    return e & 511;
+  }
+  // canonical walk, one bit at a time (codes longer than kLutBits)
+  int code = 0, first = 0, index = 0;
+  for (int l = 1; l < 16; ++l) {
+    code |= (int)(br.buf & 1ULL);
+    br.buf >>= 1;
+    br.cnt -= 1;
+    const int c = h.count[l];
+    if (code - c < first) return h.sym[index + (code - first)];
+    index += c;
+    first = (first + c) << 1;
+    code <<= 1;
+  }
+  return -1;
+}
+
+__constant__ uint16_t c_lbase[29] = {3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 15, 17, 19, 23, 27, 31,
+                                     35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t c_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t c_dbase[30] = {1, 2, 3, 4, 5, 7, 9, 13, 17, 25, 33, 49, 65, 97, 129, 193,
+                                     257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+__constant__ uint8_t c_clorder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+__global__ void __launch_bounds__(32 * kInfWarps)
+k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict__ comp_off, uint64_t nstreams,
+          uint8_t* __restrict__ out, uint64_t out_stride, const unsigned long long* __restrict__ out_off,
+          unsigned* __restrict__ status, unsigned long long* __restrict__ produced) {
+  __shared__ InfState sst[kInfWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t s = (uint64_t)blockIdx.x * kInfWarps + w;
+  if (s >= nstreams) return;
+  InfState& st = sst[w];
+  Bits br;
+  br.p = comp + comp_off[s];
+  br.len = comp_off[s + 1] - comp_off[s];
+  br.pos = 0;
+  br.buf = 0;
+  br.cnt = 0;
+  uint8_t* dst = out + (out_off ? out_off[s] : s * out_stride);
+  const uint64_t cap = out_stride;
+  uint64_t pos = 0;
+  unsigned err = kInfOk;
+  bool final_seen = false;
+  while (!err && !final_seen) {
+    final_seen = br.get(1);
+    const uint32_t type = br.get(2);
+    if (type == 0) {   // stored: align to a byte, LEN, NLEN, raw bytes
+      const int drop = br.cnt & 7;
+      br.buf >>= drop;
+      br.cnt -= drop;
+      const uint32_t ln = br.get(16), nln = br.get(16);
+      if (ln != (~nln & 0xffffu)) { err = kInfBadStored; break; }
+      // the buffered whole bytes come first, then the input
+      const uint64_t in0 = br.pos - (uint64_t)(br.cnt >> 3);
+      if (in0 + ln > br.len) { err = kInfTruncated; break; }
+      if (pos + ln > cap) { err = kInfOverflow; break; }
+      for (uint32_t j = lane; j < ln; j += 32) dst[pos + j] = __ldg(br.p + in0 + j);
+      pos += ln;
+      br.pos = in0 + ln;
+      br.buf = 0;
+      br.cnt = 0;
+      __syncwarp();
+      continue;
+    }
+    if (type == 3) { err = kInfBadBlockType; break; }
+    if (type == 1) {   // fixed codes
+      for (int i = lane; i < 288; i += 32) st.lens[i] = i < 144 ? 8 : i < 256 ? 9 : i < 280 ? 7 : 8;
+      for (int i = lane; i < 30; i += 32) st.lens[288 + i] = 5;
+      __syncwarp();
+      huff_build(st.lit, st.lens, 288, 1, st);
+      huff_build(st.dist, st.lens + 288, 30, 1, st);
+    } else {           // dynamic
+      const int hlit = (int)br.get(5) + 257, hdist = (int)br.get(5) + 1, hclen = (int)br.get(4) + 4;
+      if (hlit > 286 || hdist > 30) { err = kInfBadHeader; break; }
+      uint8_t cl[19];
+      for (int i = 0; i < 19; ++i) cl[i] = 0;
+      for (int i = 0; i < hclen; ++i) cl[c_clorder[i]] = (uint8_t)br.get(3);
+      for (int i = lane; i < 19; i += 32) st.lens[i] = cl[i];
+      __syncwarp();
+      if (!huff_build(st.dist, st.lens, 19, 0, st)) { err = kInfBadCode; break; }   // dist table as scratch
+      uint8_t l8[320];
+      int i = 0;
+      while (i < hlit + hdist && !err) {
+        const int sym = huff_decode(st.dist, br);
+        if (sym < 0) { err = kInfBadCode; break; }
+        if (sym < 16) { l8[i++] = (uint8_t)sym; continue; }
+        int rep, val = 0;
+        if (sym == 16) {
+          if (i == 0) { err = kInfBadHeader; break; }
+          val = l8[i - 1];
+          rep = 3 + (int)br.get(2);
+        } else if (sym == 17) {
+          rep = 3 + (int)br.get(3);
+        } else {
+          rep = 11 + (int)br.get(7);
+        }
+        if (i + rep > hlit + hdist) { err = kInfBadHeader; break; }
+        while (rep--) l8[i++] = (uint8_t)val;
+      }
+      if (err) break;
+      if (l8[256] == 0) { err = kInfBadHeader; break; }
+      for (int j = lane; j < hlit + hdist; j += 32) st.lens[j] = l8[j];
+      __syncwarp();
+      if (!huff_build(st.lit, st.lens, hlit, 1, st)) { err = kInfBadCode; break; }
+      __syncwarp();
+      if (!huff_build(st.dist, st.lens + hlit, hdist, 1, st)) { err = kInfBadCode; break; }
+    }
+    // symbols
+    while (true) {
+      const int sym = huff_decode(st.lit, br);
+      if (sym < 0 || sym > 285) { err = kInfBadCode; break; }
+      if (sym < 256) {
+        if (pos >= cap) { err = kInfOverflow; break; }
+        if (lane == 0) dst[pos] = (uint8_t)sym;
+        ++pos;
+        continue;
+      }
+      if (sym == 256) break;
+      const int li = sym - 257;
+      const uint32_t len = c_lbase[li] + br.get(c_lext[li]);
+      const int ds = huff_decode(st.dist, br);
+      if (ds < 0 || ds > 29) { err = kInfBadDistance; break; }
+      const uint32_t dist = c_dbase[ds] + br.get(c_dext[ds]);
+      if (dist > pos) { err = kInfBadDistance; break; }
+      if (pos + len > cap) { err = kInfOverflow; break; }
+      __syncwarp();   // earlier bytes (other lanes' stores) are visible
+      const uint64_t src = pos - dist;
+      for (uint32_t j = lane; j < len; j += 32) dst[pos + j] = dst[src + (j < dist ? j : j % dist)];
+      __syncwarp();
+      pos += len;
+    }
+    if (!err && br.overrun()) err = kInfTruncated;
+  }
+  if (!err) {
+    // bytes consumed = ceil(bits / 8); anything after them is trailing data
+    const uint64_t used = (br.pos * 8 - (uint64_t)br.cnt + 7) / 8;
+    if (br.overrun()) err = kInfTruncated;
+    else if (used < br.len) err = kInfTrailing;
+  }
+  if (lane == 0) {
+    status[s] = err;
+    produced[s] = pos;
+  }
+}
+
+}  // namespace nmk
+
+using namespace nmk;
+
+extern "C" int nmk_inflate(const uint8_t* comp, const unsigned long long* comp_off, uint64_t nstreams, uint8_t* out,
+                           uint64_t out_stride, const unsigned long long* out_off, unsigned* status,
+                           unsigned long long* produced, void* stream) {
+  if (nstreams == 0) return NMK_OK;
+  if (!comp || !comp_off || !out || !status || !produced || out_stride == 0)
+    return set_error(NMK_ERR_ARG, "nmk_inflate: bad argument");
+  const uint64_t grid = (nstreams + kInfWarps - 1) / kInfWarps;
+  k_inflate<<<(unsigned)grid, 32 * kInfWarps, 0, (cudaStream_t)stream>>>(comp, comp_off, nstreams, out, out_stride,
+                                                                         out_off, status, produced);
+  return check_launch("k_inflate");
+}
