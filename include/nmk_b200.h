@@ -225,7 +225,8 @@ int nmk_deflate(const uint8_t* packed, uint64_t block_stride, uint64_t nblocks, 
 
 /* -- lossless stage, decode half (codec.decompress_block, codec.py:119-128)
  * Inflates nstreams raw RFC 1951 streams -- stream s is comp[comp_off[s] ..
- * comp_off[s+1]) (comp_off: device, nstreams + 1 entries) -- into
+ * comp_off[s+1]) (comp_off: device, nstreams + 1 entries; comp 8-byte aligned
+ * and readable 16 bytes past comp_off[nstreams]) -- into
  * out + out_off[s] (out_off: device, nullable = s * out_stride), capacity
  * out_stride bytes each, one warp per stream.  Any raw DEFLATE stream (zlib's or nmk_deflate's) is accepted.
  * status[s]: 0 ok, 1 bad block type, 2 stored LEN/NLEN mismatch, 3 bad

@@ -182,7 +182,7 @@ def gpu_inflate_blocks(blobs, out_stride: int, device=None, slots=None, nslots: 
         d_slot = torch.from_numpy(np.asarray(slots, dtype=np.int64) * out_stride).to(dev)
     off = np.zeros(nb + 1, dtype=np.int64)
     off[1:] = np.cumsum([len(b) for b in blobs])
-    comp = np.frombuffer(b"".join(blobs) or b"\0", dtype=np.uint8)
+    comp = np.frombuffer(b"".join(blobs) + bytes(16), dtype=np.uint8)   # k_inflate reads 8-byte words: pad
     d_comp = torch.from_numpy(comp.copy()).to(dev)
     d_off = torch.from_numpy(off).to(dev)
     status = torch.empty(nb, dtype=torch.int32, device=dev)

@@ -25,8 +25,10 @@
 
 namespace nmk {
 
-constexpr int kInfWarps = 4;          // streams per CTA
-constexpr int kLutBits = 10;
+constexpr int kInfWarps = 1;          // streams per CTA (one per SM for a block's worth of streams)
+constexpr uint32_t kWin = 32768;      // DEFLATE's window: the last 32 KB of output, in shared memory
+constexpr uint64_t kFlush = 1024;     // window -> global store granularity
+constexpr int kLutBits = 12;   // 8 KB tables: zlib's distance codes mostly fit
 constexpr int kLut = 1 << kLutBits;
 
 enum InflateStatus : unsigned {
@@ -47,7 +49,14 @@ struct Huff {
   uint16_t sym[288];
 };
 
+// Multi-literal table over the next kMBits bits: up to 4 literals whose
+// codes fit (lo = the bytes, hi = n | bits << 4), or one length / end-of-
+// block symbol (n = 0, lo = sym, bits = its length), or hi = 0: the slow path.
+constexpr int kMBits = 12;
+constexpr int kMLut = 1 << kMBits;
+
 struct InfState {
+  uint2 mlut[kMLut];
   Huff lit, dist;
   uint8_t lens[320];
   uint16_t offs[16];
@@ -60,13 +69,23 @@ struct Bits {
   uint64_t len, pos;      // input bytes, next byte to load
   uint64_t buf;
   int cnt;
+  // to >= 57 bits: the next 8 input bytes from two aligned 8-byte loads (the
+  // input buffer is padded by 16 bytes on both sides), bytes at or past the
+  // stream's end read as zero
   __device__ __forceinline__ void refill() {
-    while (cnt <= 56) {
-      const uint64_t b = pos < len ? (uint64_t)__ldg(p + pos) : 0ULL;
-      ++pos;
-      buf |= b << cnt;
-      cnt += 8;
-    }
+    const int nb = (63 - cnt) >> 3;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p) + pos;
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~(uintptr_t)7);
+    const int sh = (int)(a & 7) * 8;
+    const uint64_t lo = __ldg(w), hi = __ldg(w + 1);
+    uint64_t v = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+    const uint64_t left = pos < len ? len - pos : 0;
+    const int keep = (int)(left < (uint64_t)nb ? left : (uint64_t)nb);   // bytes of real input
+    v = keep >= 8 ? v : (v & ((1ULL << (8 * keep)) - 1ULL));
+    if (nb < 8) v &= (1ULL << (8 * nb)) - 1ULL;
+    buf |= v << cnt;
+    pos += nb;
+    cnt += 8 * nb;
   }
   __device__ __forceinline__ uint32_t get(int n) {   // n <= 32
     if (cnt < n) refill();
@@ -128,6 +147,30 @@ __device__ bool huff_build(Huff& h, const uint8_t* lens, int n, int kind, InfSta
   return s_ok[w] != 0;
 }
 
+// mlut from the literal/length code's single-symbol table (all lanes)
+__device__ void mlut_build(InfState& st) {
+  const int lane = threadIdx.x & 31;
+  for (int idx = lane; idx < kMLut; idx += 32) {
+    uint32_t lo = 0, n = 0, used = 0, hi = 0;
+    while (n < 4) {
+      const uint16_t e = st.lit.lut[(idx >> used) & (kLut - 1)];
+      const uint32_t l = e >> 9;
+      if (!e || used + l > (uint32_t)kMBits) break;
+      const uint32_t sym = e & 511;
+      if (sym >= 256) {
+        if (n == 0) hi = (l << 4), lo = sym;   // a lone length / end-of-block symbol
+        break;
+      }
+      lo |= sym << (8 * n);
+      ++n;
+      used += l;
+    }
+    if (n) hi = n | (used << 4);
+    st.mlut[idx] = make_uint2(lo, hi);
+  }
+  __syncwarp();
+}
+
 // one symbol; -1 when no code matches
 __device__ __forceinline__ int huff_decode(const Huff& h, Bits& br) {
   if (br.cnt < 15) br.refill();
@@ -159,13 +202,28 @@ __constant__ uint8_t c_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 
 __constant__ uint16_t c_dbase[30] = {1, 2, 3, 4, 5, 7, 9, 13, 17, 25, 33, 49, 65, 97, 129, 193,
                                      257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
 __constant__ uint8_t c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+// c_mod[d][0] = 32 mod d, c_mod[d][1 + l] = l mod d (d < 32): the match copy's
+// per-lane source offsets without integer division
+struct ModTable {
+  uint8_t v[32][33];
+  constexpr ModTable() : v() {
+    for (int d = 1; d < 32; ++d) {
+      v[d][0] = (uint8_t)(32 % d);
+      for (int l = 0; l < 32; ++l) v[d][1 + l] = (uint8_t)(l % d);
+    }
+  }
+};
+__constant__ ModTable c_modt = ModTable();
+#define c_mod c_modt.v
 __constant__ uint8_t c_clorder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
 __global__ void __launch_bounds__(32 * kInfWarps)
 k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict__ comp_off, uint64_t nstreams,
           uint8_t* __restrict__ out, uint64_t out_stride, const unsigned long long* __restrict__ out_off,
           unsigned* __restrict__ status, unsigned long long* __restrict__ produced) {
-  __shared__ InfState sst[kInfWarps];
+  extern __shared__ __align__(16) uint8_t inf_smem[];   // InfState[kInfWarps], then the windows
+  InfState* sst = reinterpret_cast<InfState*>(inf_smem);
+  uint8_t* swin = inf_smem + sizeof(InfState) * kInfWarps;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint64_t s = (uint64_t)blockIdx.x * kInfWarps + w;
   if (s >= nstreams) return;
@@ -177,6 +235,18 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
   br.buf = 0;
   br.cnt = 0;
   uint8_t* dst = out + (out_off ? out_off[s] : s * out_stride);
+  uint8_t* win = swin + (size_t)w * kWin;
+  // output leaves through the window: every kFlush bytes the warp stores the
+  // finished 128-byte pieces with coalesced 4-byte stores (dst and flushed
+  // stay 16-byte aligned)
+  uint64_t flushed = 0;
+  auto flush = [&](uint64_t upto) {
+    __syncwarp();
+    for (; flushed + 128 <= upto; flushed += 128) {
+      const uint32_t o = (uint32_t)(flushed + 4 * lane) & (kWin - 1);
+      *reinterpret_cast<uint32_t*>(dst + flushed + 4 * lane) = *reinterpret_cast<const uint32_t*>(win + o);
+    }
+  };
   const uint64_t cap = out_stride;
   uint64_t pos = 0;
   unsigned err = kInfOk;
@@ -194,7 +264,11 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
       const uint64_t in0 = br.pos - (uint64_t)(br.cnt >> 3);
       if (in0 + ln > br.len) { err = kInfTruncated; break; }
       if (pos + ln > cap) { err = kInfOverflow; break; }
-      for (uint32_t j = lane; j < ln; j += 32) dst[pos + j] = __ldg(br.p + in0 + j);
+      for (uint32_t j = 0; j < ln; j += 32) {   // through the window in 32-byte pieces
+        if (j + lane < ln) win[(uint32_t)(pos + j + lane) & (kWin - 1)] = __ldg(br.p + in0 + j + lane);
+        __syncwarp();
+        if (pos + j + 32 - flushed >= kFlush) flush(pos + min(j + 32, ln));
+      }
       pos += ln;
       br.pos = in0 + ln;
       br.buf = 0;
@@ -209,6 +283,7 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
       __syncwarp();
       huff_build(st.lit, st.lens, 288, 1, st);
       huff_build(st.dist, st.lens + 288, 30, 1, st);
+      mlut_build(st);
     } else {           // dynamic
       const int hlit = (int)br.get(5) + 257, hdist = (int)br.get(5) + 1, hclen = (int)br.get(4) + 4;
       if (hlit > 286 || hdist > 30) { err = kInfBadHeader; break; }
@@ -242,17 +317,40 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
       for (int j = lane; j < hlit + hdist; j += 32) st.lens[j] = l8[j];
       __syncwarp();
       if (!huff_build(st.lit, st.lens, hlit, 1, st)) { err = kInfBadCode; break; }
+      mlut_build(st);
       __syncwarp();
       if (!huff_build(st.dist, st.lens + hlit, hdist, 1, st)) { err = kInfBadCode; break; }
     }
-    // symbols
+    // symbols: up to four literals per table lookup
     while (true) {
-      const int sym = huff_decode(st.lit, br);
+      if (br.cnt < kMBits) br.refill();
+      const uint2 me = st.mlut[br.buf & (kMLut - 1)];
+      int sym;
+      const uint32_t nlit = me.y & 15u;
+      if (nlit) {
+        if (pos + nlit > cap) { err = kInfOverflow; break; }
+        const uint32_t used = me.y >> 4;
+        br.buf >>= used;
+        br.cnt -= (int)used;
+        if ((uint32_t)lane < nlit) win[(uint32_t)(pos + lane) & (kWin - 1)] = (uint8_t)(me.x >> (8 * lane));
+        pos += nlit;
+        if (pos - flushed >= kFlush) flush(pos);
+        continue;
+      }
+      if (me.y) {   // a lone length / end-of-block symbol
+        const uint32_t used = me.y >> 4;
+        br.buf >>= used;
+        br.cnt -= (int)used;
+        sym = (int)me.x;
+      } else {
+        sym = huff_decode(st.lit, br);
+      }
       if (sym < 0 || sym > 285) { err = kInfBadCode; break; }
       if (sym < 256) {
         if (pos >= cap) { err = kInfOverflow; break; }
-        if (lane == 0) dst[pos] = (uint8_t)sym;
+        if (lane == 0) win[pos & (kWin - 1)] = (uint8_t)sym;
         ++pos;
+        if (pos - flushed >= kFlush) flush(pos);
         continue;
       }
       if (sym == 256) break;
@@ -263,13 +361,28 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
       const uint32_t dist = c_dbase[ds] + br.get(c_dext[ds]);
       if (dist > pos) { err = kInfBadDistance; break; }
       if (pos + len > cap) { err = kInfOverflow; break; }
-      __syncwarp();   // earlier bytes (other lanes' stores) are visible
-      const uint64_t src = pos - dist;
-      for (uint32_t j = lane; j < len; j += 32) dst[pos + j] = dst[src + (j < dist ? j : j % dist)];
+      __syncwarp();   // earlier bytes (other lanes' window stores) are visible
+      // lane j copies bytes j, j + 32, ...: source offset t = j mod dist,
+      // advanced by 32 mod dist per round (sources all precede pos)
+      if ((uint32_t)lane < len) {
+        const uint32_t step = dist < 32 ? c_mod[dist][0] : 32u;   // 32 mod dist
+        uint32_t t = dist < 32 ? c_mod[dist][lane + 1] : (uint32_t)lane;   // lane mod dist
+        const uint32_t src = (uint32_t)(pos - dist);
+        for (uint32_t j = lane; j < len; j += 32) {
+          win[(uint32_t)(pos + j) & (kWin - 1)] = win[(src + t) & (kWin - 1)];
+          t += step;
+          if (t >= dist) t -= dist;
+        }
+      }
       __syncwarp();
       pos += len;
+      if (pos - flushed >= kFlush) flush(pos);
     }
     if (!err && br.overrun()) err = kInfTruncated;
+  }
+  if (!err) {   // the unflushed tail (< 128 bytes)
+    __syncwarp();
+    for (uint64_t j = flushed + lane; j < pos; j += 32) dst[j] = win[(uint32_t)j & (kWin - 1)];
   }
   if (!err) {
     // bytes consumed = ceil(bits / 8); anything after them is trailing data
@@ -294,7 +407,9 @@ extern "C" int nmk_inflate(const uint8_t* comp, const unsigned long long* comp_o
   if (!comp || !comp_off || !out || !status || !produced || out_stride == 0)
     return set_error(NMK_ERR_ARG, "nmk_inflate: bad argument");
   const uint64_t grid = (nstreams + kInfWarps - 1) / kInfWarps;
-  k_inflate<<<(unsigned)grid, 32 * kInfWarps, 0, (cudaStream_t)stream>>>(comp, comp_off, nstreams, out, out_stride,
+  constexpr size_t smem = (sizeof(InfState) + kWin) * kInfWarps;
+  ensure_dyn_smem(k_inflate, smem);
+  k_inflate<<<(unsigned)grid, 32 * kInfWarps, smem, (cudaStream_t)stream>>>(comp, comp_off, nstreams, out, out_stride,
                                                                          out_off, status, produced);
   return check_launch("k_inflate");
 }
