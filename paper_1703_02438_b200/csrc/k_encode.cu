@@ -38,6 +38,12 @@ NMK_ENC_EXTERN(20) NMK_ENC_EXTERN(21) NMK_ENC_EXTERN(22) NMK_ENC_EXTERN(23) NMK_
 NMK_ENC_EXTERN(26) NMK_ENC_EXTERN(27) NMK_ENC_EXTERN(28) NMK_ENC_EXTERN(29) NMK_ENC_EXTERN(30)
 #undef NMK_ENC_EXTERN
 
+#ifndef NMK_FIN_UNROLL
+#define NMK_FIN_UNROLL 0
+#endif
+#ifndef NMK_FIN_GATHER_BIG
+#define NMK_FIN_GATHER_BIG 4   // A/B (cfg5 B12 E1e-4, 30 values per chunk): 4 beats the per-thread loop (32)
+#endif
 // Finalize: chunk offsets -> compacted exact list + per-block prefix.
 // One thread per chunk for the bookkeeping.  The values come either from
 // the chunk's scratch window (k_encode: chunks with more than a few values
@@ -62,7 +68,9 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
     const uint32_t b = geo.fd_cpb.div(g);
     return (int64_t)((uint64_t)b * geo.epb + (uint64_t)(g - b * cpb) * kChunk) - (int64_t)geo.elem0;
   };
-  const unsigned big_at = gather ? 32u : 4u;
+  // chunks with more values than this go to the warp-cooperative copy (one
+  // chunk per warp iteration, every lane's loads issued together)
+  const unsigned big_at = gather ? (unsigned)NMK_FIN_GATHER_BIG : 4u;
   for (uint32_t c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); c0 < (uint32_t)geo.nchunks; c0 += nthr) {
     const uint32_t c = c0 + lane;
     const bool in = c < (uint32_t)geo.nchunks;
@@ -108,7 +116,17 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
         }
         const int64_t li = chunk_li(cb) + lane * kGroup;
         unsigned long long o = oo + (incl - cnt);
+#if NMK_FIN_UNROLL
+        T v[kGroup];
+#pragma unroll
+        for (int e = 0; e < kGroup; ++e)
+          if (m >> e & 1u) v[e] = cur[li + e];   // independent loads, all in flight
+#pragma unroll
+        for (int e = 0; e < kGroup; ++e)
+          if (m >> e & 1u) exact[o++] = v[e];
+#else
         for (unsigned mm = m; mm; mm &= mm - 1u) exact[o++] = cur[li + __ffs(mm) - 1];
+#endif
       } else {
         const uint64_t cs = (uint64_t)cb * kChunk;
         for (unsigned i = lane; i < nn; i += 32) exact[oo + i] = scratch[cs + i];
