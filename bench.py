@@ -52,11 +52,15 @@ METRIC = "compress+decompress GB/s of input (n*L per timestep / (t_compress + t_
 NOMINAL_HBM_GBS = 8000.0
 CFG4_STRONG_N = 4_000_000_000
 # kernels per compress + decompress step of the sync-free pipeline:
-# k_minmax, k_hist_prep, k_hist_dev, k_select, k_encode_keyed, k_encode (exits when
-# the keyed kernel did the work), k_chunk_scan, k_enc_finalize | k_dec_count(_wide),
-# k_chunk_scan, k_dec_chunks x 2 (six- and five-stage rings; the one whose
-# exact-value regime does not match exits at entry)
-GPU_LAUNCHES_PER_STEP = 12
+# k_minmax (the span decision and histogram clear fused in on one rank),
+# k_hist_dev, k_select, k_encode_keyed, k_chunk_scan, k_enc_finalize |
+# k_dec_count(_wide), k_chunk_scan, k_dec_chunks: 9.  More when a hint from the
+# warm-up check is missing: + k_hist_prep with a communicator, + k_encode (the
+# snapshot-reading fallback, exits when the keyed kernel did the work), + the
+# second k_dec_chunks ring depth (exits at entry).
+def gpu_launches_per_step(pipe):
+    return 9 + (pipe.comm is not None) + (not pipe.keyed_hint) + (pipe.ring_hint == 0)
+
 
 WORKLOADS = {
     "cfg2": dict(desc="cfg2: 512^3 fp64 8^3-block field, E=1e-3, B=8, top-k, 1 MiB index blocks",
@@ -516,6 +520,7 @@ def main():
             spans.append(pipe.check()["nbins"])
         pipe.fit_comm_bins(max(spans))
     graphs = []
+    launches_per_step = gpu_launches_per_step(pipe)   # the hints the captures below are made with
     try:
         for b, c in pairs:
             graphs.append(pipe.capture(b, c, out))
@@ -631,7 +636,7 @@ def main():
             "roofline_all": roof_all,
             "e2e": e2e,
             "series_e2e": series,
-            "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "cpu_baseline": cpu,
             "clocks": clk,
         }

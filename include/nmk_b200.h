@@ -297,6 +297,41 @@ int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint64_t first_
                    const uint64_t* h_seg_out, int nseg, nmk_segment_info* seg_info,
                    nmk_decode_err* err, void* ws, size_t ws_bytes, void* stream);
 
+/* Launch-count hints for a pipeline that repeats (one kernel fewer each in
+ * the captured step); like K2's hints they come from the previous step's
+ * host check and never change a result:
+ *  - nmk_minmax_prep: nmk_minmax + nmk_hist_prep in one launch, for a
+ *    single-rank pipeline (no exchange of the stats in between): every CTA
+ *    clears its share of counts up front and the last CTA decides the span.
+ *  - nmk_encode_keyed_dev2, keyed_hint = 1: the keyed kernel applied on the
+ *    previous step (mode word 1 at nmk_encode_ws_mode_offset in ws), so the
+ *    snapshot-reading fallback kernel is not launched; should the keyed mode
+ *    not apply after all, the keyed kernel finishes on its exact per-element
+ *    path (mode word 2: correct, slower -- drop the hint).
+ *  - nmk_decode_dev2, ring_hint = nmk_decode_ring_for(n_exact, n_elems) of
+ *    the previous step: only that TMA ring depth is launched (0: both, the
+ *    device picks). */
+int nmk_minmax_prep(const void* base, const void* cur, uint64_t n, int dtype, nmk_stats* stats,
+                    float* keys, double width, uint64_t cap_bins, unsigned long long* counts,
+                    void* ws, size_t ws_bytes, void* stream);
+int nmk_encode_keyed_dev2(const float* keys, const nmk_stats* stats, double width,
+                          const void* base, const void* cur, uint64_t n_local, uint64_t elem0,
+                          uint64_t n_total, int dtype, const double* centers, const double* cuts,
+                          const nmk_model* model, int k_cap, int bits, double tolerance, uint64_t epb,
+                          uint8_t* packed, uint64_t block_stride, void* exact,
+                          unsigned long long* prefix, unsigned long long* n_inc, void* recon,
+                          int keyed_hint, void* ws, size_t ws_bytes, void* stream);
+size_t nmk_encode_ws_mode_offset(uint64_t n_local, uint64_t elem0, uint64_t epb, int dtype);
+int nmk_decode_dev2(const uint8_t* packed, uint64_t block_stride, uint64_t first_block,
+                    int bits, uint64_t epb, uint64_t n_total,
+                    const unsigned long long* prefix_rel, const double* centers,
+                    const nmk_model* model, const void* exact,
+                    const unsigned long long* n_exact, const void* base, void* out, int dtype,
+                    const uint64_t* h_seg_start, const uint64_t* h_seg_count,
+                    const uint64_t* h_seg_out, int nseg, nmk_segment_info* seg_info,
+                    nmk_decode_err* err, int ring_hint, void* ws, size_t ws_bytes, void* stream);
+int nmk_decode_ring_for(uint64_t n_exact, uint64_t n_elems);
+
 /* -- standalone codec kernels (codec.py:83-105) ---------------------------- */
 int nmk_pack(const uint32_t* codes, uint64_t n, int bits, uint8_t* out, void* stream);
 int nmk_unpack(const uint8_t* packed, uint64_t n, int bits, uint32_t* codes, void* stream);

@@ -88,6 +88,13 @@ SIGNATURES = {
                                    u64, vp, vp, vp, vp, vp, sz, vp]),
     "nmk_decode_dev": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, i32,
                              u64p, u64p, u64p, i32, vp, vp, vp, sz, vp]),
+    "nmk_minmax_prep": (i32, [vp, vp, u64, i32, vp, vp, dbl, u64, vp, vp, sz, vp]),
+    "nmk_encode_keyed_dev2": (i32, [vp, vp, dbl, vp, vp, u64, u64, u64, i32, vp, vp, vp, i32, i32, dbl, u64, vp,
+                                    u64, vp, vp, vp, vp, i32, vp, sz, vp]),
+    "nmk_encode_ws_mode_offset": (sz, [u64, u64, u64, i32]),
+    "nmk_decode_dev2": (i32, [vp, u64, u64, i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, i32,
+                              u64p, u64p, u64p, i32, vp, vp, i32, vp, sz, vp]),
+    "nmk_decode_ring_for": (i32, [u64, u64]),
     "nmk_deflate_ws_bytes": (sz, [u64, u64, u32]),
     "nmk_deflate_bound": (u64, [u64, u64, u32]),
     "nmk_deflate": (i32, [vp, u64, u64, u64, u64, u32, vp, vp, vp, sz, vp]),

@@ -6,6 +6,7 @@
 // PipelineError(phase, ...), CodecError — pipeline.py:28-33, codec.py:24-25).
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -54,6 +55,14 @@ int sm_count() {
     sms[dev] = v > 0 ? v : 148;
   }
   return sms[dev];
+}
+
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = getenv("NMK_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 }  // namespace nmk

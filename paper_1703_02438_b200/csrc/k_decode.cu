@@ -76,6 +76,7 @@ struct DecodeGeom {
   uint32_t cpb_d;      // decode chunks (DC elements) per block: k_dec_chunks' work items
   FastDiv fd_cpb_d;
   int nseg, k;
+  ZeroList zl;   // scan tile status, segment info and error words: zeroed by the count pass
 };
 
 // One chunk: block b, in-block chunk ci, element/byte extents (32-bit).
@@ -259,6 +260,8 @@ template <int B>
 __global__ void __launch_bounds__(kDecThreads)
 k_dec_count(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  pdl_enter();
+  zero_list_run(geo.zl);
   const uint32_t nwarps = gridDim.x * (kDecThreads / 32);
   const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
   // (A/B on cfg3 / cfg5 B12: 2, 4 or 8 chunks per warp iteration no faster)
@@ -312,6 +315,8 @@ k_dec_count_wide(const uint8_t* __restrict__ packed, DecodeGeom geo, uint32_t* _
   static_assert(B == 8 || B == 16, "byte-aligned codes only");
   constexpr int kPer = (32 * B / 16) / 16;   // 16-byte vectors per lane per chunk (1 or 2)
   const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+  pdl_enter();
+  zero_list_run(geo.zl);
   const uint32_t g0 = (uint32_t)(geo.first_block * geo.cpb);
   const uint32_t nch = (uint32_t)geo.nchunks;
   const uint32_t nwarps = gridDim.x * (kDecThreads / 32);
@@ -538,6 +543,7 @@ k_dec_chunks(const uint8_t* __restrict__ packed, DecodeGeom geo, const Seg* __re
   constexpr bool kOpcSmem = ((1 << B) - 1) <= kOpcMax;
   double* s_opc = reinterpret_cast<double*>(dsm + DecStage<T, B, S>::kSmem);   // [2^B - 1] when kOpcSmem
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  pdl_enter();
   if (model) {                       // sync-free path: scalars from the device
     if (model->status != 0) return;
     geo.k = model->k;
@@ -875,9 +881,8 @@ static void launch_dec_chunks(const uint8_t* packed, const DecodeGeom& geo, cons
   uint64_t grid = (uint64_t)sms * per_sm;
   const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;   // nitems: decode chunks
   if (grid > need) grid = need;
-  k_dec_chunks<T, B, S><<<(unsigned)grid, kTmaThreads, smem, s>>>(packed, geo, segs, sp, offsets, prefix_rel, centers,
-                                                                   (const T*)exact, (const T*)base, (T*)out, info,
-                                                                   err, model, n_exact_dev, regime);
+  launch_chain(k_dec_chunks<T, B, S>, (unsigned)grid, kTmaThreads, smem, s, packed, geo, segs, sp, offsets, prefix_rel,
+               centers, (const T*)exact, (const T*)base, (T*)out, info, err, model, n_exact_dev, regime);
 }
 
 template <typename T, int B>
@@ -885,26 +890,30 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
                           uint32_t* counts, unsigned long long* offsets, void* scan_ws,
                           const unsigned long long* prefix_rel, const double* centers, const void* exact,
                           const void* base, void* out, nmk_segment_info* info, nmk_decode_err* err,
-                          const nmk_model* model, const unsigned long long* n_exact_dev, cudaStream_t s) {
+                          const nmk_model* model, const unsigned long long* n_exact_dev, int ring_hint,
+                          cudaStream_t s) {
   const int sms = sm_count_d();
   if constexpr (B == 8 || B == 16) {
     const uint64_t per_cta = (uint64_t)(kDecThreads / 32) * 2 * kDecPairs;
     const uint64_t g1 = (geo.nchunks + per_cta - 1) / per_cta;
     const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * NMK_CNT_CTAS ? g1 : (uint64_t)sms * NMK_CNT_CTAS);
-    k_dec_count_wide<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
+    launch_chain(k_dec_count_wide<B>, grid1, kDecThreads, 0, s, packed, geo, counts);
   } else {
     const uint64_t g1 = (geo.nchunks + 7) / 8;
     const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
-    k_dec_count<B><<<grid1, kDecThreads, 0, s>>>(packed, geo, counts);
+    launch_chain(k_dec_count<B>, grid1, kDecThreads, 0, s, packed, geo, counts);
   }
-  chunk_scan(counts, geo.nchunks, offsets, scan_ws, s);
+  chunk_scan(counts, geo.nchunks, offsets, scan_ws, s, true);
   // The host knows the exact count on the host-scalar path and picks one ring.
   // The sync-free path only knows it on the device: both rings launch and
   // the one whose regime does not match exits at entry.  (CUDA graph IF
   // nodes set by the count pass were measured slower than the empty launch:
   // cfg2 +25 us, cfg3 +19 us per step.)
-  if (!n_exact_dev) {
-    if (dec_dense(geo.n_exact, geo.nchunks))
+  // ring_hint (1 sparse, 2 dense: the regime the caller observed on the
+  // previous step) launches that ring alone; either ring decodes any stream,
+  // so the hint only affects speed.
+  if (!n_exact_dev || ring_hint == 1 || ring_hint == 2) {
+    if (n_exact_dev ? ring_hint == 2 : dec_dense(geo.n_exact, geo.nchunks))
       launch_dec_chunks<T, B, Rings<T>::kD>(packed, geo, segs, sp, offsets, prefix_rel, centers, exact, base, out,
                                             info, err, model, n_exact_dev, 0, s);
     else
@@ -923,11 +932,12 @@ static int dispatch_decode(int bits, const uint8_t* packed, const DecodeGeom& ge
                            const SegParams& sp, uint32_t* counts, unsigned long long* offsets, void* scan_ws,
                            const unsigned long long* prefix_rel, const double* centers, const void* exact,
                            const void* base, void* out, nmk_segment_info* info, nmk_decode_err* err,
-                           const nmk_model* model, const unsigned long long* n_exact_dev, cudaStream_t s) {
+                           const nmk_model* model, const unsigned long long* n_exact_dev, int ring_hint,
+                           cudaStream_t s) {
   switch (bits) {
 #define NMK_DEC_CASE(BB)                                                                                    \
   case BB: launch_decode<T, BB>(packed, geo, segs, sp, counts, offsets, scan_ws, prefix_rel, centers, exact, \
-                                base, out, info, err, model, n_exact_dev, s); break;
+                                base, out, info, err, model, n_exact_dev, ring_hint, s); break;
     NMK_DEC_CASE(2) NMK_DEC_CASE(3) NMK_DEC_CASE(4) NMK_DEC_CASE(5) NMK_DEC_CASE(6) NMK_DEC_CASE(7)
     NMK_DEC_CASE(8) NMK_DEC_CASE(9) NMK_DEC_CASE(10) NMK_DEC_CASE(11) NMK_DEC_CASE(12) NMK_DEC_CASE(13)
     NMK_DEC_CASE(14) NMK_DEC_CASE(15) NMK_DEC_CASE(16) NMK_DEC_CASE(17) NMK_DEC_CASE(18) NMK_DEC_CASE(19)
@@ -954,7 +964,8 @@ static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t fi
                        const nmk_model* model, const void* exact, uint64_t n_exact,
                        const unsigned long long* n_exact_dev, const void* base, void* out, int dtype,
                        const uint64_t* h_seg_start, const uint64_t* h_seg_count, const uint64_t* h_seg_out, int nseg,
-                       nmk_segment_info* seg_info, nmk_decode_err* err, void* ws, size_t ws_bytes, cudaStream_t s) {
+                       nmk_segment_info* seg_info, nmk_decode_err* err, void* ws, size_t ws_bytes, cudaStream_t s,
+                       int ring_hint = 0) {
   if (nseg < 1 || !h_seg_start || !h_seg_count || !h_seg_out || !seg_info || !err || !ws)
     return set_error(NMK_ERR_ARG, "nmk_decode: bad argument");
   if (bits < 2 || bits > 30 || epb == 0 || k < 1) return set_error(NMK_ERR_ARG, "nmk_decode: bad geometry");
@@ -988,8 +999,6 @@ static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t fi
   uint32_t* counts = (uint32_t*)(w + p.off_counts);
   unsigned long long* offsets = (unsigned long long*)(w + p.off_offsets);
   Seg* dsegs = (Seg*)(w + p.off_segs);
-  cudaMemsetAsync(seg_info, 0, sizeof(nmk_segment_info) * (size_t)nseg, s);
-  cudaMemsetAsync(err, 0, sizeof(nmk_decode_err), s);
   // a pageable H2D cudaMemcpyAsync returns after staging the source, so the
   // host table can be released immediately (no stream synchronisation)
   SegParams sp{};
@@ -1015,11 +1024,18 @@ static int decode_impl(const uint8_t* packed, uint64_t block_stride, uint64_t fi
   geo.fd_cpb_d.init((uint32_t)p.cpb_d);
   geo.nseg = nseg;
   geo.k = k;
+  // zeroed by the count pass (block 0) for the kernels behind it on the stream
+  geo.zl.p[0] = (unsigned long long*)(w + p.off_scan);
+  geo.zl.n[0] = chunk_scan_tiles(p.nchunks);
+  geo.zl.p[1] = (unsigned long long*)seg_info;
+  geo.zl.n[1] = (uint32_t)nseg * (uint32_t)(sizeof(nmk_segment_info) / 8);
+  geo.zl.p[2] = (unsigned long long*)err;
+  geo.zl.n[2] = (uint32_t)(sizeof(nmk_decode_err) / 8);
   if (dtype == NMK_F64)
     return dispatch_decode<double>(bits, packed, geo, dsegs, sp, counts, offsets, w + p.off_scan, prefix_rel,
-                                   centers, exact, base, out, seg_info, err, model, n_exact_dev, s);
+                                   centers, exact, base, out, seg_info, err, model, n_exact_dev, ring_hint, s);
   return dispatch_decode<float>(bits, packed, geo, dsegs, sp, counts, offsets, w + p.off_scan, prefix_rel, centers,
-                                exact, base, out, seg_info, err, model, n_exact_dev, s);
+                                exact, base, out, seg_info, err, model, n_exact_dev, ring_hint, s);
 }
 
 extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
@@ -1033,6 +1049,19 @@ extern "C" int nmk_decode(const uint8_t* packed, uint64_t block_stride, uint64_t
                      ws_bytes, (cudaStream_t)stream);
 }
 
+extern "C" int nmk_decode_dev2(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
+                               uint64_t epb, uint64_t n_total, const unsigned long long* prefix_rel,
+                               const double* centers, const nmk_model* model, const void* exact,
+                               const unsigned long long* n_exact, const void* base, void* out, int dtype,
+                               const uint64_t* h_seg_start, const uint64_t* h_seg_count, const uint64_t* h_seg_out,
+                               int nseg, nmk_segment_info* seg_info, nmk_decode_err* err, int ring_hint, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (!model || !n_exact) return set_error(NMK_ERR_ARG, "nmk_decode_dev: model and n_exact required");
+  return decode_impl(packed, block_stride, first_block, bits, epb, n_total, prefix_rel, centers, 1, model, exact, 0,
+                     n_exact, base, out, dtype, h_seg_start, h_seg_count, h_seg_out, nseg, seg_info, err, ws, ws_bytes,
+                     (cudaStream_t)stream, ring_hint);
+}
+
 extern "C" int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint64_t first_block, int bits,
                               uint64_t epb, uint64_t n_total, const unsigned long long* prefix_rel,
                               const double* centers, const nmk_model* model, const void* exact,
@@ -1040,8 +1069,13 @@ extern "C" int nmk_decode_dev(const uint8_t* packed, uint64_t block_stride, uint
                               const uint64_t* h_seg_start, const uint64_t* h_seg_count, const uint64_t* h_seg_out,
                               int nseg, nmk_segment_info* seg_info, nmk_decode_err* err, void* ws, size_t ws_bytes,
                               void* stream) {
-  if (!model || !n_exact) return set_error(NMK_ERR_ARG, "nmk_decode_dev: model and n_exact required");
-  return decode_impl(packed, block_stride, first_block, bits, epb, n_total, prefix_rel, centers, 1, model, exact, 0,
-                     n_exact, base, out, dtype, h_seg_start, h_seg_count, h_seg_out, nseg, seg_info, err, ws, ws_bytes,
-                     (cudaStream_t)stream);
+  return nmk_decode_dev2(packed, block_stride, first_block, bits, epb, n_total, prefix_rel, centers, model, exact,
+                         n_exact, base, out, dtype, h_seg_start, h_seg_count, h_seg_out, nseg, seg_info, err, 0, ws,
+                         ws_bytes, stream);
+}
+
+// the ring depth nmk_decode_dev2's hint should name for a span of n_elems
+// elements holding n_exact exact values (1 sparse, 2 dense)
+extern "C" int nmk_decode_ring_for(uint64_t n_exact, uint64_t n_elems) {
+  return dec_dense(n_exact, (n_elems + kDChunk - 1) / kDChunk) ? 2 : 1;
 }

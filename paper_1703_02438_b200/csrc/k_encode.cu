@@ -57,6 +57,7 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
                unsigned long long* __restrict__ n_inc, const T* __restrict__ cur,
                const uint32_t* __restrict__ keyed_done) {
   const int lane = threadIdx.x & 31;
+  pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_inc = offsets[geo.nchunks];
   const bool gather = keyed_done && *keyed_done;
   const uint8_t* masks = reinterpret_cast<const uint8_t*>(scratch);
@@ -295,7 +296,8 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
   EncodeChunks et = encode_chunks(n_local, elem0, epb);
   if (epb >= (1ULL << 31) || (n_total + kChunk - 1) / kChunk >= (1ULL << 32))
     return set_error(NMK_ERR_ARG, "nmk_encode: block or stream too large for 32-bit chunk indexing");
-  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride, FastDiv{}, 0, 0, false};
+  EncodeGeom geo{n_local, elem0, n_total, epb, et.cpb, et.g0, et.nchunks, et.b0, block_stride, FastDiv{}, 0, 0, false,
+                 ZeroList{}};
   geo.fd_cpb.init((uint32_t)et.cpb);
   {
     auto chunk_lo = [&](uint64_t c) {   // first element of local chunk c
@@ -311,6 +313,8 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
   }
   EncodeWs w = encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8);
   char* wb = (char*)ws;
+  geo.zl.p[0] = (unsigned long long*)(wb + w.off_scan);   // the scan's tile status: zeroed by the encode kernels
+  geo.zl.n[0] = chunk_scan_tiles(et.nchunks);
   EncodeKeys kxw = kx;
   kxw.done = (uint32_t*)(wb + w.off_total + 128);   // keyed-mode flag (k_encode_keyed -> k_encode, finalize)
   const bool keyed = kx.keys && model && k_cap <= kSmemCuts + 1;   // launch_encode_k's condition
@@ -327,15 +331,15 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
                : dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
                                         scratch, counts, model, k_cap, recon, kxw, s);
   if (rc) return rc;
-  chunk_scan(counts, et.nchunks, offsets, wb + w.off_scan, s);
+  chunk_scan(counts, et.nchunks, offsets, wb + w.off_scan, s, true);
   unsigned grid = (unsigned)((et.nchunks + 255) / 256);
   if (grid > (unsigned)sm_count_e() * 8) grid = sm_count_e() * 8;
   if (dtype == NMK_F64)
-    k_enc_finalize<double><<<grid, 256, 0, s>>>(geo, counts, offsets, (const double*)scratch, (double*)exact, prefix,
-                                                n_inc, (const double*)cur, keyed ? kxw.done : nullptr);
+    launch_chain(k_enc_finalize<double>, grid, 256, 0, s, geo, counts, offsets, (const double*)scratch, (double*)exact,
+                 prefix, n_inc, (const double*)cur, keyed ? kxw.done : nullptr);
   else
-    k_enc_finalize<float><<<grid, 256, 0, s>>>(geo, counts, offsets, (const float*)scratch, (float*)exact, prefix,
-                                               n_inc, (const float*)cur, keyed ? kxw.done : nullptr);
+    launch_chain(k_enc_finalize<float>, grid, 256, 0, s, geo, counts, offsets, (const float*)scratch, (float*)exact,
+                 prefix, n_inc, (const float*)cur, keyed ? kxw.done : nullptr);
   return check_launch("k_enc_finalize");
 }
 
@@ -345,7 +349,7 @@ extern "C" int nmk_encode(const void* base, const void* cur, uint64_t n_local, u
                           unsigned long long* prefix, unsigned long long* n_inc, void* recon, void* ws,
                           size_t ws_bytes, void* stream) {
   return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, k, nullptr, k, bits, tol_bin, tolerance,
-                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{nullptr, nullptr, 0.0, nullptr}, ws,
+                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{nullptr, nullptr, 0.0, nullptr, 0}, ws,
                      ws_bytes, (cudaStream_t)stream);
 }
 
@@ -356,8 +360,21 @@ extern "C" int nmk_encode_dev(const void* base, const void* cur, uint64_t n_loca
                               unsigned long long* n_inc, void* recon, void* ws, size_t ws_bytes, void* stream) {
   if (!model) return set_error(NMK_ERR_ARG, "nmk_encode_dev: model required");
   return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, 1, model, k_cap, bits, 0.0, tolerance,
-                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{nullptr, nullptr, 0.0, nullptr}, ws,
+                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{nullptr, nullptr, 0.0, nullptr, 0}, ws,
                      ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int nmk_encode_keyed_dev2(const float* keys, const nmk_stats* stats, double width, const void* base,
+                                     const void* cur, uint64_t n_local, uint64_t elem0, uint64_t n_total, int dtype,
+                                     const double* centers, const double* cuts, const nmk_model* model, int k_cap,
+                                     int bits, double tolerance, uint64_t epb, uint8_t* packed, uint64_t block_stride,
+                                     void* exact, unsigned long long* prefix, unsigned long long* n_inc, void* recon,
+                                     int keyed_hint, void* ws, size_t ws_bytes, void* stream) {
+  if (!model || !keys || !stats) return set_error(NMK_ERR_ARG, "nmk_encode_keyed_dev: model, keys and stats required");
+  if ((uintptr_t)keys & 15) return set_error(NMK_ERR_ARG, "nmk_encode_keyed_dev: keys must be 16-byte aligned");
+  return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, 1, model, k_cap, bits, 0.0, tolerance,
+                     epb, packed, block_stride, exact, prefix, n_inc, recon,
+                     EncodeKeys{keys, stats, width, nullptr, keyed_hint == 1 ? 1 : 0}, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int nmk_encode_keyed_dev(const float* keys, const nmk_stats* stats, double width, const void* base,
@@ -366,11 +383,14 @@ extern "C" int nmk_encode_keyed_dev(const float* keys, const nmk_stats* stats, d
                                     int bits, double tolerance, uint64_t epb, uint8_t* packed, uint64_t block_stride,
                                     void* exact, unsigned long long* prefix, unsigned long long* n_inc, void* recon,
                                     void* ws, size_t ws_bytes, void* stream) {
-  if (!model || !keys || !stats) return set_error(NMK_ERR_ARG, "nmk_encode_keyed_dev: model, keys and stats required");
-  if ((uintptr_t)keys & 15) return set_error(NMK_ERR_ARG, "nmk_encode_keyed_dev: keys must be 16-byte aligned");
-  return encode_impl(base, cur, n_local, elem0, n_total, dtype, centers, cuts, 1, model, k_cap, bits, 0.0, tolerance,
-                     epb, packed, block_stride, exact, prefix, n_inc, recon, EncodeKeys{keys, stats, width, nullptr}, ws,
-                     ws_bytes, (cudaStream_t)stream);
+  return nmk_encode_keyed_dev2(keys, stats, width, base, cur, n_local, elem0, n_total, dtype, centers, cuts, model, k_cap,
+                               bits, tolerance, epb, packed, block_stride, exact, prefix, n_inc, recon, 0, ws, ws_bytes,
+                               stream);
+}
+
+extern "C" size_t nmk_encode_ws_mode_offset(uint64_t n_local, uint64_t elem0, uint64_t epb, int dtype) {
+  EncodeChunks et = encode_chunks(n_local, elem0, epb);
+  return encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8).off_total + 128;
 }
 
 template <int B>

@@ -95,7 +95,8 @@ struct EncodeKeys {
   const float* keys;
   const nmk_stats* st;   // gmin, gmax, dense span (stats->reserved)
   double width;          // histogram width 2E
-  uint32_t* done;        // device flag: 1 when the keyed kernel did the work
+  uint32_t* done;        // device flag: 1 when the keyed kernel did the work (2: on its exact path only)
+  int only;              // no k_encode launch follows: the keyed kernel always does the work
 };
 
 struct EncodeGeom {
@@ -105,6 +106,7 @@ struct EncodeGeom {
   // key_al: every chunk start is a multiple of 4 elements from elem0
   uint32_t c_first, c_last;
   bool key_al;
+  ZeroList zl;   // the chunk scan's tile status, zeroed by the encode kernels
 };
 
 // Chunk c of this range: block, in-block chunk index and element spans.
@@ -472,6 +474,36 @@ __device__ __forceinline__ bool setup_keyed(const double* __restrict__ centers_g
   g.opc_s = opaque(smem_u32(opc));
   __syncthreads();
   return g.hi4 > 0.0f;
+}
+
+// The keyed mode does not apply but no k_encode launch follows (EncodeKeys::
+// only, a stale hint): a grid on which every key fails both key tests, so each
+// valid element takes the exact path from (b, x) -- bit-exact, only slower.
+template <bool T16>
+__device__ __forceinline__ void setup_keyed_exact_only(const double* __restrict__ centers_g, int k, uint32_t sentinel,
+                                                       uint32_t* tab, double* opc, KeyedGrid& g, double* s_kd) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) opc[i] = __dadd_rn(1.0, __ldg(centers_g + i));
+  if (threadIdx.x == 0) {
+    if constexpr (T16) reinterpret_cast<uint16_t*>(tab)[0] = (uint16_t)(sentinel | (1u << kIncBit<true>));
+    else tab[0] = sentinel | kIncFlag;
+    s_kd[0] = 0.0;
+    s_kd[1] = 0.0;
+    s_kd[2] = -1.0;   // classify_key64 never decides
+  }
+  g.kd_s = opaque(smem_u32(s_kd));
+  g.iw32 = 0.0f;
+  g.c32 = 0.0f;
+  g.ka = 0.0f;
+  g.iw2 = 0ULL;
+  g.c2 = 0ULL;
+  g.hi4 = -1.0f;      // classify_key / classify_key2 never decide
+  g.q0m1 = 0u;
+  g.rowbase = 0x4B400000u;
+  g.span2 = 1u;
+  g.tab_s = opaque(smem_u32(tab));
+  g.opc_s = opaque(smem_u32(opc));
+  __syncthreads();
 }
 
 // Branch-free: rows outside the table are clamped onto its last row (ordinal
@@ -1005,6 +1037,8 @@ k_encode(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom geo,
   __shared__ unsigned long long s_dmax;
   extern __shared__ __align__(16) double cutsp[];   // [-inf, cuts..., +inf, +inf] or centers
 
+  pdl_enter();
+  zero_list_run(geo.zl);
   if (done && *done) return;   // k_encode_keyed already encoded this range
   if (model) {   // sync-free path: the model scalars live on the device
     if (model->status != 0) {   // nothing to encode: leave empty chunks behind
@@ -1104,6 +1138,8 @@ k_encode_keyed(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom
   extern __shared__ __align__(128) double opc[];   // RN(1 + c_i) [k_cap + 2], then the key ring
   float* kring = reinterpret_cast<float*>(opc + keyed_ring_off(k_cap));
   const uint32_t sentinel = (1u << B) - 1u;
+  pdl_enter();
+  zero_list_run(geo.zl);
   if (model->status != 0) {   // nothing to encode: leave empty chunks behind
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (uint32_t)geo.nchunks; c += gridDim.x * blockDim.x)
       counts[c] = 0;
@@ -1116,8 +1152,10 @@ k_encode_keyed(const T* __restrict__ base, const T* __restrict__ cur, EncodeGeom
   const bool ok = k <= k_cap && k <= kSmemCuts + 1 &&
                   setup_keyed<T, (B <= NMK_T16_MAXB)>(centers_g, k, kx.st, kx.width, tol, tol_bin, sentinel, tab, opc, kg, &s_fail,
                                  &s_dmax, s_q, s_kd);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *kx.done = ok ? 1u : 0u;
-  if (!ok) return;
+  const bool exact_only = !ok && kx.only && k <= k_cap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *kx.done = ok ? 1u : (exact_only ? 2u : 0u);
+  if (exact_only) setup_keyed_exact_only<(B <= NMK_T16_MAXB)>(centers_g, k, sentinel, tab, opc, kg, s_kd);
+  else if (!ok) return;
   const int ncuts = k - 1;
   auto slow = [&](T b, T x) -> uint32_t {
     return classify_exact<T>(b, x, cuts_g, ncuts, centers_g, tol_bin, tol, sentinel);
@@ -1148,7 +1186,8 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
   uint64_t grid = (uint64_t)sm_count_e() * per_sm;
   uint64_t need = (geo.nchunks + 7) / 8;
   if (grid > need) grid = need;
-  if (kx.keys && model && smem_ok) {
+  const bool keyed = kx.keys && model && smem_ok;
+  if (keyed) {
     const size_t smem_k = keyed_smem_bytes(k_cap);
     ensure_dyn_smem(k_encode_keyed<T, B, kRecon>, smem_k);
     int per_sm_k = 0;
@@ -1156,13 +1195,13 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
     if (per_sm_k < 1) per_sm_k = 1;
     uint64_t grid_k = (uint64_t)sm_count_e() * per_sm_k;
     if (grid_k > need) grid_k = need;
-    k_encode_keyed<T, B, kRecon><<<(unsigned)grid_k, kEncThreads, smem_k, s>>>(
-        (const T*)base, (const T*)cur, geo, centers, cuts, tol, packed, (T*)scratch, counts, model, k_cap, (T*)recon,
-        kx);
+    launch_chain(k_encode_keyed<T, B, kRecon>, (unsigned)grid_k, kEncThreads, smem_k, s, (const T*)base, (const T*)cur,
+                 geo, centers, cuts, tol, packed, (T*)scratch, counts, model, k_cap, (T*)recon, kx);
   }
-  k_encode<T, B, kRecon><<<(unsigned)grid, kEncThreads, smem, s>>>(
-      (const T*)base, (const T*)cur, geo, centers, cuts, k, tol_bin, tol, packed, (T*)scratch, counts, model, smem_ok,
-      (T*)recon, (kx.keys && model && smem_ok) ? kx.done : nullptr);
+  if (keyed && kx.only) return;   // hint: the keyed kernel applied last time (it still finishes alone if not)
+  launch_chain(k_encode<T, B, kRecon>, (unsigned)grid, kEncThreads, smem, s, (const T*)base, (const T*)cur, geo, centers,
+               cuts, k, tol_bin, tol, packed, (T*)scratch, counts, model, smem_ok, (T*)recon,
+               keyed ? kx.done : nullptr);
 }
 
 // the fused reconstruction is a separate instantiation: the plain encode

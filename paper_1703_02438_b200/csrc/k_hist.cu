@@ -559,6 +559,7 @@ constexpr uint32_t kDevSmemBins = 12 * 1024;   // 48 KB of u32 counters per CTA
 __global__ void k_hist_prep(nmk_stats* __restrict__ st, double width, uint64_t cap_bins,
                             unsigned long long* __restrict__ counts) {
   __shared__ unsigned long long s_nb;
+  pdl_enter();
   if (threadIdx.x == 0) {
     unsigned long long nb = 0;
     if (st->nvalid) {
@@ -1097,6 +1098,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
   constexpr int kT = HistShape<kW>::kThreads;
   constexpr uint32_t kRW = HistShape<kW>::kRepWords;
   extern __shared__ uint32_t h[];
+  pdl_enter();
   const unsigned long long nb64 = st->reserved;
   if (nb64 == 0 || nb64 == NMK_SPAN_SPARSE) return;
   const uint32_t nbins = (uint32_t)nb64;
@@ -1227,7 +1229,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
 extern "C" int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins, unsigned long long* counts,
                              void* stream) {
   if (!stats || !counts || cap_bins == 0) return set_error(NMK_ERR_ARG, "nmk_hist_prep: bad argument");
-  k_hist_prep<<<sm_count_h() * 2, 256, 0, (cudaStream_t)stream>>>(stats, width, cap_bins, counts);
+  launch_chain(k_hist_prep, sm_count_h() * 2, 256, 0, (cudaStream_t)stream, stats, width, cap_bins, counts);
   return check_launch("k_hist_prep");
 }
 
@@ -1247,11 +1249,11 @@ static void launch_hist_dev(const void* base, const void* cur, const float* keys
   uint64_t grid = (uint64_t)sm_count_h() * per_sm;
   if (want < grid) grid = want ? want : 1;
   if (dtype == NMK_F64)
-    k_hist_dev<double, kW><<<(unsigned)grid, kT, smem, s>>>((const double*)base, (const double*)cur, keys, n, stats,
-                                                            width, counts, aligned);
+    launch_chain(k_hist_dev<double, kW>, (unsigned)grid, kT, smem, s, (const double*)base, (const double*)cur, keys, n,
+                 stats, width, counts, aligned);
   else
-    k_hist_dev<float, kW><<<(unsigned)grid, kT, smem, s>>>((const float*)base, (const float*)cur, keys, n, stats,
-                                                           width, counts, aligned);
+    launch_chain(k_hist_dev<float, kW>, (unsigned)grid, kT, smem, s, (const float*)base, (const float*)cur, keys, n,
+                 stats, width, counts, aligned);
 }
 
 extern "C" int nmk_hist_dense_dev2(const void* base, const void* cur, const float* keys, uint64_t n, int dtype,

@@ -132,13 +132,28 @@ __device__ __forceinline__ void vec_get(const float4& v, double* o) {
   o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 }
 
+// nmk_minmax_prep: K1 also does k_hist_prep's work (single-rank pipelines,
+// where the stats need no exchange before the span is decided)
+struct HistPrep {
+  unsigned long long* counts;   // null: plain nmk_minmax
+  double width;
+  uint64_t cap_bins, zero_words;
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kMinmaxThreads, NMK_MM_MINB)
 k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
          MinMax* __restrict__ partials, unsigned int* __restrict__ ticket,
-         nmk_stats* __restrict__ out, bool vec_ok, float* __restrict__ keys) {
+         nmk_stats* __restrict__ out, bool vec_ok, float* __restrict__ keys, HistPrep hp) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
+  pdl_enter();
+  // fused k_hist_prep, part 1: every CTA clears its share of the histogram's
+  // first zero_words slots (the span is not known yet; see the last CTA)
+  if (hp.counts)
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hp.zero_words;
+         i += (uint64_t)gridDim.x * blockDim.x)
+      hp.counts[i] = 0ULL;
   MinMax acc;
   acc.nv = 0;
   acc.lo = __longlong_as_double(0x7ff0000000000000LL);   // +inf
@@ -250,15 +265,29 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
   __syncthreads();
   if (lane == 0) warp_mm[wid] = m;
   __syncthreads();
+  __shared__ unsigned long long s_nb;
   if (threadIdx.x == 0) {
     MinMax f = warp_mm[0];
     for (int w = 1; w < kMinmaxThreads / 32; ++w) f = mm_merge(f, warp_mm[w]);
     out->gmin = f.lo;
     out->gmax = f.hi;
     out->nvalid = f.nv;
-    out->reserved = 0;
+    // fused k_hist_prep, part 2: the dense span (k_hist.cu, same f64 expression)
+    unsigned long long nb = 0;
+    if (hp.counts && f.nv) {
+      const double span = __ddiv_rn(__dsub_rn(f.hi, f.lo), hp.width);
+      nb = (finite64(span) && span < (double)hp.cap_bins) ? (unsigned long long)floor(span) + 1ULL : NMK_SPAN_SPARSE;
+    }
+    out->reserved = nb;
+    s_nb = nb;
     *ticket = 0;  // self-reset for the next launch
   }
+  if (!hp.counts) return;
+  __syncthreads();
+  // a span beyond the slots cleared up front (rare): the last CTA clears the rest
+  const unsigned long long nb = s_nb;
+  if (nb != NMK_SPAN_SPARSE)
+    for (uint64_t i = hp.zero_words + threadIdx.x; i <= nb; i += blockDim.x) hp.counts[i] = 0ULL;
 }
 
 template <typename T>
@@ -291,8 +320,8 @@ extern "C" size_t nmk_minmax_ws_bytes(uint64_t n) {
   return 256 + (size_t)g * sizeof(MinMax);
 }
 
-extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
-                          nmk_stats* stats, float* keys, void* ws, size_t ws_bytes, void* stream) {
+static int minmax_impl(const void* base, const void* cur, uint64_t n, int dtype, nmk_stats* stats, float* keys,
+                       void* ws, size_t ws_bytes, const HistPrep& hp, void* stream) {
   if (n == 0 || !base || !cur || !stats || !ws) return set_error(NMK_ERR_ARG, "nmk_minmax: bad argument");
   if (ws_bytes < nmk_minmax_ws_bytes(n)) return set_error(NMK_ERR_ARG, "nmk_minmax: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
@@ -303,14 +332,30 @@ extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dty
   // once and the kernel's last CTA resets it after every launch.
   bool aligned = (((uintptr_t)base | (uintptr_t)cur | (uintptr_t)keys) & 15) == 0;
   if (dtype == NMK_F64)
-    k_minmax<double><<<grid, kMinmaxThreads, 0, s>>>((const double*)base, (const double*)cur, n,
-                                                     partials, ticket, stats, aligned, keys);
+    launch_chain(k_minmax<double>, grid, kMinmaxThreads, 0, s, (const double*)base, (const double*)cur, n, partials,
+                 ticket, stats, aligned, keys, hp);
   else if (dtype == NMK_F32)
-    k_minmax<float><<<grid, kMinmaxThreads, 0, s>>>((const float*)base, (const float*)cur, n,
-                                                    partials, ticket, stats, aligned, keys);
+    launch_chain(k_minmax<float>, grid, kMinmaxThreads, 0, s, (const float*)base, (const float*)cur, n, partials,
+                 ticket, stats, aligned, keys, hp);
   else
     return set_error(NMK_ERR_ARG, "nmk_minmax: bad dtype %d", dtype);
   return check_launch("k_minmax");
+}
+
+extern "C" int nmk_minmax(const void* base, const void* cur, uint64_t n, int dtype,
+                          nmk_stats* stats, float* keys, void* ws, size_t ws_bytes, void* stream) {
+  return minmax_impl(base, cur, n, dtype, stats, keys, ws, ws_bytes, HistPrep{nullptr, 0.0, 0, 0}, stream);
+}
+
+extern "C" int nmk_minmax_prep(const void* base, const void* cur, uint64_t n, int dtype, nmk_stats* stats,
+                               float* keys, double width, uint64_t cap_bins, unsigned long long* counts,
+                               void* ws, size_t ws_bytes, void* stream) {
+  if (!counts || cap_bins == 0 || !(width > 0.0)) return set_error(NMK_ERR_ARG, "nmk_minmax_prep: bad argument");
+  // slots cleared by all CTAs before the span is known; a wider span's rest
+  // is cleared by the last CTA
+  const uint64_t zero_words = cap_bins + 1 < 65537 ? cap_bins + 1 : 65537;
+  return minmax_impl(base, cur, n, dtype, stats, keys, ws, ws_bytes, HistPrep{counts, width, cap_bins, zero_words},
+                     stream);
 }
 
 extern "C" int nmk_ratio(const void* base, const void* cur, uint64_t n, int dtype,

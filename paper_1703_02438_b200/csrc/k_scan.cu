@@ -8,8 +8,9 @@
 // 4 bytes read and 8 written per 256 elements.  Tiles of 8192 items go to
 // CTAs in blockIdx order; each CTA publishes its tile aggregate, then looks
 // back over its predecessors' (flag, value) words until it meets an
-// inclusive prefix.  The tile-status words are zeroed by a memset node in
-// front of the kernel, so no state survives between launches.
+// inclusive prefix.  The tile-status words are zeroed in front of the kernel
+// (by the counting kernel that precedes it on the stream, or a memset node),
+// so no state survives between launches.
 #include "nmk_common.cuh"
 #include "nmk_scan.cuh"
 
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(kScanThreads)
 k_chunk_scan(const uint32_t* __restrict__ counts, uint64_t n, unsigned long long* __restrict__ offsets,
              unsigned long long* __restrict__ status) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  pdl_enter();
   const uint64_t tile = blockIdx.x;
   const uint64_t w0 = tile * kScanTile + (uint64_t)wid * kScanWarpItems;
   const bool vec = ((reinterpret_cast<uintptr_t>(counts) & 15) == 0);
@@ -136,11 +138,14 @@ k_chunk_scan(const uint32_t* __restrict__ counts, uint64_t n, unsigned long long
 
 size_t chunk_scan_ws_bytes(uint64_t n) { return ((n + 1 + kScanTile - 1) / kScanTile) * 8 + 256; }
 
-void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets, void* ws, cudaStream_t s) {
-  const uint64_t ntiles = (n + 1 + kScanTile - 1) / kScanTile;
+uint32_t chunk_scan_tiles(uint64_t n) { return (uint32_t)((n + 1 + kScanTile - 1) / kScanTile); }
+
+void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets, void* ws, cudaStream_t s,
+                bool status_zeroed) {
+  const uint64_t ntiles = chunk_scan_tiles(n);
   unsigned long long* status = reinterpret_cast<unsigned long long*>(ws);
-  cudaMemsetAsync(status, 0, ntiles * 8, s);
-  k_chunk_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(counts, n, offsets, status);
+  if (!status_zeroed) cudaMemsetAsync(status, 0, ntiles * 8, s);
+  launch_chain(k_chunk_scan, (unsigned)ntiles, kScanThreads, 0, s, counts, n, offsets, status);
 }
 
 }  // namespace nmk

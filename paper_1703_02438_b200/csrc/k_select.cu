@@ -101,6 +101,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
   extern __shared__ unsigned long long s_cache[];
 
   const int tid = threadIdx.x;
+  pdl_enter();
   const uint64_t nvalid = st->nvalid;
   if (nvalid == 0 && cov_out) {   // coverage of an empty histogram
     if (tid < auto_n) cov_out[tid] = 0;
@@ -372,13 +373,11 @@ extern "C" int nmk_select(const unsigned long long* keys, const unsigned long lo
   ensure_dyn_smem(k_select<double, kNSel>, kSelCache * 8);
   ensure_dyn_smem(k_select<float, kNSel>, kSelCache * 8);
   if (dtype == NMK_F64)
-    k_select<double, kNSel><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits,
-                                                         n_total, centers, cuts, (double*)centers_t, cap_k, model,
-                                                         kAutoLo, kNSel, nullptr);
+    launch_chain(k_select<double, kNSel>, 1, kSelThreads, smem, s, keys, counts, m_max, nruns, stats, width, tolerance,
+                 bits, n_total, centers, cuts, (double*)centers_t, cap_k, model, kAutoLo, kNSel, nullptr);
   else if (dtype == NMK_F32)
-    k_select<float, kNSel><<<1, kSelThreads, smem, s>>>(keys, counts, m_max, nruns, stats, width, tolerance, bits,
-                                                        n_total, centers, cuts, (float*)centers_t, cap_k, model,
-                                                        kAutoLo, kNSel, nullptr);
+    launch_chain(k_select<float, kNSel>, 1, kSelThreads, smem, s, keys, counts, m_max, nruns, stats, width, tolerance,
+                 bits, n_total, centers, cuts, (float*)centers_t, cap_k, model, kAutoLo, kNSel, nullptr);
   else
     return set_error(NMK_ERR_ARG, "nmk_select: bad dtype");
   return check_launch("k_select");

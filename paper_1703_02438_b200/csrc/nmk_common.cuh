@@ -291,6 +291,19 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- programmatic dependent launch (sm_90+) -------------------------------
+// The sync-free step is a fixed chain of kernels on one stream.  Launched with
+// the programmatic-stream-serialization attribute (launch_chain below), a
+// kernel's CTAs may become resident while the previous kernel drains; every
+// chained kernel therefore runs pdl_enter() before its first global access:
+// griddepcontrol.wait returns when the previous grid has completed and its
+// writes are visible, then launch_dependents lets the next kernel in.  Both
+// are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- division by a run-time invariant (Granlund-Montgomery) ---------------
 // q = n / d for any 32-bit n with one mul-hi, an add and two shifts.
 struct FastDiv {
@@ -324,4 +337,22 @@ template <typename F>
 inline void ensure_dyn_smem(F* func, size_t bytes) { ensure_dyn_smem(reinterpret_cast<const void*>(func), bytes); }
 // multiprocessor count of the current device (cached per device)
 int sm_count();
+// programmatic dependent launch of the chained kernels (env NMK_PDL=0 turns it off)
+bool pdl_on();
+// <<<grid, block, smem, s>>> with the programmatic-stream-serialization
+// attribute; the kernel must call pdl_enter() before touching global memory
+template <typename... KA, typename... A>
+inline void launch_chain(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, KA(args)...);
+}
 }  // namespace nmk

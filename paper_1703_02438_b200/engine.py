@@ -436,6 +436,10 @@ class DevicePipeline:
         # counts never depend on it
         self.span_hint = 0
         self.spread_hint = 0
+        # launch-count hints, also from check(): the keyed K4 applied (its
+        # fallback kernel is not launched) and the K5 ring depth that matched
+        self.keyed_hint = 0
+        self.ring_hint = 0
         # dense span capacity; with a comm it is also the all-reduced histogram
         # length (fit_comm_bins sizes it to the observed span)
         self.cap_bins = (comm_bins or ASYNC_COMM_BINS) if comm is not None else DENSE_MAX_BINS
@@ -460,7 +464,8 @@ class DevicePipeline:
         self.mm_bytes = lib.nmk_minmax_ws_bytes(self.n_local)
         self.mm_ws = torch.zeros(self.mm_bytes, dtype=torch.uint8, device=dev)
         self.e_bytes = lib.nmk_encode_ws_bytes(self.n_local, self.elem0, self.epb, self.dt)
-        self.e_ws = torch.empty(self.e_bytes, dtype=torch.uint8, device=dev)
+        self.e_ws = torch.zeros(self.e_bytes, dtype=torch.uint8, device=dev)
+        self.mode_off = lib.nmk_encode_ws_mode_offset(self.n_local, self.elem0, self.epb, self.dt)
         seg = (ctypes.c_uint64 * 1)
         self.s_start, self.s_count, self.s_out = seg(self.elem0), seg(self.n_local), seg(0)
         self.d_bytes = lib.nmk_decode_ws_bytes(self.s_start, self.s_count, 1, self.epb, self.b0)
@@ -492,12 +497,18 @@ class DevicePipeline:
         lib, st = N.lib(), _stream()
         P = lambda t: t.data_ptr()  # noqa: E731
         mark = mark or (lambda name: None)
-        N.check(lib.nmk_minmax(P(base), P(cur), self.n_local, self.dt, P(self.stats), P(self.keys), P(self.mm_ws),
-                               self.mm_bytes, st))
-        if self.comm is not None:
+        if self.comm is None:
+            # one rank: K1's last CTA decides the span and the histogram is
+            # cleared inside K1 (no nmk_hist_prep launch)
+            N.check(lib.nmk_minmax_prep(P(base), P(cur), self.n_local, self.dt, P(self.stats), P(self.keys),
+                                        self.width, self.cap_bins, P(self.counts), P(self.mm_ws), self.mm_bytes, st))
+            mark("K1_minmax")
+        else:
+            N.check(lib.nmk_minmax(P(base), P(cur), self.n_local, self.dt, P(self.stats), P(self.keys),
+                                   P(self.mm_ws), self.mm_bytes, st))
             self.comm.allreduce_stats_device(self.stats)
-        mark("K1_minmax")
-        N.check(lib.nmk_hist_prep(P(self.stats), self.width, self.cap_bins, P(self.counts), st))
+            mark("K1_minmax")
+            N.check(lib.nmk_hist_prep(P(self.stats), self.width, self.cap_bins, P(self.counts), st))
         N.check(lib.nmk_hist_dense_dev2(P(base), P(cur), P(self.keys), self.n_local, self.dt, P(self.stats),
                                         self.width, P(self.counts), self.span_hint, self.spread_hint, st))
         if self.comm is not None:
@@ -508,11 +519,12 @@ class DevicePipeline:
                                st))
         mark("K3_select")
         # K4 classifies from the keys (4 bytes per element instead of 2L)
-        N.check(lib.nmk_encode_keyed_dev(P(self.keys), P(self.stats), self.width, P(base), P(cur), self.n_local,
-                                         self.elem0, self.n, self.dt, P(self.centers), P(self.cuts), P(self.model),
-                                         self.k_cap, self.bits, self.tol, self.epb, P(self.packed), self.stride,
-                                         P(self.exact), P(self.prefix), P(self.n_inc),
-                                         P(recon) if recon is not None else None, P(self.e_ws), self.e_bytes, st))
+        N.check(lib.nmk_encode_keyed_dev2(P(self.keys), P(self.stats), self.width, P(base), P(cur), self.n_local,
+                                          self.elem0, self.n, self.dt, P(self.centers), P(self.cuts), P(self.model),
+                                          self.k_cap, self.bits, self.tol, self.epb, P(self.packed), self.stride,
+                                          P(self.exact), P(self.prefix), P(self.n_inc),
+                                          P(recon) if recon is not None else None, self.keyed_hint, P(self.e_ws),
+                                          self.e_bytes, st))
         mark("K4_encode")
         if self.comm is not None:
             # global positions of this rank's exact values / block prefixes;
@@ -522,10 +534,10 @@ class DevicePipeline:
     def decode(self, base, out):
         lib, st = N.lib(), _stream()
         P = lambda t: t.data_ptr()  # noqa: E731
-        N.check(lib.nmk_decode_dev(P(self.packed), self.stride, self.b0, self.bits, self.epb, self.n, P(self.prefix),
-                                   P(self.centers), P(self.model), P(self.exact), P(self.n_inc), P(base), P(out),
-                                   self.dt, self.s_start, self.s_count, self.s_out, 1, P(self.seg_info),
-                                   P(self.err), P(self.d_ws), self.d_bytes, st))
+        N.check(lib.nmk_decode_dev2(P(self.packed), self.stride, self.b0, self.bits, self.epb, self.n, P(self.prefix),
+                                    P(self.centers), P(self.model), P(self.exact), P(self.n_inc), P(base), P(out),
+                                    self.dt, self.s_start, self.s_count, self.s_out, 1, P(self.seg_info),
+                                    P(self.err), self.ring_hint, P(self.d_ws), self.d_bytes, st))
 
     def step(self, base, cur, out, mark=None):
         self.encode(base, cur, mark)
@@ -561,9 +573,17 @@ class DevicePipeline:
             # ratios (K3 leaves the two largest selectable counts in coverage[0..1])
             top2 = int(model.coverage[0]) + int(model.coverage[1])
             self.spread_hint = int(4 * top2 < 3 * int(sv.nvalid))
+        # K4's mode word: 1 = the keyed kernel applied (skip the fallback
+        # launch next time), 2 = it ran on its exact path only (stale hint), 0 =
+        # the snapshot-reading kernel did the work
+        k4_mode = int(self.e_ws[self.mode_off:self.mode_off + 4].view(_torch().int32).item())
+        self.keyed_hint = int(model.status == 0 and k4_mode == 1)
+        if model.status == 0:
+            self.ring_hint = int(N.lib().nmk_decode_ring_for(
+                n_inc, self.n_local + self.elem0 - self.b0 * self.epb))
         return {"status": int(model.status), "bits": int(model.bits), "k": int(model.k), "n_inc": n_inc,
                 "gmin": float(sv.gmin), "gmax": float(sv.gmax), "nvalid": int(sv.nvalid), "nbins": int(sv.reserved),
-                "tripwire": trip, "bad_index": bool(e.bad_index), "exhausted": bool(e.exhausted),
+                "tripwire": trip, "bad_index": bool(e.bad_index), "exhausted": bool(e.exhausted), "k4_mode": k4_mode,
                 "n_sentinel": int(self.seg_info[1].item())}
 
     def encoding(self) -> DeviceEncoding:

@@ -165,3 +165,80 @@ def test_pipeline_small_and_ragged(n, dtype):
     assert _host_blocks(enc) == o["blocks"]
     assert enc.exact.cpu().numpy().tobytes() == o["exact"].tobytes()
     assert out.cpu().numpy().tobytes() == O.decode(o, b).tobytes()
+
+
+def _pipeline_bytes(pipe, base, cur):
+    out = torch.empty_like(base)
+    pipe.step(base, cur, out)
+    chk = pipe.check()
+    assert chk["status"] == 0 and not chk["bad_index"] and not chk["exhausted"] and chk["tripwire"] == 0
+    enc = pipe.encoding()
+    return (chk, _host_blocks(enc), enc.exact.cpu().numpy().tobytes(), enc.prefix.cpu().numpy().tobytes(),
+            out.cpu().numpy().tobytes())
+
+
+@pytest.mark.parametrize("case", ["keyed", "keyed_f32", "not_keyed"])
+def test_pipeline_launch_hints_never_change_bytes(case):
+    """The launch-count hints (keyed K4 without its fallback launch, a single
+    K5 ring depth) are speed-only: every forced combination -- including a
+    keyed hint on a field where the keyed mode does not apply, which runs the
+    keyed kernel on its exact path -- gives the oracle's bytes."""
+    if case == "keyed":
+        b, c = workloads.cfg5_host(300_001, seed=8); E, bits, bb = 1e-3, 8, 1 << 15
+    elif case == "keyed_f32":
+        b, c = _special_mix(250_003, 36, np.float32, 0.05); E, bits, bb = 1e-3, 9, 1 << 14
+    else:   # top bins scattered over ~50 000 bins: wider than the keyed table
+        rng = np.random.default_rng(37)
+        b = rng.uniform(0.5, 2.0, 400_003)
+        c = b * (1.0 + rng.uniform(-1.0, 1.0, b.size))
+        E, bits, bb = 2e-5, 8, 1 << 15
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    o = O.encode(b, c, E, bits, bb)
+    want_out = O.decode(o, b).tobytes()
+    pipe = engine.DevicePipeline(base.numel(), base.dtype, E, bits, bb)
+    chk, blocks, exact, prefix, out = _pipeline_bytes(pipe, base, cur)     # no hints: every kernel launched
+    assert blocks == o["blocks"] and exact == o["exact"].tobytes() and out == want_out
+    assert chk["k4_mode"] == (0 if case == "not_keyed" else 1)
+    assert pipe.keyed_hint == (0 if case == "not_keyed" else 1) and pipe.ring_hint in (1, 2)
+    for keyed_hint in (0, 1):
+        for ring_hint in (0, 1, 2):
+            pipe.keyed_hint, pipe.ring_hint = keyed_hint, ring_hint
+            chk2, blocks2, exact2, prefix2, out2 = _pipeline_bytes(pipe, base, cur)
+            assert (blocks2, exact2, prefix2, out2) == (blocks, exact, prefix, out), (keyed_hint, ring_hint)
+            if case == "not_keyed":
+                assert chk2["k4_mode"] == (2 if keyed_hint else 0)   # 2: the keyed kernel's exact path
+                assert pipe.keyed_hint == 0                          # check() drops the stale hint
+    # hinted pipeline captured in a graph
+    g = pipe.capture(base, cur, torch.empty_like(base))
+    g.replay()
+    assert _host_blocks(pipe.encoding()) == o["blocks"]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_minmax_prep_clears_wide_histograms(dtype):
+    """nmk_minmax_prep = nmk_minmax + nmk_hist_prep in one launch: a span wider
+    than the slots every CTA clears up front (65 537) is finished by the last
+    CTA; stale counts from a previous, different step must not survive."""
+    rng = np.random.default_rng(41)
+    n = 600_001
+    b = rng.uniform(0.5, 2.0, n)
+    c = b * (1.0 + rng.uniform(-0.5, 0.5, n))
+    b, c = b.astype(dtype), c.astype(dtype)
+    E = 2e-6                                   # ~250 000 bins
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(n, base.dtype, E, 8, 1 << 15)
+    pipe.counts.fill_(7)                       # garbage the fused prep has to clear
+    out = torch.empty_like(base)
+    pipe.step(base, cur, out)
+    chk = pipe.check()
+    assert chk["status"] == 0 and chk["tripwire"] == 0 and chk["nbins"] > 65_537
+    r, v = O.ratios_of(b, c)
+    ordinals, counts = O.histogram(r[v], float(r[v].min()), 2 * E)
+    got = pipe.counts[: chk["nbins"]].cpu().numpy()
+    dense = np.zeros(chk["nbins"], dtype=np.int64)
+    dense[np.asarray(ordinals, dtype=np.int64)] = counts
+    assert np.array_equal(got, dense)
+    assert int(got.sum()) == chk["nvalid"]
+    o = O.encode(b, c, E, 8, 1 << 15)
+    assert _host_blocks(pipe.encoding()) == o["blocks"]
+    assert out.cpu().numpy().tobytes() == O.decode(o, b).tobytes()
