@@ -15,9 +15,9 @@
 // 32*B bytes start 16-byte aligned.  Warps run independently (no block-wide
 // barrier): a chunk writes its packed bytes, its incompressible count and
 // its incompressible values into its own 256-slot scratch window.  A short
-// finalize pass (k_scan.cu + k_enc_finalize) turns the counts into positions,
-// moves the (rare) values into the compacted list and fills the per-block
-// prefix table.
+// finalize pass (k_enc_finalize: tile scan with look-back + gather) turns the
+// counts into positions, moves the (rare) values into the compacted list and
+// fills the per-block prefix table.
 #include "k_encode.cuh"
 #include "nmk_scan.cuh"
 
@@ -44,25 +44,77 @@ NMK_ENC_EXTERN(26) NMK_ENC_EXTERN(27) NMK_ENC_EXTERN(28) NMK_ENC_EXTERN(29) NMK_
 #ifndef NMK_FIN_GATHER_BIG
 #define NMK_FIN_GATHER_BIG 4   // A/B (cfg5 B12 E1e-4, 30 values per chunk): 4 beats the per-thread loop (32)
 #endif
-// Finalize: chunk offsets -> compacted exact list + per-block prefix.
-// One thread per chunk for the bookkeeping.  The values come either from
-// the chunk's scratch window (k_encode: chunks with more than a few values
-// are copied by the whole warp, one chunk at a time) or, after
-// k_encode_keyed (*keyed_done), straight from `cur` at the positions of the
-// chunk's 256-bit mask (one byte per lane of the encoding warp).
+// Finalize: chunk counts -> compacted exact list + per-block prefix, in one
+// launch.  A CTA takes a tile of kFinTile consecutive chunks (lane = chunk,
+// kFinRounds rounds per warp), scans their counts (warp shuffles + one CTA
+// step), obtains the tile's exclusive prefix by decoupled look-back over the
+// tile-status words (nmk_scan.cuh; cleared by the encode kernel in front) and
+// then moves the values with the offsets still in registers -- no offsets
+// array, no separate scan launch.  The values come either from the chunk's
+// scratch window (k_encode: chunks with more than a few values are copied by
+// the whole warp, one chunk at a time) or, after k_encode_keyed
+// (*keyed_done), straight from `cur` at the positions of the chunk's 256-bit
+// mask (one byte per lane of the encoding warp).
+constexpr int kFinThreads = 256;
+#ifndef NMK_FIN_ROUNDS
+#define NMK_FIN_ROUNDS 2   // A/B on cfg2: 1 -> 1.121 ms step, 2 -> 1.115, 4 -> 1.123 (fewer, longer-lived threads)
+#endif
+constexpr int kFinRounds = NMK_FIN_ROUNDS;
+constexpr int kFinTile = kFinThreads * kFinRounds;   // chunks per CTA
+
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsigned long long* __restrict__ offsets,
+__global__ void __launch_bounds__(kFinThreads)
+k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, unsigned long long* __restrict__ status,
                const T* __restrict__ scratch, T* __restrict__ exact, unsigned long long* __restrict__ prefix,
                unsigned long long* __restrict__ n_inc, const T* __restrict__ cur,
                const uint32_t* __restrict__ keyed_done) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   pdl_enter();
-  if (blockIdx.x == 0 && threadIdx.x == 0) *n_inc = offsets[geo.nchunks];
+  const uint32_t nch = (uint32_t)geo.nchunks;
+  const uint32_t wc0 = blockIdx.x * (uint32_t)kFinTile + (uint32_t)wid * (32 * kFinRounds);   // the warp's first chunk
+  // ---- scan of the tile's counts -----------------------------------------
+  unsigned cnt[kFinRounds], ex[kFinRounds];
+#pragma unroll
+  for (int q = 0; q < kFinRounds; ++q) {
+    const uint32_t c = wc0 + q * 32 + lane;
+    cnt[q] = c < nch ? __ldcs(counts + c) : 0u;
+  }
+  unsigned wsum = 0;   // warp running total (uniform; a tile holds <= kFinTile * 256 values)
+#pragma unroll
+  for (int q = 0; q < kFinRounds; ++q) {
+    unsigned incl = cnt[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    ex[q] = wsum + incl - cnt[q];
+    wsum += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __shared__ unsigned s_warp[kFinThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  if (lane == 0) s_warp[wid] = wsum;
+  __syncthreads();
+  unsigned wbase = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kFinThreads / 32; ++w) {
+    const unsigned x = s_warp[w];
+    wbase += w < wid ? x : 0u;
+    agg += x;
+  }
+  if (wid == 0) {
+    const unsigned long long p = scan_lookback(status, blockIdx.x, agg, lane);
+    if (lane == 0) {
+      s_prefix = p;
+      if (blockIdx.x == gridDim.x - 1) *n_inc = p + agg;   // the last tile knows the total
+    }
+  }
+  __syncthreads();
+  const unsigned long long wstart = s_prefix + wbase;
+  // ---- the values ------------------------------------------------------------
   const bool gather = keyed_done && *keyed_done;
   const uint8_t* masks = reinterpret_cast<const uint8_t*>(scratch);
   const uint32_t cpb = (uint32_t)geo.cpb;
-  const uint32_t nthr = gridDim.x * blockDim.x;
   // local index of element 0 of lane l's group in chunk c: chunk_lo - elem0 + 8 l
   auto chunk_li = [&](uint32_t c) -> int64_t {
     const uint32_t g = (uint32_t)geo.g0 + c;
@@ -72,11 +124,14 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
   // chunks with more values than this go to the warp-cooperative copy (one
   // chunk per warp iteration, every lane's loads issued together)
   const unsigned big_at = gather ? (unsigned)NMK_FIN_GATHER_BIG : 4u;
-  for (uint32_t c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); c0 < (uint32_t)geo.nchunks; c0 += nthr) {
+#pragma unroll
+  for (int q = 0; q < kFinRounds; ++q) {
+    const uint32_t c0 = wc0 + q * 32;
+    if (c0 >= nch) break;   // warp-uniform
     const uint32_t c = c0 + lane;
-    const bool in = c < (uint32_t)geo.nchunks;
-    const unsigned n = in ? counts[c] : 0u;
-    const unsigned long long off = in ? offsets[c] : 0ULL;
+    const bool in = c < nch;
+    const unsigned n = cnt[q];
+    const unsigned long long off = wstart + ex[q];
     if (in) {
       const uint32_t g = (uint32_t)geo.g0 + c;
       const uint32_t b = geo.fd_cpb.div(g);
@@ -89,10 +144,10 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
           const int64_t li = chunk_li(c);
           unsigned long long o = off;
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            for (uint32_t m = mw[q]; m; m &= m - 1u) {   // bit 8 l + e of the mask = element 8 l + e
+          for (int w = 0; w < 8; ++w)
+            for (uint32_t m = mw[w]; m; m &= m - 1u) {   // bit 8 l + e of the mask = element 8 l + e
               const int bit = __ffs(m) - 1;
-              exact[o++] = cur[li + q * 32 + bit];
+              exact[o++] = cur[li + w * 32 + bit];
             }
         } else {
           for (unsigned i = 0; i < n; ++i) exact[off + i] = scratch[(uint64_t)c * kChunk + i];
@@ -108,15 +163,15 @@ k_enc_finalize(EncodeGeom geo, const uint32_t* __restrict__ counts, const unsign
       const uint32_t cb = c0 + src;
       if (gather) {   // lane l handles its byte of the mask: warp scan for the output slot
         const unsigned m = masks[(uint64_t)cb * 32 + lane];
-        const unsigned cnt = __popc(m);
-        unsigned incl = cnt;
+        const unsigned mc = __popc(m);
+        unsigned incl = mc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += v;
         }
         const int64_t li = chunk_li(cb) + lane * kGroup;
-        unsigned long long o = oo + (incl - cnt);
+        unsigned long long o = oo + (incl - mc);
 #if NMK_FIN_UNROLL
         T v[kGroup];
 #pragma unroll
@@ -219,18 +274,17 @@ static EncodeChunks encode_chunks(uint64_t n_local, uint64_t elem0, uint64_t epb
 
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// workspace: counts u32[nchunks] | offsets u64[nchunks] | total | scan ws | scratch T[nchunks*256]
+// workspace: counts u32[nchunks] | flags | finalize tile status | scratch T[nchunks*256]
 struct EncodeWs {
-  size_t off_counts, off_offsets, off_total, off_scan, off_scratch, total;
+  size_t off_counts, off_total, off_scan, off_scratch, total;
 };
 
 static EncodeWs encode_ws_layout(uint64_t nchunks, int elem_bytes) {
   EncodeWs w{};
   w.off_counts = 0;
-  w.off_offsets = al256(nchunks * 4);
-  w.off_total = w.off_offsets + al256(nchunks * 8 + 8);   // offsets[nchunks] = total
+  w.off_total = al256(nchunks * 4);   // 256 bytes of flags (the keyed-mode word at + 128)
   w.off_scan = w.off_total + 256;
-  w.off_scratch = w.off_scan + al256(chunk_scan_ws_bytes(nchunks));
+  w.off_scratch = w.off_scan + al256(((nchunks + kFinTile - 1) / kFinTile) * 8 + 256);   // finalize tile status
   w.total = w.off_scratch + al256(nchunks * kChunk * (size_t)elem_bytes);
   return w;
 }
@@ -314,12 +368,11 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
   EncodeWs w = encode_ws_layout(et.nchunks, dtype == NMK_F32 ? 4 : 8);
   char* wb = (char*)ws;
   geo.zl.p[0] = (unsigned long long*)(wb + w.off_scan);   // the scan's tile status: zeroed by the encode kernels
-  geo.zl.n[0] = chunk_scan_tiles(et.nchunks);
+  geo.zl.n[0] = (uint32_t)((et.nchunks + kFinTile - 1) / kFinTile);
   EncodeKeys kxw = kx;
   kxw.done = (uint32_t*)(wb + w.off_total + 128);   // keyed-mode flag (k_encode_keyed -> k_encode, finalize)
   const bool keyed = kx.keys && model && k_cap <= kSmemCuts + 1;   // launch_encode_k's condition
   uint32_t* counts = (uint32_t*)(wb + w.off_counts);
-  unsigned long long* offsets = (unsigned long long*)(wb + w.off_offsets);
   void* scratch = wb + w.off_scratch;
   // A range starting inside a block: zero the packed bytes of the chunks in
   // front of it so they decode as non-sentinel codes and OR-merge neutrally.
@@ -331,15 +384,14 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
                : dispatch_encode<float>(bits, base, cur, geo, centers, cuts, k, tol_bin, tolerance, packed,
                                         scratch, counts, model, k_cap, recon, kxw, s);
   if (rc) return rc;
-  chunk_scan(counts, et.nchunks, offsets, wb + w.off_scan, s, true);
-  unsigned grid = (unsigned)((et.nchunks + 255) / 256);
-  if (grid > (unsigned)sm_count_e() * 8) grid = sm_count_e() * 8;
+  unsigned long long* status = (unsigned long long*)(wb + w.off_scan);
+  const unsigned grid = (unsigned)((et.nchunks + kFinTile - 1) / kFinTile);
   if (dtype == NMK_F64)
-    launch_chain(k_enc_finalize<double>, grid, 256, 0, s, geo, counts, offsets, (const double*)scratch, (double*)exact,
-                 prefix, n_inc, (const double*)cur, keyed ? kxw.done : nullptr);
+    launch_chain(k_enc_finalize<double>, grid, kFinThreads, 0, s, geo, counts, status, (const double*)scratch,
+                 (double*)exact, prefix, n_inc, (const double*)cur, keyed ? kxw.done : nullptr);
   else
-    launch_chain(k_enc_finalize<float>, grid, 256, 0, s, geo, counts, offsets, (const float*)scratch, (float*)exact,
-                 prefix, n_inc, (const float*)cur, keyed ? kxw.done : nullptr);
+    launch_chain(k_enc_finalize<float>, grid, kFinThreads, 0, s, geo, counts, status, (const float*)scratch,
+                 (float*)exact, prefix, n_inc, (const float*)cur, keyed ? kxw.done : nullptr);
   return check_launch("k_enc_finalize");
 }
 

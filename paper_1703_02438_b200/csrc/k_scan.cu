@@ -23,19 +23,6 @@ constexpr int kScanThreads = 256;
 constexpr int kScanRounds = NMK_SCAN_ROUNDS;                      // uint4 per lane
 constexpr int kScanWarpItems = 32 * 4 * kScanRounds;              // 1024 contiguous counts per warp
 constexpr int kScanTile = (kScanThreads / 32) * kScanWarpItems;   // 8192 per CTA (few tiles: short look-back)
-constexpr unsigned long long kFlagAgg = 1ULL << 62;    // tile aggregate published
-constexpr unsigned long long kFlagPre = 2ULL << 62;    // inclusive prefix published
-constexpr unsigned long long kValMask = (1ULL << 62) - 1;
-
-__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 // Each warp owns 1024 contiguous items; in round q lane l holds items
 // w0 + 128 q + 4 l .. + 3 (coalesced 512-byte loads, 1 KB stores).
 __global__ void __launch_bounds__(kScanThreads)
@@ -86,32 +73,8 @@ k_chunk_scan(const uint32_t* __restrict__ counts, uint64_t n, unsigned long long
     wbase += w < wid ? x : 0ULL;
     agg += x;
   }
-  // look-back (warp 0): lane j inspects tile - 1 - j - 32 r
-  if (wid == 0) {
-    unsigned long long prefix = 0;
-    if (tile == 0) {
-      if (lane == 0) st_status(status, kFlagPre | agg);
-    } else {
-      if (lane == 0) st_status(status + tile, kFlagAgg | agg);
-      int64_t base = (int64_t)tile - 1;
-      while (true) {
-        const int64_t t = base - lane;
-        unsigned long long s = t >= 0 ? ld_status(status + t) : kFlagPre;   // before tile 0: prefix 0
-        // wait until every inspected predecessor has published something
-        while (__any_sync(0xffffffffu, s == 0)) {
-          if (s == 0) s = ld_status(status + t);
-        }
-        const unsigned pre = __ballot_sync(0xffffffffu, (s & kFlagPre) != 0);
-        const int stop = pre ? __ffs(pre) - 1 : 32;   // first (nearest) inclusive prefix
-        unsigned long long part = (lane <= stop && t >= 0) ? (s & kValMask) : 0ULL;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        prefix += part;
-        if (pre) break;
-        base -= 32;
-      }
-      if (lane == 0) st_status(status + tile, kFlagPre | (prefix + agg));
-    }
+  if (wid == 0) {   // look-back (nmk_scan.cuh)
+    const unsigned long long prefix = scan_lookback(status, tile, agg, lane);
     if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
