@@ -2,60 +2,57 @@
 // (codec.compress_block, pkg/src/nmk/codec.py:108-116).
 //
 // Each index block (pipeline.py:290-304: one raw RFC 1951 stream per block)
-// is cut into segments of seg_bytes.  One thread compresses one segment:
-// LZ77 over the segment (3-byte hash, 4-way buckets, run candidate, one-step
-// lazy evaluation, window = the segment), a counting pass builds the
-// segment's own length-limited Huffman codes, and the emitting pass writes a
-// dynamic-Huffman block (BTYPE = 10) -- or the fixed code (BTYPE = 01) when
-// that is not larger.  The segment's block is then closed with the end-of-block
-// symbol followed by an empty stored block (BTYPE = 00, LEN = 0), which
-// byte-aligns the bit stream -- so the segments of a block concatenate into
-// one valid raw DEFLATE stream by a plain byte copy (the last segment's
-// stored block carries BFINAL).  Any inflater (zlib included) reproduces the
-// packed bytes exactly; the compressed bytes differ from zlib's, which the
-// reference does not pin, so this stage is opt-in.
+// is cut into segments of seg_bytes.  One WARP compresses one segment:
+//  * LZ77, 32 positions per step: every lane hashes the 3 bytes at its
+//    position, reads the candidate the table held before this step, and the
+//    lanes insert their positions (highest lane per hash value wins, so both
+//    passes see the same table).  A lane extends three candidates -- the
+//    previous byte (runs), the last distance used (periodic B-bit codes) and
+//    the hash candidate -- 4 bytes per compare.  The greedy parse over the
+//    step's 32 results is done with ballots: literals up to the next lane
+//    holding a match leave together, the match jumps the cursor.
+//  * pass 1 counts symbols (shared-memory atomics); the segment's own
+//    length-limited Huffman codes are built by a warp-parallel rank sort and
+//    a two-queue merge; pass 2 repeats the parse and emits: every lane turns
+//    its token into <= 48 bits, a warp scan gives the bit offsets, the bits
+//    are OR-ed into a shared-memory ring whose complete words are flushed
+//    coalesced.  The fixed code (BTYPE = 01) is used when not larger.
+// The segment's block is closed with the end-of-block symbol followed by an
+// empty stored block (BTYPE = 00, LEN = 0), which byte-aligns the bit stream
+// -- so the segments of a block concatenate into one valid raw DEFLATE stream
+// by a plain byte copy (the last segment's stored block carries BFINAL).  Any
+// inflater (zlib included) reproduces the packed bytes exactly; the
+// compressed bytes differ from zlib's, which the reference does not pin
+// (SURVEY 8c), so this stage is opt-in.
 //
-// Pipeline: k_deflate_segments (thread per segment, per-thread hash table in
-// shared memory) -> chunk_scan over segment lengths -> k_deflate_gather
-// (warp per segment, 16-byte copies into the compact output).
+// Pipeline: k_deflate_segments (warp per segment) -> chunk_scan over segment
+// lengths -> k_deflate_gather (warp per segment into the compact output).
 #include "nmk_common.cuh"
 #include "nmk_scan.cuh"
 
 namespace nmk {
 
-constexpr int kDefThreads = 32;                  // 64 KB of hash tables per CTA (3 CTAs / SM)
-constexpr int kDefHashBits = 8;                  // 256 buckets x 4 ways (u16 positions in a u64) per thread
-constexpr int kDefHash = 1 << kDefHashBits;
-constexpr uint64_t kEmptyBucket = ~0ULL;         // four 0xffff slots
+#ifndef NMK_DEF_WARPS
+#define NMK_DEF_WARPS 4
+#endif
+constexpr int kDefWarps = NMK_DEF_WARPS;
+constexpr int kDefThreads = 32 * kDefWarps;
+constexpr int kDefHashBits = 11;
+constexpr int kDefHash = 1 << kDefHashBits;      // buckets of two u16 positions (newest low): 8 KB per warp
+constexpr uint32_t kNoPos = 0xffffu;
+constexpr uint32_t kEmptyBucket = 0xffffffffu;
 constexpr int kMinMatch = 3, kMaxMatch = 258;
+// estimated bits of a match's length symbol / a near (1 or repeated) / any other distance symbol,
+// and the length from which a match is always taken (tuned on cfg2's index stream: ratio 4.9 -> 6.4 in a CPU model)
+constexpr int kProbe = 32;   // bytes a lane compares per candidate
+constexpr uint32_t kCostLen = 4, kCostNear = 1, kCostDist = 6, kCostLong = 24;
+constexpr int kStageWords = 128;                 // output bit ring per warp (a step emits <= 17 words)
+constexpr unsigned FULLW = 0xffffffffu;
 
 // worst case of one segment: the fixed code (chosen whenever the dynamic one
 // is not smaller) spends <= 9 bits per byte, plus the block headers,
 // end-of-block and the empty stored block, rounded up to 16 bytes
 __host__ __device__ inline uint32_t seg_bound(uint32_t seg_bytes) { return ((seg_bytes * 9 + 7) / 8 + 32 + 15) & ~15u; }
-
-struct BitWriter {
-  uint32_t* out;      // word-aligned
-  unsigned long long acc;
-  int nbits;
-  uint32_t nwords;
-  __device__ __forceinline__ void put(uint32_t bits, int len) {   // LSB-first
-    acc |= (unsigned long long)bits << nbits;
-    nbits += len;
-    if (nbits >= 32) {
-      out[nwords++] = (uint32_t)acc;
-      acc >>= 32;
-      nbits -= 32;
-    }
-  }
-  // pad to a byte boundary (zeros)
-  __device__ __forceinline__ void align() { nbits = (nbits + 7) & ~7; }
-  __device__ __forceinline__ uint32_t finish() {   // bytes written (byte-aligned stream)
-    const uint32_t bytes = nwords * 4 + (uint32_t)(nbits >> 3);
-    if (nbits) out[nwords] = (uint32_t)acc;   // the partial word (bytes past `bytes` are ignored)
-    return bytes;
-  }
-};
 
 __device__ __forceinline__ uint32_t rev_bits(uint32_t v, int len) { return __brev(v) >> (32 - len); }
 
@@ -99,158 +96,278 @@ __device__ __forceinline__ void dist_symbol(uint32_t dist, uint32_t& code, uint3
   }
 }
 
-// Greedy LZ77 over one segment: distance-1 candidate (runs) and one hash
-// candidate, 32-bit compare-extend; deterministic, so the counting pass and
-// the emitting pass make identical decisions.
-// LZ77 over one segment: candidates are the previous byte (runs) and the
-// four most recent positions of the 3-byte hash bucket (a u64 holding four
-// u16 positions, newest in the low bits); one-step lazy evaluation defers a
-// short match when the next position matches longer.  Deterministic, so the
-// counting pass and the emitting pass make identical decisions.
-template <typename Lit, typename Match>
-__device__ __forceinline__ void lz77(const uint8_t* __restrict__ src, uint32_t n, uint64_t* ht, Lit&& lit,
-                                     Match&& match) {
-  for (int i = 0; i < kDefHash; ++i) ht[i] = kEmptyBucket;
-  auto word_at = [&](uint32_t i) -> uint32_t {   // bytes past n read as 0
-    uint32_t v = 0;
-    if (i + 4 <= n) {
-      v = (uint32_t)src[i] | ((uint32_t)src[i + 1] << 8) | ((uint32_t)src[i + 2] << 16) | ((uint32_t)src[i + 3] << 24);
-    } else {
-      for (uint32_t k = 0; k < 4 && i + k < n; ++k) v |= (uint32_t)src[i + k] << (8 * k);
-    }
-    return v;
+// ---- per-warp shared memory ----------------------------------------------------
+constexpr int kHuffMax = 288;
+struct HuffWork {          // scratch of the code construction (aliases the hash table between the passes)
+  uint32_t f0[kHuffMax];   // used symbols' frequencies, symbol order
+  uint32_t f[kHuffMax];    // sorted by (frequency, symbol)
+  uint32_t nf[2 * kHuffMax];
+  uint16_t leaf0[kHuffMax], leaf[kHuffMax];
+  uint16_t par[2 * kHuffMax];
+  uint8_t dep[2 * kHuffMax];
+};
+struct __align__(16) DefWarp {
+  union {
+    uint32_t hash[kDefHash];
+    HuffWork hw;
   };
-  auto extend = [&](uint32_t j, uint32_t i) -> uint32_t {
-    const uint32_t maxl = min((uint32_t)kMaxMatch, n - i);
-    uint32_t l = 0;
-    while (l + 4 <= maxl && word_at(j + l) == word_at(i + l)) l += 4;
-    while (l < maxl && src[j + l] == src[i + l]) ++l;
-    return l;
-  };
-  // longest match at i (0 if none); inserts i into its bucket
-  auto find = [&](uint32_t i, uint32_t& dist) -> uint32_t {
-    uint32_t best = 0;
-    if (i + kMinMatch > n) return 0;
-    const uint32_t h = hash3(word_at(i));
-    const uint64_t bucket = ht[h];
-    ht[h] = (bucket << 16) | i;
-    if (i >= 1) {
-      best = extend(i - 1, i);
-      dist = 1;
+  uint32_t lf[kHuffMax];   // literal/length symbol counts
+  uint32_t df[32];         // distance symbol counts
+  uint32_t cf[32];         // code-length symbol counts
+  uint32_t stage[kStageWords];
+  uint16_t lc[kHuffMax], dc[32], cc[32];   // codes (bit-reversed)
+  uint8_t ll[kHuffMax], dl[32], cl[32];    // code lengths
+  uint8_t rs[320], rx[320];                // run-length coded code lengths and their extra values
+  uint16_t cost[256];                      // literal cost estimate, 1/8 bit: -log2 of the byte's share of the segment
+};
+static_assert(kCostLong <= (uint32_t)kProbe, "the cost filter reads the probe window");
+static_assert(sizeof(HuffWork) <= kDefHash * 4, "Huffman scratch must fit the hash table");
+
+// bytes p .. p + 3 of the segment (little-endian); words beyond the segment read 0
+__device__ __forceinline__ uint32_t word_at(const uint32_t* __restrict__ W, uint32_t nw, uint32_t p) {
+  const uint32_t k = p >> 2;
+  const uint32_t a = k < nw ? __ldg(W + k) : 0u;
+  const uint32_t b = k + 1 < nw ? __ldg(W + k + 1) : 0u;
+  return __funnelshift_r(a, b, (p & 3u) * 8u);
+}
+
+// common prefix of the bytes at j and i (j < i), at most maxl
+__device__ __forceinline__ uint32_t extend(const uint32_t* __restrict__ W, uint32_t nw, uint32_t j, uint32_t i,
+                                           uint32_t maxl) {
+  uint32_t l = 0;
+  while (l < maxl) {
+    const uint32_t x = word_at(W, nw, j + l) ^ word_at(W, nw, i + l);
+    if (x) {
+      l += (uint32_t)(__ffs((int)x) - 1) >> 3;
+      break;
     }
+    l += 4;
+  }
+  return min(l, maxl);
+}
+
+// The whole warp extends one match beyond the l0 bytes already known equal:
+// lane l compares bytes l0 + 4 l .. + 3 of each 128-byte stretch.
+__device__ __forceinline__ uint32_t extend_coop(const uint32_t* __restrict__ W, uint32_t nw, uint32_t j, uint32_t i,
+                                                uint32_t maxl, uint32_t l0, int lane) {
+  uint32_t l = l0;
+  while (l < maxl) {
+    const uint32_t k = l + 4u * (uint32_t)lane;
+    const uint32_t x = k < maxl ? word_at(W, nw, j + k) ^ word_at(W, nw, i + k) : 0u;
+    const unsigned mm = __ballot_sync(FULLW, x != 0u);
+    if (mm) {
+      const int f = __ffs((int)mm) - 1;
+      const uint32_t xf = __shfl_sync(FULLW, x, f);
+      l += 4u * (uint32_t)f + ((uint32_t)(__ffs((int)xf) - 1) >> 3);
+      break;
+    }
+    l += 128u;
+  }
+  return min(l, maxl);
+}
+
+// Warp-cooperative LZ77 over one segment.  `tokens(nlit_lo, nlit_hi, byte, mlane, len, dist)`
+// is called warp-uniformly once per parse step: lanes in [nlit_lo, nlit_hi)
+// each hold a literal (`byte` = their own), and lane `mlane` (32: none) holds
+// a match (len, dist) that follows those literals.  Deterministic: both passes
+// produce the same token sequence.
+template <typename Tokens>
+__device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32_t n, uint32_t* hash,
+                                          const uint16_t* cost, int lane, Tokens&& tokens) {
+  const uint32_t nw = (n + 3) >> 2;
+  for (int k = lane; k < kDefHash; k += 32) hash[k] = kEmptyBucket;
+  __syncwarp();
+  uint32_t pos = 0, rep = 0;
+  while (pos < n) {
+    const uint32_t i = pos + lane;
+    const bool valid = i < n;
+    // the lane's own kProbe bytes, read once for all of its candidates
+    uint32_t a[kProbe / 4];
+    {
+      uint32_t v[kProbe / 4 + 1];
+      const uint32_t k0 = i >> 2;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t j = (uint32_t)(bucket >> (16 * w)) & 0xffffu;
-      if (j == 0xffffu || j + 1 >= i || i - j > 32768u) continue;   // j = i-1 already tried; RFC 1951 window
-      const uint32_t l = extend(j, i);
-      if (l > best) { best = l; dist = i - j; }
+      for (int q = 0; q <= kProbe / 4; ++q) v[q] = (valid && k0 + q < nw) ? __ldg(W + k0 + q) : 0u;
+#pragma unroll
+      for (int q = 0; q < kProbe / 4; ++q) a[q] = __funnelshift_r(v[q], v[q + 1], (i & 3u) * 8u);
     }
-    return best;
-  };
-  auto insert = [&](uint32_t p) {
-    if (p + kMinMatch <= n) {
-      const uint32_t h = hash3(word_at(p));
-      ht[h] = (ht[h] << 16) | p;
+    const uint32_t w0 = a[0];
+    const bool hashed = valid && i + kMinMatch <= n;
+    const uint32_t h = hash3(w0);
+    const uint32_t bucket = hashed ? hash[h] : kEmptyBucket;   // the table as it was before this step
+    __syncwarp();
+    const unsigned grp = __match_any_sync(FULLW, hashed ? h : (0x80000000u | (uint32_t)lane));
+    if (hashed && lane == 31 - __clz(grp)) hash[h] = (bucket << 16) | i;   // highest lane (latest position) wins
+    __syncwarp();
+    uint32_t best = 0, bd = 0;
+    if (hashed) {
+      // lanes measure their candidates up to kProbe bytes (all loads of a
+      // candidate in flight together); the match the parse takes is then
+      // extended to its full length by the whole warp
+      const uint32_t maxl = min((uint32_t)kProbe, n - i);
+      auto consider = [&](uint32_t d) {
+        if (best >= maxl || d == 0 || d > i || d > 32768u) return;
+        const uint32_t j = i - d, k0 = j >> 2;
+        uint32_t v[kProbe / 4 + 1];
+#pragma unroll
+        for (int q = 0; q <= kProbe / 4; ++q) v[q] = k0 + q < nw ? __ldg(W + k0 + q) : 0u;
+        uint32_t l = kProbe;
+#pragma unroll
+        for (int q = kProbe / 4 - 1; q >= 0; --q) {
+          const uint32_t x = a[q] ^ __funnelshift_r(v[q], v[q + 1], (j & 3u) * 8u);
+          if (x) l = 4u * q + ((uint32_t)(__ffs((int)x) - 1) >> 3);
+        }
+        l = min(l, maxl);
+        if (l > best) { best = l; bd = d; }
+      };
+      consider(1);                                   // runs
+      if (rep > 1) consider(rep);                    // the last distance used (periodic codes)
+      const unsigned lower = grp & ((1u << lane) - 1u);
+      const uint32_t d_in = lower ? (uint32_t)(lane - (31 - __clz(lower))) : 0u;   // same hash earlier in this step
+      if (d_in > 1 && d_in != rep) consider(d_in);
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const uint32_t j = (bucket >> (16 * w)) & 0xffffu;
+        if (j == kNoPos) continue;
+        const uint32_t d = i - j;
+        if (d != 1 && d != rep && d != d_in) consider(d);
+      }
+      if (best == (uint32_t)kMinMatch && bd > 4096u) best = 0;   // a far 3-byte match costs more than 3 literals
+      // Index streams are dominated by one or two byte values whose Huffman
+      // codes take 1-2 bits, so a short match is often dearer than its bytes
+      // as literals (zlib level 1-3 loses to Huffman-only on them): keep a
+      // short match only if its estimated cost beats the literals' (1/8 bit).
+      if (best >= (uint32_t)kMinMatch && best < (uint32_t)kCostLong) {
+        uint32_t litc = 0;
+#pragma unroll
+        for (int w = 0; w < (int)(kCostLong + 3) / 4; ++w) {   // the match's bytes are in a[]
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if ((uint32_t)(4 * w + q) < best) litc += cost[(a[w] >> (8 * q)) & 0xffu];
+        }
+        uint32_t sy, ebl, ebd, ev;
+        len_symbol(best, sy, ebl, ev);
+        dist_symbol(bd, sy, ebd, ev);
+        const uint32_t mc = 8u * (kCostLen + ebl + ((bd == 1 || bd == rep) ? kCostNear : kCostDist + ebd));
+        if (mc >= litc) best = 0;
+      }
     }
-  };
-  uint32_t i = 0;
-  uint32_t dist = 0;
-  uint32_t best = find(0, dist);
-  while (i < n) {
-    if (best >= kMinMatch) {
-      if (best < 32 && i + 1 < n) {   // lazy: a longer match one byte later wins
-        uint32_t d2 = 0;
-        const uint32_t b2 = find(i + 1, d2);
-        if (b2 > best) {
-          lit(src[i]);
-          ++i;
-          best = b2;
-          dist = d2;
+    const unsigned m3 = __ballot_sync(FULLW, best >= (uint32_t)kMinMatch);
+    const uint32_t lim = min(32u, n - pos);   // positions of this step inside the segment
+    uint32_t c = 0, scan = 0;
+    while (true) {
+      const unsigned ahead = scan < 32 ? (m3 >> scan) << scan : 0u;
+      const uint32_t nxt = ahead ? (uint32_t)__ffs((int)ahead) - 1u : 32u;
+      if (nxt >= lim) {   // literals to the end of the step
+        tokens(c, lim, w0 & 0xffu, 32u, 0u, 0u);
+        c = lim;
+        break;
+      }
+      uint32_t L = __shfl_sync(FULLW, best, (int)nxt);
+      const uint32_t D = __shfl_sync(FULLW, bd, (int)nxt);
+      if (nxt + 1 < lim && L < (uint32_t)kProbe) {   // lazy: a longer match one byte later wins
+        const uint32_t L1 = __shfl_sync(FULLW, best, (int)nxt + 1);
+        if (L1 > L) {
+          scan = nxt + 1;
           continue;
         }
-        // i+1 is inserted already; emit the match at i
-        match(best, dist);
-        const uint32_t end = i + best;
-        for (uint32_t p = i + 2; p < end && p < i + 8; ++p) insert(p);
-        i = end;
-      } else {
-        match(best, dist);
-        const uint32_t end = i + best;
-        for (uint32_t p = i + 1; p < end && p < i + 8; ++p) insert(p);
-        i = end;
       }
-    } else {
-      lit(src[i]);
-      ++i;
+      if (L == (uint32_t)kProbe) {
+        const uint32_t ip = pos + nxt;
+        L = extend_coop(W, nw, ip - D, ip, min((uint32_t)kMaxMatch, n - ip), L, lane);
+      }
+      tokens(c, nxt, w0 & 0xffu, nxt, L, D);
+      rep = D;
+      c = nxt + L;
+      scan = c;
+      if (c >= lim) break;
     }
-    if (i < n) best = find(i, dist);
+    pos += c;
   }
 }
 
-// Huffman code lengths <= maxlen for freq[0..nsym) (0 for unused symbols):
-// two-queue construction over the sorted leaves, frequencies halved (>= 1)
-// until the depth fits.  A lone used symbol gets a partner so every code is
-// complete.  Work arrays are per thread (local memory).
-constexpr int kHuffMax = 288;
-__device__ void huff_lengths(const uint32_t* freq, int nsym, int maxlen, uint8_t* len) {
-  uint32_t f[kHuffMax];
-  uint16_t leaf[kHuffMax];
-  uint32_t nf[2 * kHuffMax];
-  uint16_t par[2 * kHuffMax];
-  uint8_t dep[2 * kHuffMax];
+// ---- Huffman code lengths <= maxlen for freq[0 .. nsym), whole warp -------------
+// Used symbols are ranked by (frequency, symbol) with an all-pairs count (each
+// lane ranks its symbols), lane 0 runs the two-queue merge over the sorted
+// leaves and the depths; frequencies are halved (>= 1) until the depth fits.
+// A lone used symbol gets a partner so every code is complete.
+__device__ void huff_lengths_warp(const uint32_t* freq, int nsym, int maxlen, uint8_t* len, HuffWork& hw, int lane) {
   int m = 0;
-  for (int s = 0; s < nsym; ++s) {
-    len[s] = 0;
-    if (freq[s]) { leaf[m] = (uint16_t)s; f[m] = freq[s]; ++m; }
+  for (int s0 = 0; s0 < nsym; s0 += 32) {
+    const int s = s0 + lane;
+    const bool used = s < nsym && freq[s] != 0;
+    if (s < nsym) len[s] = 0;
+    const unsigned mk = __ballot_sync(FULLW, used);
+    if (used) {
+      const int idx = m + __popc(mk & ((1u << lane) - 1u));
+      hw.leaf0[idx] = (uint16_t)s;
+      hw.f0[idx] = freq[s];
+    }
+    m += __popc(mk);
   }
+  __syncwarp();
   if (m == 0) return;
   if (m == 1) {   // one symbol: length 1 plus an unused partner of length 1
-    len[leaf[0]] = 1;
-    len[leaf[0] == 0 ? 1 : 0] = 1;
+    if (lane == 0) {
+      const int s = hw.leaf0[0];
+      len[s] = 1;
+      len[s == 0 ? 1 : 0] = 1;
+    }
+    __syncwarp();
     return;
   }
   for (;;) {
-    // insertion sort of the leaves by (freq, symbol)
-    for (int a = 1; a < m; ++a) {
-      const uint32_t fa = f[a];
-      const uint16_t la = leaf[a];
-      int b = a - 1;
-      while (b >= 0 && (f[b] > fa || (f[b] == fa && leaf[b] > la))) { f[b + 1] = f[b]; leaf[b + 1] = leaf[b]; --b; }
-      f[b + 1] = fa;
-      leaf[b + 1] = la;
+    for (int a = lane; a < m; a += 32) {   // leaves are in symbol order: ties rank by index
+      const uint32_t fa = hw.f0[a];
+      int r = 0;
+      for (int b = 0; b < m; ++b) {
+        const uint32_t fb = hw.f0[b];
+        r += (fb < fa) || (fb == fa && b < a);
+      }
+      hw.f[r] = fa;
+      hw.leaf[r] = hw.leaf0[a];
     }
-    for (int a = 0; a < m; ++a) nf[a] = f[a];
-    int li = 0, ii = m, nn = m;
-    auto take = [&]() -> int {
-      if (li < m && (ii >= nn || nf[li] <= nf[ii])) return li++;
-      return ii++;
-    };
-    while (nn < 2 * m - 1) {
-      const int x = take(), y = take();
-      nf[nn] = nf[x] + nf[y];
-      par[x] = par[y] = (uint16_t)nn;
-      ++nn;
-    }
-    dep[nn - 1] = 0;
+    __syncwarp();
     int maxd = 0;
-    for (int k = nn - 2; k >= 0; --k) {
-      dep[k] = dep[par[k]] + 1;
-      if (k < m && dep[k] > maxd) maxd = dep[k];
+    if (lane == 0) {
+      for (int a = 0; a < m; ++a) hw.nf[a] = hw.f[a];
+      int li = 0, ii = m, nn = m;
+      auto take = [&]() -> int {
+        if (li < m && (ii >= nn || hw.nf[li] <= hw.nf[ii])) return li++;
+        return ii++;
+      };
+      while (nn < 2 * m - 1) {
+        const int x = take(), y = take();
+        hw.nf[nn] = hw.nf[x] + hw.nf[y];
+        hw.par[x] = hw.par[y] = (uint16_t)nn;
+        ++nn;
+      }
+      hw.dep[nn - 1] = 0;
+      for (int k = nn - 2; k >= 0; --k) {
+        const int d = hw.dep[hw.par[k]] + 1;
+        hw.dep[k] = (uint8_t)d;
+        if (k < m && d > maxd) maxd = d;
+      }
     }
+    maxd = __shfl_sync(FULLW, maxd, 0);
+    __syncwarp();
     if (maxd <= maxlen) {
-      for (int a = 0; a < m; ++a) len[leaf[a]] = dep[a];
+      for (int a = lane; a < m; a += 32) len[hw.leaf[a]] = hw.dep[a];
+      __syncwarp();
       return;
     }
-    for (int a = 0; a < m; ++a) f[a] = max(1u, f[a] >> 1);
+    for (int a = lane; a < m; a += 32) hw.f0[a] = max(1u, hw.f0[a] >> 1);
+    __syncwarp();
   }
 }
 
-// canonical codes (RFC 1951 3.2.2), bit-reversed for LSB-first output
+// canonical codes (RFC 1951 3.2.2), bit-reversed for LSB-first output (lane 0)
 __device__ void huff_codes(const uint8_t* len, int nsym, uint16_t* code) {
   uint32_t cnt[16] = {0}, next[16];
   for (int s = 0; s < nsym; ++s) ++cnt[len[s]];
   cnt[0] = 0;
   uint32_t c = 0;
+  next[0] = 0;
   for (int b = 1; b < 16; ++b) {
     c = (c + cnt[b - 1]) << 1;
     next[b] = c;
@@ -261,142 +378,233 @@ __device__ void huff_codes(const uint8_t* len, int nsym, uint16_t* code) {
 
 __constant__ uint8_t kClOrder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
+// Every lane with nb > 0 appends its nb (<= 48) bits v, in lane order, at
+// *bitpos of the segment's output; complete 32-bit words leave the ring.
+__device__ __forceinline__ void emit_bits(unsigned long long v, uint32_t nb, uint32_t& bitpos, uint32_t* stage,
+                                          uint32_t* __restrict__ out, int lane) {
+  uint32_t incl = nb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULLW, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(FULLW, incl, 31);
+  if (nb) {
+    const uint32_t o = bitpos + incl - nb;
+    const uint32_t w = o >> 5, s = o & 31u;
+    atomicOr(&stage[w & (kStageWords - 1)], (uint32_t)(v << s));
+    const unsigned long long rest = s ? (v >> (32u - s)) : (v >> 32);
+    if (rest) {
+      atomicOr(&stage[(w + 1) & (kStageWords - 1)], (uint32_t)rest);
+      if (rest >> 32) atomicOr(&stage[(w + 2) & (kStageWords - 1)], (uint32_t)(rest >> 32));
+    }
+  }
+  __syncwarp();
+  const uint32_t w0 = bitpos >> 5, w1 = (bitpos + total) >> 5;
+  for (uint32_t w = w0 + lane; w < w1; w += 32) {
+    out[w] = stage[w & (kStageWords - 1)];
+    stage[w & (kStageWords - 1)] = 0u;
+  }
+  __syncwarp();
+  bitpos += total;
+}
+
 __global__ void __launch_bounds__(kDefThreads)
 k_deflate_segments(const uint8_t* __restrict__ packed, uint64_t stride, uint64_t nblocks, uint64_t block_len,
                    uint64_t last_len, uint32_t seg_bytes, uint32_t segs_per_block, uint8_t* __restrict__ scratch,
                    uint32_t* __restrict__ seg_len) {
-  extern __shared__ uint64_t s_hash[];   // kDefThreads x kDefHash buckets
+  extern __shared__ __align__(16) uint8_t s_def[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  DefWarp& m = reinterpret_cast<DefWarp*>(s_def)[wid];
   const uint64_t nseg = nblocks * segs_per_block;
-  uint64_t* ht = s_hash + (size_t)threadIdx.x * kDefHash;
-  for (uint64_t sg = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
-       sg += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t sg = (uint64_t)blockIdx.x * kDefWarps + wid; sg < nseg; sg += (uint64_t)gridDim.x * kDefWarps) {
     const uint64_t b = sg / segs_per_block;
     const uint32_t s = (uint32_t)(sg - b * segs_per_block);
     const uint64_t blen = (b + 1 == nblocks) ? last_len : block_len;
     const uint64_t lo = (uint64_t)s * seg_bytes;
-    uint8_t* dst = scratch + sg * (uint64_t)seg_bound(seg_bytes);
     if (lo >= blen) {   // segment past a short last block: nothing
-      seg_len[sg] = 0;
+      if (lane == 0) seg_len[sg] = 0;
       continue;
     }
     const uint32_t n = (uint32_t)min((uint64_t)seg_bytes, blen - lo);
     const bool last = lo + n == blen;
-    const uint8_t* src = packed + b * stride + lo;
+    // the segment starts 16-byte aligned (stride and seg_bytes are multiples of 16)
+    const uint32_t* W = reinterpret_cast<const uint32_t*>(packed + b * stride + lo);
+    uint32_t* out = reinterpret_cast<uint32_t*>(scratch + sg * (uint64_t)seg_bound(seg_bytes));
 
+    // ---- pass 0: byte shares -> literal cost estimates ----
+    for (int k = lane; k < 256; k += 32) m.lf[k] = 0;
+    __syncwarp();
+    for (uint32_t w = lane; w < ((n + 3) >> 2); w += 32) {
+      const uint32_t x = __ldg(W + w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * w + q < n) atomicAdd(&m.lf[(x >> (8 * q)) & 0xffu], 1u);
+    }
+    __syncwarp();
+    {
+      const float lgn = __log2f((float)n);
+      for (int k = lane; k < 256; k += 32) {
+        const uint32_t c = m.lf[k];
+        m.cost[k] = (uint16_t)(c ? __float2int_rn(8.0f * (lgn - __log2f((float)c))) : 255);
+      }
+    }
+    __syncwarp();
     // ---- pass 1: symbol statistics ----
-    uint32_t lf[286], df[30];
-    for (int k = 0; k < 286; ++k) lf[k] = 0;
-    for (int k = 0; k < 30; ++k) df[k] = 0;
-    uint64_t extra = 0;
-    lz77(src, n, ht, [&](uint32_t byte) { ++lf[byte]; },
-         [&](uint32_t len, uint32_t dist) {
-           uint32_t sy, eb, ev;
-           len_symbol(len, sy, eb, ev);
-           ++lf[sy];
-           extra += eb;
-           dist_symbol(dist, sy, eb, ev);
-           ++df[sy];
-           extra += eb;
-         });
-    lf[256] = 1;   // end of block
+    for (int k = lane; k < kHuffMax; k += 32) m.lf[k] = 0;
+    m.df[lane] = 0;
+    m.cf[lane] = 0;
+    for (int k = lane; k < kStageWords; k += 32) m.stage[k] = 0;
+    __syncwarp();
+    lz77_warp(W, n, m.hash, m.cost, lane, [&](uint32_t c0, uint32_t c1, uint32_t byte, uint32_t ml, uint32_t L, uint32_t D) {
+      if ((uint32_t)lane >= c0 && (uint32_t)lane < c1) atomicAdd(&m.lf[byte], 1u);
+      if ((uint32_t)lane == ml) {
+        uint32_t sy, eb, ev;
+        len_symbol(L, sy, eb, ev);
+        atomicAdd(&m.lf[sy], 1u);
+        dist_symbol(D, sy, eb, ev);
+        atomicAdd(&m.df[sy], 1u);
+      }
+    });
+    if (lane == 0) m.lf[256] = 1;   // end of block
+    __syncwarp();
 
     // ---- dynamic code: lengths, run-length coded lengths, their code ----
-    uint8_t ll[286], dl[30];
-    huff_lengths(lf, 286, 15, ll);
-    huff_lengths(df, 30, 15, dl);
-    int hlit = 286, hdist = 30;
-    while (hlit > 257 && ll[hlit - 1] == 0) --hlit;
-    while (hdist > 1 && dl[hdist - 1] == 0) --hdist;
-    uint8_t rs[316], rx[316];   // RLE symbols and their extra values
-    int nr = 0;
-    {
-      auto L = [&](int i) -> uint32_t { return i < hlit ? ll[i] : dl[i - hlit]; };
+    huff_lengths_warp(m.lf, 286, 15, m.ll, m.hw, lane);
+    huff_lengths_warp(m.df, 30, 15, m.dl, m.hw, lane);
+    int hlit = 0, hdist = 0, nr = 0;
+    if (lane == 0) {
+      hlit = 286;
+      hdist = 30;
+      while (hlit > 257 && m.ll[hlit - 1] == 0) --hlit;
+      while (hdist > 1 && m.dl[hdist - 1] == 0) --hdist;
+      auto LN = [&](int i) -> uint32_t { return i < hlit ? m.ll[i] : m.dl[i - hlit]; };
       const int tot = hlit + hdist;
       int i = 0;
       while (i < tot) {
-        const uint32_t v = L(i);
+        const uint32_t v = LN(i);
         int run = 1;
-        while (i + run < tot && L(i + run) == v) ++run;
+        while (i + run < tot && LN(i + run) == v) ++run;
         if (v == 0) {
           int r = run;
-          while (r >= 11) { const int t = min(r, 138); rs[nr] = 18; rx[nr++] = (uint8_t)(t - 11); r -= t; }
-          if (r >= 3) { rs[nr] = 17; rx[nr++] = (uint8_t)(r - 3); r = 0; }
-          while (r > 0) { rs[nr] = 0; rx[nr++] = 0; --r; }
+          while (r >= 11) { const int t = min(r, 138); m.rs[nr] = 18; m.rx[nr++] = (uint8_t)(t - 11); r -= t; }
+          if (r >= 3) { m.rs[nr] = 17; m.rx[nr++] = (uint8_t)(r - 3); r = 0; }
+          while (r > 0) { m.rs[nr] = 0; m.rx[nr++] = 0; --r; }
         } else {
-          rs[nr] = (uint8_t)v; rx[nr++] = 0;
+          m.rs[nr] = (uint8_t)v; m.rx[nr++] = 0;
           int r = run - 1;
-          while (r >= 3) { const int t = min(r, 6); rs[nr] = 16; rx[nr++] = (uint8_t)(t - 3); r -= t; }
-          while (r > 0) { rs[nr] = (uint8_t)v; rx[nr++] = 0; --r; }
+          while (r >= 3) { const int t = min(r, 6); m.rs[nr] = 16; m.rx[nr++] = (uint8_t)(t - 3); r -= t; }
+          while (r > 0) { m.rs[nr] = (uint8_t)v; m.rx[nr++] = 0; --r; }
         }
         i += run;
       }
+      for (int k = 0; k < nr; ++k) ++m.cf[m.rs[k]];
     }
-    uint32_t cf[19];
-    for (int k = 0; k < 19; ++k) cf[k] = 0;
-    for (int k = 0; k < nr; ++k) ++cf[rs[k]];
-    uint8_t cl[19];
-    huff_lengths(cf, 19, 7, cl);
+    hlit = __shfl_sync(FULLW, hlit, 0);
+    hdist = __shfl_sync(FULLW, hdist, 0);
+    nr = __shfl_sync(FULLW, nr, 0);
+    __syncwarp();
+    huff_lengths_warp(m.cf, 19, 7, m.cl, m.hw, lane);
     int hclen = 19;
-    while (hclen > 4 && cl[kClOrder[hclen - 1]] == 0) --hclen;
+    while (hclen > 4 && m.cl[kClOrder[hclen - 1]] == 0) --hclen;
     // cost of the two encodings (extra bits are the same for both)
-    uint64_t dyn = 14 + 3 * (uint64_t)hclen, fix = 0;
-    for (int k = 0; k < nr; ++k) dyn += cl[rs[k]] + (rs[k] == 16 ? 2 : rs[k] == 17 ? 3 : rs[k] == 18 ? 7 : 0);
-    for (int k = 0; k < 286; ++k) {
-      if (!lf[k]) continue;
-      dyn += (uint64_t)lf[k] * ll[k];
-      fix += (uint64_t)lf[k] * (k < 144 ? 8 : k < 256 ? 9 : k < 280 ? 7 : 8);
+    unsigned long long dyn = 0, fix = 0;
+    for (int k = lane; k < nr; k += 32) {
+      const uint32_t r = m.rs[k];
+      dyn += m.cl[r] + (r == 16 ? 2 : r == 17 ? 3 : r == 18 ? 7 : 0);
     }
-    for (int k = 0; k < 30; ++k) { dyn += (uint64_t)df[k] * dl[k]; fix += (uint64_t)df[k] * 5; }
+    for (int k = lane; k < 286; k += 32) {
+      const unsigned long long f = m.lf[k];
+      dyn += f * m.ll[k];
+      fix += f * (k < 144 ? 8 : k < 256 ? 9 : k < 280 ? 7 : 8);
+    }
+    if (lane < 30) { dyn += (unsigned long long)m.df[lane] * m.dl[lane]; fix += (unsigned long long)m.df[lane] * 5; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dyn += __shfl_xor_sync(FULLW, dyn, o);
+      fix += __shfl_xor_sync(FULLW, fix, o);
+    }
+    dyn += 14 + 3 * (unsigned long long)hclen;
     const bool use_dyn = dyn < fix;
-    (void)extra;
 
     // ---- pass 2: emit ----
-    BitWriter w{reinterpret_cast<uint32_t*>(dst), 0ULL, 0, 0};
-    uint16_t lc[286], dc[30];
+    uint32_t bitpos = 0;
     if (use_dyn) {
-      uint16_t cc[19];
-      huff_codes(ll, 286, lc);
-      huff_codes(dl, 30, dc);
-      huff_codes(cl, 19, cc);
-      w.put(0u | (2u << 1), 3);   // BFINAL = 0, BTYPE = 10 (dynamic Huffman)
-      w.put((uint32_t)(hlit - 257), 5);
-      w.put((uint32_t)(hdist - 1), 5);
-      w.put((uint32_t)(hclen - 4), 4);
-      for (int k = 0; k < hclen; ++k) w.put(cl[kClOrder[k]], 3);
-      for (int k = 0; k < nr; ++k) {
-        w.put(cc[rs[k]], cl[rs[k]]);
-        if (rs[k] == 16) w.put(rx[k], 2);
-        else if (rs[k] == 17) w.put(rx[k], 3);
-        else if (rs[k] == 18) w.put(rx[k], 7);
+      if (lane == 0) {
+        huff_codes(m.ll, 286, m.lc);
+        huff_codes(m.dl, 30, m.dc);
+        huff_codes(m.cl, 19, m.cc);
+      }
+      __syncwarp();
+      // BFINAL = 0, BTYPE = 10 | HLIT | HDIST | HCLEN
+      const uint32_t hdr = 0u | (2u << 1) | ((uint32_t)(hlit - 257) << 3) | ((uint32_t)(hdist - 1) << 8) |
+                           ((uint32_t)(hclen - 4) << 13);
+      emit_bits(hdr, lane == 0 ? 17u : 0u, bitpos, m.stage, out, lane);
+      emit_bits(lane < hclen ? m.cl[kClOrder[lane < 19 ? lane : 0]] : 0u, lane < hclen ? 3u : 0u, bitpos, m.stage, out,
+                lane);
+      for (int k0 = 0; k0 < nr; k0 += 32) {
+        const int k = k0 + lane;
+        unsigned long long v = 0;
+        uint32_t nb = 0;
+        if (k < nr) {
+          const uint32_t r = m.rs[k];
+          nb = m.cl[r];
+          v = m.cc[r];
+          const uint32_t xb = r == 16 ? 2u : r == 17 ? 3u : r == 18 ? 7u : 0u;
+          v |= (unsigned long long)m.rx[k] << nb;
+          nb += xb;
+        }
+        emit_bits(v, nb, bitpos, m.stage, out, lane);
       }
     } else {
-      for (int k = 0; k < 286; ++k) {
+      for (int k = lane; k < 286; k += 32) {
         uint32_t c;
         int l;
         fixed_litlen((uint32_t)k, c, l);
-        lc[k] = (uint16_t)c;
-        ll[k] = (uint8_t)l;
+        m.lc[k] = (uint16_t)c;
+        m.ll[k] = (uint8_t)l;
       }
-      for (int k = 0; k < 30; ++k) { dc[k] = (uint16_t)rev_bits((uint32_t)k, 5); dl[k] = 5; }
-      w.put(0u | (1u << 1), 3);   // BFINAL = 0, BTYPE = 01 (fixed Huffman)
+      if (lane < 30) { m.dc[lane] = (uint16_t)rev_bits((uint32_t)lane, 5); m.dl[lane] = 5; }
+      __syncwarp();
+      emit_bits(0u | (1u << 1), lane == 0 ? 3u : 0u, bitpos, m.stage, out, lane);   // BFINAL = 0, BTYPE = 01
     }
-    lz77(src, n, ht, [&](uint32_t byte) { w.put(lc[byte], ll[byte]); },
-         [&](uint32_t len, uint32_t dist) {
-           uint32_t sy, eb, ev;
-           len_symbol(len, sy, eb, ev);
-           w.put(lc[sy], ll[sy]);
-           if (eb) w.put(ev, (int)eb);
-           dist_symbol(dist, sy, eb, ev);
-           w.put(dc[sy], dl[sy]);
-           if (eb) w.put(ev, (int)eb);
-         });
-    w.put(lc[256], ll[256]);    // end of block
-    // an empty stored block byte-aligns the stream (BFINAL on the last segment)
-    w.put(last ? 1u : 0u, 3);
-    w.align();
-    w.put(0x0000u, 16);         // LEN
-    w.put(0xffffu, 16);         // NLEN
-    seg_len[sg] = w.finish();
+    lz77_warp(W, n, m.hash, m.cost, lane, [&](uint32_t c0, uint32_t c1, uint32_t byte, uint32_t ml, uint32_t L, uint32_t D) {
+      unsigned long long v = 0;
+      uint32_t nb = 0;
+      if ((uint32_t)lane >= c0 && (uint32_t)lane < c1) {
+        v = m.lc[byte];
+        nb = m.ll[byte];
+      } else if ((uint32_t)lane == ml) {
+        uint32_t sy, eb, ev;
+        len_symbol(L, sy, eb, ev);
+        v = m.lc[sy];
+        nb = m.ll[sy];
+        v |= (unsigned long long)ev << nb;
+        nb += eb;
+        dist_symbol(D, sy, eb, ev);
+        v |= (unsigned long long)m.dc[sy] << nb;
+        nb += m.dl[sy];
+        v |= (unsigned long long)ev << nb;
+        nb += eb;
+      }
+      emit_bits(v, nb, bitpos, m.stage, out, lane);
+    });
+    // end of block, then an empty stored block byte-aligns the stream (BFINAL
+    // on the last segment): 3 header bits, zero padding, LEN = 0, NLEN = 0xffff
+    {
+      unsigned long long v = m.lc[256];
+      uint32_t nb = m.ll[256];
+      v |= (unsigned long long)(last ? 1u : 0u) << nb;
+      nb += 3;
+      emit_bits(v, lane == 0 ? nb : 0u, bitpos, m.stage, out, lane);
+      const uint32_t pad = (8u - (bitpos & 7u)) & 7u;
+      emit_bits(0xffff0000ULL << pad, lane == 0 ? pad + 32u : 0u, bitpos, m.stage, out, lane);
+    }
+    if (lane == 0) {
+      if (bitpos & 31u) out[bitpos >> 5] = m.stage[(bitpos >> 5) & (kStageWords - 1)];   // the partial word
+      seg_len[sg] = bitpos >> 3;
+    }
+    __syncwarp();
   }
 }
 
@@ -466,9 +674,10 @@ extern "C" int nmk_deflate(const uint8_t* packed, uint64_t block_stride, uint64_
   uint8_t* scratch = (uint8_t*)(wb + p.off_scratch);
   uint32_t* seg_len = (uint32_t*)(wb + p.off_len);
   unsigned long long* offsets = (unsigned long long*)(wb + p.off_offsets);
-  const size_t smem = (size_t)kDefThreads * kDefHash * sizeof(uint64_t);
+  const size_t smem = (size_t)kDefWarps * sizeof(DefWarp);
   ensure_dyn_smem(k_deflate_segments, smem);
-  const uint64_t g1 = (p.nseg + kDefThreads - 1) / kDefThreads;
+  uint64_t g1 = (p.nseg + kDefWarps - 1) / kDefWarps;
+  if (g1 > (uint64_t)sm_count() * 16) g1 = (uint64_t)sm_count() * 16;
   k_deflate_segments<<<(unsigned)g1, kDefThreads, smem, s>>>(packed, block_stride, nblocks, block_len, last_len,
                                                              seg_bytes, (uint32_t)p.segs_per_block, scratch,
                                                              seg_len);
