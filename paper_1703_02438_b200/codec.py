@@ -282,15 +282,14 @@ def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_off
     if base_inc < exact_offset:
         raise ValueError("exact values start after the covering block")
     d_exact = torch.from_numpy(ex).to(dev) if ex.size else torch.empty(0, dtype=_tdt(base.dtype), device=dev)
-    base = np.asarray(base)
-    d_base = (torch.from_numpy(base) if base.flags.writeable and base.flags.c_contiguous
-              else torch.from_numpy(np.array(base, copy=True))).to(dev)
+    from . import staging
+    d_base = staging.h2d(np.asarray(base), dev)
     res = engine.decode(d_packed, stride, first, bits, epb, n, d_prefix_rel, d_centers, d_exact, d_base,
                         [(start, count, 0)])
     need = int(res.n_sentinel[0])
     avail = ex.shape[0] - int(res.inc_before[0])
     have = max(0, min(need, avail))
-    return res.out.cpu().numpy(), need, have, res.bad_index, res.max_bad_index
+    return staging.d2h(res.out), need, have, res.bad_index, res.max_bad_index
 
 
 def _tdt(np_dtype):

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from . import codec, container, engine
+from . import codec, container, engine, staging
 from .core import TemporalPair, Tolerance
 
 DEFAULT_TOLERANCE = 1e-3
@@ -109,28 +109,14 @@ def _pinned_buf(key: str, nbytes: int):
 
 
 def to_device(a: np.ndarray, key: str = "h2d"):
-    """numpy -> CUDA tensor through a reusable pinned staging buffer."""
-    import torch
-    a = np.ascontiguousarray(a)
-    tdt = torch.float64 if a.dtype.itemsize == 8 and a.dtype.kind == "f" else None
-    if a.dtype.kind == "f" and a.dtype.itemsize == 4:
-        tdt = torch.float32
-    st = _pinned_buf(key, a.nbytes)
-    st[: a.nbytes].numpy()[:] = a.view(np.uint8).reshape(-1)
-    dev = torch.empty(a.nbytes, dtype=torch.uint8, device="cuda")
-    dev.copy_(st[: a.nbytes], non_blocking=True)
-    torch.cuda.current_stream().synchronize()   # staging buffer is reused
-    return dev.view(tdt) if tdt is not None else dev
+    """numpy -> CUDA tensor (staging.h2d: threaded fills of two pinned chunks
+    overlapped with their DMA)."""
+    return staging.h2d(a)
 
 
 def _to_host(t, key: str) -> np.ndarray:
-    """CUDA tensor -> numpy copy (through pinned memory)."""
-    import torch
-    nbytes = t.numel() * t.element_size()
-    st = _pinned_buf(key, nbytes)
-    st[:nbytes].copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    return st[:nbytes].numpy().copy()
+    """CUDA tensor -> fresh numpy array (staging.d2h)."""
+    return staging.d2h(t)
 
 
 def _encoding_to_host(enc: engine.DeviceEncoding):

@@ -31,6 +31,25 @@ def _blocks_on_device(blocks, stride):
     return torch.from_numpy(buf).cuda()
 
 
+def test_index_stream_shapes_compress(tmp_path):
+    """B = 10 (period-5 byte pattern) and B = 12 noisy streams: exact round
+    trip, and the ratio stays within reach of zlib's (fewer match candidates
+    than zlib's hash chains: 6.2 vs 8.4 on cfg3, 1.19 vs 1.20 on cfg5)."""
+    for (b, c), E, bits, lo in ((workloads.cfg5_host(1 << 19, seed=5), 1e-4, 12, 0.97),
+                                (tuple(workloads.cfg3_host(shape=(4, 240, 480), steps=2, seed=3)[:2]), 5e-3, 10, 0.6)):
+        enc = engine.encode(torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda(), E, bits, 1 << 16)
+        lens = enc.block_lengths()
+        gpu = codec.gpu_deflate_blocks(enc.packed, enc.stride, lens)
+        packed = enc.packed.cpu().numpy()
+        tot_gpu = tot_zlib = 0
+        for i, (g, ln) in enumerate(zip(gpu, lens)):
+            raw = packed[i * enc.stride: i * enc.stride + int(ln)].tobytes()
+            assert _inflate(g) == raw
+            tot_gpu += len(g)
+            tot_zlib += len(codec.compress_block(raw))
+        assert tot_zlib > lo * tot_gpu, (bits, tot_gpu, tot_zlib)
+
+
 def _patterns(rng, n):
     yield rng.integers(0, 256, n, dtype=np.uint8).tobytes()                      # incompressible
     yield bytes(n)                                                                # one long run
@@ -57,7 +76,9 @@ def test_streams_inflate_exactly(seg, n, last):
 
 
 def test_compression_of_real_index_streams():
-    """cfg2 packed stream: inflates exactly and compresses within 2x of zlib."""
+    """cfg2 packed stream: inflates exactly and compresses about as well as
+    zlib level 6 (the cost-aware parse: ratio 6.21 vs 6.20 on the 512^3 stream,
+    10.6 vs 11.9 on this 256^3 one, whose longer repeats favour zlib's chains)."""
     base, cur = workloads.cfg2_device(256, seed=0)
     enc = engine.encode(base, cur, 1e-3, 8)
     lens = enc.block_lengths()
@@ -69,7 +90,7 @@ def test_compression_of_real_index_streams():
         assert _inflate(g) == raw
         tot_gpu += len(g)
         tot_zlib += len(codec.compress_block(raw))
-    assert tot_gpu < 2.0 * tot_zlib, (tot_gpu, tot_zlib)
+    assert tot_gpu < 1.2 * tot_zlib, (tot_gpu, tot_zlib)
     assert tot_gpu < 0.25 * int(sum(lens))
 
 
