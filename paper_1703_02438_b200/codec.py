@@ -160,14 +160,17 @@ _INFLATE_ERRORS = {
 }
 
 
-def gpu_inflate_blocks(blobs, out_stride: int, device=None, slots=None, nslots: int | None = None):
+def gpu_inflate_blocks(blobs, out_stride: int, device=None, slots=None, nslots: int | None = None,
+                       defer: bool = False):
     """Inflate raw DEFLATE streams on the GPU (k_inflate.cu), the decode half
     of the lossless stage (codec.py:119-128): stream i lands at
     ``out[j*out_stride : j*out_stride + produced[i]]`` of the returned device
     buffer, j = slots[i] (default i) of ``nslots`` slots -- the strided
     packed-block layout K5 reads.  Returns ``(out, produced)``; a stream that
     zlib would reject raises CodecError (truncated or trailing bytes with the
-    reference's message)."""
+    reference's message).  ``defer=True`` returns a function that waits for
+    the kernel and yields that pair, so the caller can do host work (e.g. the
+    upload of the base snapshot) while the streams inflate."""
     import torch
     N.require_cuda()
     blobs = [bytes(b) for b in blobs]
@@ -176,7 +179,8 @@ def gpu_inflate_blocks(blobs, out_stride: int, device=None, slots=None, nslots: 
     total_slots = nslots if nslots is not None else nb
     out = torch.zeros(max(total_slots * out_stride, 1), dtype=torch.uint8, device=dev)
     if nb == 0:
-        return out, np.zeros(0, dtype=np.int64)
+        res = (out, np.zeros(0, dtype=np.int64))
+        return (lambda: res) if defer else res
     d_slot = None
     if slots is not None:
         d_slot = torch.from_numpy(np.asarray(slots, dtype=np.int64) * out_stride).to(dev)
@@ -190,11 +194,15 @@ def gpu_inflate_blocks(blobs, out_stride: int, device=None, slots=None, nslots: 
     N.check(N.lib().nmk_inflate(d_comp.data_ptr(), d_off.data_ptr(), nb, out.data_ptr(), out_stride,
                                 d_slot.data_ptr() if d_slot is not None else None, status.data_ptr(),
                                 produced.data_ptr(), torch.cuda.current_stream().cuda_stream))
-    st = status.cpu().numpy()
-    bad = np.flatnonzero(st)
-    if bad.size:
-        raise CodecError(_INFLATE_ERRORS.get(int(st[bad[0]]), "inflate failed"))
-    return out, produced.cpu().numpy()
+    def finish():
+        st = status.cpu().numpy()
+        bad = np.flatnonzero(st)
+        if bad.size:
+            raise CodecError(_INFLATE_ERRORS.get(int(st[bad[0]]), "inflate failed"))
+        _ = d_comp, d_off, d_slot   # inputs stay alive until the kernel is done
+        return out, produced.cpu().numpy()
+
+    return finish if defer else finish()
 
 
 def gpu_decompress_block(data: bytes, capacity: int | None = None) -> bytes:
@@ -229,23 +237,31 @@ def _block_bytes_of(variable, ordinal: int) -> bytes:
     return variable.index_table[lo:hi]
 
 
-def _inflate_covering(compressed, first, bits, epb, n):
+def _inflate_covering(compressed, first, bits, epb, n, defer: bool = False):
     """The covering blocks' DEFLATE streams inflated on the GPU straight into
     the strided packed layout K5 reads (k_inflate.cu): only compressed bytes
     cross PCIe.  A block that inflates to fewer bytes than its element count
-    needs fails as unpack_block would (codec.py:97-99)."""
+    needs fails as unpack_block would (codec.py:97-99).  ``defer=True``: the
+    kernel is launched and a function returning the buffer (after the checks)
+    comes back."""
     from . import engine
     stride = engine.block_stride(epb, bits)
-    d_packed, produced = gpu_inflate_blocks(compressed, stride)
-    for i in range(len(compressed)):
-        s, e = (first + i) * epb, min((first + i + 1) * epb, n)
-        need_b = packed_size(e - s, bits)
-        if int(produced[i]) < need_b:
-            raise CodecError(f"short buffer: {int(produced[i])} bytes, need {need_b}")
-    return d_packed
+    pending = gpu_inflate_blocks(compressed, stride, defer=True)
+
+    def finish():
+        d_packed, produced = pending()
+        for i in range(len(compressed)):
+            s, e = (first + i) * epb, min((first + i + 1) * epb, n)
+            need_b = packed_size(e - s, bits)
+            if int(produced[i]) < need_b:
+                raise CodecError(f"short buffer: {int(produced[i])} bytes, need {need_b}")
+        return d_packed
+
+    return finish if defer else finish()
 
 
-def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_offset, start, count, base):
+def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_offset, start, count, base,
+                       d_base=None):
     """Decode [start, start+count) of the covering block ordinals first..last
     on the GPU.  ``blocks``: the blocks' packed bytes (a list of host byte
     strings) or a device buffer already in the strided layout
@@ -278,12 +294,13 @@ def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_off
     base_inc = int(pre[0])
     d_prefix_rel = torch.from_numpy(pre - base_inc).to(dev)
     d_centers = torch.tensor(np.asarray(centers64, dtype=np.float64), device=dev)   # copies (read-only ok)
-    ex = np.array(exact[max(base_inc - exact_offset, 0):], copy=True)   # covering blocks only
+    from . import staging
+    ex = np.asarray(exact)[max(base_inc - exact_offset, 0):]   # covering blocks only
     if base_inc < exact_offset:
         raise ValueError("exact values start after the covering block")
-    d_exact = torch.from_numpy(ex).to(dev) if ex.size else torch.empty(0, dtype=_tdt(base.dtype), device=dev)
-    from . import staging
-    d_base = staging.h2d(np.asarray(base), dev)
+    d_exact = staging.h2d(ex, dev) if ex.size else torch.empty(0, dtype=_tdt(base.dtype), device=dev)
+    if d_base is None:
+        d_base = staging.h2d(np.asarray(base), dev)
     res = engine.decode(d_packed, stride, first, bits, epb, n, d_prefix_rel, d_centers, d_exact, d_base,
                         [(start, count, 0)])
     need = int(res.n_sentinel[0])
@@ -295,6 +312,18 @@ def _gpu_decode_blocks(blocks, bits, epb, n, prefix, centers64, exact, exact_off
 def _tdt(np_dtype):
     import torch
     return torch.float64 if np.dtype(np_dtype).itemsize == 8 else torch.float32
+
+
+_side_streams: dict = {}
+
+
+def _upload_stream():
+    """A per-device side stream for uploads that overlap a kernel on the current stream."""
+    import torch
+    dev = torch.cuda.current_device()
+    if dev not in _side_streams:
+        _side_streams[dev] = torch.cuda.Stream()
+    return _side_streams[dev]
 
 
 def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> np.ndarray:
@@ -310,8 +339,19 @@ def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> n
     epb = variable.elements_per_block
     first = start // epb
     last = (start + count - 1) // epb
-    blocks = _inflate_covering([block_bytes(b) for b in range(first, last + 1)], first, variable.bits, epb,
-                               variable.n)
+    from . import staging
+    inflating = _inflate_covering([block_bytes(b) for b in range(first, last + 1)], first, variable.bits, epb,
+                                  variable.n, defer=True)
+    import torch
+    cur_stream = torch.cuda.current_stream()
+    side = _upload_stream()
+    with torch.cuda.stream(side):  # the host fills and the DMA run while the streams inflate
+        d_base = staging.h2d(base)
+        uploaded = torch.cuda.Event()
+        uploaded.record(side)
+    d_base.record_stream(cur_stream)
+    blocks = inflating()
+    cur_stream.wait_event(uploaded)
     inc_lo = int(variable.incompressible_prefix[first])
     exact, exact_offset = inc_slice_all(inc_lo)
     exact = np.asarray(exact)
@@ -320,7 +360,7 @@ def _decode_range(variable, start, count, base, block_bytes, inc_slice_all) -> n
     centers = variable.centers.astype(np.float64, copy=False)
     out, need, have, bad, maxbad = _gpu_decode_blocks(
         blocks, variable.bits, epb, variable.n, variable.incompressible_prefix, centers, exact,
-        exact_offset, start, count, base)
+        exact_offset, start, count, base, d_base=d_base)
     if bad:
         raise ValueError(f"index {maxbad} out of range for {len(centers)} centers")
     if have < need:

@@ -67,6 +67,16 @@ res["cfg2_compress_pair"] = {"wall_s": t_c, "gbs_wall": n * L / t_c / 1e9, "hot_
                              "phases": {p: getattr(tm, p) for p in tm.PHASES}}
 res["cfg2_decompress"] = {"wall_s": t_d, "gbs_wall": n * L / t_d / 1e9,
                           "note": "GPU inflate + K5 + H2D of compressed bytes, base and exact values + D2H"}
+# the whole compressor on the GPU: PipelineConfig(deflate="gpu") (valid DEFLATE, not zlib's bytes)
+cfg_g = nmk.PipelineConfig(tolerance=1e-3, bits=8, workers=16, deflate="gpu")
+nmk.compress_pair(pair, cfg_g)
+t_cg, (var_g, tm_g) = wall(lambda: nmk.compress_pair(pair, cfg_g))
+t_dg, out_g = wall(lambda: nmk.decompress(var_g, base))
+assert out_g.tobytes() == out.tobytes()
+res["cfg2_compress_pair_gpu_deflate"] = {"wall_s": t_cg, "gbs_wall": n * L / t_cg / 1e9, "lossless_s": tm_g.zlib,
+                                         "index_table_bytes": len(var_g.index_table),
+                                         "index_table_bytes_zlib": len(var.index_table),
+                                         "decompress_wall_s": t_dg}
 # ---- lossless stage alone ----------------------------------------------------
 blobs = [codec._block_bytes_of(var, b) for b in range(var.nblocks)]
 stride = engine.block_stride(var.elements_per_block, var.bits)
