@@ -53,13 +53,13 @@ NOMINAL_HBM_GBS = 8000.0
 CFG4_STRONG_N = 4_000_000_000
 # kernels per compress + decompress step of the sync-free pipeline:
 # k_minmax (the span decision and histogram clear fused in on one rank),
-# k_hist_dev, k_select, k_encode_keyed, k_chunk_scan, k_enc_finalize |
-# k_dec_count(_wide), k_chunk_scan, k_dec_chunks: 9.  More when a hint from the
+# k_hist_dev, k_select, k_encode_keyed, k_enc_finalize (chunk scan inside) |
+# k_dec_count(_wide), k_chunk_scan, k_dec_chunks: 8.  More when a hint from the
 # warm-up check is missing: + k_hist_prep with a communicator, + k_encode (the
 # snapshot-reading fallback, exits when the keyed kernel did the work), + the
 # second k_dec_chunks ring depth (exits at entry).
 def gpu_launches_per_step(pipe):
-    return 9 + (pipe.comm is not None) + (not pipe.keyed_hint) + (pipe.ring_hint == 0)
+    return 8 + (pipe.comm is not None) + (not pipe.keyed_hint) + (pipe.ring_hint == 0)
 
 
 WORKLOADS = {

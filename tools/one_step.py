@@ -1,7 +1,7 @@
 """One sync-free compress + decompress step on a named workload (for ncu).
     python tools/one_step.py cfg4w|cfg5|cfg2|cfg3 [n_log2] [E] [B]
-The first step launches every kernel (11); the second one runs with the
-check() hints (9 launches): ncu -s 11 -c 9 captures it."""
+The first step launches every kernel (10); the second one runs with the
+check() hints (8 launches): ncu -s 10 -c 8 captures it."""
 import sys
 
 import torch
