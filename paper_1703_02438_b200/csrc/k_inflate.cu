@@ -25,6 +25,10 @@
 
 namespace nmk {
 
+#ifndef NMK_INF_LITRUN
+#define NMK_INF_LITRUN 0   // A/B: a check-free four-lookup literal run helps literal-heavy streams (the GPU deflate's:
+                           // 48.4 -> 46.6 ms) but its repeated lookup at every match costs zlib's 40.5 -> 53.6 ms
+#endif
 constexpr int kInfWarps = 1;          // streams per CTA (one per SM for a block's worth of streams)
 constexpr uint32_t kWin = 32768;      // DEFLATE's window: the last 32 KB of output, in shared memory
 constexpr uint64_t kFlush = 1024;     // window -> global store granularity
@@ -323,6 +327,28 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
     }
     // symbols: up to four literals per table lookup
     while (true) {
+#if NMK_INF_LITRUN
+      // literal run: four table lookups per refill (4 x kMBits <= the 57 bits a
+      // refill guarantees) with no per-lookup capacity / refill / flush checks;
+      // the first entry that is not a literal group leaves it to the general step
+      if (pos + 16 <= cap) {
+        if (br.cnt < 4 * kMBits) br.refill();
+        bool run = true;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint2 e = st.mlut[br.buf & (kMLut - 1)];
+          const uint32_t nl = e.y & 15u;
+          if (!nl) { run = false; break; }
+          const uint32_t used = e.y >> 4;
+          br.buf >>= used;
+          br.cnt -= (int)used;
+          if ((uint32_t)lane < nl) win[(uint32_t)(pos + lane) & (kWin - 1)] = (uint8_t)(e.x >> (8 * lane));
+          pos += nl;
+        }
+        if (pos - flushed >= kFlush) flush(pos);
+        if (run) continue;
+      }
+#endif
       if (br.cnt < kMBits) br.refill();
       const uint2 me = st.mlut[br.buf & (kMLut - 1)];
       int sym;

@@ -117,6 +117,15 @@ __device__ __forceinline__ MinMax mm_merge(MinMax a, const MinMax& b) {
   return a;
 }
 
+#ifndef NMK_MM_LDCS
+#define NMK_MM_LDCS 0   // A/B: evict-first snapshot loads (to keep K1's keys in L2 for K2) cost K1 0.439 -> 0.450 ms on cfg2
+#endif
+#if NMK_MM_LDCS
+#define MM_LD(p) __ldcs(p)
+#else
+#define MM_LD(p) __ldg(p)
+#endif
+
 template <int VN>
 __device__ __forceinline__ void store_keys(float* p, const float (&kv)[VN]) {
   if constexpr (VN == 2) *reinterpret_cast<float2*>(p) = make_float2(kv[0], kv[1]);
@@ -175,8 +184,8 @@ k_minmax(const T* __restrict__ base, const T* __restrict__ cur, uint64_t n,
       V b[U], c[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        b[u] = __ldg(bv + i + u * nthr);
-        c[u] = __ldg(cv + i + u * nthr);
+        b[u] = MM_LD(bv + i + u * nthr);
+        c[u] = MM_LD(cv + i + u * nthr);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {

@@ -7,7 +7,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
     --log-file gpurun_out/r2_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/ncu_launch.log 2>&1
 # 2. full capture of one eager step (the second of tools/one_step.py's two steps)
-ncu --set full --clock-control none --import-source on -k regex:"k_" -s 10 -c 8 -o /tmp/r2_cfg2 \
+ncu -f --set full --clock-control none --import-source on -k regex:"k_" -s 10 -c 8 -o /tmp/r2_cfg2 \
     python tools/one_step.py cfg2 > gpurun_out/ncu_full.log 2>&1
 python tools/ncu_kernels.py /tmp/r2_cfg2.ncu-rep > gpurun_out/r2_ncu_full_kernels.txt
 python tools/ncu_traffic.py /tmp/r2_cfg2.ncu-rep "ncu --set full --clock-control none --import-source on -k regex:k_ -s 10 -c 8 python tools/one_step.py cfg2 (round 2, cfg2 512^3 f64, B=8)" > gpurun_out/r2_ncu_traffic.json
