@@ -516,6 +516,7 @@ class SeriesStreamCompressor:
         self.torch_dtype = torch.float64 if np.dtype(dtype).itemsize == 8 else torch.float32
         self.np_dtype = np.dtype("<f8") if self.torch_dtype == torch.float64 else np.dtype("<f4")
         self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self.s_x = torch.cuda.Stream()   # exact-value readback: must not queue behind the next step's D2H
         self.recon = [torch.empty(self.n, dtype=self.torch_dtype, device="cuda") for _ in range(2)]
         self.ev_recon = torch.cuda.Event()
         self.slots = []
@@ -535,10 +536,15 @@ class SeriesStreamCompressor:
         self.count = 0
 
     def start(self, first) -> None:
+        """Begin a chain at snapshot ``first`` (collect the previous chain's
+        results first).  No host synchronisation for a pinned ``first``: the
+        upload is ordered behind the previous chain's kernels and in front of
+        the next step's on the device."""
         import torch
-        with torch.cuda.stream(self.s_cmp):
+        self.s_h2d.wait_stream(self.s_cmp)       # recon[0] may still be read by the last step
+        with torch.cuda.stream(self.s_h2d):
             self.recon[0].copy_(torch.as_tensor(first), non_blocking=True)
-        self.s_cmp.synchronize()
+        self.s_cmp.wait_stream(self.s_h2d)
         self.count = 0
 
     def submit(self, cur) -> int:
@@ -587,9 +593,10 @@ class SeriesStreamCompressor:
         if n_inc > sl["h_exact"].numel():
             sl["h_exact"] = torch.empty(n_inc, dtype=self.torch_dtype, pin_memory=True)
         if n_inc:
-            with torch.cuda.stream(self.s_d2h):
+            # own stream: s_d2h already holds the next step's copies, which wait for its kernels
+            with torch.cuda.stream(self.s_x):
                 sl["h_exact"][:n_inc].copy_(p.exact[:n_inc], non_blocking=True)
-            self.s_d2h.synchronize()
+            self.s_x.synchronize()
         self.last_d2h_bytes = (p.packed.numel() + n_inc * self.np_dtype.itemsize + p.prefix.numel() * 8
                                + sl["h_scal"].numel() * 8 + p.k_cap * self.np_dtype.itemsize)
         k = int(model.k)

@@ -81,3 +81,24 @@ def test_stream_compressor_falls_back_for_wide_spans():
     o = O.encode(b, c, 1e-3, 4, 1 << 12)
     assert _blocks(h) == o["blocks"] and h.exact.tobytes() == o["exact"].tobytes()
     assert rec.tobytes() == O.decode(o, b).tobytes()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.uint8])
+def test_staging_round_trip_sizes(dtype):
+    """staging.h2d / d2h (threaded fills of two pinned chunks overlapped with
+    their DMA): empty, tiny, chunk-boundary and multi-chunk arrays, contiguous
+    or not, arrive and return bit for bit."""
+    from paper_1703_02438_b200 import staging
+    rng = np.random.default_rng(5)
+    item = np.dtype(dtype).itemsize
+    per_chunk = staging.CHUNK_BYTES // item
+    for n in (0, 1, 1000, per_chunk - 1, per_chunk, per_chunk + 1, 2 * per_chunk + 3):
+        a = rng.integers(0, 255, n * item, dtype=np.uint8).view(dtype)
+        t = staging.h2d(a)
+        assert t.numel() == n and tuple(t.shape) == (n,)
+        assert t.cpu().numpy().tobytes() == a.tobytes()
+        back = staging.d2h(t)
+        assert back.dtype == np.dtype(dtype) and back.tobytes() == a.tobytes()
+    strided = rng.normal(size=(1000, 6))[:, ::2].astype(np.float64)   # non-contiguous input is copied first
+    t = staging.h2d(strided)
+    assert t.cpu().numpy().tobytes() == np.ascontiguousarray(strided).tobytes()

@@ -208,3 +208,16 @@ def test_ref_dropin_plugin_binds_every_entry_point():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == "19"
+
+
+def test_deflate_segment_size_rule():
+    """The GPU deflate stage takes the largest segment that still leaves one
+    warp's worth of work for >= 2048 warps (codec.deflate_segment_bytes)."""
+    from paper_1703_02438_b200 import codec
+    assert codec.deflate_segment_bytes(128 << 20) == 65520
+    assert codec.deflate_segment_bytes(64 << 20 | 1) == 32768
+    assert codec.deflate_segment_bytes(39 << 20) == 16384
+    assert codec.deflate_segment_bytes(1) == 16384
+    for total in (1, 1 << 20, 1 << 27, 1 << 33):
+        seg = codec.deflate_segment_bytes(total)
+        assert seg % 16 == 0 and 64 <= seg <= 65535
