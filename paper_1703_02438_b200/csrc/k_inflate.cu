@@ -68,12 +68,31 @@ struct InfState {
 };
 
 // bit reader (identical in every lane)
+#ifndef NMK_INF_LOOKAHEAD
+#define NMK_INF_LOOKAHEAD 0   // A/B: input words held two ahead in registers (a refill never waits for its own
+                              // load) changes nothing: 40.5 -> 41.7 ms on cfg2's zlib streams -- the refill's loads
+                              // hit L1; the decode is bound by its dependent ALU / shared-memory chain
+#endif
 struct Bits {
   const uint8_t* p;
   uint64_t len, pos;      // input bytes, next byte to load
   uint64_t buf;
   int cnt;
-  // to >= 57 bits: the next 8 input bytes from two aligned 8-byte loads (the
+#if NMK_INF_LOOKAHEAD
+  // the aligned 8-byte input words at wp, wp + 1, wp + 2 (wp: the word holding
+  // byte `pos` at the last refill); loads never pass wlast (the buffer's pad)
+  const uint64_t* wp;
+  const uint64_t* wlast;
+  uint64_t w0, w1, w2;
+  __device__ __forceinline__ uint64_t ldw(const uint64_t* w) const { return __ldg(w < wlast ? w : wlast); }
+  __device__ __forceinline__ void seek() {   // (re)load the window at pos
+    wp = reinterpret_cast<const uint64_t*>((reinterpret_cast<uintptr_t>(p) + pos) & ~(uintptr_t)7);
+    w0 = ldw(wp);
+    w1 = ldw(wp + 1);
+    w2 = ldw(wp + 2);
+  }
+#endif
+  // to >= 57 bits: the next 8 input bytes from two aligned 8-byte words (the
   // input buffer is padded by 16 bytes on both sides), bytes at or past the
   // stream's end read as zero
   __device__ __forceinline__ void refill() {
@@ -81,7 +100,17 @@ struct Bits {
     const uintptr_t a = reinterpret_cast<uintptr_t>(p) + pos;
     const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~(uintptr_t)7);
     const int sh = (int)(a & 7) * 8;
+#if NMK_INF_LOOKAHEAD
+    if (w != wp) {   // pos advances <= 8 bytes per refill: at most one word further
+      w0 = w1;
+      w1 = w2;
+      wp = w;
+      w2 = ldw(w + 2);   // needed two words (>= 8 bytes of input) from now
+    }
+    const uint64_t lo = w0, hi = w1;
+#else
     const uint64_t lo = __ldg(w), hi = __ldg(w + 1);
+#endif
     uint64_t v = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
     const uint64_t left = pos < len ? len - pos : 0;
     const int keep = (int)(left < (uint64_t)nb ? left : (uint64_t)nb);   // bytes of real input
@@ -238,6 +267,12 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
   br.pos = 0;
   br.buf = 0;
   br.cnt = 0;
+#if NMK_INF_LOOKAHEAD
+  // the last whole 8-byte word inside the input's 16-byte tail pad
+  br.wlast = reinterpret_cast<const uint64_t*>(
+      (reinterpret_cast<uintptr_t>(comp) + comp_off[nstreams] + 8) & ~(uintptr_t)7);
+  br.seek();
+#endif
   uint8_t* dst = out + (out_off ? out_off[s] : s * out_stride);
   uint8_t* win = swin + (size_t)w * kWin;
   // output leaves through the window: every kFlush bytes the warp stores the
@@ -277,6 +312,9 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
       br.pos = in0 + ln;
       br.buf = 0;
       br.cnt = 0;
+#if NMK_INF_LOOKAHEAD
+      br.seek();
+#endif
       __syncwarp();
       continue;
     }
