@@ -25,13 +25,17 @@
 
 namespace nmk {
 
+#ifndef NMK_INF_POS32
+#define NMK_INF_POS32 1   // output positions in 32 bits (out_stride < 4 GiB - 64 KiB, checked by nmk_inflate): A/B on
+                          // cfg2's 128 blocks 40.5 -> 39.4 ms (zlib streams), 48.4 -> 46.9 ms (GPU deflate's)
+#endif
 #ifndef NMK_INF_LITRUN
 #define NMK_INF_LITRUN 0   // A/B: a check-free four-lookup literal run helps literal-heavy streams (the GPU deflate's:
                            // 48.4 -> 46.6 ms) but its repeated lookup at every match costs zlib's 40.5 -> 53.6 ms
 #endif
 constexpr int kInfWarps = 1;          // streams per CTA (one per SM for a block's worth of streams)
 constexpr uint32_t kWin = 32768;      // DEFLATE's window: the last 32 KB of output, in shared memory
-constexpr uint64_t kFlush = 1024;     // window -> global store granularity
+constexpr uint32_t kFlush = 1024;     // window -> global store granularity
 constexpr int kLutBits = 12;   // 8 KB tables: zlib's distance codes mostly fit
 constexpr int kLut = 1 << kLutBits;
 
@@ -278,16 +282,21 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
   // output leaves through the window: every kFlush bytes the warp stores the
   // finished 128-byte pieces with coalesced 4-byte stores (dst and flushed
   // stay 16-byte aligned)
-  uint64_t flushed = 0;
-  auto flush = [&](uint64_t upto) {
+#if NMK_INF_POS32
+  typedef uint32_t pos_t;
+#else
+  typedef uint64_t pos_t;
+#endif
+  pos_t flushed = 0;
+  auto flush = [&](pos_t upto) {
     __syncwarp();
     for (; flushed + 128 <= upto; flushed += 128) {
       const uint32_t o = (uint32_t)(flushed + 4 * lane) & (kWin - 1);
       *reinterpret_cast<uint32_t*>(dst + flushed + 4 * lane) = *reinterpret_cast<const uint32_t*>(win + o);
     }
   };
-  const uint64_t cap = out_stride;
-  uint64_t pos = 0;
+  const pos_t cap = (pos_t)out_stride;
+  pos_t pos = 0;
   unsigned err = kInfOk;
   bool final_seen = false;
   while (!err && !final_seen) {
@@ -446,7 +455,7 @@ k_inflate(const uint8_t* __restrict__ comp, const unsigned long long* __restrict
   }
   if (!err) {   // the unflushed tail (< 128 bytes)
     __syncwarp();
-    for (uint64_t j = flushed + lane; j < pos; j += 32) dst[j] = win[(uint32_t)j & (kWin - 1)];
+    for (pos_t j = flushed + lane; j < pos; j += 32) dst[j] = win[(uint32_t)j & (kWin - 1)];
   }
   if (!err) {
     // bytes consumed = ceil(bits / 8); anything after them is trailing data
@@ -470,6 +479,7 @@ extern "C" int nmk_inflate(const uint8_t* comp, const unsigned long long* comp_o
   if (nstreams == 0) return NMK_OK;
   if (!comp || !comp_off || !out || !status || !produced || out_stride == 0)
     return set_error(NMK_ERR_ARG, "nmk_inflate: bad argument");
+  if (out_stride >= (1ULL << 32) - 65536) return set_error(NMK_ERR_ARG, "nmk_inflate: out_stride must be below 4 GiB");
   const uint64_t grid = (nstreams + kInfWarps - 1) / kInfWarps;
   constexpr size_t smem = (sizeof(InfState) + kWin) * kInfWarps;
   ensure_dyn_smem(k_inflate, smem);
