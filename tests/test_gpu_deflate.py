@@ -119,3 +119,33 @@ def test_pipeline_gpu_deflate_round_trip(tmp_path, dtype):
 def test_config_rejects_unknown_engine():
     with pytest.raises(ValueError):
         pipeline.PipelineConfig(deflate="cpu")
+
+
+def test_deflate_adversarial_patterns():
+    """Warp-per-segment deflate on inputs that stress its parse: every period
+    2..40, runs that cross step and segment edges, far repeats (up to the
+    32 KiB window and beyond the segment), tiny and ragged segments."""
+    rng = np.random.default_rng(77)
+    cases = []
+    for period in list(range(2, 41)) + [63, 64, 65, 257, 258, 259, 4095, 4096, 4097]:
+        unit = rng.integers(0, 256, period, dtype=np.uint8)
+        x = np.tile(unit, 40_000 // period + 1)[:40_000].copy()
+        x[rng.choice(x.size, 200, replace=False)] ^= 0x5a          # sparse deviations
+        cases.append(x.tobytes())
+    blockrep = rng.integers(0, 256, 3000, dtype=np.uint8)
+    cases.append(np.concatenate([blockrep, rng.integers(0, 256, 29_000, dtype=np.uint8), blockrep,
+                                 rng.integers(0, 4, 20_000, dtype=np.uint8), blockrep]).tobytes())
+    cases.append(bytes([255]) * 70_001)
+    cases.append(bytes(range(256)) * 300)
+    for data in cases:
+        for seg in (64, 4096, 16384, 65520):
+            n = len(data)
+            stride = (n + 15) // 16 * 16
+            out = codec.gpu_deflate_blocks(_blocks_on_device([data], stride), stride, [n], seg)
+            assert _inflate(out[0]) == data, (n, seg)
+    for n in (1, 2, 3, 4, 5, 31, 32, 33, 63, 64, 65, 257, 258, 259, 260):   # shorter than a match, a step, a probe
+        data = bytes((7 * i) % 3 for i in range(n))
+        stride = (n + 15) // 16 * 16
+        for seg in (64, 128):
+            out = codec.gpu_deflate_blocks(_blocks_on_device([data] * 2, stride), stride, [n, n], seg)
+            assert [_inflate(o) for o in out] == [data, data], (n, seg)

@@ -242,3 +242,54 @@ def test_minmax_prep_clears_wide_histograms(dtype):
     o = O.encode(b, c, E, 8, 1 << 15)
     assert _host_blocks(pipe.encoding()) == o["blocks"]
     assert out.cpu().numpy().tobytes() == O.decode(o, b).tobytes()
+
+
+@pytest.mark.parametrize("nchunks", [1, 2, 511, 512, 513, 1024, 1025, 2049])
+@pytest.mark.parametrize("tail", [-1, 0, 1])
+def test_finalize_tile_boundaries(nchunks, tail):
+    """k_enc_finalize takes tiles of 512 chunks with a look-back across tiles:
+    element counts around every tile edge, with a few incompressible values in
+    every chunk, against the oracle."""
+    n = nchunks * 256 + tail
+    if n <= 0:
+        pytest.skip("empty")
+    rng = np.random.default_rng(1000 + nchunks)
+    b = rng.uniform(0.5, 2.0, n)
+    c = b * (1.0 + rng.normal(0.0, 2e-3, n))
+    wild = rng.uniform(size=n) < 0.01          # ~2.5 exact values per chunk
+    c[wild] = b[wild] * rng.uniform(2.0, 3.0, int(wild.sum()))
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(n, base.dtype, 1e-3, 6, 4096 * 3)   # blocks of 16384 elements: 64 chunks each
+    chk, blocks, exact, prefix, out = _pipeline_bytes(pipe, base, cur)
+    o = O.encode(b, c, 1e-3, 6, 4096 * 3)
+    assert chk["n_inc"] == o["n_inc"] and blocks == o["blocks"]
+    assert exact == o["exact"].tobytes() and prefix == o["prefix"].tobytes()
+    assert out == O.decode(o, b).tobytes()
+
+
+@pytest.mark.parametrize("nbins_target", [65535, 65536, 65537, 65538, 131075])
+def test_minmax_prep_span_boundaries(nbins_target):
+    """The fused span decision clears 65 537 histogram slots up front and the
+    rest in K1's last CTA: spans right at that edge, on a dirty buffer."""
+    E = 1e-3
+    n = 200_000
+    rng = np.random.default_rng(nbins_target)
+    b = np.ones(n)
+    r = rng.uniform(0.0, 1.0, n) * (nbins_target - 1) * 2 * E
+    r[0], r[1] = 0.0, (nbins_target - 0.5) * 2 * E          # gmin = 0, gmax inside the last bin
+    c = b * (1.0 + r)
+    base, cur = torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda()
+    pipe = engine.DevicePipeline(n, base.dtype, E, 8, 1 << 15)
+    pipe.counts.fill_(3)
+    out = torch.empty_like(base)
+    pipe.step(base, cur, out)
+    chk = pipe.check()
+    assert chk["status"] == 0 and chk["tripwire"] == 0
+    rr, v = O.ratios_of(b, c)
+    ordinals, counts = O.histogram(rr[v], float(rr[v].min()), 2 * E)
+    assert chk["nbins"] == int(ordinals.max()) + 1
+    dense = np.zeros(chk["nbins"], dtype=np.int64)
+    dense[np.asarray(ordinals, dtype=np.int64)] = counts
+    assert np.array_equal(pipe.counts[: chk["nbins"]].cpu().numpy(), dense)
+    o = O.encode(b, c, E, 8, 1 << 15)
+    assert _host_blocks(pipe.encoding()) == o["blocks"]
