@@ -15,7 +15,7 @@ from concurrent.futures import ThreadPoolExecutor, wait
 import numpy as np
 
 CHUNK_BYTES = 32 << 20
-SMALL_BYTES = 1 << 20          # below this a plain copy is as fast
+SMALL_BYTES = 16 << 20         # up to this one thread copies (<= 1.6 ms; no pool dispatch jitter on small ranges)
 _WORKERS = max(1, min(8, os.cpu_count() or 1))
 
 _executor = None
