@@ -415,8 +415,9 @@ def roofline_report(mean, ms_step, n, L, bits, alpha, nchunks, peak, peak_src, t
         # K2 reads the keys
         "K2_histogram": (4.0, 2 * L, "k_hist_dev"),
         # K4 reads the keys, writes the codes, gathers + writes the exact
-        # values, writes a 256-bit sentinel mask and 12 B of counts per chunk
-        "K4_encode": (4 + Bb + 2 * alpha * L + (32 + 12) * nchunks / n, 2 * L + Bb + alpha * L, "k_encode_keyed"),
+        # values, writes a 256-bit sentinel mask and a 4-byte count per chunk
+        # (read back once by the finalize kernel, which scans them in place)
+        "K4_encode": (4 + Bb + 2 * alpha * L + (32 + 8) * nchunks / n, 2 * L + Bb + alpha * L, "k_encode_keyed"),
         # K5 reads the codes twice (count pass + decode), base, exact; writes out
         "K5_decode": (2 * L + 2 * Bb + alpha * L, 2 * L + Bb + alpha * L, "k_dec_chunks"),
     }
