@@ -407,7 +407,7 @@ ASYNC_COMM_BINS = 1 << 16     # dense span all-reduced without a host round trip
 class DevicePipeline:
     """compress (K1..K4) + full decompress (K5) of one element range with no
     host synchronisation: the dense span, k, tol_bin and the exact-value count
-    are produced and consumed on the device (nmk_hist_prep / *_dev entry
+    are produced and consumed on the device (nmk_minmax_prep / *_dev entry
     points), all buffers are preallocated, so one step can be enqueued — or
     captured once in a CUDA graph and replayed.  ``check()`` reads the device
     scalars once and reports the rare cases that need the general path (span
