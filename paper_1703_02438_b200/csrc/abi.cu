@@ -57,12 +57,14 @@ int sm_count() {
   return sms[dev];
 }
 
-bool pdl_on() {
-  static const bool on = [] {
+unsigned pdl_mask() {
+  static const unsigned mask = [] {
     const char* e = getenv("NMK_PDL");
-    return e && e[0] == '1';
+    if (!e || !e[0]) return 0u;
+    if (e[0] == '0' && (e[1] == 'x' || e[1] == 'X')) return (unsigned)strtoul(e, nullptr, 16);
+    return e[0] == '1' ? 0xffffffffu : 0u;
   }();
-  return on;
+  return mask;
 }
 
 }  // namespace nmk

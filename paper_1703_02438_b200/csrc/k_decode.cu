@@ -881,7 +881,7 @@ static void launch_dec_chunks(const uint8_t* packed, const DecodeGeom& geo, cons
   uint64_t grid = (uint64_t)sms * per_sm;
   const uint64_t need = (geo.nitems + kTmaWarps - 1) / kTmaWarps;   // nitems: decode chunks
   if (grid > need) grid = need;
-  launch_chain(k_dec_chunks<T, B, S>, (unsigned)grid, kTmaThreads, smem, s, packed, geo, segs, sp, offsets, prefix_rel,
+  launch_chain(kPdlDecode, k_dec_chunks<T, B, S>, (unsigned)grid, kTmaThreads, smem, s, packed, geo, segs, sp, offsets, prefix_rel,
                centers, (const T*)exact, (const T*)base, (T*)out, info, err, model, n_exact_dev, regime);
 }
 
@@ -897,11 +897,11 @@ static void launch_decode(const uint8_t* packed, const DecodeGeom& geo, const Se
     const uint64_t per_cta = (uint64_t)(kDecThreads / 32) * 2 * kDecPairs;
     const uint64_t g1 = (geo.nchunks + per_cta - 1) / per_cta;
     const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * NMK_CNT_CTAS ? g1 : (uint64_t)sms * NMK_CNT_CTAS);
-    launch_chain(k_dec_count_wide<B>, grid1, kDecThreads, 0, s, packed, geo, counts);
+    launch_chain(kPdlCount, k_dec_count_wide<B>, grid1, kDecThreads, 0, s, packed, geo, counts);
   } else {
     const uint64_t g1 = (geo.nchunks + 7) / 8;
     const unsigned grid1 = (unsigned)(g1 < (uint64_t)sms * 8 ? g1 : (uint64_t)sms * 8);
-    launch_chain(k_dec_count<B>, grid1, kDecThreads, 0, s, packed, geo, counts);
+    launch_chain(kPdlCount, k_dec_count<B>, grid1, kDecThreads, 0, s, packed, geo, counts);
   }
   chunk_scan(counts, geo.nchunks, offsets, scan_ws, s, true);
   // The host knows the exact count on the host-scalar path and picks one ring.

@@ -387,10 +387,10 @@ static int nmk::encode_impl(const void* base, const void* cur, uint64_t n_local,
   unsigned long long* status = (unsigned long long*)(wb + w.off_scan);
   const unsigned grid = (unsigned)((et.nchunks + kFinTile - 1) / kFinTile);
   if (dtype == NMK_F64)
-    launch_chain(k_enc_finalize<double>, grid, kFinThreads, 0, s, geo, counts, status, (const double*)scratch,
+    launch_chain(kPdlFinalize, k_enc_finalize<double>, grid, kFinThreads, 0, s, geo, counts, status, (const double*)scratch,
                  (double*)exact, prefix, n_inc, (const double*)cur, keyed ? kxw.done : nullptr);
   else
-    launch_chain(k_enc_finalize<float>, grid, kFinThreads, 0, s, geo, counts, status, (const float*)scratch,
+    launch_chain(kPdlFinalize, k_enc_finalize<float>, grid, kFinThreads, 0, s, geo, counts, status, (const float*)scratch,
                  (float*)exact, prefix, n_inc, (const float*)cur, keyed ? kxw.done : nullptr);
   return check_launch("k_enc_finalize");
 }

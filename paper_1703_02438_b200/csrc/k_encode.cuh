@@ -1195,11 +1195,11 @@ static void launch_encode_k(const void* base, const void* cur, const EncodeGeom&
     if (per_sm_k < 1) per_sm_k = 1;
     uint64_t grid_k = (uint64_t)sm_count_e() * per_sm_k;
     if (grid_k > need) grid_k = need;
-    launch_chain(k_encode_keyed<T, B, kRecon>, (unsigned)grid_k, kEncThreads, smem_k, s, (const T*)base, (const T*)cur,
+    launch_chain(kPdlK4, k_encode_keyed<T, B, kRecon>, (unsigned)grid_k, kEncThreads, smem_k, s, (const T*)base, (const T*)cur,
                  geo, centers, cuts, tol, packed, (T*)scratch, counts, model, k_cap, (T*)recon, kx);
   }
   if (keyed && kx.only) return;   // hint: the keyed kernel applied last time (it still finishes alone if not)
-  launch_chain(k_encode<T, B, kRecon>, (unsigned)grid, kEncThreads, smem, s, (const T*)base, (const T*)cur, geo, centers,
+  launch_chain(kPdlK4Fallback, k_encode<T, B, kRecon>, (unsigned)grid, kEncThreads, smem, s, (const T*)base, (const T*)cur, geo, centers,
                cuts, k, tol_bin, tol, packed, (T*)scratch, counts, model, smem_ok, (T*)recon,
                keyed ? kx.done : nullptr);
 }

@@ -1239,7 +1239,7 @@ k_hist_dev(const T* __restrict__ base, const T* __restrict__ cur, const float* _
 extern "C" int nmk_hist_prep(nmk_stats* stats, double width, uint64_t cap_bins, unsigned long long* counts,
                              void* stream) {
   if (!stats || !counts || cap_bins == 0) return set_error(NMK_ERR_ARG, "nmk_hist_prep: bad argument");
-  launch_chain(k_hist_prep, sm_count_h() * 2, 256, 0, (cudaStream_t)stream, stats, width, cap_bins, counts);
+  launch_chain(kPdlPrep, k_hist_prep, sm_count_h() * 2, 256, 0, (cudaStream_t)stream, stats, width, cap_bins, counts);
   return check_launch("k_hist_prep");
 }
 
@@ -1259,10 +1259,10 @@ static void launch_hist_dev(const void* base, const void* cur, const float* keys
   uint64_t grid = (uint64_t)sm_count_h() * per_sm;
   if (want < grid) grid = want ? want : 1;
   if (dtype == NMK_F64)
-    launch_chain(k_hist_dev<double, kW>, (unsigned)grid, kT, smem, s, (const double*)base, (const double*)cur, keys, n,
+    launch_chain(kPdlK2, k_hist_dev<double, kW>, (unsigned)grid, kT, smem, s, (const double*)base, (const double*)cur, keys, n,
                  stats, width, counts, aligned);
   else
-    launch_chain(k_hist_dev<float, kW>, (unsigned)grid, kT, smem, s, (const float*)base, (const float*)cur, keys, n,
+    launch_chain(kPdlK2, k_hist_dev<float, kW>, (unsigned)grid, kT, smem, s, (const float*)base, (const float*)cur, keys, n,
                  stats, width, counts, aligned);
 }
 

@@ -341,10 +341,10 @@ static int minmax_impl(const void* base, const void* cur, uint64_t n, int dtype,
   // once and the kernel's last CTA resets it after every launch.
   bool aligned = (((uintptr_t)base | (uintptr_t)cur | (uintptr_t)keys) & 15) == 0;
   if (dtype == NMK_F64)
-    launch_chain(k_minmax<double>, grid, kMinmaxThreads, 0, s, (const double*)base, (const double*)cur, n, partials,
+    launch_chain(kPdlK1, k_minmax<double>, grid, kMinmaxThreads, 0, s, (const double*)base, (const double*)cur, n, partials,
                  ticket, stats, aligned, keys, hp);
   else if (dtype == NMK_F32)
-    launch_chain(k_minmax<float>, grid, kMinmaxThreads, 0, s, (const float*)base, (const float*)cur, n, partials,
+    launch_chain(kPdlK1, k_minmax<float>, grid, kMinmaxThreads, 0, s, (const float*)base, (const float*)cur, n, partials,
                  ticket, stats, aligned, keys, hp);
   else
     return set_error(NMK_ERR_ARG, "nmk_minmax: bad dtype %d", dtype);

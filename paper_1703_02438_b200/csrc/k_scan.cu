@@ -108,7 +108,7 @@ void chunk_scan(const uint32_t* counts, uint64_t n, unsigned long long* offsets,
   const uint64_t ntiles = chunk_scan_tiles(n);
   unsigned long long* status = reinterpret_cast<unsigned long long*>(ws);
   if (!status_zeroed) cudaMemsetAsync(status, 0, ntiles * 8, s);
-  launch_chain(k_chunk_scan, (unsigned)ntiles, kScanThreads, 0, s, counts, n, offsets, status);
+  launch_chain(kPdlScan, k_chunk_scan, (unsigned)ntiles, kScanThreads, 0, s, counts, n, offsets, status);
 }
 
 }  // namespace nmk

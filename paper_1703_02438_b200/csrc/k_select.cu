@@ -373,10 +373,10 @@ extern "C" int nmk_select(const unsigned long long* keys, const unsigned long lo
   ensure_dyn_smem(k_select<double, kNSel>, kSelCache * 8);
   ensure_dyn_smem(k_select<float, kNSel>, kSelCache * 8);
   if (dtype == NMK_F64)
-    launch_chain(k_select<double, kNSel>, 1, kSelThreads, smem, s, keys, counts, m_max, nruns, stats, width, tolerance,
+    launch_chain(kPdlK3, k_select<double, kNSel>, 1, kSelThreads, smem, s, keys, counts, m_max, nruns, stats, width, tolerance,
                  bits, n_total, centers, cuts, (double*)centers_t, cap_k, model, kAutoLo, kNSel, nullptr);
   else if (dtype == NMK_F32)
-    launch_chain(k_select<float, kNSel>, 1, kSelThreads, smem, s, keys, counts, m_max, nruns, stats, width, tolerance,
+    launch_chain(kPdlK3, k_select<float, kNSel>, 1, kSelThreads, smem, s, keys, counts, m_max, nruns, stats, width, tolerance,
                  bits, n_total, centers, cuts, (float*)centers_t, cap_k, model, kAutoLo, kNSel, nullptr);
   else
     return set_error(NMK_ERR_ARG, "nmk_select: bad dtype");

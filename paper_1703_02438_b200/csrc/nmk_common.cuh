@@ -337,12 +337,15 @@ template <typename F>
 inline void ensure_dyn_smem(F* func, size_t bytes) { ensure_dyn_smem(reinterpret_cast<const void*>(func), bytes); }
 // multiprocessor count of the current device (cached per device)
 int sm_count();
-// programmatic dependent launch of the chained kernels (env NMK_PDL=0 turns it off)
-bool pdl_on();
+// programmatic dependent launch of the chained kernels: env NMK_PDL = 1 (every
+// kernel), 0 / unset (none) or a hex mask 0x.. of chain ids (PdlId)
+unsigned pdl_mask();
+enum PdlId { kPdlK1 = 0, kPdlPrep, kPdlK2, kPdlK3, kPdlK4, kPdlK4Fallback, kPdlFinalize, kPdlCount, kPdlScan, kPdlDecode };
 // <<<grid, block, smem, s>>> with the programmatic-stream-serialization
 // attribute; the kernel must call pdl_enter() before touching global memory
 template <typename... KA, typename... A>
-inline void launch_chain(void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+inline void launch_chain(int id, void (*kernel)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                         A&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -350,7 +353,7 @@ inline void launch_chain(void (*kernel)(KA...), dim3 grid, dim3 block, size_t sm
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = (pdl_mask() >> id) & 1u;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, KA(args)...);
