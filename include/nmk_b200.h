@@ -332,6 +332,14 @@ int nmk_decode_dev2(const uint8_t* packed, uint64_t block_stride, uint64_t first
                     nmk_decode_err* err, int ring_hint, void* ws, size_t ws_bytes, void* stream);
 int nmk_decode_ring_for(uint64_t n_exact, uint64_t n_elems);
 
+/* -- 64-bit radix sort (k_sort.cu): the sort under nmk_hist_sparse / nmk_hist_merge
+ * (np.unique / the sorted merge of binning.py:110-132), exposed for tests.
+ * Stable, ascending; vals_in may be NULL (keys only); outputs must not alias inputs. */
+size_t nmk_sort64_ws_bytes(uint64_t n, int with_vals);
+int nmk_sort64(const unsigned long long* keys_in, unsigned long long* keys_out,
+               const unsigned long long* vals_in, unsigned long long* vals_out, uint64_t n,
+               void* ws, size_t ws_bytes, void* stream);
+
 /* -- standalone codec kernels (codec.py:83-105) ---------------------------- */
 int nmk_pack(const uint32_t* codes, uint64_t n, int bits, uint8_t* out, void* stream);
 int nmk_unpack(const uint8_t* packed, uint64_t n, int bits, uint32_t* codes, void* stream);

@@ -99,6 +99,8 @@ SIGNATURES = {
     "nmk_deflate_bound": (u64, [u64, u64, u32]),
     "nmk_deflate": (i32, [vp, u64, u64, u64, u64, u32, vp, vp, vp, sz, vp]),
     "nmk_inflate": (i32, [vp, vp, u64, vp, u64, vp, vp, vp, vp]),
+    "nmk_sort64_ws_bytes": (sz, [u64, i32]),
+    "nmk_sort64": (i32, [vp, vp, vp, vp, u64, vp, sz, vp]),
     "nmk_pack": (i32, [vp, u64, i32, vp, vp]),
     "nmk_unpack": (i32, [vp, u64, i32, vp, vp]),
 }

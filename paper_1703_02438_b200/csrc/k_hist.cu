@@ -14,12 +14,11 @@
 //           run-length encode.  Output = np.unique(ords, return_counts=True).
 #include <algorithm>
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "nmk_common.cuh"
+#include "nmk_sort.cuh"
 
 namespace nmk {
 
@@ -318,7 +317,7 @@ struct RleWs {
   unsigned long long* scal;       // 4 scalars
   unsigned long long* vals_b;     // n (merge only)
   unsigned long long* incl;       // n (merge only)
-  void* cub_tmp;
+  void* cub_tmp;      // scratch of the sort / prefix sums (k_sort.cu)
   size_t cub_bytes;
   size_t total;
 };
@@ -326,20 +325,10 @@ struct RleWs {
 static RleWs rle_layout(uint64_t n, bool with_vals, void* base) {
   RleWs w{};
   uint64_t nchunks = (n + kRleChunk - 1) / kRleChunk;
-  size_t sort_bytes = 0, scan_bytes = 0, scan2 = 0;
-  if (with_vals)
-    cub::DeviceRadixSort::SortPairs((void*)nullptr, sort_bytes, (const unsigned long long*)nullptr,
-                                    (unsigned long long*)nullptr, (const unsigned long long*)nullptr,
-                                    (unsigned long long*)nullptr, n);
-  else
-    cub::DeviceRadixSort::SortKeys((void*)nullptr, sort_bytes, (const unsigned long long*)nullptr,
-                                   (unsigned long long*)nullptr, n);
-  cub::DeviceScan::ExclusiveSum((void*)nullptr, scan_bytes, (unsigned long long*)nullptr,
-                                (unsigned long long*)nullptr, nchunks ? nchunks : 1);
-  if (with_vals)
-    cub::DeviceScan::InclusiveSum((void*)nullptr, scan2, (unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, n);
-  size_t cub_bytes = sort_bytes;
+  // scratch of the sort and of the two prefix sums (used one after the other)
+  size_t cub_bytes = sort64_ws_bytes(n, with_vals);
+  const size_t scan_bytes = scan64_ws_bytes(nchunks ? nchunks : 1);
+  const size_t scan2 = with_vals ? scan64_ws_bytes(n) : 0;
   if (scan_bytes > cub_bytes) cub_bytes = scan_bytes;
   if (scan2 > cub_bytes) cub_bytes = scan2;
   char* p = (char*)base;
@@ -367,18 +356,14 @@ static int rle_tail(RleWs& w, uint64_t n, bool with_vals, unsigned long long* ou
                     unsigned long long* out_counts, unsigned long long* nruns, cudaStream_t s) {
   uint64_t nchunks = (n + kRleChunk - 1) / kRleChunk;
   k_rle_count<<<(unsigned)nchunks, kRleThreads, 0, s>>>(w.keys_b, n, w.chunk);
-  size_t tb = w.cub_bytes;
-  cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.chunk, w.chunk_off, nchunks, s);
+  scan64(w.chunk, w.chunk_off, nchunks, false, w.cub_tmp, s);
   k_rle_scatter<<<(unsigned)nchunks, kRleThreads, 0, s>>>(w.keys_b, n, w.chunk_off, out_keys,
                                                          w.run_start, nruns, nchunks);
   k_set_u64<<<1, 1, 0, s>>>(w.scal, n);  // default end = n (no invalid key)
   unsigned grid = (unsigned)((n + 255) / 256);
   if (grid > (unsigned)sm_count_h() * 8) grid = sm_count_h() * 8;
   k_valid_end<<<grid, 256, 0, s>>>(w.keys_b, n, w.scal);
-  if (with_vals) {
-    tb = w.cub_bytes;
-    cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, w.vals_b, w.incl, n, s);
-  }
+  if (with_vals) scan64(w.vals_b, w.incl, n, true, w.cub_tmp, s);
   return 0;
 }
 
@@ -471,8 +456,7 @@ extern "C" int nmk_hist_sparse(const void* base, const void* cur, uint64_t n, in
   else
     k_hist_keys<float><<<(unsigned)grid, 256, 0, s>>>((const float*)base, (const float*)cur, n, stats, width,
                                                       w.keys_a, aligned);
-  size_t tb = w.cub_bytes;
-  cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keys_a, w.keys_b, n, 0, 64, s);
+  sort64(w.keys_a, w.keys_b, nullptr, nullptr, n, w.cub_tmp, s);
   rle_tail(w, n, false, keys, counts, nruns, s);
   unsigned g2 = (unsigned)((n + 255) / 256);
   if (g2 > (unsigned)sm_count_h() * 8) g2 = sm_count_h() * 8;
@@ -490,8 +474,7 @@ extern "C" int nmk_hist_merge(unsigned long long* keys, unsigned long long* coun
   if (!keys || !counts || !nruns || !ws) return set_error(NMK_ERR_ARG, "nmk_hist_merge: bad argument");
   RleWs w = rle_layout(n_in, true, ws);
   if (ws_bytes < w.total) return set_error(NMK_ERR_ARG, "nmk_hist_merge: workspace too small");
-  size_t tb = w.cub_bytes;
-  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, keys, w.keys_b, counts, w.vals_b, n_in, 0, 64, s);
+  sort64(keys, w.keys_b, counts, w.vals_b, n_in, w.cub_tmp, s);
   rle_tail(w, n_in, true, keys, counts, nruns, s);
   unsigned g2 = (unsigned)((n_in + 255) / 256);
   if (g2 > (unsigned)sm_count_h() * 8) g2 = sm_count_h() * 8;
@@ -516,8 +499,7 @@ extern "C" int nmk_hist_values(const double* ratios, const uint8_t* valid, uint6
   unsigned grid = (unsigned)((n + 255) / 256);
   if (grid > (unsigned)sm_count_h() * 8) grid = sm_count_h() * 8;
   k_ratio_keys<<<grid, 256, 0, s>>>(ratios, valid, n, origin, width, w.keys_a);
-  size_t tb = w.cub_bytes;
-  cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, w.keys_a, w.keys_b, n, 0, 64, s);
+  sort64(w.keys_a, w.keys_b, nullptr, nullptr, n, w.cub_tmp, s);
   unsigned long long* out_keys = reinterpret_cast<unsigned long long*>(ordinals);
   rle_tail(w, n, false, out_keys, counts, nruns, s);
   k_rle_lengths_dev<<<grid, 256, 0, s>>>(w.run_start, nruns, w.scal, nullptr, counts);

@@ -143,3 +143,34 @@ def test_package_exports_binning_api():
     for name in ("Histogram", "BinModel", "build_histogram", "top_k_bins", "compressible_mask",
                  "select_index_length", "merge_histograms", "nearest_center"):
         assert hasattr(nmk, name)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 511, 512, 4095, 4096, 4097, 100_003, 1_500_001])
+@pytest.mark.parametrize("with_vals", [False, True])
+def test_radix_sort64_matches_numpy(n, with_vals):
+    """k_sort.cu (the sort under the sparse histogram and its merge): stable
+    ascending order of 64-bit keys, values carried along, at sizes around the
+    warp, warp-run and tile edges; keys with few and with many distinct values."""
+    import torch
+    from paper_1703_02438_b200 import _native as N
+    lib = N.lib()
+    rng = np.random.default_rng(n + int(with_vals))
+    for kind in ("wide", "narrow", "bitpatterns"):
+        if kind == "wide":
+            keys = rng.integers(0, np.iinfo(np.uint64).max, n, dtype=np.uint64)
+        elif kind == "narrow":
+            keys = rng.integers(0, 7, n, dtype=np.uint64) << np.uint64(40)      # many equal keys: stability matters
+        else:
+            keys = np.abs(rng.normal(0, 1e6, n)).astype(np.float64).view(np.uint64)   # ordinal bit patterns
+        vals = np.arange(n, dtype=np.uint64)
+        d_k, d_v = torch.from_numpy(keys.view(np.int64)).cuda(), torch.from_numpy(vals.view(np.int64)).cuda()
+        o_k, o_v = torch.empty_like(d_k), torch.empty_like(d_v)
+        wsb = lib.nmk_sort64_ws_bytes(n, int(with_vals))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+        N.check(lib.nmk_sort64(d_k.data_ptr(), o_k.data_ptr(), d_v.data_ptr() if with_vals else None,
+                               o_v.data_ptr() if with_vals else None, n, ws.data_ptr(), wsb, None))
+        order = np.argsort(keys, kind="stable")
+        assert np.array_equal(o_k.cpu().numpy().view(np.uint64), keys[order]), kind
+        assert np.array_equal(d_k.cpu().numpy().view(np.uint64), keys)          # input untouched
+        if with_vals:
+            assert np.array_equal(o_v.cpu().numpy().view(np.uint64), vals[order]), kind
