@@ -14,10 +14,9 @@
 //           run-length encode.  Output = np.unique(ords, return_counts=True).
 #include <algorithm>
 
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
 
 #include "nmk_common.cuh"
+#include "nmk_block.cuh"
 #include "nmk_sort.cuh"
 
 namespace nmk {
@@ -216,9 +215,8 @@ k_rle_count(const unsigned long long* __restrict__ keys, uint64_t n, unsigned lo
     uint64_t i = c0 + (uint64_t)it * kRleThreads + threadIdx.x;
     if (i < n && keys[i] != ~0ULL && (i == 0 || keys[i] != keys[i - 1])) ++cnt;
   }
-  typedef cub::BlockReduce<unsigned, kRleThreads> BR;
-  __shared__ typename BR::TempStorage tmp;
-  unsigned tot = BR(tmp).Sum(cnt);
+  __shared__ unsigned tmp[kRleThreads / 32];
+  unsigned tot = block_reduce<kRleThreads>(cnt, SumOp(), tmp);
   if (threadIdx.x == 0) chunk_heads[blockIdx.x] = tot;
 }
 
@@ -227,8 +225,7 @@ k_rle_scatter(const unsigned long long* __restrict__ keys, uint64_t n,
               const unsigned long long* __restrict__ chunk_off,
               unsigned long long* __restrict__ run_key, unsigned long long* __restrict__ run_start,
               unsigned long long* __restrict__ nruns, unsigned long long nchunks) {
-  typedef cub::BlockScan<unsigned, kRleThreads> BS;
-  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned tmp[kRleThreads / 32 + 1];
   uint64_t c0 = (uint64_t)blockIdx.x * kRleChunk;
   // thread-contiguous items so ranks follow element order
   uint64_t i0 = c0 + (uint64_t)threadIdx.x * kRleItems;
@@ -239,8 +236,8 @@ k_rle_scatter(const unsigned long long* __restrict__ keys, uint64_t n,
     flags |= (hd ? 1u : 0u) << it;
     cnt += hd;
   }
-  unsigned ex;
-  BS(tmp).ExclusiveSum(cnt, ex);
+  unsigned tot_unused;
+  const unsigned ex = block_exclusive_sum<kRleThreads>(cnt, tot_unused, tmp);
   unsigned long long pos = chunk_off[blockIdx.x] + ex;
   for (int it = 0; it < kRleItems; ++it) {
     if (flags >> it & 1u) {

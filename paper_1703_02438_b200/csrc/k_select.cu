@@ -17,10 +17,9 @@
 // the first k rows of lexsort((ordinal, -count)).  Bins arrive in ordinal
 // order and centers are monotone in the ordinal, so compacting the selected
 // bins in ordinal order yields np.unique's sorted order directly.
-#include <cub/block/block_reduce.cuh>
-#include <cub/block/block_scan.cuh>
 
 #include "nmk_common.cuh"
+#include "nmk_block.cuh"
 
 namespace nmk {
 
@@ -84,13 +83,10 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
          uint64_t n_total, double* __restrict__ centers, double* __restrict__ cuts,
          T* __restrict__ centers_t, uint64_t cap_k, nmk_model* __restrict__ model,
          int auto_lo, int auto_n, unsigned long long* __restrict__ cov_out) {
-  typedef cub::BlockReduce<unsigned long long, kSelThreads> BRed;
-  typedef cub::BlockReduce<PassA, kSelThreads> BRedA;
-  typedef cub::BlockScan<unsigned, kSelThreads> BScan;
-  __shared__ union {
-    typename BRed::TempStorage red;
-    typename BRedA::TempStorage reda;
-    typename BScan::TempStorage scan;
+  __shared__ union {   // scratch of the CTA-wide reduce / exclusive sum (nmk_block.cuh)
+    unsigned long long red[kSelThreads / 32];
+    PassA reda[kSelThreads / 32];
+    unsigned scan[kSelThreads / 32 + 1];
   } tmp;
   __shared__ unsigned hist[NS][256];
   __shared__ unsigned long long s_prefix[NS], s_mask[NS], s_left[NS], s_kk[NS];
@@ -154,7 +150,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
       else if (c > pa.b) pa.b = c;
     }
   }
-  pa = BRedA(tmp.reda).Reduce(pa, PassAOp());
+  pa = block_reduce<kSelThreads>(pa, PassAOp(), tmp.reda);
   if (tid == 0) { s_bcast[0] = pa.m; s_bcast[1] = pa.a; s_bcast[2] = pa.tot; s_bcast[3] = pa.b; }
   __syncthreads();
   unsigned long long m = s_bcast[0], maxc = s_bcast[1], tot = s_bcast[2];
@@ -253,7 +249,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      unsigned long long v = BRed(tmp.red).Sum(acc[s]);
+      unsigned long long v = block_reduce<kSelThreads>(acc[s], SumOp(), tmp.red);
       if (tid == 0) s_cov[s] = (s_kk[s] < m) ? v + s_left[s] * s_prefix[s] : tot;
       __syncthreads();
     }
@@ -300,11 +296,11 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
     unsigned long long c = (i < M) ? bv.sel_count(i) : 0ULL;
     unsigned eq = (!take_all && c && c == t) ? 1u : 0u;
     unsigned eq_ex, eq_tot;
-    BScan(tmp.scan).ExclusiveSum(eq, eq_ex, eq_tot);
+    eq_ex = block_exclusive_sum<kSelThreads>(eq, eq_tot, tmp.scan);
     __syncthreads();
     bool chosen = c && (take_all || c > t || (eq && run_eq + eq_ex < need_eq));
     unsigned ch = chosen ? 1u : 0u, ch_ex, ch_tot;
-    BScan(tmp.scan).ExclusiveSum(ch, ch_ex, ch_tot);
+    ch_ex = block_exclusive_sum<kSelThreads>(ch, ch_tot, tmp.scan);
     __syncthreads();
     if (chosen) cuts[run_pos + ch_ex] = bv.center(i);
     run_eq += eq_tot;
@@ -327,7 +323,7 @@ k_select(const unsigned long long* __restrict__ keys, const unsigned long long* 
       keep = finite64(q) && (i == 0 || !(q == prevq) || !finite64(prevq));
     }
     unsigned kp = keep ? 1u : 0u, ex, tot2;
-    BScan(tmp.scan).ExclusiveSum(kp, ex, tot2);
+    ex = block_exclusive_sum<kSelThreads>(kp, tot2, tmp.scan);
     __syncthreads();
     if (keep) centers[kq + ex] = q;
     kq += tot2;
