@@ -30,15 +30,20 @@ def _pool() -> ThreadPoolExecutor:
 
 
 def _chunks():
-    """Two pinned chunks, each with the event of the last DMA that used it."""
+    """Two pinned chunks per device, each with the event of the last DMA that
+    used it (events belong to the device they were created on)."""
     global _slots
     import torch
     if _slots is None:
-        _slots = []
+        _slots = {}
+    dev = torch.cuda.current_device()
+    if dev not in _slots:
+        sl = []
         for _ in range(2):
             t = torch.empty(CHUNK_BYTES, dtype=torch.uint8, pin_memory=True)
-            _slots.append({"t": t, "np": t.numpy(), "ev": torch.cuda.Event()})
-    return _slots
+            sl.append({"t": t, "np": t.numpy(), "ev": torch.cuda.Event()})
+        _slots[dev] = sl
+    return _slots[dev]
 
 
 def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
