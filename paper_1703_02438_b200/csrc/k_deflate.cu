@@ -27,6 +27,8 @@
 //
 // Pipeline: k_deflate_segments (warp per segment) -> chunk_scan over segment
 // lengths -> k_deflate_gather (warp per segment into the compact output).
+#include <type_traits>
+
 #include "nmk_common.cuh"
 #include "nmk_scan.cuh"
 
@@ -37,15 +39,24 @@ namespace nmk {
 #endif
 constexpr int kDefWarps = NMK_DEF_WARPS;
 constexpr int kDefThreads = 32 * kDefWarps;
-constexpr int kDefHashBits = 11;
-constexpr int kDefHash = 1 << kDefHashBits;      // buckets of two u16 positions (newest low): 8 KB per warp
+#ifndef NMK_DEF_WAYS
+#define NMK_DEF_WAYS 2   // positions per hash bucket (2: 2048 u32 buckets, 4: 1024 u64 buckets; 8 KB per warp either way).
+                         // A/B: 4 ways: cfg3 ratio 6.23 -> 6.57 (zlib 8.38) at 4.4 -> 5.1 ms; cfg2 6.21 -> 6.17 at 11.7 -> 14.6 ms
+#endif
+constexpr int kDefWays = NMK_DEF_WAYS;
+constexpr int kDefHashBits = kDefWays == 4 ? 10 : 11;
+constexpr int kDefHash = 1 << kDefHashBits;      // buckets of kDefWays u16 positions (newest low): 8 KB per warp
+typedef typename std::conditional<kDefWays == 4, unsigned long long, uint32_t>::type bucket_t;
 constexpr uint32_t kNoPos = 0xffffu;
-constexpr uint32_t kEmptyBucket = 0xffffffffu;
+constexpr bucket_t kEmptyBucket = (bucket_t)~(bucket_t)0;
 constexpr int kMinMatch = 3, kMaxMatch = 258;
 // estimated bits of a match's length symbol / a near (1 or repeated) / any other distance symbol,
 // and the length from which a match is always taken (tuned on cfg2's index stream: ratio 4.9 -> 6.4 in a CPU model)
 constexpr int kProbe = 32;   // bytes a lane compares per candidate
-constexpr uint32_t kCostLen = 4, kCostNear = 1, kCostDist = 6, kCostLong = 24;
+#ifndef NMK_DEF_COSTLONG
+#define NMK_DEF_COSTLONG 24   // matches shorter than this pass the literal-cost filter (0: off -- cfg2 ratio 6.21 -> 5.21)
+#endif
+constexpr uint32_t kCostLen = 4, kCostNear = 1, kCostDist = 6, kCostLong = NMK_DEF_COSTLONG;
 constexpr int kStageWords = 128;                 // output bit ring per warp (a step emits <= 17 words)
 constexpr unsigned FULLW = 0xffffffffu;
 
@@ -108,7 +119,7 @@ struct HuffWork {          // scratch of the code construction (aliases the hash
 };
 struct __align__(16) DefWarp {
   union {
-    uint32_t hash[kDefHash];
+    bucket_t hash[kDefHash];
     HuffWork hw;
   };
   uint32_t lf[kHuffMax];   // literal/length symbol counts
@@ -121,7 +132,7 @@ struct __align__(16) DefWarp {
   uint16_t cost[256];                      // literal cost estimate, 1/8 bit: -log2 of the byte's share of the segment
 };
 static_assert(kCostLong <= (uint32_t)kProbe, "the cost filter reads the probe window");
-static_assert(sizeof(HuffWork) <= kDefHash * 4, "Huffman scratch must fit the hash table");
+static_assert(sizeof(HuffWork) <= kDefHash * sizeof(bucket_t), "Huffman scratch must fit the hash table");
 
 // bytes p .. p + 3 of the segment (little-endian); words beyond the segment read 0
 __device__ __forceinline__ uint32_t word_at(const uint32_t* __restrict__ W, uint32_t nw, uint32_t p) {
@@ -172,7 +183,7 @@ __device__ __forceinline__ uint32_t extend_coop(const uint32_t* __restrict__ W, 
 // a match (len, dist) that follows those literals.  Deterministic: both passes
 // produce the same token sequence.
 template <typename Tokens>
-__device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32_t n, uint32_t* hash,
+__device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32_t n, bucket_t* hash,
                                           const uint16_t* cost, int lane, Tokens&& tokens) {
   const uint32_t nw = (n + 3) >> 2;
   for (int k = lane; k < kDefHash; k += 32) hash[k] = kEmptyBucket;
@@ -194,10 +205,10 @@ __device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32
     const uint32_t w0 = a[0];
     const bool hashed = valid && i + kMinMatch <= n;
     const uint32_t h = hash3(w0);
-    const uint32_t bucket = hashed ? hash[h] : kEmptyBucket;   // the table as it was before this step
+    const bucket_t bucket = hashed ? hash[h] : kEmptyBucket;   // the table as it was before this step
     __syncwarp();
     const unsigned grp = __match_any_sync(FULLW, hashed ? h : (0x80000000u | (uint32_t)lane));
-    if (hashed && lane == 31 - __clz(grp)) hash[h] = (bucket << 16) | i;   // highest lane (latest position) wins
+    if (hashed && lane == 31 - __clz(grp)) hash[h] = (bucket_t)(bucket << 16) | (bucket_t)i;   // highest lane (latest position) wins
     __syncwarp();
     uint32_t best = 0, bd = 0;
     if (hashed) {
@@ -226,8 +237,8 @@ __device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32
       const uint32_t d_in = lower ? (uint32_t)(lane - (31 - __clz(lower))) : 0u;   // same hash earlier in this step
       if (d_in > 1 && d_in != rep) consider(d_in);
 #pragma unroll
-      for (int w = 0; w < 2; ++w) {
-        const uint32_t j = (bucket >> (16 * w)) & 0xffffu;
+      for (int w = 0; w < kDefWays; ++w) {
+        const uint32_t j = (uint32_t)(bucket >> (16 * w)) & 0xffffu;
         if (j == kNoPos) continue;
         const uint32_t d = i - j;
         if (d != 1 && d != rep && d != d_in) consider(d);
@@ -240,7 +251,7 @@ __device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32
       if (best >= (uint32_t)kMinMatch && best < (uint32_t)kCostLong) {
         uint32_t litc = 0;
 #pragma unroll
-        for (int w = 0; w < (int)(kCostLong + 3) / 4; ++w) {   // the match's bytes are in a[]
+        for (int w = 0; w < (int)(kCostLong + 3) / 4 && w < kProbe / 4; ++w) {   // the match's bytes are in a[]
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if ((uint32_t)(4 * w + q) < best) litc += cost[(a[w] >> (8 * q)) & 0xffu];

@@ -132,5 +132,12 @@ t_s, (first, variables) = wall(lambda: nmk.compress_series(snaps, cfg3), reps=1)
 res["cfg3_compress_series"] = {"wall_s": t_s, "transitions": 15, "s_per_transition": t_s / 15,
                                "gbs_wall": 15 * snaps[0].size * 4 / t_s / 1e9,
                                "note": "includes host zlib of every block (reference-identical .nmk bytes)"}
+cfg3g = nmk.PipelineConfig(tolerance=5e-3, bits=10, workers=16, deflate="gpu")
+nmk.compress_series(snaps[:3], cfg3g)
+t_sg, (first_g, variables_g) = wall(lambda: nmk.compress_series(snaps, cfg3g), reps=1)
+res["cfg3_compress_series_gpu_deflate"] = {"wall_s": t_sg, "s_per_transition": t_sg / 15,
+                                           "gbs_wall": 15 * snaps[0].nbytes / t_sg / 1e9,
+                                           "index_bytes": sum(len(v.index_table) for v in variables_g),
+                                           "index_bytes_zlib": sum(len(v.index_table) for v in variables)}
 res["host"] = {"cpu_count": __import__("os").cpu_count()}
 print(json.dumps(res, indent=1))
