@@ -39,6 +39,23 @@ namespace nmk {
 #endif
 constexpr int kDefWarps = NMK_DEF_WARPS;
 constexpr int kDefThreads = 32 * kDefWarps;
+#ifndef NMK_DEF_LONGHASH
+// The two u16 slots of a bucket word are two tables: slot 0 keyed by the next
+// NMK_DEF_SHORTLEN bytes, slot 1 by the next NMK_DEF_LONGLEN.  Index streams
+// reward long contexts (their short repeats cost more than literals): against
+// a two-way 3-byte table, (6, 10) takes cfg3 (B = 10) from ratio 6.23 to 7.40
+// and cfg2 from 6.21 to 6.28, and is faster (fewer useless candidates).
+// A/B: (3,8) 7.13 / 6.23, (4,8) 7.20 / 6.25, (6,8) 7.29 / 6.28, (6,12) 7.39 / 6.26.
+#define NMK_DEF_LONGHASH 1
+#endif
+#ifndef NMK_DEF_LONGLEN
+#define NMK_DEF_LONGLEN 10   // bytes under the second table's hash (5..12)
+#endif
+constexpr uint32_t kLongMask = NMK_DEF_LONGLEN >= 8 ? 0xffffffffu : ((1u << (8 * (NMK_DEF_LONGLEN - 4))) - 1u);
+constexpr uint32_t kLongMask2 = NMK_DEF_LONGLEN >= 12 || NMK_DEF_LONGLEN <= 8 ? 0xffffffffu : ((1u << (8 * (NMK_DEF_LONGLEN - 8))) - 1u);
+#ifndef NMK_DEF_SHORTLEN
+#define NMK_DEF_SHORTLEN 6   // bytes under the first table's hash (3..6)
+#endif
 #ifndef NMK_DEF_WAYS
 #define NMK_DEF_WAYS 2   // positions per hash bucket (2: 2048 u32 buckets, 4: 1024 u64 buckets; 8 KB per warp either way).
                          // A/B: 4 ways: cfg3 ratio 6.23 -> 6.57 (zlib 8.38) at 4.4 -> 5.1 ms; cfg2 6.21 -> 6.17 at 11.7 -> 14.6 ms
@@ -76,7 +93,9 @@ __device__ __forceinline__ void fixed_litlen(uint32_t sym, uint32_t& code, int& 
   code = rev_bits(code, len);
 }
 
-__device__ __forceinline__ uint32_t hash3(uint32_t v) { return ((v & 0xffffffu) * 2654435761u) >> (32 - kDefHashBits); }
+__device__ __forceinline__ uint32_t hash3(uint32_t v) {
+  return ((NMK_DEF_SHORTLEN >= 4 ? v : v & 0xffffffu) * 2654435761u) >> (32 - kDefHashBits);
+}
 
 // length 3..258 -> litlen symbol, extra bits, extra value (RFC 1951 3.2.5)
 __device__ __forceinline__ void len_symbol(uint32_t len, uint32_t& sym, uint32_t& ebits, uint32_t& eval) {
@@ -204,12 +223,32 @@ __device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32
     }
     const uint32_t w0 = a[0];
     const bool hashed = valid && i + kMinMatch <= n;
-    const uint32_t h = hash3(w0);
+    uint32_t h = hash3(w0);
+    if (NMK_DEF_SHORTLEN > 4)
+      h = ((w0 * 2654435761u) ^ ((a[1] & ((1u << (8 * (NMK_DEF_SHORTLEN - 4))) - 1u)) * 2246822519u)) >> (32 - kDefHashBits);
+#if NMK_DEF_LONGHASH
+    // two tables in one array of u16 pairs: slot 0 keyed by the next 3 bytes, slot 1 by the next 8
+    static_assert(kDefWays == 2, "the long-hash table takes the second way");
+    uint16_t* h16 = reinterpret_cast<uint16_t*>(hash);
+    const bool hashed8 = valid && i + NMK_DEF_LONGLEN <= n;
+    uint32_t hl = (a[0] * 2654435761u) ^ ((NMK_DEF_LONGLEN >= 8 ? a[1] : a[1] & kLongMask) * 2246822519u);
+    if (NMK_DEF_LONGLEN > 8) hl ^= (NMK_DEF_LONGLEN >= 12 ? a[2] : a[2] & kLongMask2) * 3266489917u;
+    hl >>= 32 - kDefHashBits;
+    const uint32_t c3 = hashed ? h16[2 * h] : kNoPos, c8 = hashed8 ? h16[2 * hl + 1] : kNoPos;
+    const bucket_t bucket = (bucket_t)c3 | ((bucket_t)c8 << 16);   // the tables as they were before this step
+    __syncwarp();
+    const unsigned grp = __match_any_sync(FULLW, hashed ? h : (0x80000000u | (uint32_t)lane));
+    const unsigned grp8 = __match_any_sync(FULLW, hashed8 ? hl : (0x80000000u | (uint32_t)lane));
+    if (hashed && lane == 31 - __clz(grp)) h16[2 * h] = (uint16_t)i;        // highest lane (latest position) wins
+    if (hashed8 && lane == 31 - __clz(grp8)) h16[2 * hl + 1] = (uint16_t)i;
+    __syncwarp();
+#else
     const bucket_t bucket = hashed ? hash[h] : kEmptyBucket;   // the table as it was before this step
     __syncwarp();
     const unsigned grp = __match_any_sync(FULLW, hashed ? h : (0x80000000u | (uint32_t)lane));
     if (hashed && lane == 31 - __clz(grp)) hash[h] = (bucket_t)(bucket << 16) | (bucket_t)i;   // highest lane (latest position) wins
     __syncwarp();
+#endif
     uint32_t best = 0, bd = 0;
     if (hashed) {
       // lanes measure their candidates up to kProbe bytes (all loads of a

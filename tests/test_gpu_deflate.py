@@ -34,9 +34,9 @@ def _blocks_on_device(blocks, stride):
 def test_index_stream_shapes_compress(tmp_path):
     """B = 10 (period-5 byte pattern) and B = 12 noisy streams: exact round
     trip, and the ratio stays within reach of zlib's (fewer match candidates
-    than zlib's hash chains: 6.2 vs 8.4 on cfg3, 1.19 vs 1.20 on cfg5)."""
+    than zlib's hash chains: 7.4 vs 8.4 on cfg3, 1.19 vs 1.20 on cfg5)."""
     for (b, c), E, bits, lo in ((workloads.cfg5_host(1 << 19, seed=5), 1e-4, 12, 0.97),
-                                (tuple(workloads.cfg3_host(shape=(4, 240, 480), steps=2, seed=3)[:2]), 5e-3, 10, 0.6)):
+                                (tuple(workloads.cfg3_host(shape=(4, 240, 480), steps=2, seed=3)[:2]), 5e-3, 10, 0.75)):
         enc = engine.encode(torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda(), E, bits, 1 << 16)
         lens = enc.block_lengths()
         gpu = codec.gpu_deflate_blocks(enc.packed, enc.stride, lens)
