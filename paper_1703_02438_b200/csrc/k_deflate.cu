@@ -57,8 +57,8 @@ constexpr uint32_t kLongMask2 = NMK_DEF_LONGLEN >= 12 || NMK_DEF_LONGLEN <= 8 ? 
 #define NMK_DEF_SHORTLEN 6   // bytes under the first table's hash (3..6)
 #endif
 #ifndef NMK_DEF_WAYS
-#define NMK_DEF_WAYS 2   // positions per hash bucket (2: 2048 u32 buckets, 4: 1024 u64 buckets; 8 KB per warp either way).
-                         // A/B: 4 ways: cfg3 ratio 6.23 -> 6.57 (zlib 8.38) at 4.4 -> 5.1 ms; cfg2 6.21 -> 6.17 at 11.7 -> 14.6 ms
+#define NMK_DEF_WAYS 2   // u16 positions per bucket word: 2 (one per table, 2048 u32 buckets) or 4 (two per table,
+                         // 1024 u64 buckets; A/B: cfg3 ratio 7.40 -> 7.56, cfg2 unchanged, 28-40 % slower)
 #endif
 constexpr int kDefWays = NMK_DEF_WAYS;
 constexpr int kDefHashBits = kDefWays == 4 ? 10 : 11;
@@ -227,20 +227,31 @@ __device__ __forceinline__ void lz77_warp(const uint32_t* __restrict__ W, uint32
     if (NMK_DEF_SHORTLEN > 4)
       h = ((w0 * 2654435761u) ^ ((a[1] & ((1u << (8 * (NMK_DEF_SHORTLEN - 4))) - 1u)) * 2246822519u)) >> (32 - kDefHashBits);
 #if NMK_DEF_LONGHASH
-    // two tables in one array of u16 pairs: slot 0 keyed by the next 3 bytes, slot 1 by the next 8
-    static_assert(kDefWays == 2, "the long-hash table takes the second way");
-    uint16_t* h16 = reinterpret_cast<uint16_t*>(hash);
+    // two tables in one array: a bucket word's first half is keyed by the next
+    // NMK_DEF_SHORTLEN bytes, its second half by the next NMK_DEF_LONGLEN
+    // (one u16 position each with 2 ways, two -- newest low -- with 4)
     const bool hashed8 = valid && i + NMK_DEF_LONGLEN <= n;
     uint32_t hl = (a[0] * 2654435761u) ^ ((NMK_DEF_LONGLEN >= 8 ? a[1] : a[1] & kLongMask) * 2246822519u);
     if (NMK_DEF_LONGLEN > 8) hl ^= (NMK_DEF_LONGLEN >= 12 ? a[2] : a[2] & kLongMask2) * 3266489917u;
     hl >>= 32 - kDefHashBits;
-    const uint32_t c3 = hashed ? h16[2 * h] : kNoPos, c8 = hashed8 ? h16[2 * hl + 1] : kNoPos;
-    const bucket_t bucket = (bucket_t)c3 | ((bucket_t)c8 << 16);   // the tables as they were before this step
-    __syncwarp();
     const unsigned grp = __match_any_sync(FULLW, hashed ? h : (0x80000000u | (uint32_t)lane));
     const unsigned grp8 = __match_any_sync(FULLW, hashed8 ? hl : (0x80000000u | (uint32_t)lane));
-    if (hashed && lane == 31 - __clz(grp)) h16[2 * h] = (uint16_t)i;        // highest lane (latest position) wins
-    if (hashed8 && lane == 31 - __clz(grp8)) h16[2 * hl + 1] = (uint16_t)i;
+    bucket_t bucket;   // the tables as they were before this step
+    if constexpr (kDefWays == 2) {
+      uint16_t* h16 = reinterpret_cast<uint16_t*>(hash);
+      const uint32_t c3 = hashed ? h16[2 * h] : kNoPos, c8 = hashed8 ? h16[2 * hl + 1] : kNoPos;
+      bucket = (bucket_t)c3 | ((bucket_t)c8 << 16);
+      __syncwarp();
+      if (hashed && lane == 31 - __clz(grp)) h16[2 * h] = (uint16_t)i;        // highest lane (latest position) wins
+      if (hashed8 && lane == 31 - __clz(grp8)) h16[2 * hl + 1] = (uint16_t)i;
+    } else {
+      uint32_t* h32 = reinterpret_cast<uint32_t*>(hash);
+      const uint32_t c3 = hashed ? h32[2 * h] : 0xffffffffu, c8 = hashed8 ? h32[2 * hl + 1] : 0xffffffffu;
+      bucket = (bucket_t)c3 | ((bucket_t)c8 << 32);
+      __syncwarp();
+      if (hashed && lane == 31 - __clz(grp)) h32[2 * h] = (c3 << 16) | i;
+      if (hashed8 && lane == 31 - __clz(grp8)) h32[2 * hl + 1] = (c8 << 16) | i;
+    }
     __syncwarp();
 #else
     const bucket_t bucket = hashed ? hash[h] : kEmptyBucket;   // the table as it was before this step
